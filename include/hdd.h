@@ -1,0 +1,155 @@
+/*
+ * hdd.h — C ABI of libhdd_b200.so, the B200-native batched HDD likelihood.
+ *
+ * One plan = one BayesProblem of the reference (mesh level, parametrization,
+ * right-hand side f, MeasurementModel), compiled into device tables once;
+ * every forward call evaluates a whole batch Z[B, n_z] of parameter samples:
+ *
+ *     Z -> kappa(Z) -> bottom-up Schur sweep -> S(Z) = F(u) -> log L(Z)
+ *
+ * Entry points and the reference interfaces they replace
+ * (paths under /root/reference/pkg/src/hddsolve/):
+ *
+ *   hdd_plan_create    BayesProblem(...) (bayes.py:155-177) + build_mesh
+ *                      (mesh.py:90-111) + build_tree (ddtree.py:119-174) +
+ *                      FunctionalTracker.__init__ (functionals.py:146-175):
+ *                      geometry, merge plan and observation routing, built once.
+ *   hdd_forward_batch  forward_functionals (bayes.py:180-198) and
+ *                      log_likelihood / gaussian_log_likelihood
+ *                      (bayes.py:222-231), batched over Z rows; internally
+ *                      ParamField.kappa (bayes.py:73-77), leaves_to_root in
+ *                      functionals_only mode (hdd.py:289-394) and the tracker
+ *                      callbacks (functionals.py:182-224).
+ *   hdd_plan_destroy   (garbage collection of the problem / MapStore).
+ *   hdd_last_error     the reference's exceptions (errors.py:4-21): the
+ *                      status code selects ConfigError / UsageError /
+ *                      NumericalError(node_id).
+ *   hdd_plan_*info     debug views of the plan (DDNode index sets and merge
+ *                      plan, ddtree.py:40-57), used by the host-logic tests.
+ *
+ * Conventions: plain pointers and sizes only.  Device pointers are CUDA
+ * device addresses on the plan's device; `stream` is a cudaStream_t passed as
+ * void*.  All functions return HDD_OK (0) or a negative status; no call
+ * falls back to the CPU.
+ */
+#ifndef HDD_B200_H
+#define HDD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HDD_OK = 0,
+  HDD_ERR_CONFIG = -1,     /* ConfigError: invalid level, n_z, sigma, kappa  */
+  HDD_ERR_USAGE = -2,      /* UsageError: bad call / observation routing      */
+  HDD_ERR_NUMERICAL = -3,  /* NumericalError: non-SPD interface, non-finite S */
+  HDD_ERR_CUDA = -4,       /* CUDA runtime failure (message carries detail)   */
+  HDD_ERR_NOMEM = -5
+};
+
+enum { HDD_OBS_POINT = 0, HDD_OBS_MEAN = 1 };
+
+typedef struct HddPlan HddPlan;
+
+typedef struct {
+  int32_t level;           /* mesh level L: 2^L cells per side (4 <= L <= 11) */
+  int32_t n_z;             /* parameter dimension                             */
+  /* separable log-coefficient: for triangle t = 2(i N + j) + type,
+   *   log kappa_t = sum_k coef[k] z[k] sx[k][2 i + type] sy[k][2 j + type]
+   * (sine-KL: sin(pi a_k cx), sin(pi b_k cy), coef 0.5/k; reference
+   *  indicator ParamField: 0/1 interval masks, coef 1).  Row-major
+   *  [n_z][2N] host arrays.                                                   */
+  const double* sx;
+  const double* sy;
+  const double* coef;
+  const double* f;         /* nodal right-hand side [n nodes], NULL = 1       */
+  int32_t n_obs;
+  const int32_t* obs_kind; /* HDD_OBS_POINT (mesh node index) or HDD_OBS_MEAN */
+  const int64_t* obs_id;   /* (reference post-order tree node id)            */
+  const double* sigma;     /* [n_obs] noise std, > 0                          */
+  const double* y;         /* [n_obs] data, NULL = no likelihood             */
+  int32_t max_batch;       /* samples per internal sub-batch (0 = auto)       */
+  int32_t device;          /* CUDA device, -1 = host-only plan (tests)        */
+  int32_t keep_nodes;      /* 1 = keep every depth's outputs (debug hooks)    */
+} HddPlanDesc;
+
+typedef struct {
+  int32_t code;
+  int32_t sample;          /* failing sample (-1 if n/a)                      */
+  int64_t node_id;         /* failing reference tree node id (-1 if n/a)     */
+  char message[256];
+} HddError;
+
+typedef struct {
+  int32_t level, n_cells, leaf_cells, leaf_depth;
+  int32_t n_upper, n_leaves, n_obs, leaf_cols;
+  int32_t max_batch, n_kernels_per_batch;
+  int64_t workspace_bytes;
+} HddPlanInfo;
+
+typedef struct {
+  int64_t ref_id;          /* reference post-order node id                    */
+  int32_t depth, i0, i1, j0, j1;
+  int32_t son[2];          /* plan indices of the sons; -1-leaf for leaves    */
+  int32_t k, ng, nc;       /* |pruned boundary|, |interface|, output columns */
+  const int64_t* bnd;      /* [k] pruned boundary ids (sorted)                */
+  const int64_t* gamma;    /* [ng] interface ids (sorted)                     */
+  const int32_t* gmap;     /* [2][k+ng] son output row of each father index  */
+  const int32_t* csrc;     /* [nc][2] son column feeding each column, -1 none */
+  const double* ccoef;     /* [nc][2] coefficients                            */
+  const int32_t* cbirth;   /* [nc] interface position of a born point, -1    */
+} HddNodeInfo;
+
+typedef struct {
+  int64_t ref_id;
+  int32_t i0, j0, ncols, has_mean;
+  const int32_t* birth;    /* [ncols][3]: in-leaf level, node, gamma pos     */
+} HddLeafInfo;
+
+typedef struct {
+  int32_t kind;            /* 0 = root column, 1 = constant                   */
+  int32_t col;
+  double value;
+} HddObsInfo;
+
+int hdd_plan_create(const HddPlanDesc* desc, HddPlan** out);
+int hdd_plan_destroy(HddPlan* plan);
+
+/* Z_dev [B][n_z], S_dev [B][n_obs] (nullable), ll_dev [B] (nullable). */
+int hdd_forward_batch(HddPlan* plan, const double* Z_dev, int64_t B,
+                      double* S_dev, double* ll_dev, void* stream);
+
+/* Same call with HOST buffers: copies in, runs, copies out (pinned staging). */
+int hdd_forward_batch_host(HddPlan* plan, const double* Z_host, int64_t B,
+                           double* S_host, double* ll_host);
+
+/* Per-triangle kappa for a batch (parity hook for the assembly kernel). */
+int hdd_kappa_batch(HddPlan* plan, const double* Z_dev, int64_t B,
+                    double* kappa_dev, void* stream);
+
+int hdd_last_error(const HddPlan* plan, HddError* out);
+/* Error of the last failed hdd_plan_create (no plan exists then). */
+int hdd_create_error(HddError* out);
+
+int hdd_plan_info(const HddPlan* plan, HddPlanInfo* out);
+int hdd_plan_node_info(const HddPlan* plan, int32_t idx, HddNodeInfo* out);
+int hdd_plan_leaf_info(const HddPlan* plan, int32_t idx, HddLeafInfo* out);
+int hdd_plan_obs_info(const HddPlan* plan, int32_t idx, HddObsInfo* out);
+/* In-leaf template: level r = 0..7 -> K, k, ng and the son gather maps. */
+int hdd_leaf_template(int32_t r, int32_t* K, int32_t* k, int32_t* ng,
+                      const int32_t** map1, const int32_t** map2);
+
+/* Debug: copy node `idx` (plan index; leaves are -1-leaf) outputs of the last
+ * forward call for sample b: psi [k][k], R [k][nc], sigma [nc] to host. */
+int hdd_debug_node_output(HddPlan* plan, int32_t idx, int32_t b,
+                          double* psi, double* R, double* sigma);
+
+const char* hdd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HDD_B200_H */

@@ -1,0 +1,28 @@
+"""B200-native batched HDD likelihood (arXiv 1708.02207 hot path).
+
+Z[B, n_z] -> kappa(Z) -> bottom-up Schur-complement sweep over the
+hierarchical domain decomposition -> observation functionals F(u) ->
+Gaussian log-likelihood, all in fp64 sm_100a CUDA kernels behind the C ABI of
+libhdd_b200.so (include/hdd.h).  The Python surface mirrors the reference
+package `hddsolve` (bayes.py / mesh.py / ddtree.py / errors.py).
+"""
+from .bayes import (  # noqa: F401
+    BayesProblem,
+    MeasurementModel,
+    ParamField,
+    Prior,
+    SineKLField,
+    aligned_partition,
+    forward_functionals,
+    forward_functionals_batch,
+    gaussian_log_likelihood,
+    kl_pairs,
+    log_likelihood,
+    log_likelihood_batch,
+    mean_observations,
+    posterior_weights,
+)
+from .errors import ConfigError, GeometryError, NumericalError, UsageError  # noqa: F401
+from .geometry import DDTree, Mesh, Rect, boundary_nodes, build_mesh, build_tree, interior_nodes  # noqa: F401
+
+__version__ = "0.1.0"

@@ -1,0 +1,423 @@
+"""Bayesian likelihood API — drop-in for the reference's likelihood path.
+
+Same names, argument meaning and error behaviour as
+/root/reference/pkg/src/hddsolve/bayes.py, with the forward map running on
+the B200 through libhdd_b200.so:
+
+  reference                                   here
+  ParamField.build / .kappa (bayes.py:50-77)  ParamField (indicator) / SineKLField
+  Prior (bayes.py:80-120)                     Prior (same draw order)
+  MeasurementModel (bayes.py:123-147)         MeasurementModel
+  mean_observations (bayes.py:150-152)        mean_observations
+  BayesProblem (bayes.py:155-177)             BayesProblem (+ device, max_batch)
+  forward_functionals (bayes.py:180-198)      forward_functionals  (B = 1 wrapper)
+  gaussian_log_likelihood (bayes.py:222-224)  gaussian_log_likelihood
+  log_likelihood (bayes.py:227-231)           log_likelihood       (B = 1 wrapper)
+  posterior_grid weights (bayes.py:325-330)   posterior_weights
+  (per-sample Python loop)                    forward_functionals_batch /
+                                              log_likelihood_batch (one C call)
+
+Only f and g of the BASELINE problem class are supported on the device path:
+any nodal f, and g = 0 (the Dirichlet rows are pruned).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, UsageError
+from .geometry import DDTree, Mesh, Rect, cell_centroid_tables
+
+__all__ = [
+    "ParamField", "SineKLField", "Prior", "MeasurementModel", "BayesProblem", "mean_observations",
+    "aligned_partition", "kl_pairs", "forward_functionals", "forward_functionals_batch", "log_likelihood",
+    "log_likelihood_batch", "gaussian_log_likelihood", "posterior_weights",
+]
+
+
+def aligned_partition(count: int):
+    """Tree-aligned power-of-two partition of the unit square (bayes.py:29-47)."""
+    if count < 1 or count & (count - 1):
+        raise ConfigError(f"partition size must be a power of two, got {count}")
+    rects = [Rect(0.0, 1.0, 0.0, 1.0)]
+    depth = 0
+    while len(rects) < count:
+        nxt = []
+        for r in rects:
+            if depth % 2 == 0:
+                mid = 0.5 * (r.x0 + r.x1)
+                nxt += [Rect(r.x0, mid, r.y0, r.y1), Rect(mid, r.x1, r.y0, r.y1)]
+            else:
+                mid = 0.5 * (r.y0 + r.y1)
+                nxt += [Rect(r.x0, r.x1, r.y0, mid), Rect(r.x0, r.x1, mid, r.y1)]
+        rects = nxt
+        depth += 1
+    return rects
+
+
+def kl_pairs(n: int):
+    """Positive-integer pairs (a, b) ordered by a + b, then a (BASELINE.json)."""
+    out, s = [], 2
+    while len(out) < n:
+        for a in range(1, s):
+            out.append((a, s - a))
+            if len(out) == n:
+                break
+        s += 1
+    return out
+
+
+class _Separable:
+    """log kappa_t = sum_k coef_k z_k sx_k(cx_t) sy_k(cy_t) — the form the
+    device kernel evaluates (csrc/hdd_kernels.cu, kappa_kernel)."""
+
+    n_z: int
+    sx: np.ndarray
+    sy: np.ndarray
+    coef: np.ndarray
+    mesh: Mesh
+
+    def kappa_values(self, z) -> np.ndarray:
+        """Host evaluation (API convenience; the batched path computes kappa on the GPU)."""
+        z = np.asarray(z, dtype=float)
+        if z.shape != (self.n_z,):
+            raise ConfigError(f"parameter vector must have length {self.n_z}")
+        N = self.mesh.n_cells
+        sx = self.sx.reshape(self.n_z, N, 2)
+        sy = self.sy.reshape(self.n_z, N, 2)
+        q = np.einsum("k,kit,kjt->ijt", self.coef * z, sx, sy)
+        return np.exp(q).reshape(-1)
+
+    def kappa(self, z):
+        return self.kappa_values(z)
+
+
+class SineKLField(_Separable):
+    """BASELINE field kappa = exp(0.5 sum_k z_k/k sin(pi a_k x1) sin(pi b_k x2))
+    at triangle centroids."""
+
+    kind = "sine_kl"
+
+    def __init__(self, tree_or_mesh, n_z: int):
+        self.mesh = tree_or_mesh.mesh if isinstance(tree_or_mesh, DDTree) else tree_or_mesh
+        if n_z < 1:
+            raise ConfigError("n_z must be positive")
+        self.n_z = int(n_z)
+        self.pairs = kl_pairs(self.n_z)
+        cx, cy = cell_centroid_tables(self.mesh)
+        a = np.array([p[0] for p in self.pairs], dtype=float)
+        b = np.array([p[1] for p in self.pairs], dtype=float)
+        self.sx = np.ascontiguousarray(np.sin(math.pi * a[:, None] * cx[None, :]))
+        self.sy = np.ascontiguousarray(np.sin(math.pi * b[:, None] * cy[None, :]))
+        self.coef = 0.5 / np.arange(1, self.n_z + 1, dtype=float)
+
+
+@dataclass(frozen=True)
+class ParamField(_Separable):
+    """Reference indicator parametrization kappa_t = exp(z[region(t)])
+    over `aligned_partition(n_z)` (bayes.py:50-77)."""
+
+    n_z: int
+    regions: tuple
+    mesh: Mesh
+    sx: np.ndarray = field(repr=False)
+    sy: np.ndarray = field(repr=False)
+    coef: np.ndarray = field(repr=False)
+    kind = "indicator"
+
+    @classmethod
+    def build(cls, tree: DDTree, n_z: int) -> "ParamField":
+        regions = aligned_partition(n_z)
+        cx, cy = cell_centroid_tables(tree.mesh)
+        sx = np.stack([((cx >= r.x0) & (cx <= r.x1)).astype(float) for r in regions])
+        sy = np.stack([((cy >= r.y0) & (cy <= r.y1)).astype(float) for r in regions])
+        # every centroid must be covered exactly once (bayes.py:69-70)
+        cover = np.einsum("kx,ky->xy", sx, sy)
+        if not np.all(cover >= 1):
+            raise ConfigError("partition does not cover the mesh")
+        return cls(n_z, tuple(regions), tree.mesh, np.ascontiguousarray(sx), np.ascontiguousarray(sy),
+                   np.ones(n_z))
+
+
+@dataclass(frozen=True)
+class Prior:
+    """Independent per-component prior, standard normal or uniform (bayes.py:80-120)."""
+
+    components: tuple
+
+    @classmethod
+    def normal(cls, n_z):
+        return cls(tuple(("normal",) for _ in range(n_z)))
+
+    @classmethod
+    def uniform(cls, n_z, a, b):
+        if not a < b:
+            raise ConfigError("uniform prior requires a < b")
+        return cls(tuple(("uniform", float(a), float(b)) for _ in range(n_z)))
+
+    @property
+    def n_z(self):
+        return len(self.components)
+
+    def log_pdf(self, z) -> float:
+        z = np.atleast_1d(np.asarray(z, dtype=float))
+        total = 0.0
+        for zi, comp in zip(z, self.components):
+            if comp[0] == "normal":
+                total += -0.5 * zi * zi - 0.5 * math.log(2.0 * math.pi)
+            else:
+                if zi < comp[1] or zi > comp[2]:
+                    return -np.inf
+                total += -math.log(comp[2] - comp[1])
+        return total
+
+    def sample(self, rng, size=None):
+        cols = [rng.standard_normal(size) if c[0] == "normal" else rng.uniform(c[1], c[2], size)
+                for c in self.components]
+        return np.stack(cols, axis=-1)
+
+
+@dataclass(frozen=True)
+class MeasurementModel:
+    """Observation functionals ("point", node index) / ("mean", tree node id),
+    noise levels and data (bayes.py:123-147)."""
+
+    observations: tuple
+    sigma: np.ndarray
+    y: np.ndarray | None = None
+
+    def __post_init__(self):
+        sigma = np.asarray(self.sigma, dtype=float)
+        if sigma.shape != (len(self.observations),) or not np.all(sigma > 0):
+            raise ConfigError("one positive noise level per observation required")
+        object.__setattr__(self, "sigma", sigma)
+        if self.y is not None:
+            y = np.asarray(self.y, dtype=float)
+            if y.shape != sigma.shape:
+                raise ConfigError("data vector length must match the observations")
+            object.__setattr__(self, "y", y)
+
+    @property
+    def n_y(self):
+        return len(self.observations)
+
+    def with_data(self, y):
+        return MeasurementModel(self.observations, self.sigma, np.asarray(y, dtype=float))
+
+
+def mean_observations(tree: DDTree, depth: int):
+    """One mean observation per tree node at `depth`, post-order (bayes.py:150-152)."""
+    return tuple(("mean", nd.id) for nd in tree.nodes_at_depth(depth))
+
+
+class _Plan:
+    """Owns one HddPlan* (device tables + workspace)."""
+
+    def __init__(self, problem: "BayesProblem", device: int, max_batch: int, keep_nodes: bool = False):
+        L = _lib.lib()
+        mesh = problem.tree.mesh
+        param = problem.param
+        model = problem.model
+        obs = model.observations
+        kinds = np.array([_lib.HDD_OBS_POINT if k == "point" else
+                          (_lib.HDD_OBS_MEAN if k == "mean" else -1) for k, _ in obs], dtype=np.int32)
+        if (kinds < 0).any():
+            bad = [k for k, _ in obs if k not in ("point", "mean")][0]
+            raise ConfigError(f"unknown observation kind {bad!r}")
+        self._keep = dict(
+            sx=np.ascontiguousarray(param.sx, dtype=np.float64),
+            sy=np.ascontiguousarray(param.sy, dtype=np.float64),
+            coef=np.ascontiguousarray(param.coef, dtype=np.float64),
+            f=None if problem._f_is_one else np.ascontiguousarray(problem.f, dtype=np.float64),
+            kind=kinds, ids=np.array([int(i) for _, i in obs], dtype=np.int64),
+            sigma=np.ascontiguousarray(model.sigma, dtype=np.float64),
+            y=None if model.y is None else np.ascontiguousarray(model.y, dtype=np.float64))
+        k = self._keep
+        ptr = lambda a, t: None if a is None else a.ctypes.data_as(t)  # noqa: E731
+        desc = _lib.HddPlanDesc(
+            level=mesh.level, n_z=param.n_z,
+            sx=ptr(k["sx"], _lib._f64p), sy=ptr(k["sy"], _lib._f64p), coef=ptr(k["coef"], _lib._f64p),
+            f=ptr(k["f"], _lib._f64p), n_obs=len(obs), obs_kind=ptr(k["kind"], _lib._i32p),
+            obs_id=ptr(k["ids"], _lib._i64p), sigma=ptr(k["sigma"], _lib._f64p), y=ptr(k["y"], _lib._f64p),
+            max_batch=int(max_batch), device=int(device), keep_nodes=int(keep_nodes))
+        h = C.c_void_p()
+        rc = L.hdd_plan_create(C.byref(desc), C.byref(h))
+        if rc != _lib.HDD_OK:
+            e = _lib.HddError()
+            L.hdd_create_error(C.byref(e))
+            _lib.raise_for(rc, e)
+        self.handle = h
+        self.lib = L
+        self.n_z = param.n_z
+        self.n_obs = len(obs)
+        self.device = device
+
+    def check(self, rc):
+        if rc != _lib.HDD_OK:
+            e = _lib.HddError()
+            self.lib.hdd_last_error(self.handle, C.byref(e))
+            _lib.raise_for(rc, e)
+
+    def info(self) -> _lib.HddPlanInfo:
+        out = _lib.HddPlanInfo()
+        self.check(self.lib.hdd_plan_info(self.handle, C.byref(out)))
+        return out
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self.lib.hdd_plan_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+@dataclass
+class BayesProblem:
+    """Forward setup shared by every likelihood evaluation (bayes.py:155-177).
+
+    `compression` (a ToleranceSpec) is accepted for API compatibility; the
+    device path computes the maps densely, i.e. exactly, which is within every
+    truncation tolerance of the reference low-rank path.  `device` selects the
+    CUDA device; `max_batch` caps the internal sub-batch (0 = size to memory).
+    """
+
+    tree: DDTree
+    param: object
+    f: np.ndarray
+    g: np.ndarray
+    model: MeasurementModel
+    compression: object = None
+    threads: int = 1
+    forward_calls: int = 0
+    device: int = 0
+    max_batch: int = 0
+    _plan: object = field(default=None, repr=False)
+
+    def __post_init__(self):
+        mesh = self.tree.mesh
+        f = np.asarray(self.f, dtype=float)
+        g = np.asarray(self.g, dtype=float)
+        if f.shape != (mesh.n_nodes,):
+            raise UsageError("data sizes do not match the mesh")
+        if g.shape != (4 * mesh.n_cells,):
+            raise UsageError("data sizes do not match the mesh")
+        if np.any(g != 0.0):
+            raise ConfigError("the device likelihood path supports g = 0 only (Dirichlet rows are pruned)")
+        self.f = f
+        self.g = g
+        self._f_is_one = bool(np.all(f == 1.0))
+
+    def plan(self) -> _Plan:
+        if self._plan is None:
+            self._plan = _Plan(self, self.device, self.max_batch)
+        return self._plan
+
+
+def _as_batch(Z, n_z):
+    try:
+        import torch
+    except ImportError:   # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(Z, torch.Tensor):
+        if Z.dim() == 1:
+            Z = Z[None]
+        if Z.shape[-1] != n_z:
+            raise ConfigError(f"parameter vector must have length {n_z}")
+        return Z
+    Z = np.asarray(Z, dtype=np.float64)
+    if Z.ndim == 1:
+        Z = Z[None]
+    if Z.ndim != 2 or Z.shape[1] != n_z:
+        raise ConfigError(f"parameter vector must have length {n_z}")
+    return np.ascontiguousarray(Z)
+
+
+def _run(problem: BayesProblem, Z, want_S: bool, want_ll: bool):
+    plan = problem.plan()
+    Zb = _as_batch(Z, plan.n_z)
+    B = Zb.shape[0]
+    if isinstance(Zb, np.ndarray):
+        S = np.empty((B, plan.n_obs)) if want_S else None
+        ll = np.empty(B) if want_ll else None
+        f64 = _lib._f64p
+        rc = plan.lib.hdd_forward_batch_host(
+            plan.handle, Zb.ctypes.data_as(f64), B,
+            S.ctypes.data_as(f64) if S is not None else None,
+            ll.ctypes.data_as(f64) if ll is not None else None)
+        plan.check(rc)
+        return S, ll
+    import torch
+    if not Zb.is_cuda:
+        raise UsageError("torch inputs must live on the plan's CUDA device")
+    Zb = Zb.to(torch.float64).contiguous()
+    S = torch.empty((B, plan.n_obs), dtype=torch.float64, device=Zb.device) if want_S else None
+    ll = torch.empty(B, dtype=torch.float64, device=Zb.device) if want_ll else None
+    stream = torch.cuda.current_stream(Zb.device).cuda_stream
+    rc = plan.lib.hdd_forward_batch(plan.handle, C.c_void_p(Zb.data_ptr()), B,
+                                    C.c_void_p(S.data_ptr()) if S is not None else None,
+                                    C.c_void_p(ll.data_ptr()) if ll is not None else None,
+                                    C.c_void_p(stream))
+    plan.check(rc)
+    return S, ll
+
+
+def forward_functionals_batch(problem: BayesProblem, Z):
+    """S[B, n_y] for every row of Z (numpy host array or CUDA torch tensor)."""
+    S, _ = _run(problem, Z, True, False)
+    problem.forward_calls += int(S.shape[0])
+    return S
+
+
+def log_likelihood_batch(problem: BayesProblem, Z):
+    """ll[B] for every row of Z; raises UsageError without data (bayes.py:228-229)."""
+    if problem.model.y is None:
+        raise UsageError("measurement model carries no data")
+    _, ll = _run(problem, Z, False, True)
+    problem.forward_calls += int(ll.shape[0])
+    return ll
+
+
+def forward_functionals(problem: BayesProblem, z) -> np.ndarray:
+    """Observation vector S(z) (bayes.py:180-198), one sample."""
+    z = np.asarray(z, dtype=float)
+    if z.shape != (problem.param.n_z,):
+        raise ConfigError(f"parameter vector must have length {problem.param.n_z}")
+    return forward_functionals_batch(problem, z[None])[0]
+
+
+def gaussian_log_likelihood(y, s, sigma) -> float:
+    resid = (np.asarray(y) - np.asarray(s)) / sigma
+    return float(-0.5 * np.sum(resid ** 2) - np.sum(np.log(sigma * math.sqrt(2.0 * math.pi))))
+
+
+def log_likelihood(problem: BayesProblem, z, forward=None) -> float:
+    """bayes.py:227-231; `forward` keeps the reference's plug-in point."""
+    if problem.model.y is None:
+        raise UsageError("measurement model carries no data")
+    if forward is None:
+        z = np.asarray(z, dtype=float)
+        if z.shape != (problem.param.n_z,):
+            raise ConfigError(f"parameter vector must have length {problem.param.n_z}")
+        return float(log_likelihood_batch(problem, z[None])[0])
+    s = forward(problem, z)
+    return gaussian_log_likelihood(problem.model.y, s, problem.model.sigma)
+
+
+def posterior_weights(log_like, log_prior=None):
+    """Self-normalised posterior weights and the mode index.
+
+    joint = log_prior + log_like (prior omitted for prior draws), weights =
+    exp(joint - logsumexp(joint)), index = argmax(joint) with numpy's
+    first-occurrence tie rule — the pieces of posterior_grid reused for
+    batches (bayes.py:325-330)."""
+    ll = np.asarray(log_like, dtype=float)
+    joint = ll if log_prior is None else ll + np.asarray(log_prior, dtype=float)
+    mx = np.max(joint)
+    lse = mx + math.log(np.sum(np.exp(joint - mx)))
+    return np.exp(joint - lse), int(np.argmax(joint)), float(lse)

@@ -1,0 +1,497 @@
+// C ABI of libhdd_b200.so (see include/hdd.h): plan lifetime, device memory,
+// sub-batch scheduling of the kernels, error mapping.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "hdd.h"
+#include "hdd_device.h"
+#include "hdd_plan.h"
+
+using namespace hdd;
+
+struct HddPlan {
+  Plan plan;
+  DevPlan dev{};
+  int device = -1;
+  int bcap = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<void*> allocs;
+  DevUpper* d_upper = nullptr;
+  std::vector<DevUpper> h_upper;
+  std::vector<size_t> depth_smem;      // merge smem per depth
+  size_t leaf_smem = 0;
+  HddError err{};
+  // host-API staging
+  double* h_Z = nullptr;               // device copies for hdd_forward_batch_host
+  double* d_Z = nullptr;
+  double* d_S = nullptr;
+  double* d_ll = nullptr;
+  int64_t io_cap = 0;
+  int n_launches = 0;
+};
+
+static HddError g_create_err{};
+static std::mutex g_mu;
+
+static int set_err(HddError* e, int code, const std::string& msg, int sample = -1, int64_t node = -1) {
+  e->code = code;
+  e->sample = sample;
+  e->node_id = node;
+  std::snprintf(e->message, sizeof(e->message), "%s", msg.c_str());
+  return code;
+}
+
+#define CU(call)                                                                            \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return set_err(&pl->err, HDD_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+static int upload(HddPlan* pl, const std::vector<T>& v, const T** out) {
+  if (v.empty()) { *out = nullptr; return 0; }
+  void* p = nullptr;
+  CU(cudaMalloc(&p, v.size() * sizeof(T)));
+  pl->allocs.push_back(p);
+  CU(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  *out = static_cast<const T*>(p);
+  return 0;
+}
+
+static size_t merge_smem_bytes(const UpperNode& U, int ldp) {
+  int ngp = (U.ng + 3) & ~3;
+  size_t d = size_t(ngp) * ldp + ((U.nc + 1) & ~1) + 2 * size_t(U.nc);
+  size_t i = 2 * size_t(U.K) + 3 * size_t(U.nc);
+  return d * sizeof(double) + i * sizeof(int) + 64;
+}
+
+static int panel_ld(const UpperNode& U) {
+  int ldp = U.K + U.nc;
+  ldp += ((8 - ldp % 16) + 16) % 16;   // ldp = 8 (mod 16): conflict-free DMMA fragment loads
+  return ldp;
+}
+
+static int setup_device(HddPlan* pl, int max_batch) {
+  Plan& P = pl->plan;
+  CU(cudaSetDevice(pl->device));
+  CU(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking));
+  if (upload_leaf_template() != 0) return set_err(&pl->err, HDD_ERR_CUDA, "leaf template upload failed");
+  DevPlan& D = pl->dev;
+  D.N = P.N;
+  D.m = P.m;
+  D.n_z = P.n_z;
+  D.n_obs = int(P.obs_kind.size());
+  D.n_leaves = int(P.leaves.size());
+  D.leaf_cols = P.leaf_cols;
+  D.leaf_ld = P.leaf_ld;
+  D.h = P.h;
+  D.leaf_elems = P.leaf_elems;
+  D.leaf_buf = P.leaf_buf;
+  if (P.leaf_cols > 8)
+    return set_err(&pl->err, HDD_ERR_CONFIG,
+                   "more than 7 observations strictly inside one 16x16-cell leaf are not supported");
+  int rc;
+  if ((rc = upload(pl, P.sx, &D.sx))) return rc;
+  if ((rc = upload(pl, P.sy, &D.sy))) return rc;
+  if ((rc = upload(pl, P.coef, &D.coef))) return rc;
+  D.f = nullptr;
+  if (!P.f_is_one && (rc = upload(pl, P.f, &D.f))) return rc;
+  // leaves
+  std::vector<DevLeaf> dl(P.leaves.size());
+  for (size_t l = 0; l < P.leaves.size(); ++l) {
+    const Leaf& L = P.leaves[l];
+    DevLeaf& d = dl[l];
+    std::memset(&d, 0, sizeof(d));
+    d.i0 = L.i0;
+    d.j0 = L.j0;
+    d.ncols = int(L.cols.size());
+    d.ref_id = L.ref_id;
+    for (int c = 0; c < 16; ++c) { d.ctype[c] = 2; d.birth_r[c] = -1; d.birth_q[c] = -1; d.birth_g[c] = -1; }
+    for (int c = 0; c < d.ncols; ++c) {
+      d.ctype[c] = L.cols[c].kind == COL_LOAD ? 0 : (L.cols[c].kind == COL_MEAN ? 1 : 2);
+      d.birth_r[c] = L.birth[3 * c];
+      d.birth_q[c] = L.birth[3 * c + 1];
+      d.birth_g[c] = L.birth[3 * c + 2];
+    }
+  }
+  if ((rc = upload(pl, dl, &D.leaves))) return rc;
+  // upper nodes
+  std::vector<int32_t> gmap, csrc, cbirth;
+  std::vector<double> ccoef;
+  pl->h_upper.resize(P.upper.size());
+  pl->depth_smem.assign(P.upper_by_depth.size(), 0);
+  for (size_t u = 0; u < P.upper.size(); ++u) {
+    const UpperNode& U = P.upper[u];
+    DevUpper& d = pl->h_upper[u];
+    std::memset(&d, 0, sizeof(d));
+    d.k = U.k; d.ng = U.ng; d.K = U.K; d.nc = U.nc;
+    d.ldp = panel_ld(U);
+    d.out_ld = U.out_ld;
+    d.out_elems = U.out_elems;
+    d.out_off = U.out_off;
+    d.buf = U.buf;
+    d.ref_id = U.ref_id;
+    for (int sn = 0; sn < 2; ++sn) {
+      int s = U.son[sn];
+      if (s >= 0) {
+        const UpperNode& S = P.upper[s];
+        d.son_buf[sn] = S.buf;
+        d.son_k[sn] = S.k;
+        d.son_ld[sn] = S.out_ld;
+        d.son_elems[sn] = S.out_elems;
+        d.son_off[sn] = S.out_off;
+      } else {
+        int l = -1 - s;
+        d.son_buf[sn] = P.leaf_buf;
+        d.son_k[sn] = kLeafPerim;
+        d.son_ld[sn] = P.leaf_ld;
+        d.son_elems[sn] = P.leaf_elems;
+        d.son_off[sn] = int64_t(l) * P.leaf_elems;
+      }
+    }
+    d.gmap_off = int(gmap.size());
+    gmap.insert(gmap.end(), U.gmap.begin(), U.gmap.end());
+    d.col_off = int(cbirth.size());
+    csrc.insert(csrc.end(), U.csrc.begin(), U.csrc.end());
+    ccoef.insert(ccoef.end(), U.ccoef.begin(), U.ccoef.end());
+    cbirth.insert(cbirth.end(), U.cbirth.begin(), U.cbirth.end());
+    size_t sm = merge_smem_bytes(U, d.ldp);
+    if (sm > 227 * 1024)
+      return set_err(&pl->err, HDD_ERR_CONFIG,
+                     "interface panel of node " + std::to_string(U.ref_id) + " (" + std::to_string(U.ng) + "x" +
+                         std::to_string(U.K + U.nc) + ") exceeds shared memory; the global-panel merge tier is "
+                         "not built in this version");
+    pl->depth_smem[U.depth] = std::max(pl->depth_smem[U.depth], sm);
+  }
+  if ((rc = upload(pl, gmap, &D.gmap))) return rc;
+  if ((rc = upload(pl, csrc, &D.csrc))) return rc;
+  if ((rc = upload(pl, ccoef, &D.ccoef))) return rc;
+  if ((rc = upload(pl, cbirth, &D.cbirth))) return rc;
+  {
+    const DevUpper* du = nullptr;
+    if ((rc = upload(pl, pl->h_upper, &du))) return rc;
+    pl->d_upper = const_cast<DevUpper*>(du);
+  }
+  // observations
+  std::vector<int32_t> rk, rcol;
+  std::vector<double> rv;
+  double llc = 0.0;
+  for (size_t o = 0; o < P.route.size(); ++o) {
+    rk.push_back(P.route[o].kind);
+    rcol.push_back(P.route[o].col);
+    rv.push_back(P.route[o].value);
+    llc += std::log(P.sigma[o] * std::sqrt(2.0 * M_PI));
+  }
+  D.ll_const = llc;
+  if ((rc = upload(pl, rk, &D.route_kind))) return rc;
+  if ((rc = upload(pl, rcol, &D.route_col))) return rc;
+  if ((rc = upload(pl, rv, &D.route_val))) return rc;
+  if ((rc = upload(pl, P.sigma, &D.sigma))) return rc;
+  D.y = nullptr;
+  if (P.has_y && (rc = upload(pl, P.y, &D.y))) return rc;
+  // buffers: size the sub-batch
+  int64_t per_sample = int64_t(2) * P.N * P.N;
+  for (int64_t e : P.buf_elems_per_sample) per_sample += e;
+  int64_t bytes_per_sample = per_sample * 8;
+  int bcap = max_batch;
+  if (bcap <= 0) {
+    size_t freeb = 0, totb = 0;
+    CU(cudaMemGetInfo(&freeb, &totb));
+    int64_t budget = int64_t(double(freeb) * 0.6);
+    bcap = int(std::min<int64_t>(4096, std::max<int64_t>(1, budget / bytes_per_sample)));
+  }
+  pl->bcap = bcap;
+  D.bcap = bcap;
+  for (int b = 0; b < kMaxBuffers; ++b) D.buf[b] = nullptr;
+  if (P.n_buffers > kMaxBuffers) return set_err(&pl->err, HDD_ERR_CONFIG, "tree too deep for debug buffers");
+  for (int b = 0; b < P.n_buffers; ++b) {
+    void* p = nullptr;
+    size_t nb = size_t(P.buf_elems_per_sample[b]) * bcap * sizeof(double);
+    if (nb == 0) continue;
+    if (cudaMalloc(&p, nb) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(&pl->err, HDD_ERR_NOMEM, "device allocation of " + std::to_string(nb) + " bytes failed");
+    }
+    pl->allocs.push_back(p);
+    D.buf[b] = static_cast<double*>(p);
+  }
+  {
+    void* p = nullptr;
+    CU(cudaMalloc(&p, size_t(2) * P.N * P.N * bcap * sizeof(double)));
+    pl->allocs.push_back(p);
+    D.kappa = static_cast<double*>(p);
+    CU(cudaMalloc(&p, sizeof(DevError)));
+    pl->allocs.push_back(p);
+    D.err = static_cast<DevError*>(p);
+    CU(cudaMemset(p, 0, sizeof(DevError)));
+  }
+  if (P.root >= 0) {
+    const UpperNode& R = P.upper[P.root];
+    D.root_buf = R.buf;
+    D.root_off = R.out_off * bcap;
+    D.root_elems = R.out_elems;
+    D.root_sig = int64_t(R.k) * R.out_ld;
+  } else {
+    D.root_buf = P.leaf_buf;
+    D.root_off = 0;
+    D.root_elems = P.leaf_elems;
+    D.root_sig = int64_t(kLeafPerim) * P.leaf_ld;
+  }
+  pl->leaf_smem = leaf_smem_bytes(P.leaf_cols <= 2 ? 2 : (P.leaf_cols <= 4 ? 4 : 8));
+  pl->n_launches = 3 + int(P.upper_by_depth.size());
+  return HDD_OK;
+}
+
+extern "C" {
+
+const char* hdd_version(void) { return "hdd_b200 0.1 (sm_100a)"; }
+
+int hdd_create_error(HddError* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (out) *out = g_create_err;
+  return HDD_OK;
+}
+
+int hdd_plan_create(const HddPlanDesc* desc, HddPlan** out) {
+  if (!out) return HDD_ERR_USAGE;
+  *out = nullptr;
+  HddPlan* pl = new HddPlan();
+  int code = HDD_OK;
+  std::string msg = build_plan(desc, pl->plan, &code);
+  if (code != HDD_OK) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    set_err(&g_create_err, code, msg);
+    delete pl;
+    return code;
+  }
+  pl->device = desc->device;
+  if (pl->device >= 0) {
+    int rc = setup_device(pl, desc->max_batch);
+    if (rc != HDD_OK) {
+      std::lock_guard<std::mutex> lk(g_mu);
+      g_create_err = pl->err;
+      hdd_plan_destroy(pl);
+      return rc;
+    }
+  }
+  *out = pl;
+  return HDD_OK;
+}
+
+int hdd_plan_destroy(HddPlan* pl) {
+  if (!pl) return HDD_OK;
+  if (pl->device >= 0) {
+    cudaSetDevice(pl->device);
+    if (pl->stream) cudaStreamSynchronize(pl->stream);
+    for (void* p : pl->allocs) cudaFree(p);
+    if (pl->d_Z) cudaFree(pl->d_Z);
+    if (pl->d_S) cudaFree(pl->d_S);
+    if (pl->d_ll) cudaFree(pl->d_ll);
+    if (pl->stream) cudaStreamDestroy(pl->stream);
+  }
+  delete pl;
+  return HDD_OK;
+}
+
+static int run_sub_batch(HddPlan* pl, const double* Z, int B, double* S, double* ll, cudaStream_t st) {
+  Plan& P = pl->plan;
+  DevPlan& D = pl->dev;
+  CU(launch_kappa(D, Z, B, D.kappa, st));
+  CU(launch_leaf(D, B, st, nullptr));
+  for (int dep = int(P.upper_by_depth.size()) - 1; dep >= 0; --dep) {
+    const auto& ids = P.upper_by_depth[dep];
+    if (ids.empty()) continue;
+    CU(launch_merge_m(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->depth_smem[dep], st));
+  }
+  CU(launch_finalize(D, B, S, ll, st));
+  return HDD_OK;
+}
+
+static int check_device_error(HddPlan* pl, cudaStream_t st, int64_t b0) {
+  DevError e{};
+  CU(cudaMemcpyAsync(&e, pl->dev.err, sizeof(e), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (e.code != 0) {
+    CU(cudaMemsetAsync(pl->dev.err, 0, sizeof(DevError), st));
+    CU(cudaStreamSynchronize(st));
+    std::string msg;
+    if (e.code == HDD_ERR_NUMERICAL)
+      msg = e.node >= 0 ? "interface block at node " + std::to_string(e.node) + " is not positive definite"
+                        : "non-finite forward observation";
+    else
+      msg = "coefficient values must be positive finite reals";
+    return set_err(&pl->err, e.code, msg, int(b0 + e.sample), e.node);
+  }
+  return HDD_OK;
+}
+
+int hdd_forward_batch(HddPlan* pl, const double* Z, int64_t B, double* S, double* ll, void* stream) {
+  if (!pl) return HDD_ERR_USAGE;
+  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan cannot run a forward batch");
+  if (B < 0 || (B > 0 && !Z)) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : pl->stream;
+  const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
+  int64_t done = 0;
+  while (done < B) {
+    int b = int(std::min<int64_t>(pl->bcap, B - done));
+    int rc = run_sub_batch(pl, Z + done * nz, b, S ? S + done * no : nullptr, ll ? ll + done : nullptr, st);
+    if (rc != HDD_OK) return rc;
+    done += b;
+  }
+  return check_device_error(pl, st, 0);
+}
+
+int hdd_forward_batch_host(HddPlan* pl, const double* Zh, int64_t B, double* Sh, double* llh) {
+  if (!pl) return HDD_ERR_USAGE;
+  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan cannot run a forward batch");
+  if (B <= 0) return B == 0 ? HDD_OK : set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  CU(cudaSetDevice(pl->device));
+  const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
+  if (B > pl->io_cap) {
+    if (pl->d_Z) cudaFree(pl->d_Z);
+    if (pl->d_S) cudaFree(pl->d_S);
+    if (pl->d_ll) cudaFree(pl->d_ll);
+    CU(cudaMalloc(&pl->d_Z, size_t(B) * nz * 8));
+    CU(cudaMalloc(&pl->d_S, size_t(B) * no * 8));
+    CU(cudaMalloc(&pl->d_ll, size_t(B) * 8));
+    pl->io_cap = B;
+  }
+  cudaStream_t st = pl->stream;
+  CU(cudaMemcpyAsync(pl->d_Z, Zh, size_t(B) * nz * 8, cudaMemcpyHostToDevice, st));
+  int rc = hdd_forward_batch(pl, pl->d_Z, B, Sh ? pl->d_S : nullptr, llh ? pl->d_ll : nullptr, st);
+  if (rc != HDD_OK) return rc;
+  if (Sh) CU(cudaMemcpyAsync(Sh, pl->d_S, size_t(B) * no * 8, cudaMemcpyDeviceToHost, st));
+  if (llh) CU(cudaMemcpyAsync(llh, pl->d_ll, size_t(B) * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return HDD_OK;
+}
+
+int hdd_kappa_batch(HddPlan* pl, const double* Z, int64_t B, double* kappa, void* stream) {
+  if (!pl) return HDD_ERR_USAGE;
+  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan");
+  CU(cudaSetDevice(pl->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : pl->stream;
+  const int64_t nt = int64_t(2) * pl->plan.N * pl->plan.N;
+  for (int64_t done = 0; done < B;) {
+    int b = int(std::min<int64_t>(pl->bcap, B - done));
+    CU(launch_kappa(pl->dev, Z + done * pl->plan.n_z, b, kappa + done * nt, st));
+    done += b;
+  }
+  return check_device_error(pl, st, 0);
+}
+
+int hdd_last_error(const HddPlan* pl, HddError* out) {
+  if (!pl || !out) return HDD_ERR_USAGE;
+  *out = pl->err;
+  return HDD_OK;
+}
+
+int hdd_plan_info(const HddPlan* pl, HddPlanInfo* out) {
+  if (!pl || !out) return HDD_ERR_USAGE;
+  const Plan& P = pl->plan;
+  out->level = P.level;
+  out->n_cells = P.N;
+  out->leaf_cells = kLeafCells;
+  out->leaf_depth = P.leaf_depth;
+  out->n_upper = int(P.upper.size());
+  out->n_leaves = int(P.leaves.size());
+  out->n_obs = int(P.obs_kind.size());
+  out->leaf_cols = P.leaf_cols;
+  out->max_batch = pl->bcap;
+  out->n_kernels_per_batch = 3 + int(P.upper_by_depth.size());
+  int64_t ws = int64_t(2) * P.N * P.N;
+  for (int64_t e : P.buf_elems_per_sample) ws += e;
+  out->workspace_bytes = ws * 8 * std::max(1, pl->bcap);
+  return HDD_OK;
+}
+
+int hdd_plan_node_info(const HddPlan* pl, int32_t idx, HddNodeInfo* out) {
+  if (!pl || !out || idx < 0 || idx >= int(pl->plan.upper.size())) return HDD_ERR_USAGE;
+  const UpperNode& U = pl->plan.upper[idx];
+  out->ref_id = U.ref_id;
+  out->depth = U.depth;
+  out->i0 = U.i0; out->i1 = U.i1; out->j0 = U.j0; out->j1 = U.j1;
+  out->son[0] = U.son[0];
+  out->son[1] = U.son[1];
+  out->k = U.k; out->ng = U.ng; out->nc = U.nc;
+  out->bnd = U.bnd.data();
+  out->gamma = U.gamma.data();
+  out->gmap = U.gmap.data();
+  out->csrc = U.csrc.data();
+  out->ccoef = U.ccoef.data();
+  out->cbirth = U.cbirth.data();
+  return HDD_OK;
+}
+
+int hdd_plan_leaf_info(const HddPlan* pl, int32_t idx, HddLeafInfo* out) {
+  if (!pl || !out || idx < 0 || idx >= int(pl->plan.leaves.size())) return HDD_ERR_USAGE;
+  const Leaf& L = pl->plan.leaves[idx];
+  out->ref_id = L.ref_id;
+  out->i0 = L.i0;
+  out->j0 = L.j0;
+  out->ncols = int(L.cols.size());
+  out->has_mean = L.own_mean ? 1 : 0;
+  out->birth = L.birth.data();
+  return HDD_OK;
+}
+
+int hdd_plan_obs_info(const HddPlan* pl, int32_t idx, HddObsInfo* out) {
+  if (!pl || !out || idx < 0 || idx >= int(pl->plan.route.size())) return HDD_ERR_USAGE;
+  out->kind = pl->plan.route[idx].kind;
+  out->col = pl->plan.route[idx].col;
+  out->value = pl->plan.route[idx].value;
+  return HDD_OK;
+}
+
+int hdd_leaf_template(int32_t r, int32_t* K, int32_t* k, int32_t* ng, const int32_t** map1, const int32_t** map2) {
+  const auto& T = leaf_template();
+  if (r < 0 || r >= int(T.size())) return HDD_ERR_USAGE;
+  if (K) *K = T[r].K;
+  if (k) *k = T[r].k;
+  if (ng) *ng = T[r].ng;
+  if (map1) *map1 = T[r].map1.data();
+  if (map2) *map2 = T[r].map2.data();
+  return HDD_OK;
+}
+
+int hdd_debug_node_output(HddPlan* pl, int32_t idx, int32_t b, double* psi, double* R, double* sigma) {
+  if (!pl || pl->device < 0) return HDD_ERR_USAGE;
+  const Plan& P = pl->plan;
+  if (P.n_buffers != P.leaf_depth + 1) return set_err(&pl->err, HDD_ERR_USAGE, "plan was not created with keep_nodes");
+  if (b < 0 || b >= pl->bcap) return set_err(&pl->err, HDD_ERR_USAGE, "sample index out of range");
+  const double* base;
+  int k, ld, nc;
+  if (idx >= 0) {
+    if (idx >= int(P.upper.size())) return HDD_ERR_USAGE;
+    const UpperNode& U = P.upper[idx];
+    base = pl->dev.buf[U.buf] + U.out_off * pl->bcap + int64_t(b) * U.out_elems;
+    k = U.k; ld = U.out_ld; nc = U.nc;
+  } else {
+    int l = -1 - idx;
+    if (l >= int(P.leaves.size())) return HDD_ERR_USAGE;
+    base = pl->dev.buf[P.leaf_buf] + int64_t(l) * P.leaf_elems * pl->bcap + int64_t(b) * P.leaf_elems;
+    k = kLeafPerim; ld = P.leaf_ld; nc = int(P.leaves[l].cols.size());
+  }
+  std::vector<double> tmp(size_t(k) * ld + ld);
+  CU(cudaSetDevice(pl->device));
+  CU(cudaStreamSynchronize(pl->stream));
+  CU(cudaMemcpy(tmp.data(), base, (size_t(k) * ld + nc) * 8, cudaMemcpyDeviceToHost));
+  for (int a = 0; a < k; ++a) {
+    if (psi) for (int c = 0; c < k; ++c) psi[size_t(a) * k + c] = tmp[size_t(a) * ld + c];
+    if (R) for (int c = 0; c < nc; ++c) R[size_t(a) * nc + c] = tmp[size_t(a) * ld + k + c];
+  }
+  if (sigma) for (int c = 0; c < nc; ++c) sigma[c] = tmp[size_t(k) * ld + c];
+  return HDD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// Device-side plan tables and kernel launchers (internal header).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hdd {
+
+constexpr int kMaxBuffers = 24;
+
+// One upper (merge) node as the merge kernels see it.
+struct DevUpper {
+  int k, ng, K, nc;
+  int ldp;                 // panel leading dimension (tier M smem / tier L global)
+  int out_ld;
+  int64_t out_elems, out_off;
+  int buf;
+  int son_buf[2];
+  int son_k[2];            // son output rows (= Psi width)
+  int son_ld[2];
+  int64_t son_elems[2], son_off[2];
+  int gmap_off;            // offset into the gmap pool: [2][K]
+  int col_off;             // offset into column pools: csrc/ccoef [nc][2], cbirth [nc]
+  int64_t ref_id;
+};
+
+// One kernel leaf.
+struct DevLeaf {
+  int i0, j0;
+  int ncols;
+  int pad;
+  int64_t ref_id;
+  // per column: coefficient type (0 = load, 1 = mean, 2 = point) and birth
+  int ctype[16];
+  int birth_r[16], birth_q[16], birth_g[16];
+};
+
+struct DevError {
+  int code;                // 0 ok, else HDD_ERR_*
+  int sample;
+  long long node;          // reference node id
+};
+
+struct DevPlan {
+  int N, m, n_z, n_obs, n_leaves, leaf_cols, leaf_ld;
+  double h;
+  int64_t leaf_elems;
+  int leaf_buf;
+  int bcap;                // allocated sub-batch capacity
+  const double* sx;        // [n_z][2N]
+  const double* sy;
+  const double* coef;
+  const double* f;         // nullptr = 1
+  const DevLeaf* leaves;
+  const DevUpper* upper;
+  const int32_t* gmap;
+  const int32_t* csrc;
+  const double* ccoef;
+  const int32_t* cbirth;
+  const int32_t* route_kind;
+  const int32_t* route_col;
+  const double* route_val;
+  const double* sigma;
+  const double* y;         // nullptr = no likelihood
+  double ll_const;         // sum log(sigma sqrt(2 pi))
+  int root_buf;            // root output: buffer, sample-0 offset, per-sample stride,
+  int64_t root_off;        // and the offset of its sigma row inside a sample block
+  int64_t root_elems;
+  int64_t root_sig;
+  double* buf[kMaxBuffers];
+  double* kappa;           // [bcap][2 N^2]
+  DevError* err;
+};
+
+// launchers (hdd_kernels.cu); all return cudaError_t of the launch
+cudaError_t launch_kappa(const DevPlan& p, const double* Z, int B, double* kappa, cudaStream_t s);
+cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_out);
+cudaError_t launch_merge_m(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B,
+                           size_t smem, cudaStream_t s);
+cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cudaStream_t s);
+size_t leaf_smem_bytes(int leaf_cols);
+int upload_leaf_template();
+
+}  // namespace hdd

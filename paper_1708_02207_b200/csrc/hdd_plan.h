@@ -1,0 +1,99 @@
+// Host-side plan of the batched HDD likelihood (internal header).
+//
+// The plan is the compiled form of one reference BayesProblem: the
+// alternating-bisection tree truncated at 16x16-cell "kernel leaves", the
+// pruned (Dirichlet-free) boundary/interface index sets of every upper node,
+// the gather maps that replace the reference's scatter-add merge plan
+// (ddtree.py:40-57 bpos/opos, hdd.py:216-238), and the column plan that
+// routes the load vector and every observation functional up the tree
+// (functionals.py:146-224).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "hdd.h"
+
+namespace hdd {
+
+constexpr int kLeafCells = 16;                 // kernel-leaf subdomain (cells per side)
+constexpr int kLeafPerim = 4 * kLeafCells;     // 64 perimeter nodes
+constexpr int kLeafLevels = 8;                 // in-leaf merge levels r = 0..7
+
+enum ColKind { COL_LOAD = 0, COL_MEAN = 1, COL_OBS = 2 };
+
+struct Col {
+  int kind;      // ColKind
+  int obs;       // observation index for COL_OBS
+};
+
+struct UpperNode {
+  int64_t ref_id = -1;
+  int depth = 0, i0 = 0, i1 = 0, j0 = 0, j1 = 0;
+  int son[2] = {0, 0};          // >= 0 upper index, < 0: -1 - leaf index
+  int k = 0, ng = 0, K = 0, nc = 0;
+  bool own_mean = false;
+  std::vector<int64_t> bnd, gamma;
+  std::vector<int32_t> gmap;    // [2][K]
+  std::vector<int32_t> csrc;    // [nc][2]
+  std::vector<double> ccoef;    // [nc][2]
+  std::vector<int32_t> cbirth;  // [nc]
+  std::vector<Col> cols;
+  // output layout (per sample): rows k, leading dim ld, then nc sigmas
+  int out_ld = 0;
+  int64_t out_elems = 0;
+  int64_t out_off = 0;          // element offset of sample 0 in its depth buffer
+  int buf = 0;                  // output buffer id
+  int tier = 0;                 // 0 = smem panel, 1 = global panel
+};
+
+struct Leaf {
+  int64_t ref_id = -1;
+  int i0 = 0, j0 = 0;
+  bool own_mean = false;
+  std::vector<Col> cols;
+  std::vector<int32_t> birth;   // [ncols][3] (level r, node q, gamma pos) or -1
+};
+
+struct ObsRoute {
+  int kind;      // 0 = root column, 1 = constant
+  int col;
+  double value;
+};
+
+struct LeafLevel {                // in-leaf template level r (father shape)
+  int w, h, K, k, ng, kson;
+  std::vector<int32_t> map1, map2; // [K]
+};
+
+struct Plan {
+  int level = 0, N = 0, m = 0, n_z = 0, leaf_depth = 0;
+  double h = 0;
+  std::vector<double> sx, sy, coef, f;
+  bool f_is_one = true;
+  std::vector<int32_t> obs_kind;
+  std::vector<int64_t> obs_id;
+  std::vector<double> sigma, y;
+  bool has_y = false;
+  std::vector<UpperNode> upper;               // grouped by depth, deepest first
+  std::vector<std::vector<int>> upper_by_depth;  // depth -> indices
+  std::vector<Leaf> leaves;                   // post-order (left to right)
+  int leaf_cols = 1;                          // NCL (max columns over leaves)
+  int leaf_ld = 0;
+  int64_t leaf_elems = 0;
+  int leaf_buf = 0;
+  std::vector<ObsRoute> route;
+  int root = -1;                              // upper index of the root, or -1 (root is leaf 0)
+  int root_nc = 0;
+  int n_buffers = 2;
+  std::vector<int64_t> buf_elems_per_sample;  // per buffer
+};
+
+// Build the plan; returns empty string on success, else the ConfigError /
+// UsageError message (code in *code).
+std::string build_plan(const HddPlanDesc* desc, Plan& plan, int* code);
+
+const std::vector<LeafLevel>& leaf_template();
+int64_t postorder_id(int level, const std::vector<int>& path);
+
+}  // namespace hdd
