@@ -122,6 +122,15 @@ int hdd_plan_destroy(HddPlan* plan);
 int hdd_forward_batch(HddPlan* plan, const double* Z_dev, int64_t B,
                       double* S_dev, double* ll_dev, void* stream);
 
+/* Same as hdd_forward_batch, plus per-stage device time (CUDA events on the
+ * launching stream), accumulated over the internal sub-batches into
+ * stage_ms[n_stages]: [0] kappa, [1] leaf, [2 + i] merges of depth
+ * leaf_depth-1-i (deepest first), [n_stages-1] finalize.  n_stages must be
+ * leaf_depth + 3. Synchronizes the stream. */
+int hdd_forward_batch_timed(HddPlan* plan, const double* Z_dev, int64_t B,
+                            double* S_dev, double* ll_dev, void* stream,
+                            double* stage_ms, int32_t n_stages);
+
 /* Same call with HOST buffers: copies in, runs, copies out (pinned staging). */
 int hdd_forward_batch_host(HddPlan* plan, const double* Z_host, int64_t B,
                            double* S_host, double* ll_host);

@@ -20,6 +20,17 @@ from .geometry import Grid
 _DENSE_LIMIT = 4000
 
 
+def element_stiffness(coords, kappa: float) -> np.ndarray:
+    """3x3 P1 stiffness kappa/(2 det) G G^T of one triangle (fem.py:75-81)."""
+    c = np.asarray(coords, dtype=float)
+    x, y = c[:, 0], c[:, 1]
+    det = (x[1] - x[0]) * (y[2] - y[0]) - (x[2] - x[0]) * (y[1] - y[0])
+    if det <= 1e-14:
+        raise ValueError("triangle is degenerate or negatively oriented")
+    g = np.array([[y[(v + 1) % 3] - y[(v + 2) % 3], x[(v + 2) % 3] - x[(v + 1) % 3]] for v in range(3)])
+    return (kappa / (2.0 * det)) * (g @ g.T)
+
+
 def stiffness_and_load(grid: Grid, kappa: np.ndarray):
     kappa = np.asarray(kappa, dtype=float)
     if kappa.shape != (grid.n_triangles,):

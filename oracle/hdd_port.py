@@ -121,7 +121,9 @@ class HDDPort:
             lf += phi[1].T @ z
         return lg, lf
 
-    def forward(self, kappa: np.ndarray) -> np.ndarray:
+    def forward(self, kappa: np.ndarray, keep_psi: dict | None = None) -> np.ndarray:
+        """S(kappa); if `keep_psi` is a dict it receives {node id: (psi_g, psi_f @ f)}
+        (the reference's BuildDiagnostics(keep_psi=True), hdd.py:158, :376-391)."""
         kappa = np.asarray(kappa, dtype=float)
         N = self.grid.N
         live = {}
@@ -142,6 +144,8 @@ class HDDPort:
                 s1, s2 = nd.sons
                 psi, phi = self._eliminate(nd, live[s1], live[s2])
                 live[nd.id] = psi
+                if keep_psi is not None:
+                    keep_psi[nd.id] = (psi[0], psi[1] @ self.f[nd.omega])
                 done.append(nd)
                 for idx in self.born.get(nd.id, ()):
                     e = np.zeros(nd.gamma.size)

@@ -26,3 +26,4 @@ from .errors import ConfigError, GeometryError, NumericalError, UsageError  # no
 from .geometry import DDTree, Mesh, Rect, boundary_nodes, build_mesh, build_tree, interior_nodes  # noqa: F401
 
 __version__ = "0.1.0"
+from . import configs, parallel  # noqa: E402,F401

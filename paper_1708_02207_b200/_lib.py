@@ -71,6 +71,8 @@ EXPORTS = {
     "hdd_plan_create": (C.c_int, [C.POINTER(HddPlanDesc), C.POINTER(C.c_void_p)]),
     "hdd_plan_destroy": (C.c_int, [C.c_void_p]),
     "hdd_forward_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hdd_forward_batch_timed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          _f64p, C.c_int32]),
     "hdd_forward_batch_host": (C.c_int, [C.c_void_p, _f64p, C.c_int64, _f64p, _f64p]),
     "hdd_kappa_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "hdd_last_error": (C.c_int, [C.c_void_p, C.POINTER(HddError)]),

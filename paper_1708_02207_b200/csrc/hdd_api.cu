@@ -301,17 +301,24 @@ int hdd_plan_destroy(HddPlan* pl) {
   return HDD_OK;
 }
 
-static int run_sub_batch(HddPlan* pl, const double* Z, int B, double* S, double* ll, cudaStream_t st) {
+static int run_sub_batch(HddPlan* pl, const double* Z, int B, double* S, double* ll, cudaStream_t st,
+                         cudaEvent_t* ev = nullptr) {
   Plan& P = pl->plan;
   DevPlan& D = pl->dev;
+  int e = 0;
+  if (ev) CU(cudaEventRecord(ev[e++], st));
   CU(launch_kappa(D, Z, B, D.kappa, st));
+  if (ev) CU(cudaEventRecord(ev[e++], st));
   CU(launch_leaf(D, B, st, nullptr));
+  if (ev) CU(cudaEventRecord(ev[e++], st));
   for (int dep = int(P.upper_by_depth.size()) - 1; dep >= 0; --dep) {
     const auto& ids = P.upper_by_depth[dep];
-    if (ids.empty()) continue;
-    CU(launch_merge_m(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->depth_smem[dep], st));
+    if (!ids.empty())
+      CU(launch_merge_m(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->depth_smem[dep], st));
+    if (ev) CU(cudaEventRecord(ev[e++], st));
   }
   CU(launch_finalize(D, B, S, ll, st));
+  if (ev) CU(cudaEventRecord(ev[e++], st));
   return HDD_OK;
 }
 
@@ -348,6 +355,38 @@ int hdd_forward_batch(HddPlan* pl, const double* Z, int64_t B, double* S, double
     if (rc != HDD_OK) return rc;
     done += b;
   }
+  return check_device_error(pl, st, 0);
+}
+
+int hdd_forward_batch_timed(HddPlan* pl, const double* Z, int64_t B, double* S, double* ll, void* stream,
+                            double* stage_ms, int32_t n_stages) {
+  if (!pl) return HDD_ERR_USAGE;
+  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan cannot run a forward batch");
+  const int ns = pl->plan.leaf_depth + 3;
+  if (n_stages != ns || !stage_ms) return set_err(&pl->err, HDD_ERR_USAGE, "stage_ms must hold leaf_depth + 3 entries");
+  if (B <= 0 || !Z) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  CU(cudaSetDevice(pl->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : pl->stream;
+  std::vector<cudaEvent_t> ev(ns + 1);
+  for (auto& e : ev) CU(cudaEventCreate(&e));
+  const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
+  int64_t done = 0;
+  int rc = HDD_OK;
+  while (done < B && rc == HDD_OK) {
+    int b = int(std::min<int64_t>(pl->bcap, B - done));
+    rc = run_sub_batch(pl, Z + done * nz, b, S ? S + done * no : nullptr, ll ? ll + done : nullptr, st, ev.data());
+    if (rc == HDD_OK) {
+      CU(cudaEventSynchronize(ev[ns]));
+      for (int i = 0; i < ns; ++i) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+        stage_ms[i] += ms;
+      }
+    }
+    done += b;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (rc != HDD_OK) return rc;
   return check_device_error(pl, st, 0);
 }
 

@@ -1,0 +1,245 @@
+"""Parity of the CUDA path (through the C ABI) against the golden vectors of the
+live reference and the CPU oracle.  Tolerances: F(u) and log-likelihood
+relative 1e-10 in fp64 (BASELINE.json north star); kappa relative 1e-14;
+determinism / batch-composition invariance bitwise."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_1708_02207_b200 as hb
+import plan_emulator as pe
+from oracle import configs as ocfg, direct, fields, geometry, hdd_port
+from paper_1708_02207_b200 import _lib, configs
+from paper_1708_02207_b200.bayes import _Plan
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def test_native_library_is_loaded(torch_cuda):
+    L = _lib.lib()
+    import os
+    maps = open(f"/proc/{os.getpid()}/maps").read()
+    assert "libhdd_b200.so" in maps
+    assert L.hdd_version().startswith(b"hdd_b200")
+
+
+def test_kappa_kernel_matches_field(torch_cuda, golden):
+    torch = torch_cuda
+    for name in ["C1", "C2"]:
+        cfg = configs.CONFIGS[name]
+        prob = configs.make_problem(name)
+        plan = prob.plan()
+        Z = configs.draw_Z(cfg)[:5]
+        Zd = torch.from_numpy(Z).cuda()
+        nt = 2 * (1 << cfg.level) ** 2
+        kap = torch.empty((5, nt), dtype=torch.float64, device="cuda")
+        plan.check(plan.lib.hdd_kappa_batch(plan.handle, C.c_void_p(Zd.data_ptr()), 5, C.c_void_p(kap.data_ptr()),
+                                            None))
+        fo = fields.SineKLField(geometry.Grid(cfg.level), cfg.n_z)
+        k = kap.cpu().numpy()
+        for b in range(5):
+            assert rel(k[b], fo.kappa_values(Z[b])) <= 1e-14
+    g = golden("c1_kappa")
+    prob = configs.make_problem("C1")
+    plan = prob.plan()
+    Zd = torch.from_numpy(g["Z"]).cuda()
+    kap = torch.empty(g["kappa"].shape, dtype=torch.float64, device="cuda")
+    plan.check(plan.lib.hdd_kappa_batch(plan.handle, C.c_void_p(Zd.data_ptr()), Zd.shape[0],
+                                        C.c_void_p(kap.data_ptr()), None))
+    assert rel(kap.cpu().numpy(), g["kappa"]) <= 1e-14
+
+
+def test_c1_full_batch_matches_reference(torch_cuda, golden):
+    g = golden("cfg_C1")
+    prob = configs.make_problem("C1")
+    S = hb.forward_functionals_batch(prob, g["Z"])
+    ll = hb.log_likelihood_batch(prob, g["Z"])
+    assert S.shape == g["S"].shape
+    for b in range(S.shape[0]):
+        assert rel(S[b], g["S"][b]) <= TOL
+    assert np.max(np.abs(ll - g["ll"]) / np.abs(g["ll"])) <= TOL
+    # single-sample wrappers keep the reference signatures
+    assert abs(hb.log_likelihood(prob, g["Z"][3]) - g["ll"][3]) <= TOL * abs(g["ll"][3])
+    assert rel(hb.forward_functionals(prob, g["Z"][5]), g["S"][5]) <= TOL
+
+
+def test_c2_matches_reference(torch_cuda, golden):
+    torch = torch_cuda
+    g = golden("cfg_C2")
+    prob = configs.make_problem("C2")
+    Zd = torch.from_numpy(g["Z"]).cuda()
+    S = hb.forward_functionals_batch(prob, Zd).cpu().numpy()
+    ll = hb.log_likelihood_batch(prob, Zd).cpu().numpy()
+    for b in range(S.shape[0]):
+        assert rel(S[b], g["S"][b]) <= TOL
+    assert np.max(np.abs(ll - g["ll"]) / np.abs(g["ll"])) <= TOL
+
+
+def test_indicator_param_matches_reference(torch_cuda, golden):
+    gi = golden("c1_indicator")
+    g = golden("cfg_C1")
+    cfg = configs.CONFIGS["C1"]
+    mesh = hb.build_mesh(cfg.level)
+    tree = hb.build_tree(mesh)
+    model = hb.MeasurementModel(configs.observations(cfg), g["sigma"], g["y"])
+    prob = hb.BayesProblem(tree, hb.ParamField.build(tree, 4), np.ones(mesh.n_nodes), np.zeros(4 * mesh.n_cells),
+                           model)
+    S = hb.forward_functionals_batch(prob, gi["Z"])
+    ll = hb.log_likelihood_batch(prob, gi["Z"])
+    for b in range(S.shape[0]):
+        assert rel(S[b], gi["S"][b]) <= TOL
+    assert np.max(np.abs(ll - gi["ll"]) / np.abs(gi["ll"])) <= TOL
+
+
+def test_node_outputs_match_reference_maps(torch_cuda, golden):
+    """Leaf Schur complements (unpruned) and upper-node maps (pruned rows)
+    equal the reference's Psi^g, Psi^f f (BuildDiagnostics keep_psi)."""
+    g = golden("c1_nodes")
+    Z = golden("cfg_C1")["Z"][:2]
+    cfg = configs.CONFIGS["C1"]
+    prob = configs.make_problem("C1")
+    prob._plan = _Plan(prob, 0, 4, keep_nodes=True)
+    hb.forward_functionals_batch(prob, Z)
+    plan = prob.plan()
+    L = plan.lib
+    info = plan.info()
+    grid = geometry.Grid(cfg.level)
+    for si in range(2):
+        for li in range(info.n_leaves):
+            lf = _lib.HddLeafInfo()
+            L.hdd_plan_leaf_info(plan.handle, li, C.byref(lf))
+            psi = np.empty((64, 64))
+            R = np.empty((64, lf.ncols))
+            sg = np.empty(lf.ncols)
+            plan.check(L.hdd_debug_node_output(plan.handle, -1 - li, si, psi.ctypes.data_as(_lib._f64p),
+                                               R.ctypes.data_as(_lib._f64p), sg.ctypes.data_as(_lib._f64p)))
+            ref = g[f"s{si}_n{lf.ref_id}_g"]
+            assert rel(psi, ref) <= 1e-13
+            assert rel(R[:, 0], g[f"s{si}_n{lf.ref_id}_f"]) <= 1e-13
+        for u in range(info.n_upper):
+            nd = _lib.HddNodeInfo()
+            L.hdd_plan_node_info(plan.handle, u, C.byref(nd))
+            if nd.k == 0:
+                continue
+            psi = np.empty((nd.k, nd.k))
+            R = np.empty((nd.k, nd.nc))
+            sg = np.empty(nd.nc)
+            plan.check(L.hdd_debug_node_output(plan.handle, u, si, psi.ctypes.data_as(_lib._f64p),
+                                               R.ctypes.data_as(_lib._f64p), sg.ctypes.data_as(_lib._f64p)))
+            ref = g[f"s{si}_n{nd.ref_id}_g"]
+            bnd = g[f"n{nd.ref_id}_bnd"]
+            keep = ~grid.on_domain_boundary(bnd)
+            assert rel(psi, ref[np.ix_(keep, keep)]) <= 1e-12
+            assert rel(R[:, 0], g[f"s{si}_n{nd.ref_id}_f"][keep]) <= 1e-12
+
+
+def test_means_and_boundary_points_match_direct(torch_cuda):
+    """Nested subdomain means and points on interfaces / the boundary (level 6)."""
+    level, n_z = 6, 8
+    obs = tuple(("mean", nid) for nid, _ in geometry.nodes_at_depth(level, 2)) + \
+        tuple(("mean", nid) for nid, _ in geometry.nodes_at_depth(level, 4))[:6] + \
+        (("mean", geometry.nodes_at_depth(level, 0)[0][0]), ("point", 65 * 32 + 32), ("point", 65 * 16 + 40),
+         ("point", 0), ("point", 65 * 5 + 64))
+    mesh = hb.build_mesh(level)
+    tree = hb.build_tree(mesh)
+    prob = hb.BayesProblem(tree, hb.SineKLField(tree, n_z), np.ones(mesh.n_nodes), np.zeros(4 * mesh.n_cells),
+                           hb.MeasurementModel(obs, np.full(len(obs), 0.01)))
+    grid = geometry.Grid(level)
+    fo = fields.SineKLField(grid, n_z)
+    Z = np.random.default_rng(11).standard_normal((6, n_z))
+    S = hb.forward_functionals_batch(prob, Z)
+    for b in range(6):
+        u = direct.solve(grid, fo.kappa_values(Z[b]))
+        assert rel(S[b], ocfg.observe(grid, u, obs)) <= TOL
+
+
+def test_nodal_rhs_matches_direct(torch_cuda):
+    level, n_z = 5, 4
+    obs = configs.observations(configs.CONFIGS["C1"])
+    mesh = hb.build_mesh(level)
+    tree = hb.build_tree(mesh)
+    f = np.random.default_rng(3).uniform(-1.0, 2.0, mesh.n_nodes)
+    prob = hb.BayesProblem(tree, hb.SineKLField(tree, n_z), f, np.zeros(4 * mesh.n_cells),
+                           hb.MeasurementModel(obs, np.full(len(obs), 0.01)))
+    grid = geometry.Grid(level)
+    fo = fields.SineKLField(grid, n_z)
+    Z = np.random.default_rng(4).standard_normal((3, n_z))
+    S = hb.forward_functionals_batch(prob, Z)
+    for b in range(3):
+        u = direct.solve(grid, fo.kappa_values(Z[b]), f=f)
+        assert rel(S[b], ocfg.observe(grid, u, obs)) <= TOL
+
+
+def test_determinism_and_batch_invariance(torch_cuda):
+    """Bitwise identical per-sample results for any batch split (the GPU
+    analogue of the reference's thread invariance)."""
+    cfg = configs.CONFIGS["C2"]
+    Z = configs.draw_Z(cfg)[:40]
+    p_full = configs.make_problem("C2")
+    p_small = configs.make_problem("C2", max_batch=7)
+    a = hb.log_likelihood_batch(p_full, Z)
+    b = hb.log_likelihood_batch(p_full, Z)
+    c = hb.log_likelihood_batch(p_small, Z)
+    d = np.concatenate([hb.log_likelihood_batch(p_full, Z[i:i + 1]) for i in range(0, 40, 9)])
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    assert np.array_equal(a[::9], d)
+
+
+def test_full_c2_batch_properties(torch_cuda):
+    """Full BASELINE C2 batch: finite ll, spot rows against the direct solve."""
+    torch = torch_cuda
+    cfg = configs.CONFIGS["C2"]
+    prob = configs.make_problem("C2")
+    Z = configs.draw_Z(cfg)
+    Zd = torch.from_numpy(Z).cuda()
+    S = hb.forward_functionals_batch(prob, Zd).cpu().numpy()
+    ll = hb.log_likelihood_batch(prob, Zd).cpu().numpy()
+    assert np.all(np.isfinite(ll)) and S.shape == (1024, 64)
+    grid = geometry.Grid(cfg.level)
+    fo = fields.SineKLField(grid, cfg.n_z)
+    obs = configs.observations(cfg)
+    for b in (0, 511, 1023):
+        u = direct.solve(grid, fo.kappa_values(Z[b]))
+        assert rel(S[b], ocfg.observe(grid, u, obs)) <= TOL
+    y, sigma = configs.observed_data(cfg)
+    ll_host = np.array([hb.gaussian_log_likelihood(y, S[b], sigma) for b in range(1024)])
+    assert np.max(np.abs(ll - ll_host) / np.abs(ll_host)) <= 1e-12
+
+
+def test_invalid_parameters_raise(torch_cuda):
+    prob = configs.make_problem("C1")
+    Z = configs.draw_Z(configs.CONFIGS["C1"])[:4].copy()
+    Z[2, 1] = np.inf
+    with pytest.raises(hb.ConfigError):
+        hb.log_likelihood_batch(prob, Z)
+    Z[2, 1] = np.nan
+    with pytest.raises(hb.ConfigError):
+        hb.forward_functionals_batch(prob, Z)
+    # the plan stays usable after an error
+    ok = hb.log_likelihood_batch(prob, configs.draw_Z(configs.CONFIGS["C1"])[:4])
+    assert np.all(np.isfinite(ok))
+
+
+def test_host_and_device_entry_points_agree(torch_cuda):
+    torch = torch_cuda
+    cfg = configs.CONFIGS["C1"]
+    prob = configs.make_problem("C1")
+    Z = configs.draw_Z(cfg)
+    a = hb.log_likelihood_batch(prob, Z)
+    b = hb.log_likelihood_batch(prob, torch.from_numpy(Z).cuda()).cpu().numpy()
+    assert np.array_equal(a, b)
