@@ -29,7 +29,7 @@
  *
  * Conventions: plain pointers and sizes only.  Device pointers are CUDA
  * device addresses on the plan's device; `stream` is a cudaStream_t passed as
- * void*.  All functions return HDD_OK (0) or a negative status; no call
+ * void* (NULL = the legacy default stream, like a CUDA launch without one).  All functions return HDD_OK (0) or a negative status; no call
  * falls back to the CPU.
  */
 #ifndef HDD_B200_H

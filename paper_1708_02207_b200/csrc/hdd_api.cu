@@ -123,6 +123,19 @@ static int setup_device(HddPlan* pl, int max_batch) {
     }
   }
   if ((rc = upload(pl, dl, &D.leaves))) return rc;
+  {
+    std::vector<int32_t> order;
+    for (int cls = 0; cls < 3; ++cls) {
+      D.leaf_class_start[cls] = int(order.size());
+      const int lo = cls == 0 ? 0 : (cls == 1 ? 3 : 5), hi = cls == 0 ? 2 : (cls == 1 ? 4 : 8);
+      for (size_t l = 0; l < P.leaves.size(); ++l) {
+        int nc = int(P.leaves[l].cols.size());
+        if (nc >= lo && nc <= hi) order.push_back(int32_t(l));
+      }
+      D.leaf_class_count[cls] = int(order.size()) - D.leaf_class_start[cls];
+    }
+    if ((rc = upload(pl, order, &D.leaf_order))) return rc;
+  }
   // upper nodes
   std::vector<int32_t> gmap, csrc, cbirth;
   std::vector<double> ccoef;
@@ -246,7 +259,11 @@ static int setup_device(HddPlan* pl, int max_batch) {
     D.root_sig = int64_t(kLeafPerim) * P.leaf_ld;
   }
   pl->leaf_smem = leaf_smem_bytes(P.leaf_cols <= 2 ? 2 : (P.leaf_cols <= 4 ? 4 : 8));
-  pl->n_launches = 3 + int(P.upper_by_depth.size());
+  {
+    int ncls = 0;
+    for (int c = 0; c < 3; ++c) ncls += D.leaf_class_count[c] > 0;
+    pl->n_launches = 2 + ncls + int(P.upper_by_depth.size());
+  }
   return HDD_OK;
 }
 
@@ -346,7 +363,7 @@ int hdd_forward_batch(HddPlan* pl, const double* Z, int64_t B, double* S, double
   if (B < 0 || (B > 0 && !Z)) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
   if (B == 0) return HDD_OK;
   CU(cudaSetDevice(pl->device));
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : pl->stream;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
   const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
   int64_t done = 0;
   while (done < B) {
@@ -366,7 +383,7 @@ int hdd_forward_batch_timed(HddPlan* pl, const double* Z, int64_t B, double* S, 
   if (n_stages != ns || !stage_ms) return set_err(&pl->err, HDD_ERR_USAGE, "stage_ms must hold leaf_depth + 3 entries");
   if (B <= 0 || !Z) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
   CU(cudaSetDevice(pl->device));
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : pl->stream;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
   std::vector<cudaEvent_t> ev(ns + 1);
   for (auto& e : ev) CU(cudaEventCreate(&e));
   const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
@@ -419,7 +436,7 @@ int hdd_kappa_batch(HddPlan* pl, const double* Z, int64_t B, double* kappa, void
   if (!pl) return HDD_ERR_USAGE;
   if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan");
   CU(cudaSetDevice(pl->device));
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : pl->stream;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
   const int64_t nt = int64_t(2) * pl->plan.N * pl->plan.N;
   for (int64_t done = 0; done < B;) {
     int b = int(std::min<int64_t>(pl->bcap, B - done));
@@ -447,7 +464,7 @@ int hdd_plan_info(const HddPlan* pl, HddPlanInfo* out) {
   out->n_obs = int(P.obs_kind.size());
   out->leaf_cols = P.leaf_cols;
   out->max_batch = pl->bcap;
-  out->n_kernels_per_batch = 3 + int(P.upper_by_depth.size());
+  out->n_kernels_per_batch = pl->device >= 0 ? pl->n_launches : 3 + int(P.upper_by_depth.size());
   int64_t ws = int64_t(2) * P.N * P.N;
   for (int64_t e : P.buf_elems_per_sample) ws += e;
   out->workspace_bytes = ws * 8 * std::max(1, pl->bcap);

@@ -51,6 +51,8 @@ struct DevPlan {
   const double* coef;
   const double* f;         // nullptr = 1
   const DevLeaf* leaves;
+  const int32_t* leaf_order;   // leaf indices grouped by column class (<=2, <=4, <=8)
+  int leaf_class_start[3], leaf_class_count[3];
   const DevUpper* upper;
   const int32_t* gmap;
   const int32_t* csrc;

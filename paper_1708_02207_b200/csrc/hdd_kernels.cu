@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdio>
 
 #include "hdd.h"
@@ -127,26 +128,6 @@ int upload_leaf_template() {
   return 0;
 }
 
-// level-r buffer size (doubles) for nf nodes
-__host__ __device__ constexpr int leaf_level_doubles(int nf, int K, int ncl) {
-  return nf * (K * (K + ncl) + ncl);
-}
-
-static int leaf_buf_doubles(int ncl) {
-  const auto& T = leaf_template();
-  int mx = 0;
-  for (int r = 0; r < kLeafLevels; ++r) {
-    int v = leaf_level_doubles(1 << r, T[r].K, ncl);
-    mx = v > mx ? v : mx;
-  }
-  return (mx + 15) / 16 * 16;
-}
-
-size_t leaf_smem_bytes(int ncl) {
-  // kappa 512 + f 17x17 (pad 296) + maps (2x256 int16 = 128 doubles) + 2 buffers
-  return sizeof(double) * (512 + 296 + 128 + 2 * size_t(leaf_buf_doubles(ncl)));
-}
-
 // subtree-relative post-order id of in-leaf node (r, q) (for error reports)
 __device__ long long inleaf_ref_id(long long leaf_id, int r, int q) {
   const int H = 8;   // in-leaf height
@@ -158,221 +139,328 @@ __device__ long long inleaf_ref_id(long long leaf_id, int r, int q) {
   return leaf_id - size_leaf + 1 + id;
 }
 
-template <int NCL>
-__global__ void __launch_bounds__(256) leaf_kernel(DevPlan p, int bufd) {
+__device__ __forceinline__ int tri(int a) { return (a * (a + 1)) >> 1; }
+
+// lower-packed symmetric read
+__device__ __forceinline__ double sym(const double* P, int i, int j) {
+  return i >= j ? P[tri(i) + j] : P[tri(j) + i];
+}
+
+// Leaf smem layout (doubles): kappa[512] | f[296] | ints (maps 2x256 int16 + col info) [160] |
+// bufA[bufd] | bufB[bufd] | panel[pand]
+static void leaf_sizes(int ncl, int* bufd, int* pand) {
+  const auto& T = leaf_template();
+  int mb = 0, mp = 0;
+  for (int r = 0; r < kLeafLevels; ++r) {
+    int nf = 1 << r, k = T[r].k, K = T[r].K, ng = T[r].ng;
+    if (r >= 1) mb = std::max(mb, nf * (k * (k + 1) / 2 + k * ncl + ncl));
+    mp = std::max(mp, nf * ng * (K + ncl));
+  }
+  *bufd = (mb + 1) & ~1;
+  *pand = (mp + 1) & ~1;
+}
+
+size_t leaf_smem_bytes(int ncl) {
+  int bufd, pand;
+  leaf_sizes(ncl, &bufd, &pand);
+  return sizeof(double) * (512 + 296 + 160 + 2 * size_t(bufd) + pand);
+}
+
+// One CTA per (16x16-cell leaf, sample).  Level 6 (2x2-cell blocks) is built
+// per thread in registers straight from the cells' kappa; levels 5..0 run
+// level-synchronously in shared memory with lower-packed Schur complements:
+// gather the interface panel, warp Cholesky, column forward substitution,
+// then the streamed Schur update that gathers A11 from the sons on the fly.
+template <int NC>
+__global__ void __launch_bounds__(256, 2) leaf2_kernel(DevPlan p, const int* __restrict__ order, int bufd, int pand) {
   extern __shared__ __align__(16) double sm[];
-  const int leaf = blockIdx.x, s = blockIdx.y;
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
+  const int leaf = order[blockIdx.x], s = blockIdx.y;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = 8, NT = 256;
   const DevLeaf& L = p.leaves[leaf];
-  double* kap = sm;                  // [16 x][32 (y, type)]
-  double* fl = kap + 512;            // [17 y][17 x]
-  int16_t* mp = reinterpret_cast<int16_t*>(fl + 296);   // [2][256]
-  double* bufA = fl + 296 + 128;
+  double* kap = sm;
+  double* fl = kap + 512;
+  int16_t* mp = reinterpret_cast<int16_t*>(fl + 296);          // [2][256]
+  int* cinfo = reinterpret_cast<int*>(fl + 296 + 128);           // ctype, br, bq, bg, ncols
+  double* bufA = fl + 296 + 160;
   double* bufB = bufA + bufd;
+  double* pan = bufB + bufd;
   const int N = p.N;
   {
     const double* kb = p.kappa + int64_t(s) * 2 * N * N;
-    for (int t = tid; t < 512; t += nthr) {
+    for (int t = tid; t < 512; t += NT) {
       int x = t >> 5, r = t & 31;
       kap[t] = kb[2 * (int64_t(L.i0 + x) * N + L.j0) + r];
     }
-    for (int t = tid; t < 289; t += nthr) {
-      int y = t / 17, x = t % 17;
-      fl[t] = p.f ? p.f[int64_t(L.j0 + y) * p.m + L.i0 + x] : 1.0;
+    if (p.f)
+      for (int t = tid; t < 289; t += NT) {
+        int y = t / 17, x = t - y * 17;
+        fl[t] = p.f[int64_t(L.j0 + y) * p.m + L.i0 + x];
+      }
+    for (int t = tid; t < 512; t += NT) mp[t] = c_map[t >> 8][t & 255];
+    if (tid < NC) {
+      cinfo[tid] = tid < L.ncols ? L.ctype[tid] : 3;     // 3 = unused column
+      cinfo[NC + tid] = L.birth_r[tid];
+      cinfo[2 * NC + tid] = L.birth_q[tid];
+      cinfo[3 * NC + tid] = L.birth_g[tid];
     }
-    for (int t = tid; t < 512; t += nthr) mp[t] = c_map[t >> 8][t & 255];
   }
-  // column coefficients and cell initial values
-  const int ncols = L.ncols;
+  __syncthreads();
+  const int* ctype = cinfo;
+  const int* br = cinfo + NC;
+  const int* bq = cinfo + 2 * NC;
+  const int* bg = cinfo + 3 * NC;
   const double h2_6 = p.h * p.h / 6.0;
+
+  // ---------------- level 6: 2x2-cell blocks in registers ----------------
+  {
+    constexpr int k6 = 8;
+    const int S6 = tri(k6) + k6 * NC + NC;
+    for (int q = tid; q < 64; q += NT) {
+      const int o = c_orig[63 + q];
+      const int x0 = o & 255, y0 = o >> 8;
+      double A[45];
+      double rl[9], rm[9];
+#pragma unroll
+      for (int i = 0; i < 45; ++i) A[i] = 0.0;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) { rl[i] = 0.0; rm[i] = 0.0; }
+#pragma unroll
+      for (int cy = 0; cy < 2; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < 2; ++cx) {
+          const double k0 = kap[(x0 + cx) * 32 + 2 * (y0 + cy)];
+          const double k1 = kap[(x0 + cx) * 32 + 2 * (y0 + cy) + 1];
+          const int a = cy * 3 + cx, b = a + 1, c = a + 3, d = a + 4;
+          // P1 (a,b,d) and P2 (a,d,c) of fem.py:126-145
+          A[tri(a) + a] += fma(k0, 0.5, k1 * 0.5);
+          A[tri(b) + b] += k0;
+          A[tri(c) + c] += k1;
+          A[tri(d) + d] += fma(k0, 0.5, k1 * 0.5);
+          A[tri(b) + a] += -0.5 * k0;
+          A[tri(d) + b] += -0.5 * k0;
+          A[tri(c) + a] += -0.5 * k1;
+          A[tri(d) + c] += -0.5 * k1;
+          const int nx = x0 + cx, ny = y0 + cy;
+          const double w2 = h2_6 + h2_6;
+          if (p.f) {
+            rl[a] += w2 * fl[ny * 17 + nx];
+            rl[b] += h2_6 * fl[ny * 17 + nx + 1];
+            rl[c] += h2_6 * fl[(ny + 1) * 17 + nx];
+            rl[d] += w2 * fl[(ny + 1) * 17 + nx + 1];
+          } else {
+            rl[a] += w2; rl[b] += h2_6; rl[c] += h2_6; rl[d] += w2;
+          }
+          rm[a] += 0.25 * (1.0 / 3.0); rm[b] += 0.25 * (1.0 / 6.0);
+          rm[c] += 0.25 * (1.0 / 6.0); rm[d] += 0.25 * (1.0 / 3.0);
+        }
+      // eliminate the centre node 4
+      const double dpiv = A[tri(4) + 4];
+      if (!(dpiv > 0.0)) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, 6, q));
+      const double inv = 1.0 / sqrt(dpiv);
+      double xv[9];
+#pragma unroll
+      for (int n = 0; n < 9; ++n) xv[n] = (n == 4) ? 0.0 : (n < 4 ? A[tri(4) + n] : A[tri(n) + 4]) * inv;
+      double* out = bufA + q * S6;
+      constexpr int P8[8] = {0, 1, 2, 3, 5, 6, 7, 8};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j <= i; ++j) out[tri(i) + j] = fma(-xv[P8[i]], xv[P8[j]], A[tri(P8[i]) + P8[j]]);
+      double v[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int ct = ctype[c];
+        double rc4 = ct == 0 ? rl[4] : (ct == 1 ? rm[4] : 0.0);
+        if (br[c] == 6 && bq[c] == q) rc4 += 1.0;
+        v[c] = rc4 * inv;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const int ct = ctype[c];
+          const double rb = ct == 0 ? rl[P8[i]] : (ct == 1 ? rm[P8[i]] : 0.0);
+          out[tri(k6) + i * NC + c] = fma(-xv[P8[i]], v[c], rb);
+        }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) out[tri(k6) + k6 * NC + c] = c == 0 ? 0.0 : v[0] * v[c];
+    }
+  }
   __syncthreads();
 
-  double* in = nullptr;
-  double* out = bufA;
-  int in_ld = 0, in_K = 0, in_stride = 0;
-  for (int r = kLeafLevels - 1; r >= 0; --r) {
-    const int K = c_tmpl.K[r], k = c_tmpl.k[r], ng = c_tmpl.ng[r];
+  // ---------------- levels 5..0 in shared memory ----------------
+  double* in = bufA;
+  double* out = bufB;
+  for (int r = 5; r >= 0; --r) {
+    const int K = c_tmpl.K[r], k = c_tmpl.k[r], ng = c_tmpl.ng[r], ks = c_tmpl.kson[r];
     const int nf = 1 << r;
-    const int ldo = K + NCL;
-    const int stride = K * ldo + NCL;
+    const int Sin = tri(ks) + ks * NC + NC;
+    const int Sout = tri(k) + k * NC + NC;
+    const int W = K + NC;                // panel width
     const int16_t* m1 = mp + c_tmpl.moff[r];
     const int16_t* m2 = mp + 256 + c_tmpl.moff[r];
-    // ---- gather (assemble_father) ----
-    const int per = K * ldo;
-    for (int idx = tid; idx < nf * per; idx += nthr) {
-      const int q = idx / per;
-      const int rem = idx - q * per;
-      const int a = rem / ldo;
-      const int b = rem - a * ldo;
-      double v = 0.0;
-#pragma unroll
-      for (int sn = 0; sn < 2; ++sn) {
-        const int pa = sn ? m2[a] : m1[a];
-        if (pa < 0) continue;
-        const int qs = 2 * q + sn;
-        if (r == kLeafLevels - 1) {
-          // son = single cell: psi = k0 P1 + k1 P2, loads, mean pattern
-          const int o = c_orig[(1 << (r + 1)) - 1 + qs];
-          const int cx = o & 255, cy = o >> 8;
-          if (b < K) {
-            const int pb = sn ? m2[b] : m1[b];
-            if (pb < 0) continue;
-            const double k0 = kap[cx * 32 + 2 * cy], k1 = kap[cx * 32 + 2 * cy + 1];
-            // P1 on (0,1,3), P2 on (0,3,2) with entries +-1/2, 1 (fem.py:126-145)
-            const int lo = pa < pb ? pa : pb, hi = pa < pb ? pb : pa;
-            double p1 = 0.0, p2 = 0.0;
-            if (lo == hi) {
-              p1 = (lo == 1) ? 1.0 : ((lo == 0 || lo == 3) ? 0.5 : 0.0);
-              p2 = (lo == 2) ? 1.0 : ((lo == 0 || lo == 3) ? 0.5 : 0.0);
-            } else {
-              p1 = ((lo == 0 && hi == 1) || (lo == 1 && hi == 3)) ? -0.5 : 0.0;
-              p2 = ((lo == 0 && hi == 2) || (lo == 2 && hi == 3)) ? -0.5 : 0.0;
-            }
-            v += fma(k0, p1, k1 * p2);
-          } else {
-            const int c = b - K;
-            if (c >= ncols) continue;
-            const int ct = L.ctype[c];
-            if (ct == 0) {
-              const double w = (pa == 0 || pa == 3) ? (h2_6 + h2_6) : h2_6;
-              const int nx = cx + (pa & 1), ny = cy + (pa >> 1);
-              v += w * fl[ny * 17 + nx];
-            } else if (ct == 1) {
-              const double w = (pa == 0 || pa == 3) ? (1.0 / 3.0) : (1.0 / 6.0);
-              v += 0.5 * w;
-            }
-          }
+    const int gsz = nf >= NW ? 1 : NW / nf;     // warps per node
+    const int qstep = NW / gsz;
+    const int sub = warp % gsz;
+    // ---- panel gather [A21 | A22 | R_gamma] and sigma~ ----
+    for (int q = warp / gsz; q < nf; q += qstep) {
+      const double* s1 = in + (2 * q) * Sin;
+      const double* s2 = in + (2 * q + 1) * Sin;
+      double* P = pan + q * ng * W;
+      for (int t = sub * 32 + lane; t < ng * W; t += gsz * 32) {
+        const int g = t / W, j = t - g * W;
+        const int a = k + g;
+        const int pa1 = m1[a], pa2 = m2[a];
+        double v = 0.0;
+        if (j < K) {
+          const int pb1 = m1[j], pb2 = m2[j];
+          if (pa1 >= 0 && pb1 >= 0) v += sym(s1, pa1, pb1);
+          if (pa2 >= 0 && pb2 >= 0) v += sym(s2, pa2, pb2);
         } else {
-          const double* sd = in + qs * in_stride;
-          if (b < K) {
-            const int pb = sn ? m2[b] : m1[b];
-            if (pb < 0) continue;
-            v += sd[pa * in_ld + pb];
-          } else {
-            const int c = b - K;
-            if (c >= ncols) continue;
-            const double cf = L.ctype[c] == 1 ? 0.5 : 1.0;
-            v += cf * sd[pa * in_ld + in_K + c];
-          }
+          const int c = j - K;
+          const double cf = ctype[c] == 1 ? 0.5 : 1.0;
+          if (pa1 >= 0) v += cf * s1[tri(ks) + pa1 * NC + c];
+          if (pa2 >= 0) v += cf * s2[tri(ks) + pa2 * NC + c];
+          if (br[c] == r && bq[c] == q && bg[c] == g) v += 1.0;
         }
+        P[t] = v;
       }
-      if (b >= K) {
-        const int c = b - K;
-        if (c < ncols && L.birth_r[c] == r && L.birth_q[c] == q && a == k + L.birth_g[c]) v += 1.0;
+      if (sub == 0 && lane < NC && r > 0) {
+        const int c = lane;
+        const double cf = ctype[c] == 1 ? 0.5 : 1.0;
+        out[q * Sout + tri(k) + k * NC + c] = cf * s1[tri(ks) + ks * NC + c] + cf * s2[tri(ks) + ks * NC + c];
       }
-      out[q * stride + rem] = v;
-    }
-    for (int idx = tid; idx < nf * NCL; idx += nthr) {
-      const int q = idx / NCL, c = idx - q * NCL;
-      double v = 0.0;
-      if (r < kLeafLevels - 1 && c < ncols) {
-        const double cf = L.ctype[c] == 1 ? 0.5 : 1.0;
-        v = cf * in[(2 * q) * in_stride + in_K * in_ld + c] + cf * in[(2 * q + 1) * in_stride + in_K * in_ld + c];
-      }
-      out[q * stride + K * ldo + c] = v;
     }
     __syncthreads();
-    if (ng > 0) {
-      // ---- Cholesky of the interface block, one warp per node ----
-      for (int q = warp; q < nf; q += nwarp) {
-        double* A = out + q * stride;
-        for (int c = 0; c < ng; ++c) {
-          const double d = A[(k + c) * ldo + k + c];
-          if (!(d > 0.0) && lane == 0)
-            record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, r, q));
-          const double l = sqrt(d), inv = 1.0 / l;
-          __syncwarp();
-          for (int rr = c + 1 + lane; rr < ng; rr += 32) A[(k + rr) * ldo + k + c] *= inv;
-          if (lane == 0) A[(k + c) * ldo + k + c] = l;
-          __syncwarp();
-          const int rem = ng - c - 1;
-          for (int t = lane; t < rem * rem; t += 32) {
-            const int i1 = c + 1 + t / rem, i2 = c + 1 + t % rem;
-            if (i2 <= i1) A[(k + i1) * ldo + k + i2] -= A[(k + i1) * ldo + k + c] * A[(k + i2) * ldo + k + c];
-          }
-          __syncwarp();
+    // ---- Cholesky of A22 (warp per node) ----
+    for (int q = warp; q < nf; q += NW) {
+      double* P = pan + q * ng * W;
+      for (int c = 0; c < ng; ++c) {
+        const double d = P[c * W + k + c];
+        if (!(d > 0.0) && lane == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, r, q));
+        const double l = sqrt(d), inv = 1.0 / l;
+        __syncwarp();
+        for (int rr = c + 1 + lane; rr < ng; rr += 32) P[rr * W + k + c] *= inv;
+        if (lane == 0) P[c * W + k + c] = l;
+        __syncwarp();
+        const int rem = ng - c - 1;
+        for (int t = lane; t < rem * rem; t += 32) {
+          const int i1 = c + 1 + t / rem, i2 = c + 1 + t % rem;
+          if (i2 <= i1) P[i1 * W + k + i2] -= P[i1 * W + k + c] * P[i2 * W + k + c];
         }
+        __syncwarp();
       }
-      __syncthreads();
-      // ---- forward substitution X = L^-1 [A21 | R_gamma], in place ----
-      const int wcols = k + NCL;
-      for (int idx = tid; idx < nf * wcols; idx += nthr) {
-        const int q = idx / wcols, bb = idx - q * wcols;
-        const int b = bb < k ? bb : K + (bb - k);
-        double* A = out + q * stride;
-        for (int g = 0; g < ng; ++g) {
-          double x = A[(k + g) * ldo + b];
-          for (int hh = 0; hh < g; ++hh) x -= A[(k + g) * ldo + k + hh] * A[(k + hh) * ldo + b];
-          A[(k + g) * ldo + b] = x / A[(k + g) * ldo + k + g];
-        }
-      }
-      __syncthreads();
-      // ---- Schur update [A11 | R_B] -= X^T X ; sigma += v^T X ----
-      const int per2 = k * wcols;
-      for (int idx = tid; idx < nf * (per2 + NCL); idx += nthr) {
-        const int q = idx / (per2 + NCL);
-        const int rem = idx - q * (per2 + NCL);
-        double* A = out + q * stride;
-        if (rem < per2) {
-          const int a = rem / wcols, bb = rem - a * wcols;
-          const int b = bb < k ? bb : K + (bb - k);
-          double acc = A[a * ldo + b];
-          for (int g = 0; g < ng; ++g) acc = fma(-A[(k + g) * ldo + a], A[(k + g) * ldo + b], acc);
-          A[a * ldo + b] = acc;
-        } else {
-          const int c = rem - per2;
-          if (c >= 1) {
-            double acc = A[K * ldo + c];
-            for (int g = 0; g < ng; ++g) acc = fma(A[(k + g) * ldo + K], A[(k + g) * ldo + K + c], acc);
-            A[K * ldo + c] = acc;
-          }
-        }
-      }
-      __syncthreads();
     }
+    __syncthreads();
+    // ---- forward substitution over [A21 | R_gamma] columns ----
+    {
+      const int wc = k + NC;
+      for (int q = warp / gsz; q < nf; q += qstep) {
+        double* P = pan + q * ng * W;
+        for (int t = sub * 32 + lane; t < wc; t += gsz * 32) {
+          const int j = t < k ? t : K + (t - k);
+          for (int g = 0; g < ng; ++g) {
+            double x = P[g * W + j];
+            for (int hh = 0; hh < g; ++hh) x = fma(-P[g * W + k + hh], P[hh * W + j], x);
+            P[g * W + j] = x / P[g * W + k + g];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- streamed Schur update: out = A~ - X^T [X | V]; sigma += V0 . V ----
+    const int E = tri(k) + k * NC;
+    for (int q = warp / gsz; q < nf; q += qstep) {
+      const double* s1 = in + (2 * q) * Sin;
+      const double* s2 = in + (2 * q + 1) * Sin;
+      const double* P = pan + q * ng * W;
+      double* o = out + q * Sout;
+      double* gdst = nullptr;
+      if (r == 0)
+        gdst = p.buf[p.leaf_buf] + int64_t(leaf) * p.leaf_elems * p.bcap + int64_t(s) * p.leaf_elems;
+      for (int t = sub * 32 + lane; t < E; t += gsz * 32) {
+        int a, b, c = -1;
+        if (t < tri(k)) {
+          a = int((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+          if (tri(a + 1) <= t) ++a;
+          if (tri(a) > t) --a;
+          b = t - tri(a);
+        } else {
+          a = (t - tri(k)) / NC;
+          c = t - tri(k) - a * NC;
+          b = K + c;
+        }
+        const int pa1 = m1[a], pa2 = m2[a];
+        double v = 0.0;
+        if (c < 0) {
+          const int pb1 = m1[b], pb2 = m2[b];
+          if (pa1 >= 0 && pb1 >= 0) v += sym(s1, pa1, pb1);
+          if (pa2 >= 0 && pb2 >= 0) v += sym(s2, pa2, pb2);
+        } else {
+          const double cf = ctype[c] == 1 ? 0.5 : 1.0;
+          if (pa1 >= 0) v += cf * s1[tri(ks) + pa1 * NC + c];
+          if (pa2 >= 0) v += cf * s2[tri(ks) + pa2 * NC + c];
+        }
+        for (int g = 0; g < ng; ++g) v = fma(-P[g * W + a], P[g * W + b], v);
+        if (r > 0) {
+          o[t] = v;
+        } else {
+          const int ld = p.leaf_ld;
+          if (c < 0) {
+            gdst[a * ld + b] = v;
+            gdst[b * ld + a] = v;
+          } else if (c < p.leaf_cols) {
+            gdst[a * ld + kLeafPerim + c] = v;
+          }
+        }
+      }
+      if (sub == 0 && lane < NC) {
+        const int c = lane;
+        double sg;
+        if (r > 0) sg = o[tri(k) + k * NC + c];
+        else {
+          const double cf = ctype[c] == 1 ? 0.5 : 1.0;
+          sg = cf * s1[tri(ks) + ks * NC + c] + cf * s2[tri(ks) + ks * NC + c];
+        }
+        if (c >= 1)
+          for (int g = 0; g < ng; ++g) sg = fma(P[g * W + K], P[g * W + K + c], sg);
+        if (r > 0) o[tri(k) + k * NC + c] = sg;
+        else if (c < p.leaf_cols) gdst[kLeafPerim * p.leaf_ld + c] = sg;
+      }
+    }
+    __syncthreads();
+    double* tmp = in;
     in = out;
-    in_ld = ldo;
-    in_K = K;
-    in_stride = stride;
-    out = (out == bufA) ? bufB : bufA;
+    out = tmp;
   }
-  // ---- write the leaf output: Psi [64][64], R [64][ncl], sigma ----
-  const int ld = p.leaf_ld;
-  double* dst = p.buf[p.leaf_buf] + int64_t(leaf) * p.leaf_elems * p.bcap + int64_t(s) * p.leaf_elems;
-  const int lc = p.leaf_cols;
-  for (int idx = tid; idx < kLeafPerim * ld; idx += nthr) {
-    const int a = idx / ld, b = idx - a * ld;
-    dst[idx] = b < kLeafPerim ? in[a * in_ld + b] : in[a * in_ld + in_K + (b - kLeafPerim)];
-  }
-  for (int c = tid; c < lc; c += nthr) dst[kLeafPerim * ld + c] = in[in_K * in_ld + c];
 }
 
 cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_out) {
-  const int ncl = p.leaf_cols <= 2 ? 2 : (p.leaf_cols <= 4 ? 4 : 8);
-  size_t smem = leaf_smem_bytes(ncl);
-  if (smem_out) *smem_out = smem;
-  dim3 grid(p.n_leaves, B);
-  int bufd = leaf_buf_doubles(ncl);
-  cudaError_t e;
-  switch (ncl) {
-    case 2:
-      e = cudaFuncSetAttribute(leaf_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      if (e != cudaSuccess) return e;
-      leaf_kernel<2><<<grid, 256, smem, s>>>(p, bufd);
-      break;
-    case 4:
-      e = cudaFuncSetAttribute(leaf_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      if (e != cudaSuccess) return e;
-      leaf_kernel<4><<<grid, 256, smem, s>>>(p, bufd);
-      break;
-    default:
-      e = cudaFuncSetAttribute(leaf_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      if (e != cudaSuccess) return e;
-      leaf_kernel<8><<<grid, 256, smem, s>>>(p, bufd);
-      break;
+  for (int cls = 0; cls < 3; ++cls) {
+    const int cnt = p.leaf_class_count[cls];
+    if (cnt == 0) continue;
+    const int ncl = cls == 0 ? 2 : (cls == 1 ? 4 : 8);
+    int bufd, pand;
+    leaf_sizes(ncl, &bufd, &pand);
+    size_t smem = leaf_smem_bytes(ncl);
+    if (smem_out) *smem_out = smem;
+    dim3 grid(cnt, B);
+    const int* ord = p.leaf_order + p.leaf_class_start[cls];
+    cudaError_t e;
+#define HDD_LAUNCH_LEAF(NCV)                                                                              \
+  e = cudaFuncSetAttribute(leaf2_kernel<NCV>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));   \
+  if (e != cudaSuccess) return e;                                                                         \
+  leaf2_kernel<NCV><<<grid, 256, smem, s>>>(p, ord, bufd, pand);
+    if (ncl == 2) { HDD_LAUNCH_LEAF(2) }
+    else if (ncl == 4) { HDD_LAUNCH_LEAF(4) }
+    else { HDD_LAUNCH_LEAF(8) }
+#undef HDD_LAUNCH_LEAF
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
   }
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 // ---------------------------------------------------------------------------

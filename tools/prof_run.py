@@ -1,0 +1,30 @@
+"""Minimal driver for ncu captures: one warm forward + one profiled forward.
+usage: python tools/prof_run.py CONFIG BATCH"""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import ctypes as C  # noqa: E402
+
+import torch  # noqa: E402
+
+from paper_1708_02207_b200 import _lib, configs  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "C2"
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+cfg = configs.CONFIGS[name]
+prob = configs.make_problem(name)
+plan = prob.plan()
+info = plan.info()
+Z = torch.from_numpy(configs.draw_Z(cfg, batch=max(B, cfg.batch))[:B].copy()).cuda()
+ll = torch.empty(B, dtype=torch.float64, device="cuda")
+ns = info.leaf_depth + 3
+for it in range(2):
+    st = np.zeros(ns)
+    plan.check(plan.lib.hdd_forward_batch_timed(plan.handle, C.c_void_p(Z.data_ptr()), B, None,
+                                                C.c_void_p(ll.data_ptr()), None, st.ctypes.data_as(_lib._f64p), ns))
+torch.cuda.synchronize()
+names = ["kappa", "leaf"] + [f"merge_d{d}" for d in range(info.leaf_depth - 1, -1, -1)] + ["finalize"]
+print(name, B, {n: round(float(v), 3) for n, v in zip(names, st)}, "total", round(float(st.sum()), 3))
