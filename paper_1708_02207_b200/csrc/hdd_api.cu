@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -26,6 +27,9 @@ struct HddPlan {
   DevUpper* d_upper = nullptr;
   std::vector<DevUpper> h_upper;
   std::vector<size_t> depth_smem;      // merge smem per depth
+  std::vector<int> depth_tier;         // 0 = shared-memory panel, 1 = global panel
+  std::vector<int64_t> depth_ws;       // tier-L panel doubles per (node, sample)
+  double* ws = nullptr;                // tier-L workspace
   size_t leaf_smem = 0;
   HddError err{};
   // host-API staging
@@ -141,12 +145,25 @@ static int setup_device(HddPlan* pl, int max_batch) {
   std::vector<double> ccoef;
   pl->h_upper.resize(P.upper.size());
   pl->depth_smem.assign(P.upper_by_depth.size(), 0);
+  pl->depth_tier.assign(P.upper_by_depth.size(), 0);
+  pl->depth_ws.assign(P.upper_by_depth.size(), 0);
+  const char* force_l = std::getenv("HDD_FORCE_TIER_L");   // test hook: every depth on the global panel
+  for (size_t u = 0; u < P.upper.size(); ++u) {
+    const UpperNode& U = P.upper[u];
+    if (merge_smem_bytes(U, panel_ld(U)) > 200 * 1024 || (force_l && force_l[0] == '1'))
+      pl->depth_tier[U.depth] = 1;
+  }
   for (size_t u = 0; u < P.upper.size(); ++u) {
     const UpperNode& U = P.upper[u];
     DevUpper& d = pl->h_upper[u];
     std::memset(&d, 0, sizeof(d));
     d.k = U.k; d.ng = U.ng; d.K = U.K; d.nc = U.nc;
     d.ldp = panel_ld(U);
+    if (pl->depth_tier[U.depth]) {
+      const int ngp = (U.ng + 31) / 32 * 32;
+      d.ldp = (U.k + ngp + U.nc + 3) / 4 * 4;
+      pl->depth_ws[U.depth] = std::max<int64_t>(pl->depth_ws[U.depth], int64_t(ngp) * d.ldp);
+    }
     d.out_ld = U.out_ld;
     d.out_elems = U.out_elems;
     d.out_off = U.out_off;
@@ -176,12 +193,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
     csrc.insert(csrc.end(), U.csrc.begin(), U.csrc.end());
     ccoef.insert(ccoef.end(), U.ccoef.begin(), U.ccoef.end());
     cbirth.insert(cbirth.end(), U.cbirth.begin(), U.cbirth.end());
-    size_t sm = merge_smem_bytes(U, d.ldp);
-    if (sm > 227 * 1024)
-      return set_err(&pl->err, HDD_ERR_CONFIG,
-                     "interface panel of node " + std::to_string(U.ref_id) + " (" + std::to_string(U.ng) + "x" +
-                         std::to_string(U.K + U.nc) + ") exceeds shared memory; the global-panel merge tier is "
-                         "not built in this version");
+    size_t sm = pl->depth_tier[U.depth] ? merge_l_smem_bytes() : merge_smem_bytes(U, d.ldp);
     pl->depth_smem[U.depth] = std::max(pl->depth_smem[U.depth], sm);
   }
   if ((rc = upload(pl, gmap, &D.gmap))) return rc;
@@ -213,6 +225,10 @@ static int setup_device(HddPlan* pl, int max_batch) {
   // buffers: size the sub-batch
   int64_t per_sample = int64_t(2) * P.N * P.N;
   for (int64_t e : P.buf_elems_per_sample) per_sample += e;
+  int64_t ws_per_sample = 0;
+  for (size_t d = 0; d < P.upper_by_depth.size(); ++d)
+    ws_per_sample = std::max<int64_t>(ws_per_sample, pl->depth_ws[d] * int64_t(P.upper_by_depth[d].size()));
+  per_sample += ws_per_sample;
   int64_t bytes_per_sample = per_sample * 8;
   int bcap = max_batch;
   if (bcap <= 0) {
@@ -235,6 +251,15 @@ static int setup_device(HddPlan* pl, int max_batch) {
     }
     pl->allocs.push_back(p);
     D.buf[b] = static_cast<double*>(p);
+  }
+  if (ws_per_sample > 0) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, size_t(ws_per_sample) * bcap * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(&pl->err, HDD_ERR_NOMEM, "device allocation of the merge workspace failed");
+    }
+    pl->allocs.push_back(p);
+    pl->ws = static_cast<double*>(p);
   }
   {
     void* p = nullptr;
@@ -330,8 +355,12 @@ static int run_sub_batch(HddPlan* pl, const double* Z, int B, double* S, double*
   if (ev) CU(cudaEventRecord(ev[e++], st));
   for (int dep = int(P.upper_by_depth.size()) - 1; dep >= 0; --dep) {
     const auto& ids = P.upper_by_depth[dep];
-    if (!ids.empty())
-      CU(launch_merge_m(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->depth_smem[dep], st));
+    if (!ids.empty()) {
+      if (pl->depth_tier[dep])
+        CU(launch_merge_l(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->ws, pl->depth_ws[dep], st));
+      else
+        CU(launch_merge_m(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->depth_smem[dep], st));
+    }
     if (ev) CU(cudaEventRecord(ev[e++], st));
   }
   CU(launch_finalize(D, B, S, ll, st));

@@ -78,6 +78,9 @@ cudaError_t launch_kappa(const DevPlan& p, const double* Z, int B, double* kappa
 cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_out);
 cudaError_t launch_merge_m(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B,
                            size_t smem, cudaStream_t s);
+cudaError_t launch_merge_l(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
+                           int64_t ws_node_stride, cudaStream_t s);
+size_t merge_l_smem_bytes();
 cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cudaStream_t s);
 size_t leaf_smem_bytes(int leaf_cols);
 int upload_leaf_template();

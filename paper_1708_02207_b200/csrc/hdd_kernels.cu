@@ -86,6 +86,22 @@ cudaError_t launch_kappa(const DevPlan& p, const double* Z, int B, double* kappa
 // ---------------------------------------------------------------------------
 // K2: leaf condensation
 // ---------------------------------------------------------------------------
+// compile-time in-leaf level shapes (checked against leaf_template() at upload)
+struct LeafLevelShape {
+  int K, k, ng, ks;
+};
+__host__ __device__ constexpr LeafLevelShape leaf_shape(int r) {
+  return r == 0 ? LeafLevelShape{79, 64, 15, 48}
+       : r == 1 ? LeafLevelShape{55, 48, 7, 32}
+       : r == 2 ? LeafLevelShape{39, 32, 7, 24}
+       : r == 3 ? LeafLevelShape{27, 24, 3, 16}
+       : r == 4 ? LeafLevelShape{19, 16, 3, 12}
+       : r == 5 ? LeafLevelShape{13, 12, 1, 8}
+       : r == 6 ? LeafLevelShape{9, 8, 1, 6}
+                : LeafLevelShape{6, 6, 0, 4};
+}
+__host__ __device__ constexpr int ctri(int a) { return (a * (a + 1)) / 2; }
+
 struct LeafTmplDev {
   int K[8], k[8], ng[8], kson[8], moff[8];
 };
@@ -99,6 +115,8 @@ int upload_leaf_template() {
   int16_t maps[2][256] = {};
   int off = 0;
   for (int r = 0; r < kLeafLevels; ++r) {
+    const LeafLevelShape sh = leaf_shape(r);
+    if (sh.K != T[r].K || sh.k != T[r].k || sh.ng != T[r].ng || sh.ks != T[r].kson) return -2;
     t.K[r] = T[r].K;
     t.k[r] = T[r].k;
     t.ng[r] = T[r].ng;
@@ -154,7 +172,7 @@ static void leaf_sizes(int ncl, int* bufd, int* pand) {
   for (int r = 0; r < kLeafLevels; ++r) {
     int nf = 1 << r, k = T[r].k, K = T[r].K, ng = T[r].ng;
     if (r >= 1) mb = std::max(mb, nf * (k * (k + 1) / 2 + k * ncl + ncl));
-    mp = std::max(mp, nf * ng * (K + ncl));
+    mp = std::max(mp, nf * ng * ((K + ncl) + (k + ncl) + ng));
   }
   *bufd = (mb + 1) & ~1;
   *pand = (mp + 1) & ~1;
@@ -164,6 +182,220 @@ size_t leaf_smem_bytes(int ncl) {
   int bufd, pand;
   leaf_sizes(ncl, &bufd, &pand);
   return sizeof(double) * (512 + 296 + 160 + 2 * size_t(bufd) + pand);
+}
+
+// Panel region layout per level: P [nf][ng][W] | X [nf][ng][k+NC] | Linv [nf][ng][ng]
+template <int R, int NC>
+__host__ __device__ constexpr int leaf_panel_doubles() {
+  constexpr LeafLevelShape S = leaf_shape(R);
+  return (1 << R) * S.ng * ((S.K + NC) + (S.k + NC) + S.ng);
+}
+
+// One in-leaf level: sons (level R+1, packed) in `in`, outputs (level R) to `out`
+// (or straight to the global leaf output at R = 0).
+template <int R, int NC>
+__device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __restrict__ in, double* __restrict__ out,
+                                           double* __restrict__ pan, const int16_t* __restrict__ mp,
+                                           const int* __restrict__ cinfo, int leaf, int s, long long leaf_ref) {
+  constexpr LeafLevelShape S = leaf_shape(R);
+  constexpr int K = S.K, k = S.k, ng = S.ng, ks = S.ks;
+  constexpr int nf = 1 << R;
+  constexpr int Sin = ctri(ks) + ks * NC + NC;
+  constexpr int Sout = ctri(k) + k * NC + NC;
+  constexpr int W = K + NC;
+  constexpr int WX = k + NC;
+  constexpr int NW = 8, NT = 256;
+  constexpr int gsz = nf >= NW ? 1 : NW / nf;
+  constexpr int qstep = NW / gsz;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sub = warp % gsz;
+  const int* ctype = cinfo;
+  const int* br = cinfo + NC;
+  const int* bq = cinfo + 2 * NC;
+  const int* bg = cinfo + 3 * NC;
+  const int16_t* m1 = mp + c_tmpl.moff[R];
+  const int16_t* m2 = mp + 256 + c_tmpl.moff[R];
+  double* Pp = pan;
+  double* Xp = pan + nf * ng * W;
+  double* Lp = Xp + nf * ng * WX;
+
+  // ---- A: gather the interface panel [A21 | A22 | R_gamma] and sigma~ ----
+  for (int q = warp / gsz; q < nf; q += qstep) {
+    const double* s1 = in + (2 * q) * Sin;
+    const double* s2 = in + (2 * q + 1) * Sin;
+    double* P = Pp + q * ng * W;
+    for (int t = sub * 32 + lane; t < ng * W; t += gsz * 32) {
+      const int g = t / W, j = t - g * W;
+      const int a = k + g;
+      const int pa1 = m1[a], pa2 = m2[a];
+      double v = 0.0;
+      if (j < K) {
+        const int pb1 = m1[j], pb2 = m2[j];
+        if (pa1 >= 0 && pb1 >= 0) v += sym(s1, pa1, pb1);
+        if (pa2 >= 0 && pb2 >= 0) v += sym(s2, pa2, pb2);
+      } else {
+        const int c = j - K;
+        const double cf = ctype[c] == 1 ? 0.5 : 1.0;
+        if (pa1 >= 0) v += cf * s1[ctri(ks) + pa1 * NC + c];
+        if (pa2 >= 0) v += cf * s2[ctri(ks) + pa2 * NC + c];
+        if (br[c] == R && bq[c] == q && bg[c] == g) v += 1.0;
+      }
+      P[t] = v;
+    }
+  }
+  __syncthreads();
+  // ---- B: Cholesky of A22 and its inverse Linv ----
+  if constexpr (ng <= 3) {
+    for (int q = tid; q < nf; q += NT) {
+      const double* P = Pp + q * ng * W;
+      double l[ng][ng], li[ng][ng];
+#pragma unroll
+      for (int c = 0; c < ng; ++c) {
+#pragma unroll
+        for (int r2 = c; r2 < ng; ++r2) {
+          double v = P[r2 * W + k + c];
+#pragma unroll
+          for (int h = 0; h < c; ++h) v = fma(-l[r2][h], l[c][h], v);
+          if (r2 == c) {
+            if (!(v > 0.0)) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(leaf_ref, R, q));
+            l[c][c] = sqrt(v);
+          } else {
+            l[r2][c] = v / l[c][c];
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < ng; ++c)
+#pragma unroll
+        for (int r2 = 0; r2 < ng; ++r2) {
+          if (r2 < c) { li[r2][c] = 0.0; continue; }
+          double v = r2 == c ? 1.0 : 0.0;
+#pragma unroll
+          for (int h = c; h < r2; ++h) v = fma(-l[r2][h], li[h][c], v);
+          li[r2][c] = v / l[r2][r2];
+        }
+      double* Li = Lp + q * ng * ng;
+#pragma unroll
+      for (int a = 0; a < ng; ++a)
+#pragma unroll
+        for (int b = 0; b < ng; ++b) Li[a * ng + b] = li[a][b];
+    }
+  } else {
+    for (int q = warp; q < nf; q += NW) {
+      double* P = Pp + q * ng * W;
+      for (int c = 0; c < ng; ++c) {
+        const double d = P[c * W + k + c];
+        if (!(d > 0.0) && lane == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(leaf_ref, R, q));
+        const double l = sqrt(d), inv = 1.0 / l;
+        __syncwarp();
+        if (lane > c && lane < ng) P[lane * W + k + c] *= inv;
+        if (lane == 0) P[c * W + k + c] = l;
+        __syncwarp();
+        constexpr int rem_max = ng;
+        (void)rem_max;
+        const int rem = ng - c - 1;
+        for (int t = lane; t < rem * rem; t += 32) {
+          const int i1 = c + 1 + t / rem, i2 = c + 1 + t % rem;
+          if (i2 <= i1) P[i1 * W + k + i2] = fma(-P[i1 * W + k + c], P[i2 * W + k + c], P[i1 * W + k + i2]);
+        }
+        __syncwarp();
+      }
+      // Linv column `lane`
+      double* Li = Lp + q * ng * ng;
+      if (lane < ng) {
+        const int c = lane;
+        double x[ng];
+#pragma unroll
+        for (int r2 = 0; r2 < ng; ++r2) {
+          if (r2 < c) { x[r2] = 0.0; continue; }
+          double v = r2 == c ? 1.0 : 0.0;
+#pragma unroll
+          for (int h = 0; h < r2; ++h)
+            if (h >= c) v = fma(-P[r2 * W + k + h], x[h], v);
+          x[r2] = v / P[r2 * W + k + r2];
+        }
+#pragma unroll
+        for (int r2 = 0; r2 < ng; ++r2) Li[r2 * ng + c] = x[r2];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- C: X = Linv [A21 | R_gamma]  (all threads, no serial chains) ----
+  for (int q = warp / gsz; q < nf; q += qstep) {
+    const double* P = Pp + q * ng * W;
+    const double* Li = Lp + q * ng * ng;
+    double* X = Xp + q * ng * WX;
+    for (int t = sub * 32 + lane; t < ng * WX; t += gsz * 32) {
+      const int g = t / WX, jj = t - g * WX;
+      const int j = jj < k ? jj : K + (jj - k);
+      double v = 0.0;
+#pragma unroll
+      for (int h = 0; h < ng; ++h)
+        if (h <= g) v = fma(Li[g * ng + h], P[h * W + j], v);
+      X[t] = v;
+    }
+  }
+  __syncthreads();
+  // ---- D: streamed Schur update out = A~ - X^T [X | V]; sigma += V0 . V ----
+  constexpr int E = ctri(k) + k * NC;
+  for (int q = warp / gsz; q < nf; q += qstep) {
+    const double* s1 = in + (2 * q) * Sin;
+    const double* s2 = in + (2 * q + 1) * Sin;
+    const double* X = Xp + q * ng * WX;
+    double* o = out + q * Sout;
+    double* gdst = nullptr;
+    if constexpr (R == 0)
+      gdst = p.buf[p.leaf_buf] + int64_t(leaf) * p.leaf_elems * p.bcap + int64_t(s) * p.leaf_elems;
+    for (int t = sub * 32 + lane; t < E; t += gsz * 32) {
+      int a, b, c = -1;
+      if (t < ctri(k)) {
+        a = int((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+        if (ctri(a + 1) <= t) ++a;
+        if (ctri(a) > t) --a;
+        b = t - ctri(a);
+      } else {
+        a = (t - ctri(k)) / NC;
+        c = t - ctri(k) - a * NC;
+        b = k + c;
+      }
+      const int pa1 = m1[a], pa2 = m2[a];
+      double v = 0.0;
+      if (c < 0) {
+        // perimeter maps are monotone, so b <= a implies m(b) <= m(a)
+        const int pb1 = m1[b], pb2 = m2[b];
+        if (pa1 >= 0 && pb1 >= 0) v += s1[ctri(pa1) + pb1];
+        if (pa2 >= 0 && pb2 >= 0) v += s2[ctri(pa2) + pb2];
+      } else {
+        const double cf = ctype[c] == 1 ? 0.5 : 1.0;
+        if (pa1 >= 0) v += cf * s1[ctri(ks) + pa1 * NC + c];
+        if (pa2 >= 0) v += cf * s2[ctri(ks) + pa2 * NC + c];
+      }
+#pragma unroll
+      for (int g = 0; g < ng; ++g) v = fma(-X[g * WX + a], X[g * WX + b], v);
+      if constexpr (R > 0) {
+        o[t] = v;
+      } else {
+        const int ld = p.leaf_ld;
+        if (c < 0) {
+          gdst[a * ld + b] = v;
+          gdst[b * ld + a] = v;
+        } else if (c < p.leaf_cols) {
+          gdst[a * ld + kLeafPerim + c] = v;
+        }
+      }
+    }
+    if (sub == 0 && lane < NC) {
+      const int c = lane;
+      const double cf = ctype[c] == 1 ? 0.5 : 1.0;
+      double sg = cf * s1[ctri(ks) + ks * NC + c] + cf * s2[ctri(ks) + ks * NC + c];
+      if (c >= 1)
+#pragma unroll
+        for (int g = 0; g < ng; ++g) sg = fma(X[g * WX + k], X[g * WX + k + c], sg);
+      if constexpr (R > 0) o[ctri(k) + k * NC + c] = sg;
+      else if (c < p.leaf_cols) gdst[kLeafPerim * p.leaf_ld + c] = sg;
+    }
+  }
+  __syncthreads();
 }
 
 // One CTA per (16x16-cell leaf, sample).  Level 6 (2x2-cell blocks) is built
@@ -291,150 +523,12 @@ __global__ void __launch_bounds__(256, 2) leaf2_kernel(DevPlan p, const int* __r
   __syncthreads();
 
   // ---------------- levels 5..0 in shared memory ----------------
-  double* in = bufA;
-  double* out = bufB;
-  for (int r = 5; r >= 0; --r) {
-    const int K = c_tmpl.K[r], k = c_tmpl.k[r], ng = c_tmpl.ng[r], ks = c_tmpl.kson[r];
-    const int nf = 1 << r;
-    const int Sin = tri(ks) + ks * NC + NC;
-    const int Sout = tri(k) + k * NC + NC;
-    const int W = K + NC;                // panel width
-    const int16_t* m1 = mp + c_tmpl.moff[r];
-    const int16_t* m2 = mp + 256 + c_tmpl.moff[r];
-    const int gsz = nf >= NW ? 1 : NW / nf;     // warps per node
-    const int qstep = NW / gsz;
-    const int sub = warp % gsz;
-    // ---- panel gather [A21 | A22 | R_gamma] and sigma~ ----
-    for (int q = warp / gsz; q < nf; q += qstep) {
-      const double* s1 = in + (2 * q) * Sin;
-      const double* s2 = in + (2 * q + 1) * Sin;
-      double* P = pan + q * ng * W;
-      for (int t = sub * 32 + lane; t < ng * W; t += gsz * 32) {
-        const int g = t / W, j = t - g * W;
-        const int a = k + g;
-        const int pa1 = m1[a], pa2 = m2[a];
-        double v = 0.0;
-        if (j < K) {
-          const int pb1 = m1[j], pb2 = m2[j];
-          if (pa1 >= 0 && pb1 >= 0) v += sym(s1, pa1, pb1);
-          if (pa2 >= 0 && pb2 >= 0) v += sym(s2, pa2, pb2);
-        } else {
-          const int c = j - K;
-          const double cf = ctype[c] == 1 ? 0.5 : 1.0;
-          if (pa1 >= 0) v += cf * s1[tri(ks) + pa1 * NC + c];
-          if (pa2 >= 0) v += cf * s2[tri(ks) + pa2 * NC + c];
-          if (br[c] == r && bq[c] == q && bg[c] == g) v += 1.0;
-        }
-        P[t] = v;
-      }
-      if (sub == 0 && lane < NC && r > 0) {
-        const int c = lane;
-        const double cf = ctype[c] == 1 ? 0.5 : 1.0;
-        out[q * Sout + tri(k) + k * NC + c] = cf * s1[tri(ks) + ks * NC + c] + cf * s2[tri(ks) + ks * NC + c];
-      }
-    }
-    __syncthreads();
-    // ---- Cholesky of A22 (warp per node) ----
-    for (int q = warp; q < nf; q += NW) {
-      double* P = pan + q * ng * W;
-      for (int c = 0; c < ng; ++c) {
-        const double d = P[c * W + k + c];
-        if (!(d > 0.0) && lane == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, r, q));
-        const double l = sqrt(d), inv = 1.0 / l;
-        __syncwarp();
-        for (int rr = c + 1 + lane; rr < ng; rr += 32) P[rr * W + k + c] *= inv;
-        if (lane == 0) P[c * W + k + c] = l;
-        __syncwarp();
-        const int rem = ng - c - 1;
-        for (int t = lane; t < rem * rem; t += 32) {
-          const int i1 = c + 1 + t / rem, i2 = c + 1 + t % rem;
-          if (i2 <= i1) P[i1 * W + k + i2] -= P[i1 * W + k + c] * P[i2 * W + k + c];
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    // ---- forward substitution over [A21 | R_gamma] columns ----
-    {
-      const int wc = k + NC;
-      for (int q = warp / gsz; q < nf; q += qstep) {
-        double* P = pan + q * ng * W;
-        for (int t = sub * 32 + lane; t < wc; t += gsz * 32) {
-          const int j = t < k ? t : K + (t - k);
-          for (int g = 0; g < ng; ++g) {
-            double x = P[g * W + j];
-            for (int hh = 0; hh < g; ++hh) x = fma(-P[g * W + k + hh], P[hh * W + j], x);
-            P[g * W + j] = x / P[g * W + k + g];
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // ---- streamed Schur update: out = A~ - X^T [X | V]; sigma += V0 . V ----
-    const int E = tri(k) + k * NC;
-    for (int q = warp / gsz; q < nf; q += qstep) {
-      const double* s1 = in + (2 * q) * Sin;
-      const double* s2 = in + (2 * q + 1) * Sin;
-      const double* P = pan + q * ng * W;
-      double* o = out + q * Sout;
-      double* gdst = nullptr;
-      if (r == 0)
-        gdst = p.buf[p.leaf_buf] + int64_t(leaf) * p.leaf_elems * p.bcap + int64_t(s) * p.leaf_elems;
-      for (int t = sub * 32 + lane; t < E; t += gsz * 32) {
-        int a, b, c = -1;
-        if (t < tri(k)) {
-          a = int((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-          if (tri(a + 1) <= t) ++a;
-          if (tri(a) > t) --a;
-          b = t - tri(a);
-        } else {
-          a = (t - tri(k)) / NC;
-          c = t - tri(k) - a * NC;
-          b = K + c;
-        }
-        const int pa1 = m1[a], pa2 = m2[a];
-        double v = 0.0;
-        if (c < 0) {
-          const int pb1 = m1[b], pb2 = m2[b];
-          if (pa1 >= 0 && pb1 >= 0) v += sym(s1, pa1, pb1);
-          if (pa2 >= 0 && pb2 >= 0) v += sym(s2, pa2, pb2);
-        } else {
-          const double cf = ctype[c] == 1 ? 0.5 : 1.0;
-          if (pa1 >= 0) v += cf * s1[tri(ks) + pa1 * NC + c];
-          if (pa2 >= 0) v += cf * s2[tri(ks) + pa2 * NC + c];
-        }
-        for (int g = 0; g < ng; ++g) v = fma(-P[g * W + a], P[g * W + b], v);
-        if (r > 0) {
-          o[t] = v;
-        } else {
-          const int ld = p.leaf_ld;
-          if (c < 0) {
-            gdst[a * ld + b] = v;
-            gdst[b * ld + a] = v;
-          } else if (c < p.leaf_cols) {
-            gdst[a * ld + kLeafPerim + c] = v;
-          }
-        }
-      }
-      if (sub == 0 && lane < NC) {
-        const int c = lane;
-        double sg;
-        if (r > 0) sg = o[tri(k) + k * NC + c];
-        else {
-          const double cf = ctype[c] == 1 ? 0.5 : 1.0;
-          sg = cf * s1[tri(ks) + ks * NC + c] + cf * s2[tri(ks) + ks * NC + c];
-        }
-        if (c >= 1)
-          for (int g = 0; g < ng; ++g) sg = fma(P[g * W + K], P[g * W + K + c], sg);
-        if (r > 0) o[tri(k) + k * NC + c] = sg;
-        else if (c < p.leaf_cols) gdst[kLeafPerim * p.leaf_ld + c] = sg;
-      }
-    }
-    __syncthreads();
-    double* tmp = in;
-    in = out;
-    out = tmp;
-  }
+  leaf_level<5, NC>(p, bufA, bufB, pan, mp, cinfo, leaf, s, L.ref_id);
+  leaf_level<4, NC>(p, bufB, bufA, pan, mp, cinfo, leaf, s, L.ref_id);
+  leaf_level<3, NC>(p, bufA, bufB, pan, mp, cinfo, leaf, s, L.ref_id);
+  leaf_level<2, NC>(p, bufB, bufA, pan, mp, cinfo, leaf, s, L.ref_id);
+  leaf_level<1, NC>(p, bufA, bufB, pan, mp, cinfo, leaf, s, L.ref_id);
+  leaf_level<0, NC>(p, bufB, bufA, pan, mp, cinfo, leaf, s, L.ref_id);
 }
 
 cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_out) {
@@ -609,6 +703,270 @@ cudaError_t launch_merge_m(const DevPlan& p, const DevUpper* nodes_dev, int n_no
   if (e != cudaSuccess) return e;
   dim3 grid(B, n_nodes);
   merge_m_kernel<<<grid, 256, smem, s>>>(p, nodes_dev);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K3L: upper merge with the interface panel in global memory (tier L)
+// ---------------------------------------------------------------------------
+// Panel columns: [0,k) A21 | [k, k+ngp) A22 (padded to 32 rows, identity in the
+// padding) | [k+ngp, W) R_gamma.  Rows: the ngp interface rows.
+// TN warp GEMM: acc[i][j] += sum_kk A[kk][m0+..] * B[kk][n0+..] over kd (multiple of 4),
+// A and B in shared memory, k-major.
+template <int FM, int FN>
+__device__ __forceinline__ void warp_gemm_tn(double (&acc)[FM][FN][2], const double* __restrict__ A, int lda, int m0,
+                                             const double* __restrict__ B, int ldb, int n0, int kd) {
+  const int lane = threadIdx.x & 31;
+  const int gq = lane & 3, gr = lane >> 2;
+  for (int k0 = 0; k0 < kd; k0 += 4) {
+    double av[FM], bv[FN];
+#pragma unroll
+    for (int i = 0; i < FM; ++i) av[i] = A[(k0 + gq) * lda + m0 + 8 * i + gr];
+#pragma unroll
+    for (int j = 0; j < FN; ++j) bv[j] = B[(k0 + gq) * ldb + n0 + 8 * j + gr];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) dmma884(acc[i][j], av[i], bv[j]);
+  }
+}
+
+constexpr int kLB = 32;     // elimination block (rows)
+constexpr int kLC = 64;     // column chunk
+constexpr int kLds = 72;    // smem leading dim for 64-wide tiles (= 8 mod 16)
+constexpr int kLdd = 40;    // smem leading dim for 32-wide tiles (= 8 mod 16)
+
+size_t merge_l_smem_bytes() {
+  // D/LiT [32][kLdd] x2, Xb chunk [32][kLds], Lt [32][kLdd], E: two [32][kLds]
+  return sizeof(double) * (2 * 32 * kLdd + 32 * kLds + 32 * kLdd + 2 * 32 * kLds) + 1024;
+}
+
+__global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
+                                                          double* __restrict__ ws, int64_t ws_node_stride) {
+  extern __shared__ __align__(16) double sm[];
+  const int node_idx = blockIdx.y;
+  const DevUpper& U = nodes[node_idx];
+  const int s = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = U.k, ng = U.ng, K = U.K, nc = U.nc, ldp = U.ldp;
+  const int ngp = (ng + kLB - 1) / kLB * kLB;
+  const int Kp = k + ngp;
+  const int W = Kp + nc;
+  double* P = ws + int64_t(node_idx) * ws_node_stride * p.bcap + int64_t(s) * ws_node_stride;
+  const int32_t* gm = p.gmap + U.gmap_off;
+  const int32_t* csrc = p.csrc + 2 * U.col_off;
+  const double* ccoef = p.ccoef + 2 * U.col_off;
+  const int32_t* cbirth = p.cbirth + U.col_off;
+  const double* son[2];
+#pragma unroll
+  for (int sn = 0; sn < 2; ++sn)
+    son[sn] = p.buf[U.son_buf[sn]] + U.son_off[sn] * p.bcap + int64_t(s) * U.son_elems[sn];
+  const int sk0 = U.son_k[0], sk1 = U.son_k[1], sl0 = U.son_ld[0], sl1 = U.son_ld[1];
+  double* D = sm;                         // [32][kLdd]
+  double* LiT = D + 32 * kLdd;            // [32][kLdd]
+  double* Xc = LiT + 32 * kLdd;           // [32][kLds]
+  double* Lt = Xc + 32 * kLds;            // [32][kLdd]
+  double* Ea = Lt + 32 * kLdd;            // [32][kLds]
+  double* Eb = Ea + 32 * kLds;            // [32][kLds]
+  __shared__ int s_bad;
+  // ---- G: gather the panel into global workspace ----
+  for (int g = warp; g < ngp; g += 8) {
+    double* row = P + int64_t(g) * ldp;
+    if (g >= ng) {
+      for (int b = lane; b < W; b += 32) row[b] = (b == k + g) ? 1.0 : 0.0;
+      continue;
+    }
+    const int a = k + g;
+    const int pa0 = gm[a], pa1 = gm[K + a];
+    const double* r0 = pa0 >= 0 ? son[0] + size_t(pa0) * sl0 : nullptr;
+    const double* r1 = pa1 >= 0 ? son[1] + size_t(pa1) * sl1 : nullptr;
+    for (int b = lane; b < W; b += 32) {
+      double v = 0.0;
+      if (b < k + ng) {
+        const int j = b;   // father index
+        if (r0) { int pb = gm[j]; if (pb >= 0) v += r0[pb]; }
+        if (r1) { int pb = gm[K + j]; if (pb >= 0) v += r1[pb]; }
+      } else if (b >= Kp) {
+        const int c = b - Kp;
+        if (r0 && csrc[2 * c] >= 0) v += ccoef[2 * c] * r0[sk0 + csrc[2 * c]];
+        if (r1 && csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * r1[sk1 + csrc[2 * c + 1]];
+        if (cbirth[c] == g) v += 1.0;
+      }
+      row[b] = v;
+    }
+  }
+  __syncthreads();
+  // ---- F: blocked right-looking elimination of the interface rows ----
+  for (int r0 = 0; r0 < ngp; r0 += kLB) {
+    // F1: factor the 32x32 diagonal block, LiT = (L^-1)^T
+    for (int t = tid; t < 32 * 32; t += 256) {
+      const int i = t >> 5, j = t & 31;
+      D[i * kLdd + j] = P[int64_t(r0 + i) * ldp + k + r0 + j];
+    }
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    if (warp == 0) {
+      for (int c = 0; c < 32; ++c) {
+        const double d = D[c * kLdd + c];
+        if (!(d > 0.0) && lane == 0) s_bad = 1;
+        const double l = sqrt(d), inv = 1.0 / l;
+        __syncwarp();
+        if (lane > c) D[lane * kLdd + c] *= inv;
+        if (lane == c) D[c * kLdd + c] = l;
+        __syncwarp();
+        if (lane > c) {
+          const double lr = D[lane * kLdd + c];
+          for (int j = c + 1; j <= lane; ++j) D[lane * kLdd + j] = fma(-lr, D[j * kLdd + c], D[lane * kLdd + j]);
+        }
+        __syncwarp();
+      }
+      // column `lane` of L^-1 -> row `lane` of LiT
+      const int c = lane;
+      for (int r = 0; r < 32; ++r) {
+        double v;
+        if (r < c) v = 0.0;
+        else {
+          v = (r == c) ? 1.0 : 0.0;
+          for (int h = c; h < r; ++h) v = fma(-D[r * kLdd + h], LiT[c * kLdd + h], v);
+          v /= D[r * kLdd + r];
+        }
+        LiT[c * kLdd + r] = v;
+      }
+    }
+    __syncthreads();
+    if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
+    // F2: X_b = L^-1 P[b rows][cols not yet eliminated] in 64-column chunks.
+    // The eliminated A22 columns [k, k + r0 + 32) are skipped (not needed later).
+    for (int c0 = 0; c0 < W; c0 += kLC) {
+      if (c0 + kLC > k && c0 < k + r0 + kLB) {
+        // chunk overlaps the eliminated block: handle element-wise below
+      }
+      for (int t = tid; t < 32 * kLC; t += 256) {
+        const int i = t >> 6, j = t & 63;
+        const int col = c0 + j;
+        Xc[i * kLds + j] = col < W ? P[int64_t(r0 + i) * ldp + col] : 0.0;
+      }
+      __syncthreads();
+      {
+        // warp tile 16 x 16: warps 0..7 -> (m 2) x (n 4)
+        const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * 16;
+        double acc[2][2][2] = {};
+        warp_gemm_tn<2, 2>(acc, LiT, kLdd, m0, Xc, kLds, n0, 32);
+        __syncthreads();
+        const int gq = lane & 3, gr = lane >> 2;
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int row = m0 + 8 * i + gr, col = c0 + n0 + 8 * j + 2 * gq + e;
+              if (col < W) P[int64_t(r0 + row) * ldp + col] = acc[i][j][e];
+            }
+      }
+      __syncthreads();
+    }
+    // F3: trailing rows r >= r0+32:  P[r][j] -= sum_h X_b[h][k + r] X_b[h][j]
+    if (r0 + kLB < ngp) {
+      for (int c0 = 0; c0 < W; c0 += kLC) {
+        if (c0 + kLC <= k + r0 + kLB && c0 >= k) continue;   // fully eliminated A22 columns
+        for (int t = tid; t < 32 * kLC; t += 256) {
+          const int i = t >> 6, j = t & 63;
+          const int col = c0 + j;
+          Xc[i * kLds + j] = col < W ? P[int64_t(r0 + i) * ldp + col] : 0.0;
+        }
+        for (int rt = r0 + kLB; rt < ngp; rt += kLB) {
+          for (int t = tid; t < 32 * 32; t += 256) {
+            const int h = t >> 5, r = t & 31;
+            Lt[h * kLdd + r] = P[int64_t(r0 + h) * ldp + k + rt + r];
+          }
+          __syncthreads();
+          const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * 16;
+          double acc[2][2][2] = {};
+          warp_gemm_tn<2, 2>(acc, Lt, kLdd, m0, Xc, kLds, n0, 32);
+          const int gq = lane & 3, gr = lane >> 2;
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int row = rt + m0 + 8 * i + gr, col = c0 + n0 + 8 * j + 2 * gq + e;
+                if (col < W) P[int64_t(row) * ldp + col] -= acc[i][j][e];
+              }
+          __syncthreads();
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- S: sigma = sigma~ + v^T X ----
+  double* dst = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
+  for (int c = tid; c < nc; c += 256) {
+    double v = 0.0;
+    if (csrc[2 * c] >= 0) v += ccoef[2 * c] * son[0][size_t(sk0) * sl0 + csrc[2 * c]];
+    if (csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * son[1][size_t(sk1) * sl1 + csrc[2 * c + 1]];
+    if (c >= 1)
+      for (int g = 0; g < ng; ++g) v = fma(P[int64_t(g) * ldp + Kp], P[int64_t(g) * ldp + Kp + c], v);
+    dst[size_t(k) * U.out_ld + c] = v;
+  }
+  // ---- E: out = A~[B, B | R] - X_B^T [X_B | X_R], 32 x 64 output tiles ----
+  const int ow = k + nc;
+  for (int a0 = 0; a0 < k; a0 += 32) {
+    for (int b0 = 0; b0 < ow; b0 += 64) {
+      const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * 16;
+      double acc[2][2][2] = {};
+      for (int g0 = 0; g0 < ngp; g0 += 32) {
+        __syncthreads();
+        for (int t = tid; t < 32 * 32; t += 256) {
+          const int g = t >> 5, i = t & 31;
+          const int a = a0 + i;
+          Ea[g * kLds + i] = a < k ? P[int64_t(g0 + g) * ldp + a] : 0.0;
+        }
+        for (int t = tid; t < 32 * 64; t += 256) {
+          const int g = t >> 6, j = t & 63;
+          const int b = b0 + j;
+          const int col = b < k ? b : (b < ow ? Kp + (b - k) : -1);
+          Eb[g * kLds + j] = col >= 0 ? P[int64_t(g0 + g) * ldp + col] : 0.0;
+        }
+        __syncthreads();
+        warp_gemm_tn<2, 2>(acc, Ea, kLds, m0, Eb, kLds, n0, 32);
+      }
+      const int gq = lane & 3, gr = lane >> 2;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int a = a0 + m0 + 8 * i + gr;
+        if (a >= k) continue;
+        const int pa0 = gm[a], pa1 = gm[K + a];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int b = b0 + n0 + 8 * j + 2 * gq + e;
+            if (b >= ow) continue;
+            double v = 0.0;
+            if (b < k) {
+              if (pa0 >= 0) { int pb = gm[b]; if (pb >= 0) v += son[0][size_t(pa0) * sl0 + pb]; }
+              if (pa1 >= 0) { int pb = gm[K + b]; if (pb >= 0) v += son[1][size_t(pa1) * sl1 + pb]; }
+            } else {
+              const int c = b - k;
+              if (pa0 >= 0 && csrc[2 * c] >= 0) v += ccoef[2 * c] * son[0][size_t(pa0) * sl0 + sk0 + csrc[2 * c]];
+              if (pa1 >= 0 && csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * son[1][size_t(pa1) * sl1 + sk1 + csrc[2 * c + 1]];
+            }
+            dst[size_t(a) * U.out_ld + b] = v - acc[i][j][e];
+          }
+      }
+    }
+  }
+}
+
+cudaError_t launch_merge_l(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
+                           int64_t ws_node_stride, cudaStream_t s) {
+  const size_t smem = merge_l_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(merge_l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  dim3 grid(B, n_nodes);
+  merge_l_kernel<<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_node_stride);
   return cudaGetLastError();
 }
 

@@ -243,3 +243,30 @@ def test_host_and_device_entry_points_agree(torch_cuda):
     a = hb.log_likelihood_batch(prob, Z)
     b = hb.log_likelihood_batch(prob, torch.from_numpy(Z).cuda()).cpu().numpy()
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_large_configs_match_reference(torch_cuda, golden, name):
+    """C3 (reference HDD), C4 / C5 (reference direct solve) golden rows; these
+    configs run their top merges on the global-panel tier."""
+    g = golden(f"cfg_{name}")
+    prob = configs.make_problem(name)
+    S = hb.forward_functionals_batch(prob, g["Z"])
+    ll = hb.log_likelihood_batch(prob, g["Z"])
+    for b in range(S.shape[0]):
+        assert rel(S[b], g["S"][b]) <= TOL
+    assert np.max(np.abs(ll - g["ll"]) / np.abs(g["ll"])) <= TOL
+
+
+def test_global_panel_tier_matches_shared_tier(torch_cuda, golden, monkeypatch):
+    """Force every merge depth onto the global-panel tier (HDD_FORCE_TIER_L) and
+    compare with the shared-memory tier and the reference on C1 / C2."""
+    g1, g2 = golden("cfg_C1"), golden("cfg_C2")
+    a1 = hb.forward_functionals_batch(configs.make_problem("C1"), g1["Z"][:16])
+    a2 = hb.forward_functionals_batch(configs.make_problem("C2"), g2["Z"])
+    monkeypatch.setenv("HDD_FORCE_TIER_L", "1")
+    b1 = hb.forward_functionals_batch(configs.make_problem("C1"), g1["Z"][:16])
+    b2 = hb.forward_functionals_batch(configs.make_problem("C2"), g2["Z"])
+    assert rel(b1, a1) <= 1e-13 and rel(b2, a2) <= 1e-13
+    for b in range(b2.shape[0]):
+        assert rel(b2[b], g2["S"][b]) <= TOL
