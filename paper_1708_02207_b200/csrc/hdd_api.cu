@@ -28,7 +28,9 @@ struct HddPlan {
   std::vector<DevUpper> h_upper;
   std::vector<size_t> depth_smem;      // merge smem per depth
   std::vector<int> depth_tier;         // 0 = shared-memory panel, 1 = global panel
-  std::vector<int64_t> depth_ws;       // tier-L panel doubles per (node, sample)
+  std::vector<int64_t> depth_ws;       // panel doubles per (node, sample)
+  std::vector<int> depth_rows;         // max k + ngp over the depth's nodes
+  std::vector<int> depth_nb;           // elimination block rows (16 or 32)
   double* ws = nullptr;                // tier-L workspace
   size_t leaf_smem = 0;
   HddError err{};
@@ -68,19 +70,6 @@ static int upload(HddPlan* pl, const std::vector<T>& v, const T** out) {
   CU(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
   *out = static_cast<const T*>(p);
   return 0;
-}
-
-static size_t merge_smem_bytes(const UpperNode& U, int ldp) {
-  int ngp = (U.ng + 3) & ~3;
-  size_t d = size_t(ngp) * ldp + ((U.nc + 1) & ~1) + 2 * size_t(U.nc);
-  size_t i = 2 * size_t(U.K) + 3 * size_t(U.nc);
-  return d * sizeof(double) + i * sizeof(int) + 64;
-}
-
-static int panel_ld(const UpperNode& U) {
-  int ldp = U.K + U.nc;
-  ldp += ((8 - ldp % 16) + 16) % 16;   // ldp = 8 (mod 16): conflict-free DMMA fragment loads
-  return ldp;
 }
 
 static int setup_device(HddPlan* pl, int max_batch) {
@@ -147,23 +136,33 @@ static int setup_device(HddPlan* pl, int max_batch) {
   pl->depth_smem.assign(P.upper_by_depth.size(), 0);
   pl->depth_tier.assign(P.upper_by_depth.size(), 0);
   pl->depth_ws.assign(P.upper_by_depth.size(), 0);
-  const char* force_l = std::getenv("HDD_FORCE_TIER_L");   // test hook: every depth on the global panel
+  pl->depth_rows.assign(P.upper_by_depth.size(), 0);
+  pl->depth_nb.assign(P.upper_by_depth.size(), 32);
+  const char* force_l = std::getenv("HDD_FORCE_TIER_L");   // test hook: every depth on the HBM panel
   for (size_t u = 0; u < P.upper.size(); ++u) {
     const UpperNode& U = P.upper[u];
-    if (merge_smem_bytes(U, panel_ld(U)) > 200 * 1024 || (force_l && force_l[0] == '1'))
-      pl->depth_tier[U.depth] = 1;
+    const int ngp32 = (U.ng + 31) / 32 * 32;
+    const int ldp32 = (U.k + ngp32 + U.nc + 15) / 16 * 16 + 8;
+    if (merge_m2_smem_bytes(ngp32, ldp32) > 220 * 1024 || (force_l && force_l[0] == '1')) pl->depth_tier[U.depth] = 1;
+  }
+  for (size_t u = 0; u < P.upper.size(); ++u) {
+    const UpperNode& U = P.upper[u];
+    const int nbk = (pl->depth_tier[U.depth] || U.ng > 16) ? 32 : 16;
+    const int ngp = (U.ng + nbk - 1) / nbk * nbk;
+    const int ldp = (U.k + ngp + U.nc + 15) / 16 * 16 + 8;
+    pl->depth_nb[U.depth] = nbk;
+    pl->depth_ws[U.depth] = std::max<int64_t>(pl->depth_ws[U.depth], int64_t(ngp) * ldp);
+    pl->depth_rows[U.depth] = std::max(pl->depth_rows[U.depth], U.k + ngp);
   }
   for (size_t u = 0; u < P.upper.size(); ++u) {
     const UpperNode& U = P.upper[u];
     DevUpper& d = pl->h_upper[u];
     std::memset(&d, 0, sizeof(d));
     d.k = U.k; d.ng = U.ng; d.K = U.K; d.nc = U.nc;
-    d.ldp = panel_ld(U);
-    if (pl->depth_tier[U.depth]) {
-      const int ngp = (U.ng + 31) / 32 * 32;
-      d.ldp = (U.k + ngp + U.nc + 3) / 4 * 4;
-      pl->depth_ws[U.depth] = std::max<int64_t>(pl->depth_ws[U.depth], int64_t(ngp) * d.ldp);
-    }
+    const int nbk = pl->depth_nb[U.depth];
+    const int ngp_u = (U.ng + nbk - 1) / nbk * nbk;
+    d.ldp = (U.k + ngp_u + U.nc + 15) / 16 * 16 + 8;
+    d.nb = nbk;
     d.out_ld = U.out_ld;
     d.out_elems = U.out_elems;
     d.out_off = U.out_off;
@@ -193,7 +192,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
     csrc.insert(csrc.end(), U.csrc.begin(), U.csrc.end());
     ccoef.insert(ccoef.end(), U.ccoef.begin(), U.ccoef.end());
     cbirth.insert(cbirth.end(), U.cbirth.begin(), U.cbirth.end());
-    size_t sm = pl->depth_tier[U.depth] ? merge_l_smem_bytes() : merge_smem_bytes(U, d.ldp);
+    size_t sm = pl->depth_tier[U.depth] ? 0 : merge_m2_smem_bytes(ngp_u, d.ldp);
     pl->depth_smem[U.depth] = std::max(pl->depth_smem[U.depth], sm);
   }
   if ((rc = upload(pl, gmap, &D.gmap))) return rc;
@@ -287,7 +286,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
   {
     int ncls = 0;
     for (int c = 0; c < 3; ++c) ncls += D.leaf_class_count[c] > 0;
-    pl->n_launches = 2 + ncls + int(P.upper_by_depth.size());
+    pl->n_launches = 2 + ncls + 2 * int(P.upper_by_depth.size());
   }
   return HDD_OK;
 }
@@ -355,12 +354,9 @@ static int run_sub_batch(HddPlan* pl, const double* Z, int B, double* S, double*
   if (ev) CU(cudaEventRecord(ev[e++], st));
   for (int dep = int(P.upper_by_depth.size()) - 1; dep >= 0; --dep) {
     const auto& ids = P.upper_by_depth[dep];
-    if (!ids.empty()) {
-      if (pl->depth_tier[dep])
-        CU(launch_merge_l(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->ws, pl->depth_ws[dep], st));
-      else
-        CU(launch_merge_m(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->depth_smem[dep], st));
-    }
+    if (!ids.empty())
+      CU(launch_merge(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->ws, pl->depth_ws[dep],
+                      pl->depth_tier[dep], pl->depth_rows[dep], pl->depth_smem[dep], pl->depth_nb[dep], st));
     if (ev) CU(cudaEventRecord(ev[e++], st));
   }
   CU(launch_finalize(D, B, S, ll, st));

@@ -10,7 +10,8 @@ constexpr int kMaxBuffers = 24;
 // One upper (merge) node as the merge kernels see it.
 struct DevUpper {
   int k, ng, K, nc;
-  int ldp;                 // panel leading dimension (tier M smem / tier L global)
+  int ldp;                 // panel leading dimension
+  int nb;                  // elimination block rows (16 or 32); panel rows = ng rounded up to nb
   int out_ld;
   int64_t out_elems, out_off;
   int buf;
@@ -76,10 +77,9 @@ struct DevPlan {
 // launchers (hdd_kernels.cu); all return cudaError_t of the launch
 cudaError_t launch_kappa(const DevPlan& p, const double* Z, int B, double* kappa, cudaStream_t s);
 cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_out);
-cudaError_t launch_merge_m(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B,
-                           size_t smem, cudaStream_t s);
-cudaError_t launch_merge_l(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
-                           int64_t ws_node_stride, cudaStream_t s);
+cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
+                         int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s);
+size_t merge_m2_smem_bytes(int ngp, int ldp);
 size_t merge_l_smem_bytes();
 cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cudaStream_t s);
 size_t leaf_smem_bytes(int leaf_cols);

@@ -558,161 +558,17 @@ cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_ou
 }
 
 // ---------------------------------------------------------------------------
-// K3: upper merge, interface panel in shared memory (tier M)
+// K3: upper merges.  Three steps per depth:
+//   assemble_kernel   gathers the sons into the father's output block (lower
+//                     part of A11 and R_B: assemble_father, hdd.py:216-238) and
+//                     into the interface panel [A21 | A22 (padded to 32) | R_gamma]
+//                     in HBM — memory-bound, every (row, node, sample) in parallel;
+//   merge_m2_kernel   panel <= ~200 KB: one CTA per (node, sample) loads it to
+//                     shared memory, 32-row blocked right-looking elimination with
+//                     FP64 DMMA trailing updates, then the Schur update
+//                     out -= X_B^T [X_B | X_R] on lower-triangle tiles (mirrored);
+//   merge_l2_kernel   same with the panel kept in HBM (tier L).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) merge_m_kernel(DevPlan p, const DevUpper* __restrict__ nodes) {
-  extern __shared__ __align__(16) double sm[];
-  const DevUpper& U = nodes[blockIdx.y];
-  const int s = blockIdx.x;
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
-  const int k = U.k, ng = U.ng, K = U.K, nc = U.nc, ldp = U.ldp;
-  const int ngp = (ng + 3) & ~3;
-  double* P = sm;                                  // [ngp][ldp]
-  double* sig = P + size_t(ngp) * ldp;             // [nc]
-  double* ccoef = sig + ((nc + 1) & ~1);           // [nc][2]
-  int* gm = reinterpret_cast<int*>(ccoef + 2 * nc); // [2][K]
-  int* csrc = gm + 2 * K;                          // [nc][2]
-  int* cbirth = csrc + 2 * nc;                     // [nc]
-  for (int t = tid; t < 2 * K; t += nthr) gm[t] = p.gmap[U.gmap_off + t];
-  for (int t = tid; t < 2 * nc; t += nthr) {
-    csrc[t] = p.csrc[2 * U.col_off + t];
-    ccoef[t] = p.ccoef[2 * U.col_off + t];
-  }
-  for (int t = tid; t < nc; t += nthr) cbirth[t] = p.cbirth[U.col_off + t];
-  const double* son[2];
-#pragma unroll
-  for (int sn = 0; sn < 2; ++sn)
-    son[sn] = p.buf[U.son_buf[sn]] + U.son_off[sn] * p.bcap + int64_t(s) * U.son_elems[sn];
-  const int sk0 = U.son_k[0], sk1 = U.son_k[1], sl0 = U.son_ld[0], sl1 = U.son_ld[1];
-  __syncthreads();
-  // ---- gather the interface panel [A21 | A22 | R_gamma] ----
-  const int W = K + nc;
-  for (int g = warp; g < ngp; g += nwarp) {
-    double* row = P + size_t(g) * ldp;
-    if (g >= ng) {
-      for (int b = lane; b < ldp; b += 32) row[b] = 0.0;
-      continue;
-    }
-    const int a = k + g;
-    const int pa0 = gm[a], pa1 = gm[K + a];
-    const double* r0 = pa0 >= 0 ? son[0] + size_t(pa0) * sl0 : nullptr;
-    const double* r1 = pa1 >= 0 ? son[1] + size_t(pa1) * sl1 : nullptr;
-    for (int b = lane; b < W; b += 32) {
-      double v = 0.0;
-      if (b < K) {
-        if (r0) { int pb = gm[b]; if (pb >= 0) v += r0[pb]; }
-        if (r1) { int pb = gm[K + b]; if (pb >= 0) v += r1[pb]; }
-      } else {
-        const int c = b - K;
-        if (r0 && csrc[2 * c] >= 0) v += ccoef[2 * c] * r0[sk0 + csrc[2 * c]];
-        if (r1 && csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * r1[sk1 + csrc[2 * c + 1]];
-        if (cbirth[c] == g) v += 1.0;
-      }
-      row[b] = v;
-    }
-  }
-  for (int c = tid; c < nc; c += nthr) {
-    double v = 0.0;
-    if (csrc[2 * c] >= 0) v += ccoef[2 * c] * son[0][size_t(sk0) * sl0 + csrc[2 * c]];
-    if (csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * son[1][size_t(sk1) * sl1 + csrc[2 * c + 1]];
-    sig[c] = v;
-  }
-  __syncthreads();
-  // ---- row-oriented elimination: L = chol(A22), X = L^-1 [A21 | A22 | R] ----
-  for (int c = 0; c < ng; ++c) {
-    double* rc = P + size_t(c) * ldp;
-    const double d = rc[k + c];
-    if (!(d > 0.0) && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
-    const double inv = 1.0 / sqrt(d);
-    __syncthreads();
-    for (int b = tid; b < W; b += nthr) rc[b] *= inv;
-    __syncthreads();
-    for (int rr = c + 1 + warp; rr < ng; rr += nwarp) {
-      double* rw = P + size_t(rr) * ldp;
-      const double lr = rw[k + c] * inv;
-      for (int b = lane; b < W; b += 32)
-        if (b != k + c) rw[b] = fma(-lr, rc[b], rw[b]);
-    }
-    __syncthreads();
-  }
-  // ---- sigma += v^T X (v = load column) ----
-  for (int c = 1 + tid; c < nc; c += nthr) {
-    double acc = sig[c];
-    for (int g = 0; g < ng; ++g) acc = fma(P[size_t(g) * ldp + K], P[size_t(g) * ldp + K + c], acc);
-    sig[c] = acc;
-  }
-  // ---- Schur update out = A~[B, B|cols] - X_B^T X, FP64 DMMA 16x16 warp tiles ----
-  double* dst = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
-  const int ow = k + nc;                 // output columns
-  const int mt = (k + 15) >> 4, nt = (ow + 15) >> 4;
-  const int gq = lane & 3, gr = lane >> 2;
-  for (int tile = warp; tile < mt * nt; tile += nwarp) {
-    const int a0 = (tile / nt) << 4, b0 = (tile % nt) << 4;
-    double acc[2][2][2] = {};
-    int acol[2], bcol[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      int a = a0 + 8 * i + gr;
-      acol[i] = a < k ? a : 0;
-      int b = b0 + 8 * i + gr;
-      bcol[i] = b < k ? b : (b < ow ? K + (b - k) : 0);
-    }
-    for (int g = 0; g < ngp; g += 4) {
-      const double* pr = P + size_t(g + gq) * ldp;
-      double av[2], bv[2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) { av[i] = pr[acol[i]]; bv[i] = pr[bcol[i]]; }
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma884(acc[i][j], av[i], bv[j]);
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int a = a0 + 8 * i + gr;
-      if (a >= k) continue;
-      const int pa0 = gm[a], pa1 = gm[K + a];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int b = b0 + 8 * j + 2 * gq + e;
-          if (b >= ow) continue;
-          double v = 0.0;
-          if (b < k) {
-            if (pa0 >= 0) { int pb = gm[b]; if (pb >= 0) v += son[0][size_t(pa0) * sl0 + pb]; }
-            if (pa1 >= 0) { int pb = gm[K + b]; if (pb >= 0) v += son[1][size_t(pa1) * sl1 + pb]; }
-          } else {
-            const int c = b - k;
-            if (pa0 >= 0 && csrc[2 * c] >= 0) v += ccoef[2 * c] * son[0][size_t(pa0) * sl0 + sk0 + csrc[2 * c]];
-            if (pa1 >= 0 && csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * son[1][size_t(pa1) * sl1 + sk1 + csrc[2 * c + 1]];
-          }
-          dst[size_t(a) * U.out_ld + b] = v - acc[i][j][e];
-        }
-      }
-    }
-  }
-  __syncthreads();
-  for (int c = tid; c < nc; c += nthr) dst[size_t(k) * U.out_ld + c] = sig[c];
-}
-
-cudaError_t launch_merge_m(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, size_t smem,
-                           cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(merge_m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
-  dim3 grid(B, n_nodes);
-  merge_m_kernel<<<grid, 256, smem, s>>>(p, nodes_dev);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// K3L: upper merge with the interface panel in global memory (tier L)
-// ---------------------------------------------------------------------------
-// Panel columns: [0,k) A21 | [k, k+ngp) A22 (padded to 32 rows, identity in the
-// padding) | [k+ngp, W) R_gamma.  Rows: the ngp interface rows.
-// TN warp GEMM: acc[i][j] += sum_kk A[kk][m0+..] * B[kk][n0+..] over kd (multiple of 4),
-// A and B in shared memory, k-major.
 template <int FM, int FN>
 __device__ __forceinline__ void warp_gemm_tn(double (&acc)[FM][FN][2], const double* __restrict__ A, int lda, int m0,
                                              const double* __restrict__ B, int ldb, int n0, int kd) {
@@ -736,32 +592,321 @@ constexpr int kLC = 64;     // column chunk
 constexpr int kLds = 72;    // smem leading dim for 64-wide tiles (= 8 mod 16)
 constexpr int kLdd = 40;    // smem leading dim for 32-wide tiles (= 8 mod 16)
 
+__device__ __forceinline__ int upper_ngp(const DevUpper& U) { return (U.ng + U.nb - 1) / U.nb * U.nb; }
+
+// -- assemble ----------------------------------------------------------------
+// grid (row groups of 8, node, sample); warp per father row a in [0, k + ngp]
+__global__ void __launch_bounds__(256) assemble_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
+                                                       double* __restrict__ ws, int64_t ws_stride) {
+  const DevUpper& U = nodes[blockIdx.y];
+  const int s = blockIdx.z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k = U.k, ng = U.ng, K = U.K, nc = U.nc, ldp = U.ldp;
+  const int ngp = upper_ngp(U);
+  const int Kp = k + ngp;
+  const int a = blockIdx.x * 8 + warp;
+  if (a > k + ngp) return;
+  const int32_t* gm = p.gmap + U.gmap_off;
+  const int32_t* csrc = p.csrc + 2 * U.col_off;
+  const double* ccoef = p.ccoef + 2 * U.col_off;
+  const double* son0 = p.buf[U.son_buf[0]] + U.son_off[0] * p.bcap + int64_t(s) * U.son_elems[0];
+  const double* son1 = p.buf[U.son_buf[1]] + U.son_off[1] * p.bcap + int64_t(s) * U.son_elems[1];
+  const int sk0 = U.son_k[0], sk1 = U.son_k[1], sl0 = U.son_ld[0], sl1 = U.son_ld[1];
+  double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
+  if (a == k + ngp) {   // sigma~
+    for (int c = lane; c < nc; c += 32) {
+      double v = 0.0;
+      if (csrc[2 * c] >= 0) v += ccoef[2 * c] * son0[size_t(sk0) * sl0 + csrc[2 * c]];
+      if (csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * son1[size_t(sk1) * sl1 + csrc[2 * c + 1]];
+      out[size_t(k) * U.out_ld + c] = v;
+    }
+    return;
+  }
+  if (a < k) {
+    // lower part of A11 row a, then R_B row a
+    const int pa0 = gm[a], pa1 = gm[K + a];
+    const double* r0 = pa0 >= 0 ? son0 + size_t(pa0) * sl0 : nullptr;
+    const double* r1 = pa1 >= 0 ? son1 + size_t(pa1) * sl1 : nullptr;
+    double* row = out + size_t(a) * U.out_ld;
+    for (int j = lane; j <= a; j += 32) {
+      double v = 0.0;
+      if (r0) { const int pb = gm[j]; if (pb >= 0) v += r0[pb]; }
+      if (r1) { const int pb = gm[K + j]; if (pb >= 0) v += r1[pb]; }
+      row[j] = v;
+    }
+    for (int c = lane; c < nc; c += 32) {
+      double v = 0.0;
+      if (r0 && csrc[2 * c] >= 0) v += ccoef[2 * c] * r0[sk0 + csrc[2 * c]];
+      if (r1 && csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * r1[sk1 + csrc[2 * c + 1]];
+      row[k + c] = v;
+    }
+    return;
+  }
+  // interface panel row g
+  const int g = a - k;
+  double* P = ws + int64_t(blockIdx.y) * ws_stride * p.bcap + int64_t(s) * ws_stride + int64_t(g) * ldp;
+  const int W = Kp + nc;
+  if (g >= ng) {
+    for (int j = lane; j < W; j += 32) P[j] = (j == k + g) ? 1.0 : 0.0;
+    return;
+  }
+  const int32_t* cbirth = p.cbirth + U.col_off;
+  const int pa0 = gm[a], pa1 = gm[K + a];
+  const double* r0 = pa0 >= 0 ? son0 + size_t(pa0) * sl0 : nullptr;
+  const double* r1 = pa1 >= 0 ? son1 + size_t(pa1) * sl1 : nullptr;
+  for (int j = lane; j < W; j += 32) {
+    double v = 0.0;
+    if (j < k + ng) {
+      if (r0) { const int pb = gm[j]; if (pb >= 0) v += r0[pb]; }
+      if (r1) { const int pb = gm[K + j]; if (pb >= 0) v += r1[pb]; }
+    } else if (j >= Kp) {
+      const int c = j - Kp;
+      if (r0 && csrc[2 * c] >= 0) v += ccoef[2 * c] * r0[sk0 + csrc[2 * c]];
+      if (r1 && csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * r1[sk1 + csrc[2 * c + 1]];
+      if (cbirth[c] == g) v += 1.0;
+    }
+    P[j] = v;
+  }
+}
+
+// -- shared building blocks ------------------------------------------------
+// Cholesky of the NB x NB diagonal block (rows read from `src`, ld `ld`) by one
+// warp, lane = row, the row of L in registers and L[j][c] broadcast with
+// shuffles; then L^-1 by forward row elimination with the rows of L^-1 kept in
+// LiT (LiT[c][r] = (L^-1)[r][c]).  Sets *bad on a non-positive pivot.
+template <int NB>
+__device__ __forceinline__ double reg_get(const double (&a)[NB], int c) {
+  double v = 0.0;
+#pragma unroll
+  for (int t = 0; t < NB; ++t) v = (t == c) ? a[t] : v;
+  return v;
+}
+template <int NB>
+__device__ __forceinline__ void reg_set(double (&a)[NB], int c, double v) {
+#pragma unroll
+  for (int t = 0; t < NB; ++t) a[t] = (t == c) ? v : a[t];
+}
+
+template <int NB>
+__device__ __forceinline__ void factor_diag_block(const double* src, int ld, double* LiT, int* bad) {
+  const int lane = threadIdx.x & 31;
+  double a[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) a[j] = lane < NB ? src[lane * ld + j] : (lane == j ? 1.0 : 0.0);
+  for (int c = 0; c < NB; ++c) {
+    const double ac = reg_get<NB>(a, c);
+    const double d = __shfl_sync(0xffffffffu, ac, c);
+    if (!(d > 0.0) && lane == 0) *bad = 1;
+    const double l = sqrt(d), inv = 1.0 / l;
+    const double lc = lane == c ? l : (lane > c ? ac * inv : 0.0);
+    reg_set<NB>(a, c, lane >= c ? lc : reg_get<NB>(a, c));
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const double ljc = __shfl_sync(0xffffffffu, lc, j);
+      if (j > c && lane >= j) a[j] = fma(-lc, ljc, a[j]);
+    }
+  }
+  // rows of L^-1: lane r accumulates row r in LiT[.][r]
+  if (lane < NB)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) LiT[c * kLdd + lane] = lane == c ? 1.0 : 0.0;
+  __syncwarp();
+  for (int h = 0; h < NB; ++h) {
+    const double lrh = reg_get<NB>(a, h);     // L[lane][h]
+    if (lane == h) {
+      const double inv = 1.0 / lrh;
+      for (int c = 0; c <= h; ++c) LiT[c * kLdd + h] *= inv;
+    }
+    __syncwarp();
+    if (lane > h && lane < NB)
+      for (int c = 0; c <= h; ++c) LiT[c * kLdd + lane] = fma(-lrh, LiT[c * kLdd + h], LiT[c * kLdd + lane]);
+    __syncwarp();
+  }
+}
+
+// Schur-update epilogue, 32 x 64 output tiles, lower-triangle tiles of the Psi
+// part mirrored; X rows from an smem/HBM panel P (ld ldp) via tile staging.
+// out already holds the assembled lower A11 and R_B.
+template <bool SMEM>
+__device__ __forceinline__ void schur_epilogue(const double* __restrict__ P, int ldp, int k, int ngp, int Kp, int nc,
+                                               double* __restrict__ out, int out_ld, double* Ea, double* Eb) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane & 3, gr = lane >> 2;
+  const int ow = k + nc;
+  const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * 16;
+  for (int a0 = 0; a0 < k; a0 += 32) {
+    for (int b0 = 0; b0 < ow; b0 += 64) {
+      if (b0 + 64 <= k && b0 > a0 + 31) continue;  // strictly upper Psi tile: mirrored from below
+      double acc[2][2][2] = {};
+      int acol[2], bcol[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int aa = a0 + m0 + 8 * i + gr;
+        acol[i] = aa < k ? aa : 0;
+        const int bb = b0 + n0 + 8 * i + gr;
+        bcol[i] = bb < k ? bb : (bb < ow ? Kp + (bb - k) : 0);
+      }
+      double pre[2][2][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int aa = a0 + m0 + 8 * i + gr;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int bb = b0 + n0 + 8 * j + 2 * gq + e;
+            pre[i][j][e] = (aa < k && bb < ow && (bb >= k || bb <= aa)) ? out[size_t(aa) * out_ld + bb] : 0.0;
+          }
+      }
+      if constexpr (SMEM) {
+        for (int g0 = 0; g0 < ngp; g0 += 4) {
+          const double* pr = P + size_t(g0 + gq) * ldp;
+          double av[2], bv[2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) { av[i] = pr[acol[i]]; bv[i] = pr[bcol[i]]; }
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) dmma884(acc[i][j], av[i], bv[j]);
+        }
+      } else {
+        for (int g0 = 0; g0 < ngp; g0 += 32) {
+          __syncthreads();
+          for (int t = tid; t < 32 * 32; t += 256) {
+            const int g = t >> 5, i = t & 31;
+            const int aa = a0 + i;
+            Ea[g * kLds + i] = aa < k ? P[int64_t(g0 + g) * ldp + aa] : 0.0;
+          }
+          for (int t = tid; t < 32 * 64; t += 256) {
+            const int g = t >> 6, j = t & 63;
+            const int bb = b0 + j;
+            const int col = bb < k ? bb : (bb < ow ? Kp + (bb - k) : -1);
+            Eb[g * kLds + j] = col >= 0 ? P[int64_t(g0 + g) * ldp + col] : 0.0;
+          }
+          __syncthreads();
+          warp_gemm_tn<2, 2>(acc, Ea, kLds, m0, Eb, kLds, n0, 32);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int aa = a0 + m0 + 8 * i + gr;
+        if (aa >= k) continue;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int bb = b0 + n0 + 8 * j + 2 * gq + e;
+            if (bb >= ow) continue;
+            if (bb < k) {
+              if (bb > aa) continue;
+              const double v = pre[i][j][e] - acc[i][j][e];
+              out[size_t(aa) * out_ld + bb] = v;
+              if (bb < aa) out[size_t(bb) * out_ld + aa] = v;
+            } else {
+              out[size_t(aa) * out_ld + bb] = pre[i][j][e] - acc[i][j][e];
+            }
+          }
+      }
+    }
+  }
+}
+
+// -- tier M: panel in shared memory ------------------------------------------
+size_t merge_m2_smem_bytes(int ngp, int ldp) {
+  return sizeof(double) * size_t(ngp) * ldp + 64;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(256) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
+                                                       const double* __restrict__ ws, int64_t ws_stride) {
+  extern __shared__ __align__(16) double sm[];
+  const DevUpper& U = nodes[blockIdx.y];
+  const int s = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = U.k, ng = U.ng, nc = U.nc, ldp = U.ldp;
+  const int ngp = upper_ngp(U);
+  const int Kp = k + ngp;
+  const int W = Kp + nc;
+  double* P = sm;                          // [ngp][ldp]
+  __shared__ int s_bad;
+  {
+    const double* src = ws + int64_t(blockIdx.y) * ws_stride * p.bcap + int64_t(s) * ws_stride;
+    const int n2 = (ngp * ldp) >> 1;
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    double2* d2 = reinterpret_cast<double2*>(P);
+    for (int t = tid; t < n2; t += 256) d2[t] = s2[t];
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  const int gq = lane & 3, gr = lane >> 2;
+  for (int r0 = 0; r0 < ngp; r0 += NB) {
+    // F1+F2: row elimination inside the block by all threads -> rows r0.. hold
+    // X_b = L_bb^-1 P_b (forward substitution, row oriented)
+    for (int c = r0; c < r0 + NB; ++c) {
+      double* rc = P + c * ldp;
+      __syncthreads();                    // previous pivot's updates are complete
+      const double d = rc[k + c];
+      if (!(d > 0.0) && tid == 0) s_bad = 1;
+      const double inv = 1.0 / sqrt(d);
+      for (int j = tid; j < W; j += 256)
+        if (j != k + c) rc[j] *= inv;     // the diagonal entry is never read again
+      __syncthreads();
+      const int nr = r0 + NB - c - 1;
+      for (int t = warp; t < nr; t += 8) {
+        double* rw = P + (c + 1 + t) * ldp;
+        const double lr = rw[k + c] * inv;
+        for (int j = lane; j < W; j += 32)
+          if (j != k + c) rw[j] = fma(-lr, rc[j], rw[j]);
+      }
+    }
+    __syncthreads();
+    // F3: trailing rows: P[r][j] -= sum_h X_b[h][k + r] X_b[h][j]
+    const int nrt = (ngp - r0 - NB) / 16;
+    const int nct = (W + 15) / 16;
+    for (int t = warp; t < nrt * nct; t += 8) {
+      const int rt = r0 + NB + (t / nct) * 16;
+      const int c0 = (t % nct) * 16;
+      if (c0 >= k && c0 + 16 <= k + r0 + NB) continue;
+      double acc[2][2][2] = {};
+      warp_gemm_tn<2, 2>(acc, P + r0 * ldp + k, ldp, rt, P + r0 * ldp, ldp, c0, NB);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = c0 + 8 * j + 2 * gq + e;
+            if (col < W) P[(rt + 8 * i + gr) * ldp + col] -= acc[i][j][e];
+          }
+    }
+    __syncthreads();
+  }
+  if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
+  double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
+  for (int c = 1 + tid; c < nc; c += 256) {
+    double v = out[size_t(k) * U.out_ld + c];
+    for (int g = 0; g < ng; ++g) v = fma(P[g * ldp + Kp], P[g * ldp + Kp + c], v);
+    out[size_t(k) * U.out_ld + c] = v;
+  }
+  schur_epilogue<true>(P, ldp, k, ngp, Kp, nc, out, U.out_ld, nullptr, nullptr);
+}
+
+// -- tier L: panel in HBM ----------------------------------------------------
 size_t merge_l_smem_bytes() {
-  // D/LiT [32][kLdd] x2, Xb chunk [32][kLds], Lt [32][kLdd], E: two [32][kLds]
   return sizeof(double) * (2 * 32 * kLdd + 32 * kLds + 32 * kLdd + 2 * 32 * kLds) + 1024;
 }
 
 __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
-                                                          double* __restrict__ ws, int64_t ws_node_stride) {
+                                                          double* __restrict__ ws, int64_t ws_stride) {
   extern __shared__ __align__(16) double sm[];
-  const int node_idx = blockIdx.y;
-  const DevUpper& U = nodes[node_idx];
+  const DevUpper& U = nodes[blockIdx.y];
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int k = U.k, ng = U.ng, K = U.K, nc = U.nc, ldp = U.ldp;
-  const int ngp = (ng + kLB - 1) / kLB * kLB;
+  const int k = U.k, ng = U.ng, nc = U.nc, ldp = U.ldp;
+  const int ngp = upper_ngp(U);
   const int Kp = k + ngp;
   const int W = Kp + nc;
-  double* P = ws + int64_t(node_idx) * ws_node_stride * p.bcap + int64_t(s) * ws_node_stride;
-  const int32_t* gm = p.gmap + U.gmap_off;
-  const int32_t* csrc = p.csrc + 2 * U.col_off;
-  const double* ccoef = p.ccoef + 2 * U.col_off;
-  const int32_t* cbirth = p.cbirth + U.col_off;
-  const double* son[2];
-#pragma unroll
-  for (int sn = 0; sn < 2; ++sn)
-    son[sn] = p.buf[U.son_buf[sn]] + U.son_off[sn] * p.bcap + int64_t(s) * U.son_elems[sn];
-  const int sk0 = U.son_k[0], sk1 = U.son_k[1], sl0 = U.son_ld[0], sl1 = U.son_ld[1];
+  double* P = ws + int64_t(blockIdx.y) * ws_stride * p.bcap + int64_t(s) * ws_stride;
   double* D = sm;                         // [32][kLdd]
   double* LiT = D + 32 * kLdd;            // [32][kLdd]
   double* Xc = LiT + 32 * kLdd;           // [32][kLds]
@@ -769,107 +914,38 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
   double* Ea = Lt + 32 * kLdd;            // [32][kLds]
   double* Eb = Ea + 32 * kLds;            // [32][kLds]
   __shared__ int s_bad;
-  // ---- G: gather the panel into global workspace ----
-  for (int g = warp; g < ngp; g += 8) {
-    double* row = P + int64_t(g) * ldp;
-    if (g >= ng) {
-      for (int b = lane; b < W; b += 32) row[b] = (b == k + g) ? 1.0 : 0.0;
-      continue;
-    }
-    const int a = k + g;
-    const int pa0 = gm[a], pa1 = gm[K + a];
-    const double* r0 = pa0 >= 0 ? son[0] + size_t(pa0) * sl0 : nullptr;
-    const double* r1 = pa1 >= 0 ? son[1] + size_t(pa1) * sl1 : nullptr;
-    for (int b = lane; b < W; b += 32) {
-      double v = 0.0;
-      if (b < k + ng) {
-        const int j = b;   // father index
-        if (r0) { int pb = gm[j]; if (pb >= 0) v += r0[pb]; }
-        if (r1) { int pb = gm[K + j]; if (pb >= 0) v += r1[pb]; }
-      } else if (b >= Kp) {
-        const int c = b - Kp;
-        if (r0 && csrc[2 * c] >= 0) v += ccoef[2 * c] * r0[sk0 + csrc[2 * c]];
-        if (r1 && csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * r1[sk1 + csrc[2 * c + 1]];
-        if (cbirth[c] == g) v += 1.0;
-      }
-      row[b] = v;
-    }
-  }
-  __syncthreads();
-  // ---- F: blocked right-looking elimination of the interface rows ----
+  if (tid == 0) s_bad = 0;
   for (int r0 = 0; r0 < ngp; r0 += kLB) {
-    // F1: factor the 32x32 diagonal block, LiT = (L^-1)^T
-    for (int t = tid; t < 32 * 32; t += 256) {
-      const int i = t >> 5, j = t & 31;
-      D[i * kLdd + j] = P[int64_t(r0 + i) * ldp + k + r0 + j];
-    }
-    if (tid == 0) s_bad = 0;
+    if (warp == 0) factor_diag_block<32>(P + int64_t(r0) * ldp + k + r0, ldp, LiT, &s_bad);
     __syncthreads();
-    if (warp == 0) {
-      for (int c = 0; c < 32; ++c) {
-        const double d = D[c * kLdd + c];
-        if (!(d > 0.0) && lane == 0) s_bad = 1;
-        const double l = sqrt(d), inv = 1.0 / l;
-        __syncwarp();
-        if (lane > c) D[lane * kLdd + c] *= inv;
-        if (lane == c) D[c * kLdd + c] = l;
-        __syncwarp();
-        if (lane > c) {
-          const double lr = D[lane * kLdd + c];
-          for (int j = c + 1; j <= lane; ++j) D[lane * kLdd + j] = fma(-lr, D[j * kLdd + c], D[lane * kLdd + j]);
-        }
-        __syncwarp();
-      }
-      // column `lane` of L^-1 -> row `lane` of LiT
-      const int c = lane;
-      for (int r = 0; r < 32; ++r) {
-        double v;
-        if (r < c) v = 0.0;
-        else {
-          v = (r == c) ? 1.0 : 0.0;
-          for (int h = c; h < r; ++h) v = fma(-D[r * kLdd + h], LiT[c * kLdd + h], v);
-          v /= D[r * kLdd + r];
-        }
-        LiT[c * kLdd + r] = v;
-      }
-    }
-    __syncthreads();
-    if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
-    // F2: X_b = L^-1 P[b rows][cols not yet eliminated] in 64-column chunks.
-    // The eliminated A22 columns [k, k + r0 + 32) are skipped (not needed later).
+    // F2: X_b = L^-1 P_b in 64-column chunks
     for (int c0 = 0; c0 < W; c0 += kLC) {
-      if (c0 + kLC > k && c0 < k + r0 + kLB) {
-        // chunk overlaps the eliminated block: handle element-wise below
-      }
+      if (c0 >= k && c0 + kLC <= k + r0 + kLB) continue;
       for (int t = tid; t < 32 * kLC; t += 256) {
         const int i = t >> 6, j = t & 63;
         const int col = c0 + j;
         Xc[i * kLds + j] = col < W ? P[int64_t(r0 + i) * ldp + col] : 0.0;
       }
       __syncthreads();
-      {
-        // warp tile 16 x 16: warps 0..7 -> (m 2) x (n 4)
-        const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * 16;
-        double acc[2][2][2] = {};
-        warp_gemm_tn<2, 2>(acc, LiT, kLdd, m0, Xc, kLds, n0, 32);
-        __syncthreads();
-        const int gq = lane & 3, gr = lane >> 2;
+      const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * 16;
+      double acc[2][2][2] = {};
+      warp_gemm_tn<2, 2>(acc, LiT, kLdd, m0, Xc, kLds, n0, 32);
+      const int gq = lane & 3, gr = lane >> 2;
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int row = m0 + 8 * i + gr, col = c0 + n0 + 8 * j + 2 * gq + e;
-              if (col < W) P[int64_t(r0 + row) * ldp + col] = acc[i][j][e];
-            }
-      }
+          for (int e = 0; e < 2; ++e) {
+            const int row = m0 + 8 * i + gr, col = c0 + n0 + 8 * j + 2 * gq + e;
+            if (col < W) P[int64_t(r0 + row) * ldp + col] = acc[i][j][e];
+          }
       __syncthreads();
     }
-    // F3: trailing rows r >= r0+32:  P[r][j] -= sum_h X_b[h][k + r] X_b[h][j]
+    // F3: trailing rows
     if (r0 + kLB < ngp) {
       for (int c0 = 0; c0 < W; c0 += kLC) {
-        if (c0 + kLC <= k + r0 + kLB && c0 >= k) continue;   // fully eliminated A22 columns
+        if (c0 >= k && c0 + kLC <= k + r0 + kLB) continue;
         for (int t = tid; t < 32 * kLC; t += 256) {
           const int i = t >> 6, j = t & 63;
           const int col = c0 + j;
@@ -900,73 +976,39 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
     }
     __syncthreads();
   }
-  // ---- S: sigma = sigma~ + v^T X ----
-  double* dst = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
-  for (int c = tid; c < nc; c += 256) {
-    double v = 0.0;
-    if (csrc[2 * c] >= 0) v += ccoef[2 * c] * son[0][size_t(sk0) * sl0 + csrc[2 * c]];
-    if (csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * son[1][size_t(sk1) * sl1 + csrc[2 * c + 1]];
-    if (c >= 1)
-      for (int g = 0; g < ng; ++g) v = fma(P[int64_t(g) * ldp + Kp], P[int64_t(g) * ldp + Kp + c], v);
-    dst[size_t(k) * U.out_ld + c] = v;
+  if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
+  double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
+  for (int c = 1 + tid; c < nc; c += 256) {
+    double v = out[size_t(k) * U.out_ld + c];
+    for (int g = 0; g < ng; ++g) v = fma(P[int64_t(g) * ldp + Kp], P[int64_t(g) * ldp + Kp + c], v);
+    out[size_t(k) * U.out_ld + c] = v;
   }
-  // ---- E: out = A~[B, B | R] - X_B^T [X_B | X_R], 32 x 64 output tiles ----
-  const int ow = k + nc;
-  for (int a0 = 0; a0 < k; a0 += 32) {
-    for (int b0 = 0; b0 < ow; b0 += 64) {
-      const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * 16;
-      double acc[2][2][2] = {};
-      for (int g0 = 0; g0 < ngp; g0 += 32) {
-        __syncthreads();
-        for (int t = tid; t < 32 * 32; t += 256) {
-          const int g = t >> 5, i = t & 31;
-          const int a = a0 + i;
-          Ea[g * kLds + i] = a < k ? P[int64_t(g0 + g) * ldp + a] : 0.0;
-        }
-        for (int t = tid; t < 32 * 64; t += 256) {
-          const int g = t >> 6, j = t & 63;
-          const int b = b0 + j;
-          const int col = b < k ? b : (b < ow ? Kp + (b - k) : -1);
-          Eb[g * kLds + j] = col >= 0 ? P[int64_t(g0 + g) * ldp + col] : 0.0;
-        }
-        __syncthreads();
-        warp_gemm_tn<2, 2>(acc, Ea, kLds, m0, Eb, kLds, n0, 32);
-      }
-      const int gq = lane & 3, gr = lane >> 2;
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int a = a0 + m0 + 8 * i + gr;
-        if (a >= k) continue;
-        const int pa0 = gm[a], pa1 = gm[K + a];
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int b = b0 + n0 + 8 * j + 2 * gq + e;
-            if (b >= ow) continue;
-            double v = 0.0;
-            if (b < k) {
-              if (pa0 >= 0) { int pb = gm[b]; if (pb >= 0) v += son[0][size_t(pa0) * sl0 + pb]; }
-              if (pa1 >= 0) { int pb = gm[K + b]; if (pb >= 0) v += son[1][size_t(pa1) * sl1 + pb]; }
-            } else {
-              const int c = b - k;
-              if (pa0 >= 0 && csrc[2 * c] >= 0) v += ccoef[2 * c] * son[0][size_t(pa0) * sl0 + sk0 + csrc[2 * c]];
-              if (pa1 >= 0 && csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * son[1][size_t(pa1) * sl1 + sk1 + csrc[2 * c + 1]];
-            }
-            dst[size_t(a) * U.out_ld + b] = v - acc[i][j][e];
-          }
-      }
-    }
-  }
+  schur_epilogue<false>(P, ldp, k, ngp, Kp, nc, out, U.out_ld, Ea, Eb);
 }
 
-cudaError_t launch_merge_l(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
-                           int64_t ws_node_stride, cudaStream_t s) {
-  const size_t smem = merge_l_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(merge_l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
+                         int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s) {
+  dim3 ga((max_rows + 1 + 7) / 8, n_nodes, B);
+  assemble_kernel<<<ga, 256, 0, s>>>(p, nodes_dev, ws, ws_stride);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   dim3 grid(B, n_nodes);
-  merge_l_kernel<<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_node_stride);
+  if (tier == 0) {
+    if (nb == 16) {
+      e = cudaFuncSetAttribute(merge_m2_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      merge_m2_kernel<16><<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride);
+    } else {
+      e = cudaFuncSetAttribute(merge_m2_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      merge_m2_kernel<32><<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride);
+    }
+  } else {
+    const size_t sm = merge_l_smem_bytes();
+    e = cudaFuncSetAttribute(merge_l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    if (e != cudaSuccess) return e;
+    merge_l_kernel<<<grid, 256, sm, s>>>(p, nodes_dev, ws, ws_stride);
+  }
   return cudaGetLastError();
 }
 
