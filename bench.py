@@ -296,7 +296,7 @@ def main():
         return gather_log_likelihood(ll, world)
 
     for _ in range(args.warmup):
-        step(None)
+        posterior_weights_device(step(None))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

@@ -147,7 +147,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
   }
   for (size_t u = 0; u < P.upper.size(); ++u) {
     const UpperNode& U = P.upper[u];
-    const int nbk = (pl->depth_tier[U.depth] || U.ng > 16) ? 32 : 16;
+    const int nbk = pl->depth_tier[U.depth] ? 32 : 8;
     const int ngp = (U.ng + nbk - 1) / nbk * nbk;
     const int ldp = (U.k + ngp + U.nc + 15) / 16 * 16 + 8;
     pl->depth_nb[U.depth] = nbk;

@@ -730,12 +730,15 @@ __device__ __forceinline__ void factor_diag_block(const double* src, int ld, dou
 template <bool SMEM>
 __device__ __forceinline__ void schur_epilogue(const double* __restrict__ P, int ldp, int k, int ngp, int Kp, int nc,
                                                double* __restrict__ out, int out_ld, double* Ea, double* Eb) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x & 255, lane = tid & 31, warp = tid >> 5;
+  const int grp = threadIdx.x >> 8, ngrp = SMEM ? (blockDim.x >> 8) : 1;   // 8-warp groups
   const int gq = lane & 3, gr = lane >> 2;
   const int ow = k + nc;
   const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * 16;
-  for (int a0 = 0; a0 < k; a0 += 32) {
-    for (int b0 = 0; b0 < ow; b0 += 64) {
+  const int na = (k + 31) / 32, nbt = (ow + 63) / 64;
+  for (int t = grp; t < na * nbt; t += ngrp) {
+    {
+      const int a0 = (t / nbt) * 32, b0 = (t % nbt) * 64;
       if (b0 + 64 <= k && b0 > a0 + 31) continue;  // strictly upper Psi tile: mirrored from below
       double acc[2][2][2] = {};
       int acol[2], bcol[2];
@@ -817,12 +820,13 @@ size_t merge_m2_smem_bytes(int ngp, int ldp) {
 }
 
 template <int NB>
-__global__ void __launch_bounds__(256) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
+__global__ void __launch_bounds__(512) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
                                                        const double* __restrict__ ws, int64_t ws_stride) {
   extern __shared__ __align__(16) double sm[];
   const DevUpper& U = nodes[blockIdx.y];
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = blockDim.x, NWp = NT >> 5;
   const int k = U.k, ng = U.ng, nc = U.nc, ldp = U.ldp;
   const int ngp = upper_ngp(U);
   const int Kp = k + ngp;
@@ -834,25 +838,23 @@ __global__ void __launch_bounds__(256) merge_m2_kernel(DevPlan p, const DevUpper
     const int n2 = (ngp * ldp) >> 1;
     const double2* s2 = reinterpret_cast<const double2*>(src);
     double2* d2 = reinterpret_cast<double2*>(P);
-    for (int t = tid; t < n2; t += 256) d2[t] = s2[t];
+    for (int t = tid; t < n2; t += NT) d2[t] = s2[t];
   }
   if (tid == 0) s_bad = 0;
-  __syncthreads();
   const int gq = lane & 3, gr = lane >> 2;
   for (int r0 = 0; r0 < ngp; r0 += NB) {
-    // F1+F2: row elimination inside the block by all threads -> rows r0.. hold
-    // X_b = L_bb^-1 P_b (forward substitution, row oriented)
+    // in-block row elimination (all threads): rows r0.. become X_b = L_bb^-1 P_b
     for (int c = r0; c < r0 + NB; ++c) {
       double* rc = P + c * ldp;
       __syncthreads();                    // previous pivot's updates are complete
       const double d = rc[k + c];
       if (!(d > 0.0) && tid == 0) s_bad = 1;
       const double inv = 1.0 / sqrt(d);
-      for (int j = tid; j < W; j += 256)
+      for (int j = tid; j < W; j += NT)
         if (j != k + c) rc[j] *= inv;     // the diagonal entry is never read again
       __syncthreads();
       const int nr = r0 + NB - c - 1;
-      for (int t = warp; t < nr; t += 8) {
+      for (int t = warp; t < nr; t += NWp) {
         double* rw = P + (c + 1 + t) * ldp;
         const double lr = rw[k + c] * inv;
         for (int j = lane; j < W; j += 32)
@@ -860,30 +862,28 @@ __global__ void __launch_bounds__(256) merge_m2_kernel(DevPlan p, const DevUpper
       }
     }
     __syncthreads();
-    // F3: trailing rows: P[r][j] -= sum_h X_b[h][k + r] X_b[h][j]
-    const int nrt = (ngp - r0 - NB) / 16;
-    const int nct = (W + 15) / 16;
-    for (int t = warp; t < nrt * nct; t += 8) {
-      const int rt = r0 + NB + (t / nct) * 16;
-      const int c0 = (t % nct) * 16;
-      if (c0 >= k && c0 + 16 <= k + r0 + NB) continue;
-      double acc[2][2][2] = {};
-      warp_gemm_tn<2, 2>(acc, P + r0 * ldp + k, ldp, rt, P + r0 * ldp, ldp, c0, NB);
+    // trailing rows r >= r0+NB:  P[r][j] -= sum_h X_b[h][k + r] X_b[h][j]   (DMMA, 8 x 32 tiles)
+    const int nrt = (ngp - r0 - NB) / 8;
+    const int nct = (W + 31) / 32;
+    for (int t = warp; t < nrt * nct; t += NWp) {
+      const int rt = r0 + NB + (t / nct) * 8;
+      const int c0 = (t % nct) * 32;
+      if (c0 >= k && c0 + 32 <= k + r0 + NB) continue;
+      double acc[1][4][2] = {};
+      warp_gemm_tn<1, 4>(acc, P + r0 * ldp + k, ldp, rt, P + r0 * ldp, ldp, c0, NB);
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int col = c0 + 8 * j + 2 * gq + e;
-            if (col < W) P[(rt + 8 * i + gr) * ldp + col] -= acc[i][j][e];
-          }
+        for (int e = 0; e < 2; ++e) {
+          const int col = c0 + 8 * j + 2 * gq + e;
+          if (col < W) P[(rt + gr) * ldp + col] -= acc[0][j][e];
+        }
     }
-    __syncthreads();
   }
+  __syncthreads();
   if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
   double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
-  for (int c = 1 + tid; c < nc; c += 256) {
+  for (int c = 1 + tid; c < nc; c += NT) {
     double v = out[size_t(k) * U.out_ld + c];
     for (int g = 0; g < ng; ++g) v = fma(P[g * ldp + Kp], P[g * ldp + Kp + c], v);
     out[size_t(k) * U.out_ld + c] = v;
@@ -994,15 +994,10 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
   if (e != cudaSuccess) return e;
   dim3 grid(B, n_nodes);
   if (tier == 0) {
-    if (nb == 16) {
-      e = cudaFuncSetAttribute(merge_m2_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      if (e != cudaSuccess) return e;
-      merge_m2_kernel<16><<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride);
-    } else {
-      e = cudaFuncSetAttribute(merge_m2_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      if (e != cudaSuccess) return e;
-      merge_m2_kernel<32><<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride);
-    }
+    e = cudaFuncSetAttribute(merge_m2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    const int nthr = smem > 100 * 1024 ? 512 : 256;
+    merge_m2_kernel<8><<<grid, nthr, smem, s>>>(p, nodes_dev, ws, ws_stride);
   } else {
     const size_t sm = merge_l_smem_bytes();
     e = cudaFuncSetAttribute(merge_l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
