@@ -156,6 +156,10 @@ int hdd_leaf_template(int32_t r, int32_t* K, int32_t* k, int32_t* ng,
 int hdd_debug_node_output(HddPlan* plan, int32_t idx, int32_t b,
                           double* psi, double* R, double* sigma);
 
+/* Profiling hook: clock64 stamps of leaf CTA (0,0) of the last launch
+ * ([0] start, [1] after the register base, [10 + 8 (5-r) + phase] per level). */
+int hdd_debug_leaf_clocks(long long* out64);
+
 const char* hdd_version(void);
 
 #ifdef __cplusplus

@@ -293,6 +293,8 @@ static int setup_device(HddPlan* pl, int max_batch) {
 
 extern "C" {
 
+int hdd_debug_leaf_clocks(long long* out) { return read_leaf_clocks(out); }
+
 const char* hdd_version(void) { return "hdd_b200 0.1 (sm_100a)"; }
 
 int hdd_create_error(HddError* out) {

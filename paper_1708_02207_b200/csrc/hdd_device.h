@@ -84,5 +84,6 @@ size_t merge_l_smem_bytes();
 cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cudaStream_t s);
 size_t leaf_smem_bytes(int leaf_cols);
 int upload_leaf_template();
+int read_leaf_clocks(long long* out);
 
 }  // namespace hdd

@@ -109,6 +109,28 @@ __constant__ LeafTmplDev c_tmpl;
 __constant__ int16_t c_map[2][256];
 __constant__ uint16_t c_orig[512];   // in-leaf node origin (x | y << 8), index 2^r - 1 + q
 
+// Precomputed per-level gather programs of the leaf kernel (one set per column
+// class NC = 2, 4, 8): every panel / update item of level r knows its source
+// offsets in the two sons' packed blocks, so the kernel does no index decoding.
+struct LeafItemP { int16_t o1, o2, c, pad; };     // panel item t = g * W + j
+struct LeafItemU { int16_t a, bx, o1, o2; };      // update item: row a, X column bx
+struct LeafTabDev {
+  const LeafItemP* P[3];
+  const LeafItemU* U[3];
+  int poff[3][6];
+  int uoff[3][6];
+};
+__constant__ LeafTabDev c_ltab;
+
+// per-phase clock64 stamps of CTA (0,0) of the last leaf launch (profiling hook)
+__device__ long long g_leaf_clk[64];
+#define LEAF_TICK(i) \
+  do { if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) g_leaf_clk[i] = clock64(); } while (0)
+int read_leaf_clocks(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_leaf_clk, sizeof(long long) * 64) == cudaSuccess ? 0 : -1;
+}
+
+
 int upload_leaf_template() {
   const auto& T = leaf_template();
   LeafTmplDev t{};
@@ -139,6 +161,66 @@ int upload_leaf_template() {
       }
       orig[(1 << r) - 1 + q] = uint16_t(x | (y << 8));
     }
+  }
+  {
+    static bool built = false;
+    static LeafTabDev tab{};
+    if (!built) {
+      for (int ci = 0; ci < 3; ++ci) {
+        const int NC = ci == 0 ? 2 : (ci == 1 ? 4 : 8);
+        std::vector<LeafItemP> vp;
+        std::vector<LeafItemU> vu;
+        for (int r = 0; r < 6; ++r) {
+          const LeafLevel& L = T[r];
+          const int K = L.K, k = L.k, ng = L.ng, ks = L.kson;
+          const int W = K + NC;
+          auto tri_h = [](int a) { return a * (a + 1) / 2; };
+          auto symoff = [&](int i, int j) { return i >= j ? tri_h(i) + j : tri_h(j) + i; };
+          const int zs = tri_h(ks) + ks * NC + NC;   // son zero slot
+          tab.poff[ci][r] = int(vp.size());
+          for (int g = 0; g < ng; ++g)
+            for (int j = 0; j < W; ++j) {
+              const int a = k + g;
+              LeafItemP it{int16_t(zs), int16_t(zs), -1, 0};
+              if (j < K) {
+                if (L.map1[a] >= 0 && L.map1[j] >= 0) it.o1 = int16_t(symoff(L.map1[a], L.map1[j]));
+                if (L.map2[a] >= 0 && L.map2[j] >= 0) it.o2 = int16_t(symoff(L.map2[a], L.map2[j]));
+              } else {
+                const int c = j - K;
+                it.c = int16_t(c);
+                if (L.map1[a] >= 0) it.o1 = int16_t(tri_h(ks) + L.map1[a] * NC + c);
+                if (L.map2[a] >= 0) it.o2 = int16_t(tri_h(ks) + L.map2[a] * NC + c);
+              }
+              vp.push_back(it);
+            }
+          tab.uoff[ci][r] = int(vu.size());
+          for (int a = 0; a < k; ++a)
+            for (int b = 0; b <= a; ++b) {
+              LeafItemU it{int16_t(a), int16_t(b), int16_t(zs), int16_t(zs)};
+              if (L.map1[a] >= 0 && L.map1[b] >= 0) it.o1 = int16_t(symoff(L.map1[a], L.map1[b]));
+              if (L.map2[a] >= 0 && L.map2[b] >= 0) it.o2 = int16_t(symoff(L.map2[a], L.map2[b]));
+              vu.push_back(it);
+            }
+          for (int a = 0; a < k; ++a)
+            for (int c = 0; c < NC; ++c) {
+              LeafItemU it{int16_t(a), int16_t(k + c), int16_t(zs), int16_t(zs)};
+              if (L.map1[a] >= 0) it.o1 = int16_t(tri_h(ks) + L.map1[a] * NC + c);
+              if (L.map2[a] >= 0) it.o2 = int16_t(tri_h(ks) + L.map2[a] * NC + c);
+              vu.push_back(it);
+            }
+        }
+        void* dp = nullptr;
+        void* du = nullptr;
+        if (cudaMalloc(&dp, vp.size() * sizeof(LeafItemP)) != cudaSuccess) return -1;
+        if (cudaMalloc(&du, vu.size() * sizeof(LeafItemU)) != cudaSuccess) return -1;
+        cudaMemcpy(dp, vp.data(), vp.size() * sizeof(LeafItemP), cudaMemcpyHostToDevice);
+        cudaMemcpy(du, vu.data(), vu.size() * sizeof(LeafItemU), cudaMemcpyHostToDevice);
+        tab.P[ci] = static_cast<const LeafItemP*>(dp);
+        tab.U[ci] = static_cast<const LeafItemU*>(du);
+      }
+      built = true;
+    }
+    if (cudaMemcpyToSymbol(c_ltab, &tab, sizeof(tab)) != cudaSuccess) return -1;
   }
   if (cudaMemcpyToSymbol(c_tmpl, &t, sizeof(t)) != cudaSuccess) return -1;
   if (cudaMemcpyToSymbol(c_map, maps, sizeof(maps)) != cudaSuccess) return -1;
@@ -171,8 +253,8 @@ static void leaf_sizes(int ncl, int* bufd, int* pand) {
   int mb = 0, mp = 0;
   for (int r = 0; r < kLeafLevels; ++r) {
     int nf = 1 << r, k = T[r].k, K = T[r].K, ng = T[r].ng;
-    if (r >= 1) mb = std::max(mb, nf * (k * (k + 1) / 2 + k * ncl + ncl));
-    mp = std::max(mp, nf * ng * ((K + ncl) + (k + ncl) + ng));
+    if (r >= 1) mb = std::max(mb, nf * (k * (k + 1) / 2 + k * ncl + ncl + 2));
+    mp = std::max(mp, nf * ng * ((K + ncl) + (k + ncl) + 2 * ng));
   }
   *bufd = (mb + 1) & ~1;
   *pand = (mp + 1) & ~1;
@@ -200,8 +282,8 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
   constexpr LeafLevelShape S = leaf_shape(R);
   constexpr int K = S.K, k = S.k, ng = S.ng, ks = S.ks;
   constexpr int nf = 1 << R;
-  constexpr int Sin = ctri(ks) + ks * NC + NC;
-  constexpr int Sout = ctri(k) + k * NC + NC;
+  constexpr int Sin = ctri(ks) + ks * NC + NC + 2;    // +2: zero slot at [Sin - 2] (even stride)
+  constexpr int Sout = ctri(k) + k * NC + NC + 2;
   constexpr int W = K + NC;
   constexpr int WX = k + NC;
   constexpr int NW = 8, NT = 256;
@@ -219,183 +301,148 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
   double* Xp = pan + nf * ng * W;
   double* Lp = Xp + nf * ng * WX;
 
-  // ---- A: gather the interface panel [A21 | A22 | R_gamma] and sigma~ ----
-  for (int q = warp / gsz; q < nf; q += qstep) {
-    const double* s1 = in + (2 * q) * Sin;
-    const double* s2 = in + (2 * q + 1) * Sin;
-    double* P = Pp + q * ng * W;
-    for (int t = sub * 32 + lane; t < ng * W; t += gsz * 32) {
-      const int g = t / W, j = t - g * W;
-      const int a = k + g;
-      const int pa1 = m1[a], pa2 = m2[a];
-      double v = 0.0;
-      if (j < K) {
-        const int pb1 = m1[j], pb2 = m2[j];
-        if (pa1 >= 0 && pb1 >= 0) v += sym(s1, pa1, pb1);
-        if (pa2 >= 0 && pb2 >= 0) v += sym(s2, pa2, pb2);
-      } else {
-        const int c = j - K;
-        const double cf = ctype[c] == 1 ? 0.5 : 1.0;
-        if (pa1 >= 0) v += cf * s1[ctri(ks) + pa1 * NC + c];
-        if (pa2 >= 0) v += cf * s2[ctri(ks) + pa2 * NC + c];
-        if (br[c] == R && bq[c] == q && bg[c] == g) v += 1.0;
-      }
-      P[t] = v;
-    }
-  }
-  __syncthreads();
-  // ---- B: Cholesky of A22 and its inverse Linv ----
-  if constexpr (ng <= 3) {
-    for (int q = tid; q < nf; q += NT) {
-      const double* P = Pp + q * ng * W;
-      double l[ng][ng], li[ng][ng];
-#pragma unroll
-      for (int c = 0; c < ng; ++c) {
-#pragma unroll
-        for (int r2 = c; r2 < ng; ++r2) {
-          double v = P[r2 * W + k + c];
-#pragma unroll
-          for (int h = 0; h < c; ++h) v = fma(-l[r2][h], l[c][h], v);
-          if (r2 == c) {
-            if (!(v > 0.0)) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(leaf_ref, R, q));
-            l[c][c] = sqrt(v);
-          } else {
-            l[r2][c] = v / l[c][c];
-          }
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < ng; ++c)
-#pragma unroll
-        for (int r2 = 0; r2 < ng; ++r2) {
-          if (r2 < c) { li[r2][c] = 0.0; continue; }
-          double v = r2 == c ? 1.0 : 0.0;
-#pragma unroll
-          for (int h = c; h < r2; ++h) v = fma(-l[r2][h], li[h][c], v);
-          li[r2][c] = v / l[r2][r2];
-        }
-      double* Li = Lp + q * ng * ng;
-#pragma unroll
-      for (int a = 0; a < ng; ++a)
-#pragma unroll
-        for (int b = 0; b < ng; ++b) Li[a * ng + b] = li[a][b];
-    }
-  } else {
-    for (int q = warp; q < nf; q += NW) {
+  // ---- A: gather the interface panel [A21 | A22 | R_gamma] (precomputed program) ----
+  constexpr int CI = NC == 2 ? 0 : (NC == 4 ? 1 : 2);
+  {
+    const LeafItemP* prog = c_ltab.P[CI] + c_ltab.poff[CI][R];
+    for (int q = warp / gsz; q < nf; q += qstep) {
+      const double* s1 = in + (2 * q) * Sin;
+      const double* s2 = in + (2 * q + 1) * Sin;
       double* P = Pp + q * ng * W;
-      for (int c = 0; c < ng; ++c) {
-        const double d = P[c * W + k + c];
-        if (!(d > 0.0) && lane == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(leaf_ref, R, q));
-        const double l = sqrt(d), inv = 1.0 / l;
-        __syncwarp();
-        if (lane > c && lane < ng) P[lane * W + k + c] *= inv;
-        if (lane == 0) P[c * W + k + c] = l;
-        __syncwarp();
-        constexpr int rem_max = ng;
-        (void)rem_max;
-        const int rem = ng - c - 1;
-        for (int t = lane; t < rem * rem; t += 32) {
-          const int i1 = c + 1 + t / rem, i2 = c + 1 + t % rem;
-          if (i2 <= i1) P[i1 * W + k + i2] = fma(-P[i1 * W + k + c], P[i2 * W + k + c], P[i1 * W + k + i2]);
-        }
-        __syncwarp();
-      }
-      // Linv column `lane`
-      double* Li = Lp + q * ng * ng;
-      if (lane < ng) {
-        const int c = lane;
-        double x[ng];
-#pragma unroll
-        for (int r2 = 0; r2 < ng; ++r2) {
-          if (r2 < c) { x[r2] = 0.0; continue; }
-          double v = r2 == c ? 1.0 : 0.0;
-#pragma unroll
-          for (int h = 0; h < r2; ++h)
-            if (h >= c) v = fma(-P[r2 * W + k + h], x[h], v);
-          x[r2] = v / P[r2 * W + k + r2];
-        }
-#pragma unroll
-        for (int r2 = 0; r2 < ng; ++r2) Li[r2 * ng + c] = x[r2];
+      for (int t = sub * 32 + lane; t < ng * W; t += gsz * 32) {
+        const LeafItemP it = prog[t];
+        double v = s1[it.o1] + s2[it.o2];
+        if (it.c >= 0 && br[it.c] == R && bq[it.c] == q && bg[it.c] == t / W) v += 1.0;
+        P[t] = v;
       }
     }
   }
   __syncthreads();
-  // ---- C: X = Linv [A21 | R_gamma]  (all threads, no serial chains) ----
+  LEAF_TICK(10 + 8 * (5 - R) + 0);
+  // ---- B: M = A22^-1 for every node by in-place Gauss-Jordan, all threads ----
+  // (symmetric positive definite: no pivoting; a non-positive pivot is a
+  // NumericalError exactly like the reference's failed Cholesky)
+  {
+    double* M0 = Lp;                     // [nf][ng][ng] ping
+    double* M1 = Lp + nf * ng * ng;      // pong
+    constexpr int NE = nf * ng * ng;
+    for (int t = tid; t < NE; t += NT) {
+      const int q = t / (ng * ng), e = t - q * ng * ng;
+      const int i = e / ng, j = e - i * ng;
+      M0[t] = Pp[q * ng * W + i * W + k + j];
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int pv = 0; pv < ng; ++pv) {
+      const double* Mi = (pv & 1) ? M1 : M0;
+      double* Mo = (pv & 1) ? M0 : M1;
+      for (int t = tid; t < NE; t += NT) {
+        const int q = t / (ng * ng), e = t - q * ng * ng;
+        const int i = e / ng, j = e - i * ng;
+        const double* m = Mi + q * ng * ng;
+        const double d = m[pv * ng + pv];
+        const double rd = __drcp_rn(d);
+        double v;
+        if (i == pv && j == pv) {
+          if (!(d > 0.0)) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(leaf_ref, R, q));
+          v = rd;
+        } else if (i == pv) {
+          v = m[pv * ng + j] * rd;
+        } else if (j == pv) {
+          v = -m[i * ng + pv] * rd;
+        } else {
+          v = fma(-m[i * ng + pv], m[pv * ng + j] * rd, m[i * ng + j]);
+        }
+        Mo[t] = v;
+      }
+      __syncthreads();
+    }
+    if ((ng & 1) == 1) {   // result in M1: copy back to M0
+      for (int t = tid; t < NE; t += NT) M0[t] = M1[t];
+    }
+  }
+  __syncthreads();
+  LEAF_TICK(10 + 8 * (5 - R) + 1);
+  // ---- C: Y = M [A21 | R_gamma] ----
   for (int q = warp / gsz; q < nf; q += qstep) {
     const double* P = Pp + q * ng * W;
-    const double* Li = Lp + q * ng * ng;
-    double* X = Xp + q * ng * WX;
+    const double* Mq = Lp + q * ng * ng;
+    double* Y = Xp + q * ng * WX;
     for (int t = sub * 32 + lane; t < ng * WX; t += gsz * 32) {
       const int g = t / WX, jj = t - g * WX;
       const int j = jj < k ? jj : K + (jj - k);
       double v = 0.0;
 #pragma unroll
-      for (int h = 0; h < ng; ++h)
-        if (h <= g) v = fma(Li[g * ng + h], P[h * W + j], v);
-      X[t] = v;
+      for (int h = 0; h < ng; ++h) v = fma(Mq[g * ng + h], P[h * W + j], v);
+      Y[t] = v;
     }
   }
   __syncthreads();
-  // ---- D: streamed Schur update out = A~ - X^T [X | V]; sigma += V0 . V ----
+  LEAF_TICK(10 + 8 * (5 - R) + 2);
+  // ---- D: streamed Schur update out = A~ - A21^T Y; sigma += R_g0^T Y_R ----
   constexpr int E = ctri(k) + k * NC;
+  const LeafItemU* uprog = c_ltab.U[CI] + c_ltab.uoff[CI][R];
+  constexpr int UN = 4;    // independent items per thread per iteration (ILP)
+  const double inv_area = 1.0 / (double(kLeafCells * kLeafCells) * p.h * p.h);   // exact power of two
   for (int q = warp / gsz; q < nf; q += qstep) {
     const double* s1 = in + (2 * q) * Sin;
     const double* s2 = in + (2 * q + 1) * Sin;
-    const double* X = Xp + q * ng * WX;
+    const double* P = Pp + q * ng * W;
+    const double* Y = Xp + q * ng * WX;
     double* o = out + q * Sout;
     double* gdst = nullptr;
     if constexpr (R == 0)
       gdst = p.buf[p.leaf_buf] + int64_t(leaf) * p.leaf_elems * p.bcap + int64_t(s) * p.leaf_elems;
-    for (int t = sub * 32 + lane; t < E; t += gsz * 32) {
-      int a, b, c = -1;
-      if (t < ctri(k)) {
-        a = int((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-        if (ctri(a + 1) <= t) ++a;
-        if (ctri(a) > t) --a;
-        b = t - ctri(a);
-      } else {
-        a = (t - ctri(k)) / NC;
-        c = t - ctri(k) - a * NC;
-        b = k + c;
-      }
-      const int pa1 = m1[a], pa2 = m2[a];
-      double v = 0.0;
-      if (c < 0) {
-        // perimeter maps are monotone, so b <= a implies m(b) <= m(a)
-        const int pb1 = m1[b], pb2 = m2[b];
-        if (pa1 >= 0 && pb1 >= 0) v += s1[ctri(pa1) + pb1];
-        if (pa2 >= 0 && pb2 >= 0) v += s2[ctri(pa2) + pb2];
-      } else {
-        const double cf = ctype[c] == 1 ? 0.5 : 1.0;
-        if (pa1 >= 0) v += cf * s1[ctri(ks) + pa1 * NC + c];
-        if (pa2 >= 0) v += cf * s2[ctri(ks) + pa2 * NC + c];
+    const int stride = gsz * 32;
+    for (int t0 = sub * 32 + lane; t0 < E; t0 += UN * stride) {
+      LeafItemU it[UN];
+      double v[UN];
+#pragma unroll
+      for (int u = 0; u < UN; ++u) {
+        const int t = t0 + u * stride;
+        it[u] = t < E ? uprog[t] : LeafItemU{0, 0, int16_t(Sin - 2), int16_t(Sin - 2)};
       }
 #pragma unroll
-      for (int g = 0; g < ng; ++g) v = fma(-X[g * WX + a], X[g * WX + b], v);
-      if constexpr (R > 0) {
-        o[t] = v;
-      } else {
-        const int ld = p.leaf_ld;
-        if (c < 0) {
-          gdst[a * ld + b] = v;
-          gdst[b * ld + a] = v;
-        } else if (c < p.leaf_cols) {
-          gdst[a * ld + kLeafPerim + c] = v;
+      for (int u = 0; u < UN; ++u) v[u] = s1[it[u].o1] + s2[it[u].o2];
+#pragma unroll
+      for (int g = 0; g < ng; ++g)
+#pragma unroll
+        for (int u = 0; u < UN; ++u) v[u] = fma(-P[g * W + it[u].a], Y[g * WX + it[u].bx], v[u]);
+#pragma unroll
+      for (int u = 0; u < UN; ++u) {
+        const int t = t0 + u * stride;
+        if (t >= E) continue;
+        const int a = it[u].a, bx = it[u].bx;
+        if constexpr (R > 0) {
+          o[t] = v[u];
+        } else {
+          const int ld = p.leaf_ld;
+          if (bx < k) {
+            gdst[a * ld + bx] = v[u];
+            gdst[bx * ld + a] = v[u];
+          } else if (bx - k < p.leaf_cols) {
+            const double sc = ctype[bx - k] == 1 ? inv_area : 1.0;
+            gdst[a * ld + kLeafPerim + (bx - k)] = v[u] * sc;
+          }
         }
       }
     }
     if (sub == 0 && lane < NC) {
       const int c = lane;
-      const double cf = ctype[c] == 1 ? 0.5 : 1.0;
-      double sg = cf * s1[ctri(ks) + ks * NC + c] + cf * s2[ctri(ks) + ks * NC + c];
+      double sg = s1[ctri(ks) + ks * NC + c] + s2[ctri(ks) + ks * NC + c];
       if (c >= 1)
 #pragma unroll
-        for (int g = 0; g < ng; ++g) sg = fma(X[g * WX + k], X[g * WX + k + c], sg);
-      if constexpr (R > 0) o[ctri(k) + k * NC + c] = sg;
-      else if (c < p.leaf_cols) gdst[kLeafPerim * p.leaf_ld + c] = sg;
+        for (int g = 0; g < ng; ++g) sg = fma(P[g * W + K], Y[g * WX + k + c], sg);
+      if constexpr (R > 0) {
+        o[ctri(k) + k * NC + c] = sg;
+        if (c < 2) o[Sout - 2 + c] = 0.0;    // zero slot
+      } else if (c < p.leaf_cols) {
+        gdst[kLeafPerim * p.leaf_ld + c] = sg * (ctype[c] == 1 ? inv_area : 1.0);
+      }
     }
   }
   __syncthreads();
+  LEAF_TICK(10 + 8 * (5 - R) + 3);
 }
 
 // One CTA per (16x16-cell leaf, sample).  Level 6 (2x2-cell blocks) is built
@@ -407,6 +454,7 @@ template <int NC>
 __global__ void __launch_bounds__(256, 2) leaf2_kernel(DevPlan p, const int* __restrict__ order, int bufd, int pand) {
   extern __shared__ __align__(16) double sm[];
   const int leaf = order[blockIdx.x], s = blockIdx.y;
+  LEAF_TICK(0);
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NW = 8, NT = 256;
@@ -448,7 +496,7 @@ __global__ void __launch_bounds__(256, 2) leaf2_kernel(DevPlan p, const int* __r
   // ---------------- level 6: 2x2-cell blocks in registers ----------------
   {
     constexpr int k6 = 8;
-    const int S6 = tri(k6) + k6 * NC + NC;
+    const int S6 = tri(k6) + k6 * NC + NC + 2;
     for (int q = tid; q < 64; q += NT) {
       const int o = c_orig[63 + q];
       const int x0 = o & 255, y0 = o >> 8;
@@ -484,8 +532,9 @@ __global__ void __launch_bounds__(256, 2) leaf2_kernel(DevPlan p, const int* __r
           } else {
             rl[a] += w2; rl[b] += h2_6; rl[c] += h2_6; rl[d] += w2;
           }
-          rm[a] += 0.25 * (1.0 / 3.0); rm[b] += 0.25 * (1.0 / 6.0);
-          rm[c] += 0.25 * (1.0 / 6.0); rm[d] += 0.25 * (1.0 / 3.0);
+          // mean column carried as the area integral (coefficient 1 at every
+          // in-leaf merge); rescaled by 1/|leaf| at the leaf output
+          rm[a] += w2; rm[b] += h2_6; rm[c] += h2_6; rm[d] += w2;
         }
       // eliminate the centre node 4
       const double dpiv = A[tri(4) + 4];
@@ -518,10 +567,13 @@ __global__ void __launch_bounds__(256, 2) leaf2_kernel(DevPlan p, const int* __r
         }
 #pragma unroll
       for (int c = 0; c < NC; ++c) out[tri(k6) + k6 * NC + c] = c == 0 ? 0.0 : v[0] * v[c];
+      out[S6 - 2] = 0.0;
+      out[S6 - 1] = 0.0;
     }
   }
   __syncthreads();
 
+  LEAF_TICK(1);
   // ---------------- levels 5..0 in shared memory ----------------
   leaf_level<5, NC>(p, bufA, bufB, pan, mp, cinfo, leaf, s, L.ref_id);
   leaf_level<4, NC>(p, bufB, bufA, pan, mp, cinfo, leaf, s, L.ref_id);
@@ -529,6 +581,7 @@ __global__ void __launch_bounds__(256, 2) leaf2_kernel(DevPlan p, const int* __r
   leaf_level<2, NC>(p, bufB, bufA, pan, mp, cinfo, leaf, s, L.ref_id);
   leaf_level<1, NC>(p, bufA, bufB, pan, mp, cinfo, leaf, s, L.ref_id);
   leaf_level<0, NC>(p, bufB, bufA, pan, mp, cinfo, leaf, s, L.ref_id);
+  LEAF_TICK(63);
 }
 
 cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_out) {

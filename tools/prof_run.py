@@ -28,3 +28,13 @@ for it in range(2):
 torch.cuda.synchronize()
 names = ["kappa", "leaf"] + [f"merge_d{d}" for d in range(info.leaf_depth - 1, -1, -1)] + ["finalize"]
 print(name, B, {n: round(float(v), 3) for n, v in zip(names, st)}, "total", round(float(st.sum()), 3))
+clk = (C.c_longlong * 64)()
+plan.lib.hdd_debug_leaf_clocks(clk)
+c = [int(v) for v in clk]
+print("leaf CTA(0,0) clocks: base", c[1] - c[0])
+for r in range(5, -1, -1):
+    base = 10 + 8 * (5 - r)
+    prev = c[1] if r == 5 else c[10 + 8 * (5 - (r + 1)) + 3]
+    ph = [c[base + i] - (prev if i == 0 else c[base + i - 1]) for i in range(4)]
+    print(f"  level {r}: A {ph[0]}  B {ph[1]}  C {ph[2]}  D {ph[3]}")
+print("  total", c[63] - c[0])
