@@ -74,6 +74,10 @@ typedef struct {
   int32_t max_batch;       /* samples per internal sub-batch (0 = auto)       */
   int32_t device;          /* CUDA device, -1 = host-only plan (tests)        */
   int32_t keep_nodes;      /* 1 = keep every depth's outputs (debug hooks)    */
+  int32_t mode;            /* -1 auto, 0 adjoint (all functionals carried to
+                              the root, functionals.py:138-224), 1 primal
+                              (points by the top-down interface back-solve,
+                              hdd.py:397-432, restricted to what F needs)     */
 } HddPlanDesc;
 
 typedef struct {
@@ -88,6 +92,7 @@ typedef struct {
   int32_t n_upper, n_leaves, n_obs, leaf_cols;
   int32_t max_batch, n_kernels_per_batch;
   int64_t workspace_bytes;
+  int32_t mode;
 } HddPlanInfo;
 
 typedef struct {
@@ -110,9 +115,12 @@ typedef struct {
 } HddLeafInfo;
 
 typedef struct {
-  int32_t kind;            /* 0 = root column, 1 = constant                   */
+  int32_t kind;            /* 0 root column, 1 constant, 2 leaf point (primal),
+                              3 interface point (primal)                       */
   int32_t col;
   double value;
+  int32_t node;            /* leaf (kind 2) / upper node (kind 3) plan index  */
+  int32_t slot;
 } HddObsInfo;
 
 int hdd_plan_create(const HddPlanDesc* desc, HddPlan** out);

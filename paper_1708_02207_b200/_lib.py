@@ -35,6 +35,7 @@ class HddPlanDesc(C.Structure):
         ("n_obs", C.c_int32), ("obs_kind", _i32p), ("obs_id", _i64p),
         ("sigma", _f64p), ("y", _f64p),
         ("max_batch", C.c_int32), ("device", C.c_int32), ("keep_nodes", C.c_int32),
+        ("mode", C.c_int32),
     ]
 
 
@@ -47,7 +48,7 @@ class HddPlanInfo(C.Structure):
     _fields_ = [("level", C.c_int32), ("n_cells", C.c_int32), ("leaf_cells", C.c_int32),
                 ("leaf_depth", C.c_int32), ("n_upper", C.c_int32), ("n_leaves", C.c_int32),
                 ("n_obs", C.c_int32), ("leaf_cols", C.c_int32), ("max_batch", C.c_int32),
-                ("n_kernels_per_batch", C.c_int32), ("workspace_bytes", C.c_int64)]
+                ("n_kernels_per_batch", C.c_int32), ("workspace_bytes", C.c_int64), ("mode", C.c_int32)]
 
 
 class HddNodeInfo(C.Structure):
@@ -64,7 +65,8 @@ class HddLeafInfo(C.Structure):
 
 
 class HddObsInfo(C.Structure):
-    _fields_ = [("kind", C.c_int32), ("col", C.c_int32), ("value", C.c_double)]
+    _fields_ = [("kind", C.c_int32), ("col", C.c_int32), ("value", C.c_double), ("node", C.c_int32),
+                ("slot", C.c_int32)]
 
 
 EXPORTS = {

@@ -217,7 +217,8 @@ def mean_observations(tree: DDTree, depth: int):
 class _Plan:
     """Owns one HddPlan* (device tables + workspace)."""
 
-    def __init__(self, problem: "BayesProblem", device: int, max_batch: int, keep_nodes: bool = False):
+    def __init__(self, problem: "BayesProblem", device: int, max_batch: int, keep_nodes: bool = False,
+                 mode: int = -1):
         L = _lib.lib()
         mesh = problem.tree.mesh
         param = problem.param
@@ -243,7 +244,7 @@ class _Plan:
             sx=ptr(k["sx"], _lib._f64p), sy=ptr(k["sy"], _lib._f64p), coef=ptr(k["coef"], _lib._f64p),
             f=ptr(k["f"], _lib._f64p), n_obs=len(obs), obs_kind=ptr(k["kind"], _lib._i32p),
             obs_id=ptr(k["ids"], _lib._i64p), sigma=ptr(k["sigma"], _lib._f64p), y=ptr(k["y"], _lib._f64p),
-            max_batch=int(max_batch), device=int(device), keep_nodes=int(keep_nodes))
+            max_batch=int(max_batch), device=int(device), keep_nodes=int(keep_nodes), mode=int(mode))
         h = C.c_void_p()
         rc = L.hdd_plan_create(C.byref(desc), C.byref(h))
         if rc != _lib.HDD_OK:
@@ -297,6 +298,7 @@ class BayesProblem:
     forward_calls: int = 0
     device: int = 0
     max_batch: int = 0
+    mode: int = -1          # -1 auto, 0 adjoint functionals, 1 primal top-down for points
     _plan: object = field(default=None, repr=False)
 
     def __post_init__(self):
@@ -315,7 +317,7 @@ class BayesProblem:
 
     def plan(self) -> _Plan:
         if self._plan is None:
-            self._plan = _Plan(self, self.device, self.max_batch)
+            self._plan = _Plan(self, self.device, self.max_batch, mode=self.mode)
         return self._plan
 
 

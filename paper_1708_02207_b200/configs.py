@@ -80,7 +80,8 @@ def observed_data(cfg: Config):
     return y, sigma
 
 
-def make_problem(name: str, device: int = 0, max_batch: int = 0, with_data: bool = True) -> BayesProblem:
+def make_problem(name: str, device: int = 0, max_batch: int = 0, with_data: bool = True,
+                 mode: int = -1) -> BayesProblem:
     cfg = CONFIGS[name]
     mesh = build_mesh(cfg.level)
     tree = build_tree(mesh)
@@ -91,4 +92,4 @@ def make_problem(name: str, device: int = 0, max_batch: int = 0, with_data: bool
         y, sigma = None, np.full(len(obs), cfg.sigma)
     model = MeasurementModel(obs, sigma, y)
     return BayesProblem(tree, SineKLField(tree, cfg.n_z), np.ones(mesh.n_nodes), np.zeros(4 * mesh.n_cells),
-                        model, device=device, max_batch=max_batch)
+                        model, device=device, max_batch=max_batch, mode=mode)

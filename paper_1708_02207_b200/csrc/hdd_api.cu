@@ -30,7 +30,8 @@ struct HddPlan {
   std::vector<int> depth_tier;         // 0 = shared-memory panel, 1 = global panel
   std::vector<int64_t> depth_ws;       // panel doubles per (node, sample)
   std::vector<int> depth_rows;         // max k + ngp over the depth's nodes
-  std::vector<int> depth_nb;           // elimination block rows (16 or 32)
+  std::vector<int> depth_nb;           // elimination block rows (8 or 32)
+  std::vector<int> depth_kng;          // max k + 2 ng (top-down smem)
   double* ws = nullptr;                // tier-L workspace
   size_t leaf_smem = 0;
   HddError err{};
@@ -107,15 +108,27 @@ static int setup_device(HddPlan* pl, int max_batch) {
     d.j0 = L.j0;
     d.ncols = int(L.cols.size());
     d.ref_id = L.ref_id;
-    for (int c = 0; c < 16; ++c) { d.ctype[c] = 2; d.birth_r[c] = -1; d.birth_q[c] = -1; d.birth_g[c] = -1; }
+    for (int c = 0; c < 16; ++c) {
+      d.ctype[c] = 2; d.birth_r[c] = -1; d.birth_q[c] = -1; d.birth_g[c] = -1; d.fslot[c] = -1;
+    }
     for (int c = 0; c < d.ncols; ++c) {
       d.ctype[c] = L.cols[c].kind == COL_LOAD ? 0 : (L.cols[c].kind == COL_MEAN ? 1 : 2);
       d.birth_r[c] = L.birth[3 * c];
       d.birth_q[c] = L.birth[3 * c + 1];
       d.birth_g[c] = L.birth[3 * c + 2];
+      d.fslot[c] = c < int(L.fslot.size()) ? L.fslot[c] : -1;
     }
+    d.parent = L.parent;
   }
   if ((rc = upload(pl, dl, &D.leaves))) return rc;
+  {
+    std::vector<int32_t> lc;
+    for (const Leaf& L : P.leaves) {
+      if (L.cmap.empty()) lc.insert(lc.end(), kLeafPerim, -1);
+      else lc.insert(lc.end(), L.cmap.begin(), L.cmap.end());
+    }
+    if ((rc = upload(pl, lc, &D.leaf_cmap))) return rc;
+  }
   {
     std::vector<int32_t> order;
     for (int cls = 0; cls < 3; ++cls) {
@@ -130,8 +143,9 @@ static int setup_device(HddPlan* pl, int max_batch) {
     if ((rc = upload(pl, order, &D.leaf_order))) return rc;
   }
   // upper nodes
-  std::vector<int32_t> gmap, csrc, cbirth;
+  std::vector<int32_t> gmap, csrc, cbirth, cmapool;
   std::vector<double> ccoef;
+  pl->depth_kng.assign(P.upper_by_depth.size(), 0);
   pl->h_upper.resize(P.upper.size());
   pl->depth_smem.assign(P.upper_by_depth.size(), 0);
   pl->depth_tier.assign(P.upper_by_depth.size(), 0);
@@ -188,6 +202,12 @@ static int setup_device(HddPlan* pl, int max_batch) {
     }
     d.gmap_off = int(gmap.size());
     gmap.insert(gmap.end(), U.gmap.begin(), U.gmap.end());
+    d.parent = U.parent;
+    d.cmap_off = int(cmapool.size());
+    cmapool.insert(cmapool.end(), U.cmap.begin(), U.cmap.end());
+    d.fac_off = U.fac_off;
+    d.u_off = U.u_off;
+    pl->depth_kng[U.depth] = std::max(pl->depth_kng[U.depth], U.k + 2 * U.ng);
     d.col_off = int(cbirth.size());
     csrc.insert(csrc.end(), U.csrc.begin(), U.csrc.end());
     ccoef.insert(ccoef.end(), U.ccoef.begin(), U.ccoef.end());
@@ -199,25 +219,35 @@ static int setup_device(HddPlan* pl, int max_batch) {
   if ((rc = upload(pl, csrc, &D.csrc))) return rc;
   if ((rc = upload(pl, ccoef, &D.ccoef))) return rc;
   if ((rc = upload(pl, cbirth, &D.cbirth))) return rc;
+  if ((rc = upload(pl, cmapool, &D.cmap))) return rc;
   {
     const DevUpper* du = nullptr;
     if ((rc = upload(pl, pl->h_upper, &du))) return rc;
     pl->d_upper = const_cast<DevUpper*>(du);
+    D.upper = du;
   }
   // observations
-  std::vector<int32_t> rk, rcol;
+  std::vector<int32_t> rk, rcol, rnode, rslot;
   std::vector<double> rv;
   double llc = 0.0;
   for (size_t o = 0; o < P.route.size(); ++o) {
     rk.push_back(P.route[o].kind);
     rcol.push_back(P.route[o].col);
     rv.push_back(P.route[o].value);
+    rnode.push_back(P.route[o].node);
+    rslot.push_back(P.route[o].slot);
     llc += std::log(P.sigma[o] * std::sqrt(2.0 * M_PI));
   }
   D.ll_const = llc;
   if ((rc = upload(pl, rk, &D.route_kind))) return rc;
   if ((rc = upload(pl, rcol, &D.route_col))) return rc;
   if ((rc = upload(pl, rv, &D.route_val))) return rc;
+  if ((rc = upload(pl, rnode, &D.route_node))) return rc;
+  if ((rc = upload(pl, rslot, &D.route_slot))) return rc;
+  D.mode = P.mode;
+  D.fac_elems = P.fac_elems;
+  D.u_elems = P.u_elems;
+  D.n_fslots = P.n_fslots;
   if ((rc = upload(pl, P.sigma, &D.sigma))) return rc;
   D.y = nullptr;
   if (P.has_y && (rc = upload(pl, P.y, &D.y))) return rc;
@@ -228,6 +258,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
   for (size_t d = 0; d < P.upper_by_depth.size(); ++d)
     ws_per_sample = std::max<int64_t>(ws_per_sample, pl->depth_ws[d] * int64_t(P.upper_by_depth[d].size()));
   per_sample += ws_per_sample;
+  per_sample += P.fac_elems + P.u_elems + int64_t(P.n_fslots) * 65;
   int64_t bytes_per_sample = per_sample * 8;
   int bcap = max_batch;
   if (bcap <= 0) {
@@ -250,6 +281,18 @@ static int setup_device(HddPlan* pl, int max_batch) {
     }
     pl->allocs.push_back(p);
     D.buf[b] = static_cast<double*>(p);
+  }
+  D.fac = D.ubuf = D.fbuf = nullptr;
+  for (auto pr : {std::make_pair(&D.fac, P.fac_elems), std::make_pair(&D.ubuf, P.u_elems),
+                  std::make_pair(&D.fbuf, int64_t(P.n_fslots) * 65)}) {
+    if (pr.second <= 0) continue;
+    void* q = nullptr;
+    if (cudaMalloc(&q, size_t(pr.second) * bcap * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(&pl->err, HDD_ERR_NOMEM, "device allocation of the top-down buffers failed");
+    }
+    pl->allocs.push_back(q);
+    *pr.first = static_cast<double*>(q);
   }
   if (ws_per_sample > 0) {
     void* p = nullptr;
@@ -286,7 +329,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
   {
     int ncls = 0;
     for (int c = 0; c < 3; ++c) ncls += D.leaf_class_count[c] > 0;
-    pl->n_launches = 2 + ncls + 2 * int(P.upper_by_depth.size());
+    pl->n_launches = 2 + ncls + (2 + P.mode) * int(P.upper_by_depth.size());
   }
   return HDD_OK;
 }
@@ -360,6 +403,13 @@ static int run_sub_batch(HddPlan* pl, const double* Z, int B, double* S, double*
       CU(launch_merge(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->ws, pl->depth_ws[dep],
                       pl->depth_tier[dep], pl->depth_rows[dep], pl->depth_smem[dep], pl->depth_nb[dep], st));
     if (ev) CU(cudaEventRecord(ev[e++], st));
+  }
+  if (D.mode == 1) {
+    for (int dep = 0; dep < int(P.upper_by_depth.size()); ++dep) {
+      const auto& ids = P.upper_by_depth[dep];
+      if (!ids.empty())
+        CU(launch_topdown(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->depth_kng[dep], st));
+    }
   }
   CU(launch_finalize(D, B, S, ll, st));
   if (ev) CU(cudaEventRecord(ev[e++], st));
@@ -495,6 +545,7 @@ int hdd_plan_info(const HddPlan* pl, HddPlanInfo* out) {
   int64_t ws = int64_t(2) * P.N * P.N;
   for (int64_t e : P.buf_elems_per_sample) ws += e;
   out->workspace_bytes = ws * 8 * std::max(1, pl->bcap);
+  out->mode = P.mode;
   return HDD_OK;
 }
 
@@ -533,6 +584,8 @@ int hdd_plan_obs_info(const HddPlan* pl, int32_t idx, HddObsInfo* out) {
   out->kind = pl->plan.route[idx].kind;
   out->col = pl->plan.route[idx].col;
   out->value = pl->plan.route[idx].value;
+  out->node = pl->plan.route[idx].node;
+  out->slot = pl->plan.route[idx].slot;
   return HDD_OK;
 }
 

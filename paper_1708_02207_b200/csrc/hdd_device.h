@@ -20,6 +20,9 @@ struct DevUpper {
   int son_ld[2];
   int64_t son_elems[2], son_off[2];
   int gmap_off;            // offset into the gmap pool: [2][K]
+  int parent;              // upper index of the father, -1 root (primal)
+  int cmap_off;            // offset into the cmap pool: [k] father K-index of each boundary node
+  int64_t fac_off, u_off;  // per-sample offsets in the factor / interface-solution buffers
   int col_off;             // offset into column pools: csrc/ccoef [nc][2], cbirth [nc]
   int64_t ref_id;
 };
@@ -33,6 +36,8 @@ struct DevLeaf {
   // per column: coefficient type (0 = load, 1 = mean, 2 = point) and birth
   int ctype[16];
   int birth_r[16], birth_q[16], birth_g[16];
+  int fslot[16];           // primal: functional slot of a point column, -1
+  int parent;              // upper index of the father (-1 when the leaf is the root)
 };
 
 struct DevError {
@@ -62,6 +67,16 @@ struct DevPlan {
   const int32_t* route_kind;
   const int32_t* route_col;
   const double* route_val;
+  const int32_t* route_node;
+  const int32_t* route_slot;
+  int mode;                // 0 adjoint, 1 primal
+  int64_t fac_elems, u_elems;
+  int n_fslots;
+  double* fac;             // [bcap][fac_elems]  W | L^T | v rows of every upper node
+  double* ubuf;            // [bcap][u_elems]    u_K = [u_B | u_gamma] of every upper node
+  double* fbuf;            // [bcap][n_fslots][65] leaf point functionals
+  const int32_t* cmap;     // upper cmap pool
+  const int32_t* leaf_cmap;   // [n_leaves][64]
   const double* sigma;
   const double* y;         // nullptr = no likelihood
   double ll_const;         // sum log(sigma sqrt(2 pi))
@@ -81,6 +96,7 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
                          int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s);
 size_t merge_m2_smem_bytes(int ngp, int ldp);
 size_t merge_l_smem_bytes();
+cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_ng, cudaStream_t s);
 cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cudaStream_t s);
 size_t leaf_smem_bytes(int leaf_cols);
 int upload_leaf_template();

@@ -423,6 +423,8 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
           } else if (bx - k < p.leaf_cols) {
             const double sc = ctype[bx - k] == 1 ? inv_area : 1.0;
             gdst[a * ld + kLeafPerim + (bx - k)] = v[u] * sc;
+            const int fs = cinfo[4 * NC + (bx - k)];
+            if (fs >= 0) p.fbuf[(int64_t(s) * p.n_fslots + fs) * 65 + a] = v[u];
           }
         }
       }
@@ -438,6 +440,8 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
         if (c < 2) o[Sout - 2 + c] = 0.0;    // zero slot
       } else if (c < p.leaf_cols) {
         gdst[kLeafPerim * p.leaf_ld + c] = sg * (ctype[c] == 1 ? inv_area : 1.0);
+        const int fs = cinfo[4 * NC + c];
+        if (fs >= 0) p.fbuf[(int64_t(s) * p.n_fslots + fs) * 65 + 64] = sg;
       }
     }
   }
@@ -462,7 +466,7 @@ __global__ void __launch_bounds__(256, 2) leaf2_kernel(DevPlan p, const int* __r
   double* kap = sm;
   double* fl = kap + 512;
   int16_t* mp = reinterpret_cast<int16_t*>(fl + 296);          // [2][256]
-  int* cinfo = reinterpret_cast<int*>(fl + 296 + 128);           // ctype, br, bq, bg, ncols
+  int* cinfo = reinterpret_cast<int*>(fl + 296 + 128);           // ctype, br, bq, bg, fslot
   double* bufA = fl + 296 + 160;
   double* bufB = bufA + bufd;
   double* pan = bufB + bufd;
@@ -484,6 +488,7 @@ __global__ void __launch_bounds__(256, 2) leaf2_kernel(DevPlan p, const int* __r
       cinfo[NC + tid] = L.birth_r[tid];
       cinfo[2 * NC + tid] = L.birth_q[tid];
       cinfo[3 * NC + tid] = L.birth_g[tid];
+      cinfo[4 * NC + tid] = tid < L.ncols ? L.fslot[tid] : -1;
     }
   }
   __syncthreads();
@@ -935,6 +940,21 @@ __global__ void __launch_bounds__(512) merge_m2_kernel(DevPlan p, const DevUpper
   }
   __syncthreads();
   if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
+  if (p.mode == 1) {
+    // primal mode: keep [W | L^T | v] for the top-down back-solve (hdd.py:397-432)
+    const int fw = k + ng + 1;
+    double* F = p.fac + int64_t(s) * p.fac_elems + U.fac_off;
+    for (int t = tid; t < ng * fw; t += NT) {
+      const int g = t / fw, j = t - g * fw;
+      double v;
+      if (j < k) v = P[g * ldp + j];
+      else if (j < k + ng) {
+        const int jj = j - k;
+        v = jj < g ? 0.0 : (jj == g ? sqrt(P[g * ldp + k + g]) : P[g * ldp + k + jj]);
+      } else v = P[g * ldp + Kp];
+      F[t] = v;
+    }
+  }
   double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
   for (int c = 1 + tid; c < nc; c += NT) {
     double v = out[size_t(k) * U.out_ld + c];
@@ -971,9 +991,9 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
   for (int r0 = 0; r0 < ngp; r0 += kLB) {
     if (warp == 0) factor_diag_block<32>(P + int64_t(r0) * ldp + k + r0, ldp, LiT, &s_bad);
     __syncthreads();
-    // F2: X_b = L^-1 P_b in 64-column chunks
+    // F2: X_b = L^-1 P_b in 64-column chunks (the block's own A22 columns give L_bb^T)
     for (int c0 = 0; c0 < W; c0 += kLC) {
-      if (c0 >= k && c0 + kLC <= k + r0 + kLB) continue;
+      if (c0 >= k && c0 + kLC <= k + r0) continue;
       for (int t = tid; t < 32 * kLC; t += 256) {
         const int i = t >> 6, j = t & 63;
         const int col = c0 + j;
@@ -1030,6 +1050,18 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
     __syncthreads();
   }
   if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
+  if (p.mode == 1) {
+    const int fw = k + ng + 1;
+    double* F = p.fac + int64_t(s) * p.fac_elems + U.fac_off;
+    for (int t = tid; t < ng * fw; t += 256) {
+      const int g = t / fw, j = t - g * fw;
+      double v;
+      if (j < k) v = P[int64_t(g) * ldp + j];
+      else if (j < k + ng) { const int jj = j - k; v = jj < g ? 0.0 : P[int64_t(g) * ldp + k + jj]; }
+      else v = P[int64_t(g) * ldp + Kp];
+      F[t] = v;
+    }
+  }
   double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
   for (int c = 1 + tid; c < nc; c += 256) {
     double v = out[size_t(k) * U.out_ld + c];
@@ -1063,14 +1095,110 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
 // ---------------------------------------------------------------------------
 // K4: observations + Gaussian log-likelihood
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// K4 (primal): top-down interface back-solve restricted to what F needs
+// (root_to_leaves, hdd.py:397-432): u_gamma = L^-T (v - W u_B), one CTA per
+// (node, sample), depth by depth from the root.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) topdown_kernel(DevPlan p, const DevUpper* __restrict__ nodes) {
+  extern __shared__ __align__(16) double sm[];
+  const DevUpper& U = nodes[blockIdx.y];
+  const int s = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = U.k, ng = U.ng;
+  const int fw = k + ng + 1;
+  double* uB = sm;              // [k]
+  double* y = uB + k;           // [ng]
+  double* u = y + ng;           // [ng]
+  double* ub = p.ubuf + int64_t(s) * p.u_elems;
+  const double* F = p.fac + int64_t(s) * p.fac_elems + U.fac_off;
+  // u_B from the father's u_K (cmap entries are father K-indices)
+  if (U.parent >= 0) {
+    for (int i = tid; i < k; i += 256) uB[i] = ub[p.upper[U.parent].u_off + p.cmap[U.cmap_off + i]];
+  }
+  __syncthreads();
+  // y = v - W u_B
+  for (int g = warp; g < ng; g += 8) {
+    const double* row = F + int64_t(g) * fw;
+    double acc = 0.0;
+    for (int i = lane; i < k; i += 32) acc = fma(row[i], uB[i], acc);
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) y[g] = row[k + ng] - acc;
+  }
+  __syncthreads();
+  // L^T u = y, 32-row blocks from the bottom
+  for (int i1 = ng; i1 > 0; i1 -= 32) {
+    const int i0 = i1 > 32 ? i1 - 32 : 0;
+    for (int r = i0 + warp; r < i1; r += 8) {
+      const double* row = F + int64_t(r) * fw + k;
+      double acc = 0.0;
+      for (int j = i1 + lane; j < ng; j += 32) acc = fma(row[j], u[j], acc);
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0) y[r] -= acc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int r = i1 - 1; r >= i0; --r) {
+        const double* row = F + int64_t(r) * fw + k;
+        double acc = 0.0;
+        const int j = r + 1 + lane;
+        if (j < i1) acc = row[j] * u[j];
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) u[r] = (y[r] - acc) / row[r];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+  double* mine = ub + U.u_off;
+  for (int i = tid; i < k; i += 256) mine[i] = uB[i];
+  for (int g = tid; g < ng; g += 256) mine[k + g] = u[g];
+}
+
+cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_kng,
+                           cudaStream_t s) {
+  const size_t smem = sizeof(double) * size_t(max_kng) + 64;
+  cudaError_t e = cudaFuncSetAttribute(topdown_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  dim3 grid(B, n_nodes);
+  topdown_kernel<<<grid, 256, smem, s>>>(p, nodes_dev);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K4: observations + Gaussian log-likelihood
+// ---------------------------------------------------------------------------
 __global__ void finalize_kernel(DevPlan p, int B, double* __restrict__ S, double* __restrict__ ll) {
   const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (s >= B) return;
   const double* sig = p.buf[p.root_buf] + p.root_off + int64_t(s) * p.root_elems + p.root_sig;
+  const double* ub = p.ubuf ? p.ubuf + int64_t(s) * p.u_elems : nullptr;
   double acc = 0.0;
   for (int o = lane; o < p.n_obs; o += 32) {
-    const double v = p.route_kind[o] == 0 ? sig[p.route_col[o]] : p.route_val[o];
+    const int kind = p.route_kind[o];
+    double v;
+    if (kind == 0) {
+      v = sig[p.route_col[o]];
+    } else if (kind == 1) {
+      v = p.route_val[o];
+    } else if (kind == 2) {
+      // leaf point: l^T u_B(leaf) + sigma, u_B from the father's u_K
+      const int l = p.route_node[o];
+      const double* fn = p.fbuf + (int64_t(s) * p.n_fslots + p.route_slot[o]) * 65;
+      const int par = p.leaves[l].parent;
+      const double* up = ub + p.upper[par].u_off;
+      const int32_t* cm = p.leaf_cmap + int64_t(l) * kLeafPerim;
+      double t = fn[64];
+      for (int b = 0; b < kLeafPerim; ++b) {
+        const int c = cm[b];
+        if (c >= 0) t = fma(fn[b], up[c], t);
+      }
+      v = t;
+    } else {
+      const DevUpper& U = p.upper[p.route_node[o]];
+      v = ub[U.u_off + U.k + p.route_col[o]];
+    }
     if (!isfinite(v)) record_error(p.err, HDD_ERR_NUMERICAL, s, -1);
     if (S) S[int64_t(s) * p.n_obs + o] = v;
     if (p.y) {

@@ -293,6 +293,14 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
       return "unknown observation kind " + std::to_string(P.obs_kind[o]);
     }
   }
+  // ---- adjoint vs primal (top-down back-solve) ---------------------------
+  {
+    int n_points = 0;
+    for (int o = 0; o < n_obs; ++o) n_points += births[o].where >= 0;
+    P.mode = d->mode >= 0 ? d->mode : (n_points > 32 ? 1 : 0);
+    if (dl == 0) P.mode = 0;     // the root is a kernel leaf: nothing to solve top-down
+  }
+  const bool primal = P.mode == 1;
   // own-mean flags: every node in the subtree of a requested mean node
   std::vector<char> own_mean(all.size(), 0);
   for (int o = 0; o < n_obs; ++o) {
@@ -321,9 +329,18 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
       L.cols.push_back({COL_MEAN, -1});
       L.birth.insert(L.birth.end(), {-1, -1, -1});
     }
+    L.fslot.assign(L.cols.size(), -1);
     for (int o = 0; o < n_obs; ++o) {
       if (births[o].where == 1 && births[o].node == -1 - to_plan[t]) {
-        colmap[t][o] = int(L.cols.size());
+        const int c = int(L.cols.size());
+        if (primal) {
+          L.fslot.push_back(P.n_fslots);
+          P.route[o] = ObsRoute{2, c, 0.0, -1 - to_plan[t], P.n_fslots};
+          ++P.n_fslots;
+        } else {
+          colmap[t][o] = c;
+          L.fslot.push_back(-1);
+        }
         L.cols.push_back({COL_OBS, o});
         L.birth.insert(L.birth.end(), {births[o].r, births[o].q, births[o].gpos});
       }
@@ -365,8 +382,12 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
       }
       for (int o = 0; o < n_obs; ++o) {
         if (births[o].where == 0 && births[o].node == to_plan[t]) {
-          colmap[t][o] = int(U.cols.size());
-          add({COL_OBS, o}, -1, 0.0, -1, 0.0, births[o].gpos);
+          if (primal) {
+            P.route[o] = ObsRoute{3, births[o].gpos, 0.0, to_plan[t], -1};
+          } else {
+            colmap[t][o] = int(U.cols.size());
+            add({COL_OBS, o}, -1, 0.0, -1, 0.0, births[o].gpos);
+          }
         }
         if (mean_tmp[o] == t) colmap[t][o] = mean_col;
       }
@@ -391,11 +412,45 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
   int root_tmp = 0;   // preorder index 0 is the root
   for (int o = 0; o < n_obs; ++o) {
     if (P.route[o].kind == 1 && births[o].where < 0 && mean_tmp[o] < 0) continue;  // constant
+    if (P.route[o].kind >= 2) continue;                                             // primal point
     auto it = colmap[root_tmp].find(o);
     if (it == colmap[root_tmp].end()) { *code = HDD_ERR_USAGE; return "functional was not carried to the root"; }
     P.route[o] = ObsRoute{0, it->second, 0.0};
   }
   P.root_nc = dl > 0 ? P.upper[P.root].nc : int(P.leaves[0].cols.size());
+
+  // ---- father links and child-boundary maps (primal top-down) -------------
+  for (int u = 0; u < int(P.upper.size()); ++u) {
+    UpperNode& U = P.upper[u];
+    for (int si = 0; si < 2; ++si) {
+      const int sp = U.son[si];
+      const int32_t* gm = U.gmap.data() + si * U.K;
+      if (sp >= 0) {
+        UpperNode& S = P.upper[sp];
+        S.parent = u;
+        S.cmap.assign(S.k, -1);
+        for (int a = 0; a < U.K; ++a)
+          if (gm[a] >= 0) S.cmap[gm[a]] = a;
+      } else {
+        Leaf& L = P.leaves[-1 - sp];
+        L.parent = u;
+        L.cmap.assign(kLeafPerim, -1);
+        for (int a = 0; a < U.K; ++a)
+          if (gm[a] >= 0) L.cmap[gm[a]] = a;
+      }
+    }
+  }
+  if (primal) {
+    int64_t fo = 0, uo = 0;
+    for (UpperNode& U : P.upper) {
+      U.fac_off = fo;
+      fo += int64_t(U.ng) * (U.k + U.ng + 1);
+      U.u_off = uo;
+      uo += U.K;
+    }
+    P.fac_elems = fo;
+    P.u_elems = uo;
+  }
 
   // ---- output layouts -----------------------------------------------------
   P.leaf_ld = kLeafPerim + P.leaf_cols;

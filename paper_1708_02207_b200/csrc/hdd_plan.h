@@ -45,6 +45,10 @@ struct UpperNode {
   int64_t out_off = 0;          // element offset of sample 0 in its depth buffer
   int buf = 0;                  // output buffer id
   int tier = 0;                 // 0 = smem panel, 1 = global panel
+  // primal mode: interface solution u_K = [u_B | u_gamma] and stored factors
+  int parent = -1;              // upper index of the father (-1 for the root)
+  std::vector<int32_t> cmap;    // [k] father K-index of each pruned boundary node
+  int64_t fac_off = 0, u_off = 0;   // per-sample element offsets
 };
 
 struct Leaf {
@@ -53,12 +57,17 @@ struct Leaf {
   bool own_mean = false;
   std::vector<Col> cols;
   std::vector<int32_t> birth;   // [ncols][3] (level r, node q, gamma pos) or -1
+  int parent = -1;              // upper index of the father
+  std::vector<int32_t> cmap;    // [64] father K-index of each perimeter node, -1 on the domain boundary
+  std::vector<int32_t> fslot;   // [ncols] functional slot of a primal point column, -1
 };
 
 struct ObsRoute {
-  int kind;      // 0 = root column, 1 = constant
-  int col;
+  int kind;      // 0 = root column, 1 = constant, 2 = leaf point (primal), 3 = interface point (primal)
+  int col;       // root column / leaf column / interface position
   double value;
+  int node = -1; // leaf index (kind 2) or upper index (kind 3)
+  int slot = -1; // leaf functional slot (kind 2)
 };
 
 struct LeafLevel {                // in-leaf template level r (father shape)
@@ -86,6 +95,9 @@ struct Plan {
   int root = -1;                              // upper index of the root, or -1 (root is leaf 0)
   int root_nc = 0;
   int n_buffers = 2;
+  int mode = 0;                               // 0 adjoint (functionals to the root), 1 primal top-down
+  int n_fslots = 0;                           // leaf point functionals kept for the top-down pass
+  int64_t fac_elems = 0, u_elems = 0;         // per-sample sizes of the primal buffers
   std::vector<int64_t> buf_elems_per_sample;  // per buffer
 };
 

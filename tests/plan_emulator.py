@@ -52,8 +52,9 @@ def origin(r, q):
     return x, y
 
 
-def eliminate(At, Rt, sig, k):
-    """Bordered Schur complement: returns (Psi, R, sigma)."""
+def eliminate(At, Rt, sig, k, factors=None):
+    """Bordered Schur complement: returns (Psi, R, sigma); `factors` (a list)
+    receives (L, W, v) for the primal top-down pass."""
     ng = At.shape[0] - k
     if ng == 0:
         return At[:k, :k].copy(), Rt[:k].copy(), sig.copy()
@@ -64,6 +65,8 @@ def eliminate(At, Rt, sig, k):
     R = Rt[:k] - W.T @ V
     s = sig.copy()
     s[1:] += V[:, 0] @ V[:, 1:]
+    if factors is not None:
+        factors.append((Lc, W, V[:, 0]))
     return Psi, R, s
 
 
@@ -131,6 +134,7 @@ def run(plan, level, kappa, f=None):
         nd = _lib.HddNodeInfo()
         assert L.hdd_plan_node_info(plan.handle, u, C.byref(nd)) == 0
         nodes.append(nd)
+    facs = {}
     for u, nd in enumerate(nodes):   # plan order: deepest first
         k, ng, nc = nd.k, nd.ng, nd.nc
         K = k + ng
@@ -153,11 +157,47 @@ def run(plan, level, kappa, f=None):
         for c in range(nc):
             if cb[c] >= 0:
                 Rt[k + cb[c], c] += 1.0
-        upper_out[u] = eliminate(At, Rt, sg, k)
+        fl_ = []
+        upper_out[u] = eliminate(At, Rt, sg, k, fl_)
+        facs[u] = fl_[0] if fl_ else None
     root_sig = upper_out[info.n_upper - 1][2] if info.n_upper else leaf_out[0][2]
+    # primal top-down (root first = reverse plan order): u_K = [u_B | u_gamma]
+    uK = {}
+    parent_of = {}
+    for u, nd in enumerate(nodes):
+        for si in range(2):
+            parent_of[nd.son[si]] = (u, si)
+    for u in range(info.n_upper - 1, -1, -1):
+        nd = nodes[u]
+        k, ng = nd.k, nd.ng
+        if u in parent_of:
+            pu, si = parent_of[u]
+            pg = _arr(nodes[pu].gmap, 2 * (nodes[pu].k + nodes[pu].ng), int).reshape(2, -1)[si]
+            uB = np.zeros(k)
+            sel = np.flatnonzero(pg >= 0)
+            uB[pg[sel]] = uK[pu][sel]
+        else:
+            uB = np.zeros(k)
+        Lc, W, v = facs[u]
+        ug = scipy.linalg.solve_triangular(Lc.T, v - W @ uB, lower=False)
+        uK[u] = np.concatenate([uB, ug])
     S = np.empty(info.n_obs)
     for o in range(info.n_obs):
         ob = _lib.HddObsInfo()
         assert L.hdd_plan_obs_info(plan.handle, o, C.byref(ob)) == 0
-        S[o] = root_sig[ob.col] if ob.kind == 0 else ob.value
+        if ob.kind == 0:
+            S[o] = root_sig[ob.col]
+        elif ob.kind == 1:
+            S[o] = ob.value
+        elif ob.kind == 3:
+            S[o] = uK[ob.node][nodes[ob.node].k + ob.col]
+        else:
+            leaf = -1 - ob.node if ob.node < 0 else ob.node
+            pu, si = parent_of[-1 - leaf]
+            pg = _arr(nodes[pu].gmap, 2 * (nodes[pu].k + nodes[pu].ng), int).reshape(2, -1)[si]
+            uB = np.zeros(64)
+            sel = np.flatnonzero(pg >= 0)
+            uB[pg[sel]] = uK[pu][sel]
+            psi, R, sg = leaf_out[leaf]
+            S[o] = R[:, ob.col] @ uB + sg[ob.col]
     return S, leaf_out, upper_out

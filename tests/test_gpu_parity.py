@@ -270,3 +270,16 @@ def test_global_panel_tier_matches_shared_tier(torch_cuda, golden, monkeypatch):
     assert rel(b1, a1) <= 1e-13 and rel(b2, a2) <= 1e-13
     for b in range(b2.shape[0]):
         assert rel(b2[b], g2["S"][b]) <= TOL
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_primal_and_adjoint_modes_agree(torch_cuda, golden, name):
+    """Top-down back-solve (primal) vs functionals carried to the root (adjoint)."""
+    g = golden(f"cfg_{name}")
+    Z = g["Z"][:8]
+    a = hb.forward_functionals_batch(configs.make_problem(name, mode=0), Z)
+    b = hb.forward_functionals_batch(configs.make_problem(name, mode=1), Z)
+    assert configs.make_problem(name, mode=1).plan().info().mode == 1
+    for i in range(Z.shape[0]):
+        assert rel(b[i], a[i]) <= 1e-12
+        assert rel(b[i], g["S"][i]) <= TOL

@@ -17,13 +17,13 @@ from paper_1708_02207_b200 import _lib, parallel
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def host_problem(level, n_z, obs, param="kl", sigma=0.01, y=None, f=None):
+def host_problem(level, n_z, obs, param="kl", sigma=0.01, y=None, f=None, mode=0):
     mesh = hb.build_mesh(level)
     tree = hb.build_tree(mesh)
     p = hb.SineKLField(tree, n_z) if param == "kl" else hb.ParamField.build(tree, n_z)
     model = hb.MeasurementModel(obs, np.full(len(obs), sigma), y)
     f = np.ones(mesh.n_nodes) if f is None else f
-    return hb.BayesProblem(tree, p, f, np.zeros(4 * mesh.n_cells), model, device=-1)
+    return hb.BayesProblem(tree, p, f, np.zeros(4 * mesh.n_cells), model, device=-1, mode=mode)
 
 
 def test_library_exports_header_symbols():
@@ -70,8 +70,9 @@ def test_leaf_template_shapes():
         assert ((m1 >= 0) & (m2 >= 0))[k:].all()   # interface shared by both sons
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("case", ["C1", "points6", "means6", "indicator5", "f_nodal5"])
-def test_emulated_plan_matches_direct_solve(case):
+def test_emulated_plan_matches_direct_solve(case, mode):
     rng = np.random.default_rng(5)
     f = None
     param = "kl"
@@ -94,7 +95,8 @@ def test_emulated_plan_matches_direct_solve(case):
         level, n_z = 5, 4
         obs = configs.observations(configs.CONFIGS["C1"])
         f = rng.uniform(0.5, 2.0, (33 * 33))
-    prob = host_problem(level, n_z, obs, param=param, f=f)
+    prob = host_problem(level, n_z, obs, param=param, f=f, mode=mode)
+    assert prob.plan().info().mode == mode
     grid = geometry.Grid(level)
     fo = fields.SineKLField(grid, n_z) if param == "kl" else fields.IndicatorField(grid, n_z)
     for z in rng.standard_normal((2, n_z)):
@@ -222,3 +224,20 @@ def test_sharded_likelihood_gloo_world2(tmp_path, golden):
     assert np.allclose(r["ll"], g["ll"][:11], rtol=1e-12)
     w, idx, lse = hb.posterior_weights(g["ll"][:11])
     assert int(r["idx"]) == idx and np.allclose(r["w"], w, rtol=1e-12)
+
+
+def test_primal_routing_auto_selection():
+    """Auto mode: many point observations -> primal top-down (routes 2/3),
+    few -> adjoint (root columns), means stay adjoint."""
+    cfg = configs.CONFIGS["C2"]
+    p2 = host_problem(cfg.level, cfg.n_z, configs.observations(cfg), mode=-1).plan()
+    assert p2.info().mode == 1
+    kinds = []
+    for o in range(p2.info().n_obs):
+        ob = _lib.HddObsInfo()
+        p2.lib.hdd_plan_obs_info(p2.handle, o, C.byref(ob))
+        kinds.append(ob.kind)
+    assert set(kinds) <= {1, 2, 3} and 2 in kinds and 3 in kinds
+    c1 = configs.CONFIGS["C1"]
+    p1 = host_problem(c1.level, c1.n_z, configs.observations(c1), mode=-1).plan()
+    assert p1.info().mode == 0
