@@ -165,7 +165,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
     const int ngp = (U.ng + nbk - 1) / nbk * nbk;
     const int ldp = (U.k + ngp + U.nc + 15) / 16 * 16 + 8;
     pl->depth_nb[U.depth] = nbk;
-    pl->depth_ws[U.depth] = std::max<int64_t>(pl->depth_ws[U.depth], int64_t(ngp) * ldp);
+    if (pl->depth_tier[U.depth]) pl->depth_ws[U.depth] = std::max<int64_t>(pl->depth_ws[U.depth], int64_t(ngp) * ldp);
     pl->depth_rows[U.depth] = std::max(pl->depth_rows[U.depth], U.k + ngp);
   }
   for (size_t u = 0; u < P.upper.size(); ++u) {
@@ -318,12 +318,12 @@ static int setup_device(HddPlan* pl, int max_batch) {
     D.root_buf = R.buf;
     D.root_off = R.out_off * bcap;
     D.root_elems = R.out_elems;
-    D.root_sig = int64_t(R.k) * R.out_ld;
+    D.root_sig = int64_t(R.k) * (R.k + 1) / 2 + int64_t(R.k) * R.nc;
   } else {
     D.root_buf = P.leaf_buf;
     D.root_off = 0;
     D.root_elems = P.leaf_elems;
-    D.root_sig = int64_t(kLeafPerim) * P.leaf_ld;
+    D.root_sig = int64_t(kLeafPerim) * (kLeafPerim + 1) / 2 + int64_t(kLeafPerim) * P.leaf_cols;
   }
   pl->leaf_smem = leaf_smem_bytes(P.leaf_cols <= 2 ? 2 : (P.leaf_cols <= 4 ? 4 : 8));
   {
@@ -618,15 +618,18 @@ int hdd_debug_node_output(HddPlan* pl, int32_t idx, int32_t b, double* psi, doub
     base = pl->dev.buf[P.leaf_buf] + int64_t(l) * P.leaf_elems * pl->bcap + int64_t(b) * P.leaf_elems;
     k = kLeafPerim; ld = P.leaf_ld; nc = int(P.leaves[l].cols.size());
   }
-  std::vector<double> tmp(size_t(k) * ld + ld);
+  const size_t tk = size_t(k) * (k + 1) / 2;
+  std::vector<double> tmp(tk + size_t(k) * ld + ld);
   CU(cudaSetDevice(pl->device));
   CU(cudaStreamSynchronize(pl->stream));
-  CU(cudaMemcpy(tmp.data(), base, (size_t(k) * ld + nc) * 8, cudaMemcpyDeviceToHost));
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(tmp.data(), base, (tk + size_t(k) * ld + nc) * 8, cudaMemcpyDeviceToHost));
   for (int a = 0; a < k; ++a) {
-    if (psi) for (int c = 0; c < k; ++c) psi[size_t(a) * k + c] = tmp[size_t(a) * ld + c];
-    if (R) for (int c = 0; c < nc; ++c) R[size_t(a) * nc + c] = tmp[size_t(a) * ld + k + c];
+    if (psi)
+      for (int c = 0; c < k; ++c) psi[size_t(a) * k + c] = a >= c ? tmp[size_t(a) * (a + 1) / 2 + c] : tmp[size_t(c) * (c + 1) / 2 + a];
+    if (R) for (int c = 0; c < nc; ++c) R[size_t(a) * nc + c] = tmp[tk + size_t(a) * ld + c];
   }
-  if (sigma) for (int c = 0; c < nc; ++c) sigma[c] = tmp[size_t(k) * ld + c];
+  if (sigma) for (int c = 0; c < nc; ++c) sigma[c] = tmp[tk + size_t(k) * ld + c];
   return HDD_OK;
 }
 

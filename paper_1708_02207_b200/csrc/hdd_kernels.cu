@@ -416,13 +416,11 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
         if constexpr (R > 0) {
           o[t] = v[u];
         } else {
-          const int ld = p.leaf_ld;
           if (bx < k) {
-            gdst[a * ld + bx] = v[u];
-            gdst[bx * ld + a] = v[u];
+            gdst[t] = v[u];                       // packed lower: same order as the items
           } else if (bx - k < p.leaf_cols) {
             const double sc = ctype[bx - k] == 1 ? inv_area : 1.0;
-            gdst[a * ld + kLeafPerim + (bx - k)] = v[u] * sc;
+            gdst[ctri(kLeafPerim) + a * p.leaf_cols + (bx - k)] = v[u] * sc;
             const int fs = cinfo[4 * NC + (bx - k)];
             if (fs >= 0) p.fbuf[(int64_t(s) * p.n_fslots + fs) * 65 + a] = v[u];
           }
@@ -439,7 +437,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
         o[ctri(k) + k * NC + c] = sg;
         if (c < 2) o[Sout - 2 + c] = 0.0;    // zero slot
       } else if (c < p.leaf_cols) {
-        gdst[kLeafPerim * p.leaf_ld + c] = sg * (ctype[c] == 1 ? inv_area : 1.0);
+        gdst[ctri(kLeafPerim) + kLeafPerim * p.leaf_cols + c] = sg * (ctype[c] == 1 ? inv_area : 1.0);
         const int fs = cinfo[4 * NC + c];
         if (fs >= 0) p.fbuf[(int64_t(s) * p.n_fslots + fs) * 65 + 64] = sg;
       }
@@ -652,81 +650,6 @@ constexpr int kLdd = 40;    // smem leading dim for 32-wide tiles (= 8 mod 16)
 
 __device__ __forceinline__ int upper_ngp(const DevUpper& U) { return (U.ng + U.nb - 1) / U.nb * U.nb; }
 
-// -- assemble ----------------------------------------------------------------
-// grid (row groups of 8, node, sample); warp per father row a in [0, k + ngp]
-__global__ void __launch_bounds__(256) assemble_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
-                                                       double* __restrict__ ws, int64_t ws_stride) {
-  const DevUpper& U = nodes[blockIdx.y];
-  const int s = blockIdx.z;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int k = U.k, ng = U.ng, K = U.K, nc = U.nc, ldp = U.ldp;
-  const int ngp = upper_ngp(U);
-  const int Kp = k + ngp;
-  const int a = blockIdx.x * 8 + warp;
-  if (a > k + ngp) return;
-  const int32_t* gm = p.gmap + U.gmap_off;
-  const int32_t* csrc = p.csrc + 2 * U.col_off;
-  const double* ccoef = p.ccoef + 2 * U.col_off;
-  const double* son0 = p.buf[U.son_buf[0]] + U.son_off[0] * p.bcap + int64_t(s) * U.son_elems[0];
-  const double* son1 = p.buf[U.son_buf[1]] + U.son_off[1] * p.bcap + int64_t(s) * U.son_elems[1];
-  const int sk0 = U.son_k[0], sk1 = U.son_k[1], sl0 = U.son_ld[0], sl1 = U.son_ld[1];
-  double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
-  if (a == k + ngp) {   // sigma~
-    for (int c = lane; c < nc; c += 32) {
-      double v = 0.0;
-      if (csrc[2 * c] >= 0) v += ccoef[2 * c] * son0[size_t(sk0) * sl0 + csrc[2 * c]];
-      if (csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * son1[size_t(sk1) * sl1 + csrc[2 * c + 1]];
-      out[size_t(k) * U.out_ld + c] = v;
-    }
-    return;
-  }
-  if (a < k) {
-    // lower part of A11 row a, then R_B row a
-    const int pa0 = gm[a], pa1 = gm[K + a];
-    const double* r0 = pa0 >= 0 ? son0 + size_t(pa0) * sl0 : nullptr;
-    const double* r1 = pa1 >= 0 ? son1 + size_t(pa1) * sl1 : nullptr;
-    double* row = out + size_t(a) * U.out_ld;
-    for (int j = lane; j <= a; j += 32) {
-      double v = 0.0;
-      if (r0) { const int pb = gm[j]; if (pb >= 0) v += r0[pb]; }
-      if (r1) { const int pb = gm[K + j]; if (pb >= 0) v += r1[pb]; }
-      row[j] = v;
-    }
-    for (int c = lane; c < nc; c += 32) {
-      double v = 0.0;
-      if (r0 && csrc[2 * c] >= 0) v += ccoef[2 * c] * r0[sk0 + csrc[2 * c]];
-      if (r1 && csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * r1[sk1 + csrc[2 * c + 1]];
-      row[k + c] = v;
-    }
-    return;
-  }
-  // interface panel row g
-  const int g = a - k;
-  double* P = ws + int64_t(blockIdx.y) * ws_stride * p.bcap + int64_t(s) * ws_stride + int64_t(g) * ldp;
-  const int W = Kp + nc;
-  if (g >= ng) {
-    for (int j = lane; j < W; j += 32) P[j] = (j == k + g) ? 1.0 : 0.0;
-    return;
-  }
-  const int32_t* cbirth = p.cbirth + U.col_off;
-  const int pa0 = gm[a], pa1 = gm[K + a];
-  const double* r0 = pa0 >= 0 ? son0 + size_t(pa0) * sl0 : nullptr;
-  const double* r1 = pa1 >= 0 ? son1 + size_t(pa1) * sl1 : nullptr;
-  for (int j = lane; j < W; j += 32) {
-    double v = 0.0;
-    if (j < k + ng) {
-      if (r0) { const int pb = gm[j]; if (pb >= 0) v += r0[pb]; }
-      if (r1) { const int pb = gm[K + j]; if (pb >= 0) v += r1[pb]; }
-    } else if (j >= Kp) {
-      const int c = j - Kp;
-      if (r0 && csrc[2 * c] >= 0) v += ccoef[2 * c] * r0[sk0 + csrc[2 * c]];
-      if (r1 && csrc[2 * c + 1] >= 0) v += ccoef[2 * c + 1] * r1[sk1 + csrc[2 * c + 1]];
-      if (cbirth[c] == g) v += 1.0;
-    }
-    P[j] = v;
-  }
-}
-
 // -- shared building blocks ------------------------------------------------
 // Cholesky of the NB x NB diagonal block (rows read from `src`, ld `ld`) by one
 // warp, lane = row, the row of L in registers and L[j][c] broadcast with
@@ -782,104 +705,204 @@ __device__ __forceinline__ void factor_diag_block(const double* src, int ld, dou
   }
 }
 
-// Schur-update epilogue, 32 x 64 output tiles, lower-triangle tiles of the Psi
-// part mirrored; X rows from an smem/HBM panel P (ld ldp) via tile staging.
-// out already holds the assembled lower A11 and R_B.
+// -- son views (packed-lower node outputs) ----------------------------------
+// A node output per sample is [Psi lower-packed tri(k) | R k x nc | sigma nc].
+struct SonView {
+  const double* b;
+  int k, nc;
+};
+__device__ __forceinline__ double son_psi(const SonView& s, int i, int j) {
+  return i >= j ? s.b[tri(i) + j] : s.b[tri(j) + i];
+}
+__device__ __forceinline__ double son_R(const SonView& s, int i, int c) { return s.b[tri(s.k) + i * s.nc + c]; }
+__device__ __forceinline__ double son_sig(const SonView& s, int c) { return s.b[tri(s.k) + s.k * s.nc + c]; }
+
+struct MergeCtx {
+  SonView sv[2];
+  const int32_t* gm;     // [2][K]
+  const int32_t* csrc;   // [nc][2]
+  const double* ccoef;   // [nc][2]
+  const int32_t* cbirth; // [nc]
+  int K;
+};
+
+__device__ __forceinline__ MergeCtx merge_ctx(const DevPlan& p, const DevUpper& U, int s) {
+  MergeCtx c;
+#pragma unroll
+  for (int sn = 0; sn < 2; ++sn) {
+    c.sv[sn].b = p.buf[U.son_buf[sn]] + U.son_off[sn] * p.bcap + int64_t(s) * U.son_elems[sn];
+    c.sv[sn].k = U.son_k[sn];
+    c.sv[sn].nc = U.son_ld[sn];
+  }
+  c.gm = p.gmap + U.gmap_off;
+  c.csrc = p.csrc + 2 * U.col_off;
+  c.ccoef = p.ccoef + 2 * U.col_off;
+  c.cbirth = p.cbirth + U.col_off;
+  c.K = U.K;
+  return c;
+}
+
+// assembled A~(a, j) for father indices a, j (gather form of assemble_father)
+__device__ __forceinline__ double gather_A(const MergeCtx& c, int a, int j) {
+  double v = 0.0;
+  const int pa0 = c.gm[a], pa1 = c.gm[c.K + a];
+  const int pb0 = c.gm[j], pb1 = c.gm[c.K + j];
+  if (pa0 >= 0 && pb0 >= 0) v += son_psi(c.sv[0], pa0, pb0);
+  if (pa1 >= 0 && pb1 >= 0) v += son_psi(c.sv[1], pa1, pb1);
+  return v;
+}
+// assembled R~(a, col)
+__device__ __forceinline__ double gather_R(const MergeCtx& c, int a, int col) {
+  double v = 0.0;
+  const int pa0 = c.gm[a], pa1 = c.gm[c.K + a];
+  const int s0 = c.csrc[2 * col], s1 = c.csrc[2 * col + 1];
+  if (pa0 >= 0 && s0 >= 0) v += c.ccoef[2 * col] * son_R(c.sv[0], pa0, s0);
+  if (pa1 >= 0 && s1 >= 0) v += c.ccoef[2 * col + 1] * son_R(c.sv[1], pa1, s1);
+  return v;
+}
+__device__ __forceinline__ double gather_sig(const MergeCtx& c, int col) {
+  double v = 0.0;
+  const int s0 = c.csrc[2 * col], s1 = c.csrc[2 * col + 1];
+  if (s0 >= 0) v += c.ccoef[2 * col] * son_sig(c.sv[0], s0);
+  if (s1 >= 0) v += c.ccoef[2 * col + 1] * son_sig(c.sv[1], s1);
+  return v;
+}
+
+// panel row g of [A21 | A22 (padded) | R_gamma] -> dst (smem or HBM)
+__device__ __forceinline__ void gather_panel_row(const MergeCtx& c, int k, int ng, int Kp, int W, int g,
+                                                 double* dst, int lane0, int step) {
+  if (g >= ng) {
+    for (int j = lane0; j < W; j += step) dst[j] = (j == k + g) ? 1.0 : 0.0;
+    return;
+  }
+  const int a = k + g;
+  for (int j = lane0; j < W; j += step) {
+    double v = 0.0;
+    if (j < k + ng) v = gather_A(c, a, j);
+    else if (j >= Kp) {
+      const int col = j - Kp;
+      v = gather_R(c, a, col);
+      if (c.cbirth[col] == g) v += 1.0;
+    }
+    dst[j] = v;
+  }
+}
+
+// Schur-update epilogue on 32 x 64 output tiles (lower-triangle Psi tiles and
+// the R columns), the assembled A~ values gathered from the sons and issued
+// before the DMMA loop; output packed-lower.
 template <bool SMEM>
-__device__ __forceinline__ void schur_epilogue(const double* __restrict__ P, int ldp, int k, int ngp, int Kp, int nc,
-                                               double* __restrict__ out, int out_ld, double* Ea, double* Eb) {
+__device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double* __restrict__ P, int ldp, int k,
+                                               int ngp, int Kp, int nc, double* __restrict__ out, double* Ea,
+                                               double* Eb) {
   const int tid = threadIdx.x & 255, lane = tid & 31, warp = tid >> 5;
   const int grp = threadIdx.x >> 8, ngrp = SMEM ? (blockDim.x >> 8) : 1;   // 8-warp groups
   const int gq = lane & 3, gr = lane >> 2;
   const int ow = k + nc;
   const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * 16;
   const int na = (k + 31) / 32, nbt = (ow + 63) / 64;
+  const int tk = tri(k);
   for (int t = grp; t < na * nbt; t += ngrp) {
-    {
-      const int a0 = (t / nbt) * 32, b0 = (t % nbt) * 64;
-      if (b0 + 64 <= k && b0 > a0 + 31) continue;  // strictly upper Psi tile: mirrored from below
-      double acc[2][2][2] = {};
-      int acol[2], bcol[2];
+    const int a0 = (t / nbt) * 32, b0 = (t % nbt) * 64;
+    if (b0 + 64 <= k && b0 > a0 + 31) continue;   // strictly upper Psi tile
+    double acc[2][2][2] = {};
+    int acol[2], bcol[2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int aa = a0 + m0 + 8 * i + gr;
-        acol[i] = aa < k ? aa : 0;
-        const int bb = b0 + n0 + 8 * i + gr;
-        bcol[i] = bb < k ? bb : (bb < ow ? Kp + (bb - k) : 0);
-      }
-      double pre[2][2][2];
+    for (int i = 0; i < 2; ++i) {
+      const int aa = a0 + m0 + 8 * i + gr;
+      acol[i] = aa < k ? aa : 0;
+      const int bb = b0 + n0 + 8 * i + gr;
+      bcol[i] = bb < k ? bb : (bb < ow ? Kp + (bb - k) : 0);
+    }
+    double pre[2][2][2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int aa = a0 + m0 + 8 * i + gr;
+    for (int i = 0; i < 2; ++i) {
+      const int aa = a0 + m0 + 8 * i + gr;
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < 2; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int bb = b0 + n0 + 8 * j + 2 * gq + e;
-            pre[i][j][e] = (aa < k && bb < ow && (bb >= k || bb <= aa)) ? out[size_t(aa) * out_ld + bb] : 0.0;
+        for (int e = 0; e < 2; ++e) {
+          const int bb = b0 + n0 + 8 * j + 2 * gq + e;
+          double v = 0.0;
+          if (aa < k && bb < ow) {
+            if (bb < k) { if (bb <= aa) v = gather_A(mc, aa, bb); }
+            else v = gather_R(mc, aa, bb - k);
           }
-      }
-      if constexpr (SMEM) {
-        for (int g0 = 0; g0 < ngp; g0 += 4) {
-          const double* pr = P + size_t(g0 + gq) * ldp;
-          double av[2], bv[2];
-#pragma unroll
-          for (int i = 0; i < 2; ++i) { av[i] = pr[acol[i]]; bv[i] = pr[bcol[i]]; }
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 2; ++j) dmma884(acc[i][j], av[i], bv[j]);
+          pre[i][j][e] = v;
         }
-      } else {
-        for (int g0 = 0; g0 < ngp; g0 += 32) {
-          __syncthreads();
-          for (int t = tid; t < 32 * 32; t += 256) {
-            const int g = t >> 5, i = t & 31;
-            const int aa = a0 + i;
-            Ea[g * kLds + i] = aa < k ? P[int64_t(g0 + g) * ldp + aa] : 0.0;
-          }
-          for (int t = tid; t < 32 * 64; t += 256) {
-            const int g = t >> 6, j = t & 63;
-            const int bb = b0 + j;
-            const int col = bb < k ? bb : (bb < ow ? Kp + (bb - k) : -1);
-            Eb[g * kLds + j] = col >= 0 ? P[int64_t(g0 + g) * ldp + col] : 0.0;
-          }
-          __syncthreads();
-          warp_gemm_tn<2, 2>(acc, Ea, kLds, m0, Eb, kLds, n0, 32);
+    }
+    if constexpr (SMEM) {
+      for (int g0 = 0; g0 < ngp; g0 += 4) {
+        const double* pr = P + size_t(g0 + gq) * ldp;
+        double av[2], bv[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) { av[i] = pr[acol[i]]; bv[i] = pr[bcol[i]]; }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma884(acc[i][j], av[i], bv[j]);
+      }
+    } else {
+      for (int g0 = 0; g0 < ngp; g0 += 32) {
+        __syncthreads();
+        for (int tt = tid; tt < 32 * 32; tt += 256) {
+          const int g = tt >> 5, i = tt & 31;
+          const int aa = a0 + i;
+          Ea[g * kLds + i] = aa < k ? P[int64_t(g0 + g) * ldp + aa] : 0.0;
         }
+        for (int tt = tid; tt < 32 * 64; tt += 256) {
+          const int g = tt >> 6, j = tt & 63;
+          const int bb = b0 + j;
+          const int col = bb < k ? bb : (bb < ow ? Kp + (bb - k) : -1);
+          Eb[g * kLds + j] = col >= 0 ? P[int64_t(g0 + g) * ldp + col] : 0.0;
+        }
+        __syncthreads();
+        warp_gemm_tn<2, 2>(acc, Ea, kLds, m0, Eb, kLds, n0, 32);
       }
+    }
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int aa = a0 + m0 + 8 * i + gr;
-        if (aa >= k) continue;
+    for (int i = 0; i < 2; ++i) {
+      const int aa = a0 + m0 + 8 * i + gr;
+      if (aa >= k) continue;
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < 2; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int bb = b0 + n0 + 8 * j + 2 * gq + e;
-            if (bb >= ow) continue;
-            if (bb < k) {
-              if (bb > aa) continue;
-              const double v = pre[i][j][e] - acc[i][j][e];
-              out[size_t(aa) * out_ld + bb] = v;
-              if (bb < aa) out[size_t(bb) * out_ld + aa] = v;
-            } else {
-              out[size_t(aa) * out_ld + bb] = pre[i][j][e] - acc[i][j][e];
-            }
+        for (int e = 0; e < 2; ++e) {
+          const int bb = b0 + n0 + 8 * j + 2 * gq + e;
+          if (bb >= ow) continue;
+          if (bb < k) {
+            if (bb <= aa) out[tri(aa) + bb] = pre[i][j][e] - acc[i][j][e];
+          } else {
+            out[tk + aa * nc + (bb - k)] = pre[i][j][e] - acc[i][j][e];
           }
-      }
+        }
     }
   }
 }
 
-// -- tier M: panel in shared memory ------------------------------------------
-size_t merge_m2_smem_bytes(int ngp, int ldp) {
-  return sizeof(double) * size_t(ngp) * ldp + 64;
+__device__ __forceinline__ void store_factors(const DevPlan& p, const DevUpper& U, int s, const double* P, int ldp,
+                                              int Kp, bool diag_unscaled, int tid, int nthr) {
+  const int k = U.k, ng = U.ng;
+  const int fw = k + ng + 1;
+  double* F = p.fac + int64_t(s) * p.fac_elems + U.fac_off;
+  for (int t = tid; t < ng * fw; t += nthr) {
+    const int g = t / fw, j = t - g * fw;
+    double v;
+    if (j < k) v = P[int64_t(g) * ldp + j];
+    else if (j < k + ng) {
+      const int jj = j - k;
+      v = jj < g ? 0.0 : P[int64_t(g) * ldp + k + jj];
+      if (jj == g && diag_unscaled) v = sqrt(v);
+    } else v = P[int64_t(g) * ldp + Kp];
+    F[t] = v;
+  }
 }
 
+// -- tier M: panel in shared memory ------------------------------------------
+size_t merge_m2_smem_bytes(int ngp, int ldp) { return sizeof(double) * size_t(ngp) * ldp + 64; }
+
 template <int NB>
-__global__ void __launch_bounds__(512) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
-                                                       const double* __restrict__ ws, int64_t ws_stride) {
+__global__ void __launch_bounds__(512) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes) {
   extern __shared__ __align__(16) double sm[];
   const DevUpper& U = nodes[blockIdx.y];
   const int s = blockIdx.x;
@@ -891,17 +914,11 @@ __global__ void __launch_bounds__(512) merge_m2_kernel(DevPlan p, const DevUpper
   const int W = Kp + nc;
   double* P = sm;                          // [ngp][ldp]
   __shared__ int s_bad;
-  {
-    const double* src = ws + int64_t(blockIdx.y) * ws_stride * p.bcap + int64_t(s) * ws_stride;
-    const int n2 = (ngp * ldp) >> 1;
-    const double2* s2 = reinterpret_cast<const double2*>(src);
-    double2* d2 = reinterpret_cast<double2*>(P);
-    for (int t = tid; t < n2; t += NT) d2[t] = s2[t];
-  }
+  const MergeCtx mc = merge_ctx(p, U, s);
+  for (int g = warp; g < ngp; g += NWp) gather_panel_row(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   const int gq = lane & 3, gr = lane >> 2;
   for (int r0 = 0; r0 < ngp; r0 += NB) {
-    // in-block row elimination (all threads): rows r0.. become X_b = L_bb^-1 P_b
     for (int c = r0; c < r0 + NB; ++c) {
       double* rc = P + c * ldp;
       __syncthreads();                    // previous pivot's updates are complete
@@ -909,7 +926,7 @@ __global__ void __launch_bounds__(512) merge_m2_kernel(DevPlan p, const DevUpper
       if (!(d > 0.0) && tid == 0) s_bad = 1;
       const double inv = 1.0 / sqrt(d);
       for (int j = tid; j < W; j += NT)
-        if (j != k + c) rc[j] *= inv;     // the diagonal entry is never read again
+        if (j != k + c) rc[j] *= inv;     // the diagonal keeps the pivot (L^T diag = sqrt)
       __syncthreads();
       const int nr = r0 + NB - c - 1;
       for (int t = warp; t < nr; t += NWp) {
@@ -920,7 +937,6 @@ __global__ void __launch_bounds__(512) merge_m2_kernel(DevPlan p, const DevUpper
       }
     }
     __syncthreads();
-    // trailing rows r >= r0+NB:  P[r][j] -= sum_h X_b[h][k + r] X_b[h][j]   (DMMA, 8 x 32 tiles)
     const int nrt = (ngp - r0 - NB) / 8;
     const int nct = (W + 31) / 32;
     for (int t = warp; t < nrt * nct; t += NWp) {
@@ -940,28 +956,16 @@ __global__ void __launch_bounds__(512) merge_m2_kernel(DevPlan p, const DevUpper
   }
   __syncthreads();
   if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
-  if (p.mode == 1) {
-    // primal mode: keep [W | L^T | v] for the top-down back-solve (hdd.py:397-432)
-    const int fw = k + ng + 1;
-    double* F = p.fac + int64_t(s) * p.fac_elems + U.fac_off;
-    for (int t = tid; t < ng * fw; t += NT) {
-      const int g = t / fw, j = t - g * fw;
-      double v;
-      if (j < k) v = P[g * ldp + j];
-      else if (j < k + ng) {
-        const int jj = j - k;
-        v = jj < g ? 0.0 : (jj == g ? sqrt(P[g * ldp + k + g]) : P[g * ldp + k + jj]);
-      } else v = P[g * ldp + Kp];
-      F[t] = v;
-    }
-  }
+  if (p.mode == 1) store_factors(p, U, s, P, ldp, Kp, true, tid, NT);
   double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
-  for (int c = 1 + tid; c < nc; c += NT) {
-    double v = out[size_t(k) * U.out_ld + c];
-    for (int g = 0; g < ng; ++g) v = fma(P[g * ldp + Kp], P[g * ldp + Kp + c], v);
-    out[size_t(k) * U.out_ld + c] = v;
+  const int tk = tri(k);
+  for (int c = tid; c < nc; c += NT) {
+    double v = gather_sig(mc, c);
+    if (c >= 1)
+      for (int g = 0; g < ng; ++g) v = fma(P[g * ldp + Kp], P[g * ldp + Kp + c], v);
+    out[tk + k * nc + c] = v;
   }
-  schur_epilogue<true>(P, ldp, k, ngp, Kp, nc, out, U.out_ld, nullptr, nullptr);
+  schur_epilogue<true>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
 }
 
 // -- tier L: panel in HBM ----------------------------------------------------
@@ -980,14 +984,16 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
   const int Kp = k + ngp;
   const int W = Kp + nc;
   double* P = ws + int64_t(blockIdx.y) * ws_stride * p.bcap + int64_t(s) * ws_stride;
-  double* D = sm;                         // [32][kLdd]
-  double* LiT = D + 32 * kLdd;            // [32][kLdd]
+  double* LiT = sm + 32 * kLdd;           // [32][kLdd]
   double* Xc = LiT + 32 * kLdd;           // [32][kLds]
   double* Lt = Xc + 32 * kLds;            // [32][kLdd]
   double* Ea = Lt + 32 * kLdd;            // [32][kLds]
   double* Eb = Ea + 32 * kLds;            // [32][kLds]
   __shared__ int s_bad;
+  const MergeCtx mc = merge_ctx(p, U, s);
+  for (int g = warp; g < ngp; g += 8) gather_panel_row(mc, k, ng, Kp, W, g, P + int64_t(g) * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
+  __syncthreads();
   for (int r0 = 0; r0 < ngp; r0 += kLB) {
     if (warp == 0) factor_diag_block<32>(P + int64_t(r0) * ldp + k + r0, ldp, LiT, &s_bad);
     __syncthreads();
@@ -1050,39 +1056,29 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
     __syncthreads();
   }
   if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
-  if (p.mode == 1) {
-    const int fw = k + ng + 1;
-    double* F = p.fac + int64_t(s) * p.fac_elems + U.fac_off;
-    for (int t = tid; t < ng * fw; t += 256) {
-      const int g = t / fw, j = t - g * fw;
-      double v;
-      if (j < k) v = P[int64_t(g) * ldp + j];
-      else if (j < k + ng) { const int jj = j - k; v = jj < g ? 0.0 : P[int64_t(g) * ldp + k + jj]; }
-      else v = P[int64_t(g) * ldp + Kp];
-      F[t] = v;
-    }
-  }
+  if (p.mode == 1) store_factors(p, U, s, P, ldp, Kp, false, tid, 256);
   double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
-  for (int c = 1 + tid; c < nc; c += 256) {
-    double v = out[size_t(k) * U.out_ld + c];
-    for (int g = 0; g < ng; ++g) v = fma(P[int64_t(g) * ldp + Kp], P[int64_t(g) * ldp + Kp + c], v);
-    out[size_t(k) * U.out_ld + c] = v;
+  const int tk = tri(k);
+  for (int c = tid; c < nc; c += 256) {
+    double v = gather_sig(mc, c);
+    if (c >= 1)
+      for (int g = 0; g < ng; ++g) v = fma(P[int64_t(g) * ldp + Kp], P[int64_t(g) * ldp + Kp + c], v);
+    out[tk + k * nc + c] = v;
   }
-  schur_epilogue<false>(P, ldp, k, ngp, Kp, nc, out, U.out_ld, Ea, Eb);
+  schur_epilogue<false>(mc, P, ldp, k, ngp, Kp, nc, out, Ea, Eb);
 }
 
 cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
                          int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s) {
-  dim3 ga((max_rows + 1 + 7) / 8, n_nodes, B);
-  assemble_kernel<<<ga, 256, 0, s>>>(p, nodes_dev, ws, ws_stride);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  (void)max_rows;
+  (void)nb;
+  cudaError_t e;
   dim3 grid(B, n_nodes);
   if (tier == 0) {
     e = cudaFuncSetAttribute(merge_m2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     const int nthr = smem > 100 * 1024 ? 512 : 256;
-    merge_m2_kernel<8><<<grid, nthr, smem, s>>>(p, nodes_dev, ws, ws_stride);
+    merge_m2_kernel<8><<<grid, nthr, smem, s>>>(p, nodes_dev);
   } else {
     const size_t sm = merge_l_smem_bytes();
     e = cudaFuncSetAttribute(merge_l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
@@ -1092,9 +1088,6 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------
-// K4: observations + Gaussian log-likelihood
-// ---------------------------------------------------------------------------
 // ---------------------------------------------------------------------------
 // K4 (primal): top-down interface back-solve restricted to what F needs
 // (root_to_leaves, hdd.py:397-432): u_gamma = L^-T (v - W u_B), one CTA per

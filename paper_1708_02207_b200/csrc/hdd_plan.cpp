@@ -453,8 +453,9 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
   }
 
   // ---- output layouts -----------------------------------------------------
-  P.leaf_ld = kLeafPerim + P.leaf_cols;
-  P.leaf_elems = int64_t(kLeafPerim) * P.leaf_ld + P.leaf_cols;
+  // node outputs: [Psi lower-packed | R (k x nc) | sigma (nc)]; *_ld is the R row stride
+  P.leaf_ld = P.leaf_cols;
+  P.leaf_elems = int64_t(kLeafPerim) * (kLeafPerim + 1) / 2 + int64_t(kLeafPerim) * P.leaf_cols + P.leaf_cols;
   const bool keep = d->keep_nodes != 0;
   P.n_buffers = keep ? dl + 1 : 2;
   P.buf_elems_per_sample.assign(P.n_buffers, 0);
@@ -465,8 +466,8 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     int64_t acc = 0;
     for (int u : P.upper_by_depth[dep]) {
       UpperNode& U = P.upper[u];
-      U.out_ld = U.k + U.nc;
-      U.out_elems = int64_t(U.k) * U.out_ld + U.nc;
+      U.out_ld = U.nc;
+      U.out_elems = int64_t(U.k) * (U.k + 1) / 2 + int64_t(U.k) * U.nc + U.nc;
       U.buf = b;
       U.out_off = acc;          // scaled by the sub-batch size at allocation
       acc += U.out_elems;
