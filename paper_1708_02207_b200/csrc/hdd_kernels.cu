@@ -899,42 +899,50 @@ __device__ __forceinline__ void store_factors(const DevPlan& p, const DevUpper& 
 }
 
 // -- tier M: panel in shared memory ------------------------------------------
-size_t merge_m2_smem_bytes(int ngp, int ldp) { return sizeof(double) * size_t(ngp) * ldp + 64; }
+size_t merge_m2_smem_bytes(int ngp, int ldp) { return sizeof(double) * (size_t(ngp) * ldp + 8) + 64; }
 
-template <int NB>
-__global__ void __launch_bounds__(512) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes) {
+template <int NB, int NTH>
+__global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes) {
   extern __shared__ __align__(16) double sm[];
   const DevUpper& U = nodes[blockIdx.y];
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NT = blockDim.x, NWp = NT >> 5;
+  constexpr int NT = NTH, NWp = NTH >> 5;
   const int k = U.k, ng = U.ng, nc = U.nc, ldp = U.ldp;
   const int ngp = upper_ngp(U);
   const int Kp = k + ngp;
   const int W = Kp + nc;
   double* P = sm;                          // [ngp][ldp]
+  double* piv = P + size_t(ngp) * ldp;     // [NB] pivots of the current block
   __shared__ int s_bad;
   const MergeCtx mc = merge_ctx(p, U, s);
   for (int g = warp; g < ngp; g += NWp) gather_panel_row(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   const int gq = lane & 3, gr = lane >> 2;
   for (int r0 = 0; r0 < ngp; r0 += NB) {
+    // in-block elimination with unscaled pivot rows (one barrier per pivot):
+    // row r -= (P[r][k+c] / d_c) * P[c][.]; rows are scaled by 1/sqrt(d) afterwards
     for (int c = r0; c < r0 + NB; ++c) {
-      double* rc = P + c * ldp;
+      const double* rc = P + c * ldp;
       __syncthreads();                    // previous pivot's updates are complete
       const double d = rc[k + c];
-      if (!(d > 0.0) && tid == 0) s_bad = 1;
-      const double inv = 1.0 / sqrt(d);
-      for (int j = tid; j < W; j += NT)
-        if (j != k + c) rc[j] *= inv;     // the diagonal keeps the pivot (L^T diag = sqrt)
-      __syncthreads();
+      if (tid == 0) {
+        piv[c - r0] = d;
+        if (!(d > 0.0)) s_bad = 1;
+      }
+      const double rd = 1.0 / d;
       const int nr = r0 + NB - c - 1;
       for (int t = warp; t < nr; t += NWp) {
         double* rw = P + (c + 1 + t) * ldp;
-        const double lr = rw[k + c] * inv;
+        const double lr = rw[k + c] * rd;
         for (int j = lane; j < W; j += 32)
           if (j != k + c) rw[j] = fma(-lr, rc[j], rw[j]);
       }
+    }
+    __syncthreads();
+    for (int t = tid; t < NB * W; t += NT) {
+      const int i = t / W, j = t - i * W;
+      if (j != k + r0 + i) P[(r0 + i) * ldp + j] *= rsqrt(piv[i]);
     }
     __syncthreads();
     const int nrt = (ngp - r0 - NB) / 8;
@@ -1075,10 +1083,15 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
   cudaError_t e;
   dim3 grid(B, n_nodes);
   if (tier == 0) {
-    e = cudaFuncSetAttribute(merge_m2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    const int nthr = smem > 100 * 1024 ? 512 : 256;
-    merge_m2_kernel<8><<<grid, nthr, smem, s>>>(p, nodes_dev);
+    if (smem > 100 * 1024) {
+      e = cudaFuncSetAttribute(merge_m2_kernel<8, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      merge_m2_kernel<8, 512><<<grid, 512, smem, s>>>(p, nodes_dev);
+    } else {
+      e = cudaFuncSetAttribute(merge_m2_kernel<8, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      merge_m2_kernel<8, 256><<<grid, 256, smem, s>>>(p, nodes_dev);
+    }
   } else {
     const size_t sm = merge_l_smem_bytes();
     e = cudaFuncSetAttribute(merge_l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
