@@ -377,6 +377,12 @@ def main():
                "max_rel_ll_diff_vs_gpu": float(np.max(np.abs(ll_cpu - ll_gpu) / np.abs(ll_cpu)))}
 
     launches = args.steps * info.n_kernels_per_batch * math.ceil(B / info.max_batch)
+    # measured DRAM bytes per launch of the dominant kernel (ncu --set full capture,
+    # profiles/r01_ncu_full_leaf_C2.csv: 21.8 KB per leaf-sample) scaled to this launch
+    traffic = None
+    if top == "leaf":
+        traffic = {"bytes": 21.8e3 * B * ((1 << cfg.level) // 16) ** 2,
+                   "source": "ncu dram__bytes_read+write, leaf2_kernel<4> C2, 268 MB / (12 leaves x 1024)"}
     line = {
         "metric": f"likelihood evals/s ({args.config}, {cfg.level}-level grid, n_z={cfg.n_z})",
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -388,7 +394,7 @@ def main():
                    "l2": "flushed between steps (256 MiB memset); per-step working set "
                          f"{info.workspace_bytes / 2**30:.2f} GiB > L2"},
         "roofline": {"bound": "tensor", "kernel": top, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "peak_source": FP64_PEAK_SRC,
                      "kernel_share_of_step": top_ms / sum(shares.values()),
                      "algorithmic_flops_per_launch": flops[top] * B},
