@@ -246,24 +246,27 @@ __device__ __forceinline__ double sym(const double* P, int i, int j) {
   return i >= j ? P[tri(i) + j] : P[tri(j) + i];
 }
 
-// Leaf smem layout (doubles): kappa[512] | f[296] | ints (maps 2x256 int16 + col info) [160] |
-// bufA[bufd] | bufB[bufd] | panel[pand]
-static void leaf_sizes(int ncl, int* bufd, int* pand) {
+// Leaf smem layout (doubles): ints (maps 2x256 int16 + col info) [160] | bufA[bufd] |
+// bufB[bufd] (kappa[512] and f[296] alias its head until level 5 writes it) | panel[pand] |
+// staged gather programs of the current level [tabd]
+static void leaf_sizes(int ncl, int* bufd, int* pand, int* tabd = nullptr) {
   const auto& T = leaf_template();
-  int mb = 0, mp = 0;
+  int mb = 808, mp = 0, mt = 0;
   for (int r = 0; r < kLeafLevels; ++r) {
     int nf = 1 << r, k = T[r].k, K = T[r].K, ng = T[r].ng;
-    if (r >= 1) mb = std::max(mb, nf * (k * (k + 1) / 2 + k * ncl + ncl + 2));
-    mp = std::max(mp, nf * ng * ((K + ncl) + (k + ncl) + 2 * ng));
+    if (r >= 1 && r <= 6) mb = std::max(mb, nf * (k * (k + 1) / 2 + k * ncl + ncl + 2));
+    if (r <= 5) mp = std::max(mp, nf * ng * ((K + ncl) + (k + ncl) + 2 * ng));
+    if (r <= 5) mt = std::max(mt, ng * (K + ncl) + k * (k + 1) / 2 + k * ncl);
   }
   *bufd = (mb + 1) & ~1;
   *pand = (mp + 1) & ~1;
+  if (tabd) *tabd = (mt + 1) & ~1;
 }
 
 size_t leaf_smem_bytes(int ncl) {
-  int bufd, pand;
-  leaf_sizes(ncl, &bufd, &pand);
-  return sizeof(double) * (512 + 296 + 160 + 2 * size_t(bufd) + pand);
+  int bufd, pand, tabd;
+  leaf_sizes(ncl, &bufd, &pand, &tabd);
+  return sizeof(double) * (160 + 2 * size_t(bufd) + pand + tabd);
 }
 
 // Panel region layout per level: P [nf][ng][W] | X [nf][ng][k+NC] | Linv [nf][ng][ng]
@@ -278,7 +281,8 @@ __host__ __device__ constexpr int leaf_panel_doubles() {
 template <int R, int NC>
 __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __restrict__ in, double* __restrict__ out,
                                            double* __restrict__ pan, const int16_t* __restrict__ mp,
-                                           const int* __restrict__ cinfo, int leaf, int s, long long leaf_ref) {
+                                           const int* __restrict__ cinfo, int leaf, int s, long long leaf_ref,
+                                           uint64_t* __restrict__ tabs) {
   constexpr LeafLevelShape S = leaf_shape(R);
   constexpr int K = S.K, k = S.k, ng = S.ng, ks = S.ks;
   constexpr int nf = 1 << R;
@@ -301,10 +305,18 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
   double* Xp = pan + nf * ng * W;
   double* Lp = Xp + nf * ng * WX;
 
-  // ---- A: gather the interface panel [A21 | A22 | R_gamma] (precomputed program) ----
+  // ---- stage this level's gather programs into shared memory ----
   constexpr int CI = NC == 2 ? 0 : (NC == 4 ? 1 : 2);
+  constexpr int NPI = ng * W, NUI = ctri(k) + k * NC;
   {
-    const LeafItemP* prog = c_ltab.P[CI] + c_ltab.poff[CI][R];
+    const uint64_t* gp = reinterpret_cast<const uint64_t*>(c_ltab.P[CI] + c_ltab.poff[CI][R]);
+    const uint64_t* gu = reinterpret_cast<const uint64_t*>(c_ltab.U[CI] + c_ltab.uoff[CI][R]);
+    for (int t = tid; t < NPI + NUI; t += NT) tabs[t] = t < NPI ? __ldg(gp + t) : __ldg(gu + (t - NPI));
+  }
+  __syncthreads();
+  // ---- A: gather the interface panel [A21 | A22 | R_gamma] (precomputed program) ----
+  {
+    const LeafItemP* prog = reinterpret_cast<const LeafItemP*>(tabs);
     for (int q = warp / gsz; q < nf; q += qstep) {
       const double* s1 = in + (2 * q) * Sin;
       const double* s2 = in + (2 * q + 1) * Sin;
@@ -381,7 +393,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
   LEAF_TICK(10 + 8 * (5 - R) + 2);
   // ---- D: streamed Schur update out = A~ - A21^T Y; sigma += R_g0^T Y_R ----
   constexpr int E = ctri(k) + k * NC;
-  const LeafItemU* uprog = c_ltab.U[CI] + c_ltab.uoff[CI][R];
+  const LeafItemU* uprog = reinterpret_cast<const LeafItemU*>(tabs + NPI);
   constexpr int UN = 4;    // independent items per thread per iteration (ILP)
   const double inv_area = 1.0 / (double(kLeafCells * kLeafCells) * p.h * p.h);   // exact power of two
   for (int q = warp / gsz; q < nf; q += qstep) {
@@ -461,13 +473,14 @@ __global__ void __launch_bounds__(256, 2) leaf2_kernel(DevPlan p, const int* __r
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NW = 8, NT = 256;
   const DevLeaf& L = p.leaves[leaf];
-  double* kap = sm;
-  double* fl = kap + 512;
-  int16_t* mp = reinterpret_cast<int16_t*>(fl + 296);          // [2][256]
-  int* cinfo = reinterpret_cast<int*>(fl + 296 + 128);           // ctype, br, bq, bg, fslot
-  double* bufA = fl + 296 + 160;
+  int16_t* mp = reinterpret_cast<int16_t*>(sm);                // [2][256]
+  int* cinfo = reinterpret_cast<int*>(sm + 128);                 // ctype, br, bq, bg, fslot
+  double* bufA = sm + 160;
   double* bufB = bufA + bufd;
   double* pan = bufB + bufd;
+  uint64_t* tabs = reinterpret_cast<uint64_t*>(pan + pand);
+  double* kap = bufB;             // aliases bufB until level 5 writes its outputs
+  double* fl = bufB + 512;
   const int N = p.N;
   {
     const double* kb = p.kappa + int64_t(s) * 2 * N * N;
@@ -578,12 +591,12 @@ __global__ void __launch_bounds__(256, 2) leaf2_kernel(DevPlan p, const int* __r
 
   LEAF_TICK(1);
   // ---------------- levels 5..0 in shared memory ----------------
-  leaf_level<5, NC>(p, bufA, bufB, pan, mp, cinfo, leaf, s, L.ref_id);
-  leaf_level<4, NC>(p, bufB, bufA, pan, mp, cinfo, leaf, s, L.ref_id);
-  leaf_level<3, NC>(p, bufA, bufB, pan, mp, cinfo, leaf, s, L.ref_id);
-  leaf_level<2, NC>(p, bufB, bufA, pan, mp, cinfo, leaf, s, L.ref_id);
-  leaf_level<1, NC>(p, bufA, bufB, pan, mp, cinfo, leaf, s, L.ref_id);
-  leaf_level<0, NC>(p, bufB, bufA, pan, mp, cinfo, leaf, s, L.ref_id);
+  leaf_level<5, NC>(p, bufA, bufB, pan, mp, cinfo, leaf, s, L.ref_id, tabs);
+  leaf_level<4, NC>(p, bufB, bufA, pan, mp, cinfo, leaf, s, L.ref_id, tabs);
+  leaf_level<3, NC>(p, bufA, bufB, pan, mp, cinfo, leaf, s, L.ref_id, tabs);
+  leaf_level<2, NC>(p, bufB, bufA, pan, mp, cinfo, leaf, s, L.ref_id, tabs);
+  leaf_level<1, NC>(p, bufA, bufB, pan, mp, cinfo, leaf, s, L.ref_id, tabs);
+  leaf_level<0, NC>(p, bufB, bufA, pan, mp, cinfo, leaf, s, L.ref_id, tabs);
   LEAF_TICK(63);
 }
 
