@@ -893,6 +893,96 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
   }
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Tier-L Schur update: 64 x 64 output tiles, X chunks of 32 interface rows
+// double-buffered HBM -> smem with cp.async, 8 warps as 2 x 4 of 32 x 16 DMMA tiles.
+// E: [2][2][32][kLds] smem (A chunk, B chunk) x double buffer.
+__device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const double* __restrict__ P, int ldp, int k,
+                                                 int ngp, int Kp, int nc, double* __restrict__ out, double* E) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane & 3, gr = lane >> 2;
+  const int ow = k + nc;
+  const int m0 = (warp >> 2) * 32, n0 = (warp & 3) * 16;
+  const int na = (k + 63) / 64, nbt = (ow + 63) / 64;
+  const int nch = ngp / 32;
+  for (int t = 0; t < na * nbt; ++t) {
+    const int a0 = (t / nbt) * 64, b0 = (t % nbt) * 64;
+    if (b0 + 64 <= k && b0 >= a0 + 64) continue;   // strictly upper Psi tile
+    auto stage = [&](int c, int buf) {
+      double* Ea = E + buf * 2 * 32 * kLds;
+      double* Eb = Ea + 32 * kLds;
+      const int g0 = c * 32;
+      for (int tt = tid; tt < 32 * 64; tt += 256) {
+        const int g = tt >> 6, i = tt & 63;
+        const int aa = a0 + i;
+        if (aa < k) cp_async8(Ea + g * kLds + i, P + int64_t(g0 + g) * ldp + aa);
+        else Ea[g * kLds + i] = 0.0;
+        const int bb = b0 + i;
+        const int col = bb < k ? bb : (bb < ow ? Kp + (bb - k) : -1);
+        if (col >= 0) cp_async8(Eb + g * kLds + i, P + int64_t(g0 + g) * ldp + col);
+        else Eb[g * kLds + i] = 0.0;
+      }
+      cp_async_commit();
+    };
+    __syncthreads();
+    stage(0, 0);
+    double pre[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int aa = a0 + m0 + 8 * i + gr;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int bb = b0 + n0 + 8 * j + 2 * gq + e;
+          double v = 0.0;
+          if (aa < k && bb < ow) {
+            if (bb < k) { if (bb <= aa) v = gather_A(mc, aa, bb); }
+            else v = gather_R(mc, aa, bb - k);
+          }
+          pre[i][j][e] = v;
+        }
+    }
+    double acc[4][2][2] = {};
+    for (int c = 0; c < nch; ++c) {
+      if (c + 1 < nch) {
+        stage(c + 1, (c + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const double* Ea = E + (c & 1) * 2 * 32 * kLds;
+      warp_gemm_tn<4, 2>(acc, Ea, kLds, m0, Ea + 32 * kLds, kLds, n0, 32);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int aa = a0 + m0 + 8 * i + gr;
+      if (aa >= k) continue;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int bb = b0 + n0 + 8 * j + 2 * gq + e;
+          if (bb >= ow) continue;
+          if (bb < k) {
+            if (bb <= aa) out[tri(aa) + bb] = pre[i][j][e] - acc[i][j][e];
+          } else {
+            out[tri(k) + aa * nc + (bb - k)] = pre[i][j][e] - acc[i][j][e];
+          }
+        }
+    }
+  }
+}
+
 __device__ __forceinline__ void store_factors(const DevPlan& p, const DevUpper& U, int s, const double* P, int ldp,
                                               int Kp, bool diag_unscaled, int tid, int nthr) {
   const int k = U.k, ng = U.ng;
@@ -963,7 +1053,7 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
     for (int t = warp; t < nrt * nct; t += NWp) {
       const int rt = r0 + NB + (t / nct) * 8;
       const int c0 = (t % nct) * 32;
-      if (c0 >= k && c0 + 32 <= k + r0 + NB) continue;
+      if (c0 >= k && c0 + 32 <= k + rt) continue;     // A22 columns left of the tile rows: never read again
       double acc[1][4][2] = {};
       warp_gemm_tn<1, 4>(acc, P + r0 * ldp + k, ldp, rt, P + r0 * ldp, ldp, c0, NB);
 #pragma unroll
@@ -991,7 +1081,10 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
 
 // -- tier L: panel in HBM ----------------------------------------------------
 size_t merge_l_smem_bytes() {
-  return sizeof(double) * (2 * 32 * kLdd + 32 * kLds + 32 * kLdd + 2 * 32 * kLds) + 1024;
+  // F phases: D/LiT/Xc/Lt; epilogue: 2 buffers x (A, B) chunks of 32 x kLds (reuses the same space)
+  const size_t f = 2 * 32 * kLdd + 32 * kLds + 32 * kLdd;
+  const size_t e = 4 * 32 * kLds;
+  return sizeof(double) * (f > e ? f : e) + 1024;
 }
 
 __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
@@ -1008,8 +1101,6 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
   double* LiT = sm + 32 * kLdd;           // [32][kLdd]
   double* Xc = LiT + 32 * kLdd;           // [32][kLds]
   double* Lt = Xc + 32 * kLds;            // [32][kLdd]
-  double* Ea = Lt + 32 * kLdd;            // [32][kLds]
-  double* Eb = Ea + 32 * kLds;            // [32][kLds]
   __shared__ int s_bad;
   const MergeCtx mc = merge_ctx(p, U, s);
   for (int g = warp; g < ngp; g += 8) gather_panel_row(mc, k, ng, Kp, W, g, P + int64_t(g) * ldp, lane, 32);
@@ -1052,6 +1143,7 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
           Xc[i * kLds + j] = col < W ? P[int64_t(r0 + i) * ldp + col] : 0.0;
         }
         for (int rt = r0 + kLB; rt < ngp; rt += kLB) {
+          if (c0 >= k && c0 + kLC <= k + rt) continue;   // A22 columns left of the tile rows
           for (int t = tid; t < 32 * 32; t += 256) {
             const int h = t >> 5, r = t & 31;
             Lt[h * kLdd + r] = P[int64_t(r0 + h) * ldp + k + rt + r];
@@ -1086,7 +1178,7 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
       for (int g = 0; g < ng; ++g) v = fma(P[int64_t(g) * ldp + Kp], P[int64_t(g) * ldp + Kp + c], v);
     out[tk + k * nc + c] = v;
   }
-  schur_epilogue<false>(mc, P, ldp, k, ngp, Kp, nc, out, Ea, Eb);
+  schur_epilogue_l(mc, P, ldp, k, ngp, Kp, nc, out, sm);
 }
 
 cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,

@@ -297,7 +297,7 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
   {
     int n_points = 0;
     for (int o = 0; o < n_obs; ++o) n_points += births[o].where >= 0;
-    P.mode = d->mode >= 0 ? d->mode : (n_points > 32 ? 1 : 0);
+    P.mode = d->mode >= 0 ? d->mode : (n_points > 384 ? 1 : 0);   // measured crossover
     if (dl == 0) P.mode = 0;     // the root is a kernel leaf: nothing to solve top-down
   }
   const bool primal = P.mode == 1;

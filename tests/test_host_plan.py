@@ -229,7 +229,7 @@ def test_sharded_likelihood_gloo_world2(tmp_path, golden):
 def test_primal_routing_auto_selection():
     """Auto mode: many point observations -> primal top-down (routes 2/3),
     few -> adjoint (root columns), means stay adjoint."""
-    cfg = configs.CONFIGS["C2"]
+    cfg = configs.CONFIGS["C3"]
     p2 = host_problem(cfg.level, cfg.n_z, configs.observations(cfg), mode=-1).plan()
     assert p2.info().mode == 1
     kinds = []
@@ -238,6 +238,7 @@ def test_primal_routing_auto_selection():
         p2.lib.hdd_plan_obs_info(p2.handle, o, C.byref(ob))
         kinds.append(ob.kind)
     assert set(kinds) <= {1, 2, 3} and 2 in kinds and 3 in kinds
-    c1 = configs.CONFIGS["C1"]
-    p1 = host_problem(c1.level, c1.n_z, configs.observations(c1), mode=-1).plan()
-    assert p1.info().mode == 0
+    for name in ("C1", "C2"):
+        c1 = configs.CONFIGS[name]
+        p1 = host_problem(c1.level, c1.n_z, configs.observations(c1), mode=-1).plan()
+        assert p1.info().mode == 0
