@@ -1221,6 +1221,7 @@ __global__ void __launch_bounds__(256) topdown_kernel(DevPlan p, const DevUpper*
   double* uB = sm;              // [k]
   double* y = uB + k;           // [ng]
   double* u = y + ng;           // [ng]
+  double* dblk = u + ng;        // [32][33]
   double* ub = p.ubuf + int64_t(s) * p.u_elems;
   const double* F = p.fac + int64_t(s) * p.fac_elems + U.fac_off;
   // u_B from the father's u_K (cmap entries are father K-indices)
@@ -1247,17 +1248,28 @@ __global__ void __launch_bounds__(256) topdown_kernel(DevPlan p, const DevUpper*
       for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
       if (lane == 0) y[r] -= acc;
     }
+    // stage the diagonal block (coalesced rows) for the serial part
+    {
+      const int nb = i1 - i0;
+      for (int t = tid; t < 32 * 32; t += 256) {
+        const int r = t >> 5, j = t & 31;
+        dblk[r * 33 + j] = (r < nb && j < nb) ? F[int64_t(i0 + r) * fw + k + i0 + j] : 0.0;
+      }
+    }
     __syncthreads();
     if (warp == 0) {
-      for (int r = i1 - 1; r >= i0; --r) {
-        const double* row = F + int64_t(r) * fw + k;
-        double acc = 0.0;
-        const int j = r + 1 + lane;
-        if (j < i1) acc = row[j] * u[j];
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (lane == 0) u[r] = (y[r] - acc) / row[r];
-        __syncwarp();
+      // diagonal block from smem (lane = row), column-oriented back substitution
+      const int nb = i1 - i0;
+      const int row_i = i0 + lane;
+      const double* arow = dblk + lane * 33;
+      double yv = lane < nb ? y[row_i] : 0.0;
+      double uv = 0.0;
+      for (int r = nb - 1; r >= 0; --r) {
+        if (lane == r) uv = yv / arow[r];
+        const double v = __shfl_sync(0xffffffffu, uv, r);
+        if (lane < r) yv = fma(-arow[r], v, yv);
       }
+      if (lane < nb) u[row_i] = uv;
     }
     __syncthreads();
   }
@@ -1268,7 +1280,7 @@ __global__ void __launch_bounds__(256) topdown_kernel(DevPlan p, const DevUpper*
 
 cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_kng,
                            cudaStream_t s) {
-  const size_t smem = sizeof(double) * size_t(max_kng) + 64;
+  const size_t smem = sizeof(double) * (size_t(max_kng) + 32 * 33) + 64;
   cudaError_t e = cudaFuncSetAttribute(topdown_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   dim3 grid(B, n_nodes);
