@@ -78,6 +78,11 @@ typedef struct {
                               the root, functionals.py:138-224), 1 primal
                               (points by the top-down interface back-solve,
                               hdd.py:397-432, restricted to what F needs)     */
+  /* low-rank storage of the boundary maps (reference ToleranceSpec,
+   * lowrank.py:20-30; hdd.py:280-286): eps <= 0 disables it               */
+  double lr_eps;
+  int32_t lr_kmax;
+  int32_t lr_nmin;
 } HddPlanDesc;
 
 typedef struct {

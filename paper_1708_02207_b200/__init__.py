@@ -12,6 +12,7 @@ from .bayes import (  # noqa: F401
     ParamField,
     Prior,
     SineKLField,
+    ToleranceSpec,
     aligned_partition,
     forward_functionals,
     forward_functionals_batch,

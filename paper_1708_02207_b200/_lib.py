@@ -35,7 +35,7 @@ class HddPlanDesc(C.Structure):
         ("n_obs", C.c_int32), ("obs_kind", _i32p), ("obs_id", _i64p),
         ("sigma", _f64p), ("y", _f64p),
         ("max_batch", C.c_int32), ("device", C.c_int32), ("keep_nodes", C.c_int32),
-        ("mode", C.c_int32),
+        ("mode", C.c_int32), ("lr_eps", C.c_double), ("lr_kmax", C.c_int32), ("lr_nmin", C.c_int32),
     ]
 
 

@@ -33,7 +33,7 @@ from .errors import ConfigError, UsageError
 from .geometry import DDTree, Mesh, Rect, cell_centroid_tables
 
 __all__ = [
-    "ParamField", "SineKLField", "Prior", "MeasurementModel", "BayesProblem", "mean_observations",
+    "ParamField", "SineKLField", "Prior", "ToleranceSpec", "MeasurementModel", "BayesProblem", "mean_observations",
     "aligned_partition", "kl_pairs", "forward_functionals", "forward_functionals_batch", "log_likelihood",
     "log_likelihood_batch", "gaussian_log_likelihood", "posterior_weights",
 ]
@@ -144,6 +144,21 @@ class ParamField(_Separable):
 
 
 @dataclass(frozen=True)
+class ToleranceSpec:
+    """Truncation tolerance (relative Frobenius), rank cap and dense-block size
+    of the low-rank map storage (lowrank.py:20-30).  The device path caps the
+    rank at 24 (sketch width 32)."""
+
+    eps: float = 1e-6
+    k_max: int = 64
+    n_min: int = 32
+
+    def __post_init__(self):
+        if self.eps < 0 or self.n_min < 1 or self.k_max < 1:
+            raise UsageError("invalid tolerance spec")
+
+
+@dataclass(frozen=True)
 class Prior:
     """Independent per-component prior, standard normal or uniform (bayes.py:80-120)."""
 
@@ -244,7 +259,10 @@ class _Plan:
             sx=ptr(k["sx"], _lib._f64p), sy=ptr(k["sy"], _lib._f64p), coef=ptr(k["coef"], _lib._f64p),
             f=ptr(k["f"], _lib._f64p), n_obs=len(obs), obs_kind=ptr(k["kind"], _lib._i32p),
             obs_id=ptr(k["ids"], _lib._i64p), sigma=ptr(k["sigma"], _lib._f64p), y=ptr(k["y"], _lib._f64p),
-            max_batch=int(max_batch), device=int(device), keep_nodes=int(keep_nodes), mode=int(mode))
+            max_batch=int(max_batch), device=int(device), keep_nodes=int(keep_nodes), mode=int(mode),
+            lr_eps=float(getattr(problem.compression, "eps", 0.0) or 0.0) if problem.compression is not None else 0.0,
+            lr_kmax=int(getattr(problem.compression, "k_max", 64)) if problem.compression is not None else 0,
+            lr_nmin=int(getattr(problem.compression, "n_min", 32)) if problem.compression is not None else 0)
         h = C.c_void_p()
         rc = L.hdd_plan_create(C.byref(desc), C.byref(h))
         if rc != _lib.HDD_OK:
@@ -282,9 +300,11 @@ class _Plan:
 class BayesProblem:
     """Forward setup shared by every likelihood evaluation (bayes.py:155-177).
 
-    `compression` (a ToleranceSpec) is accepted for API compatibility; the
-    device path computes the maps densely, i.e. exactly, which is within every
-    truncation tolerance of the reference low-rank path.  `device` selects the
+    `compression` (a ToleranceSpec) switches on the low-rank storage of the
+    boundary maps Psi: every admissible block of every node with more than
+    n_min boundary nodes is replaced by its rank-truncated form, as the
+    reference does (hdd.py:280-286), by the batched randomized truncated-SVD
+    kernel (csrc/hdd_kernels.cu, K5).  `device` selects the
     CUDA device; `max_batch` caps the internal sub-batch (0 = size to memory).
     """
 

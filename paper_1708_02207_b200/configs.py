@@ -81,7 +81,9 @@ def observed_data(cfg: Config):
 
 
 def make_problem(name: str, device: int = 0, max_batch: int = 0, with_data: bool = True,
-                 mode: int = -1) -> BayesProblem:
+                 mode: int = -1, compression=False) -> BayesProblem:
+    """`compression=True` applies the config's ToleranceSpec (C5: eps 1e-6,
+    k_max 16, n_min 32); a ToleranceSpec instance is used as given."""
     cfg = CONFIGS[name]
     mesh = build_mesh(cfg.level)
     tree = build_tree(mesh)
@@ -91,5 +93,11 @@ def make_problem(name: str, device: int = 0, max_batch: int = 0, with_data: bool
     else:
         y, sigma = None, np.full(len(obs), cfg.sigma)
     model = MeasurementModel(obs, sigma, y)
+    tol = None
+    if compression is True and cfg.compression is not None:
+        from .bayes import ToleranceSpec
+        tol = ToleranceSpec(*cfg.compression)
+    elif compression not in (None, False, True):
+        tol = compression
     return BayesProblem(tree, SineKLField(tree, cfg.n_z), np.ones(mesh.n_nodes), np.zeros(4 * mesh.n_cells),
-                        model, device=device, max_batch=max_batch, mode=mode)
+                        model, compression=tol, device=device, max_batch=max_batch, mode=mode)

@@ -32,6 +32,7 @@ struct HddPlan {
   std::vector<int> depth_rows;         // max k + ngp over the depth's nodes
   std::vector<int> depth_nb;           // elimination block rows (8 or 32)
   std::vector<int> depth_kng;          // max k + 2 ng (top-down smem)
+  std::vector<int> lr_blk0, lr_nblk, lr_pmax;   // low-rank blocks per depth
   double* ws = nullptr;                // tier-L workspace
   size_t leaf_smem = 0;
   HddError err{};
@@ -220,6 +221,60 @@ static int setup_device(HddPlan* pl, int max_batch) {
   if ((rc = upload(pl, ccoef, &D.ccoef))) return rc;
   if ((rc = upload(pl, cbirth, &D.cbirth))) return rc;
   if ((rc = upload(pl, cmapool, &D.cmap))) return rc;
+  // low-rank block lists, grouped by depth (node index local to the depth launch)
+  D.lr_eps = P.lr_eps;
+  D.lr_kmax = P.lr_kmax;
+  D.lr_l = std::min(32, P.lr_kmax + 8);
+  pl->lr_blk0.assign(P.upper_by_depth.size(), 0);
+  pl->lr_nblk.assign(P.upper_by_depth.size(), 0);
+  pl->lr_pmax.assign(P.upper_by_depth.size(), 0);
+  int lr_qmax = 0;
+  int lr_nodes_max = 0;
+  if (P.lr_eps > 0) {
+    std::vector<int32_t> rows, cols, blk;
+    for (size_t dep = 0; dep < P.upper_by_depth.size(); ++dep) {
+      const auto& ids = P.upper_by_depth[dep];
+      lr_nodes_max = std::max(lr_nodes_max, int(ids.size()));
+      pl->lr_blk0[dep] = int(blk.size() / 5);
+      for (size_t li = 0; li < ids.size(); ++li) {
+        const UpperNode& U = P.upper[ids[li]];
+        for (size_t b = 0; b + 3 < U.lr_desc.size(); b += 4) {
+          blk.push_back(int32_t(li));
+          blk.push_back(int32_t(rows.size()));
+          blk.push_back(U.lr_desc[b + 1]);
+          blk.push_back(int32_t(cols.size()));
+          blk.push_back(U.lr_desc[b + 3]);
+          rows.insert(rows.end(), U.lr_rows.begin() + U.lr_desc[b], U.lr_rows.begin() + U.lr_desc[b] + U.lr_desc[b + 1]);
+          cols.insert(cols.end(), U.lr_cols.begin() + U.lr_desc[b + 2], U.lr_cols.begin() + U.lr_desc[b + 2] + U.lr_desc[b + 3]);
+          pl->lr_pmax[dep] = std::max(pl->lr_pmax[dep], int(U.lr_desc[b + 1]));
+          lr_qmax = std::max(lr_qmax, int(U.lr_desc[b + 3]));
+        }
+      }
+      pl->lr_nblk[dep] = int(blk.size() / 5) - pl->lr_blk0[dep];
+      if (pl->lr_pmax[dep] > 760)
+        return set_err(&pl->err, HDD_ERR_CONFIG, "low-rank block with more than 760 rows does not fit the device sketch");
+    }
+    if ((rc = upload(pl, rows, &D.lr_rows))) return rc;
+    if ((rc = upload(pl, cols, &D.lr_cols))) return rc;
+    if ((rc = upload(pl, blk, &D.lr_blk))) return rc;
+    // fixed Gaussian test matrix (deterministic: splitmix64 + Box-Muller)
+    std::vector<double> om(size_t(std::max(lr_qmax, 1)) * 32);
+    uint64_t st = 0x9E3779B97F4A7C15ull;
+    auto next = [&]() {
+      st += 0x9E3779B97F4A7C15ull;
+      uint64_t z = st;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      return double((z ^ (z >> 31)) >> 11) * (1.0 / 9007199254740992.0);
+    };
+    for (size_t i = 0; i < om.size(); i += 2) {
+      const double u1 = std::max(next(), 1e-300), u2 = next();
+      const double rr = std::sqrt(-2.0 * std::log(u1));
+      om[i] = rr * std::cos(2.0 * M_PI * u2);
+      if (i + 1 < om.size()) om[i + 1] = rr * std::sin(2.0 * M_PI * u2);
+    }
+    if ((rc = upload(pl, om, &D.lr_omega))) return rc;
+  }
   {
     const DevUpper* du = nullptr;
     if ((rc = upload(pl, pl->h_upper, &du))) return rc;
@@ -281,6 +336,13 @@ static int setup_device(HddPlan* pl, int max_batch) {
     }
     pl->allocs.push_back(p);
     D.buf[b] = static_cast<double*>(p);
+  }
+  D.lr_scale = nullptr;
+  if (P.lr_eps > 0) {
+    void* q = nullptr;
+    CU(cudaMalloc(&q, sizeof(double) * size_t(std::max(lr_nodes_max, 1)) * bcap));
+    pl->allocs.push_back(q);
+    D.lr_scale = static_cast<double*>(q);
   }
   D.fac = D.ubuf = D.fbuf = nullptr;
   for (auto pr : {std::make_pair(&D.fac, P.fac_elems), std::make_pair(&D.ubuf, P.u_elems),
@@ -399,9 +461,13 @@ static int run_sub_batch(HddPlan* pl, const double* Z, int B, double* S, double*
   if (ev) CU(cudaEventRecord(ev[e++], st));
   for (int dep = int(P.upper_by_depth.size()) - 1; dep >= 0; --dep) {
     const auto& ids = P.upper_by_depth[dep];
-    if (!ids.empty())
+    if (!ids.empty()) {
       CU(launch_merge(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->ws, pl->depth_ws[dep],
                       pl->depth_tier[dep], pl->depth_rows[dep], pl->depth_smem[dep], pl->depth_nb[dep], st));
+      if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0)
+        CU(launch_compress(D, pl->d_upper + ids.front(), int(ids.size()), pl->lr_blk0[dep], pl->lr_nblk[dep], B,
+                           pl->lr_pmax[dep], st));
+    }
     if (ev) CU(cudaEventRecord(ev[e++], st));
   }
   if (D.mode == 1) {

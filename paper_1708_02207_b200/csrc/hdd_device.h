@@ -70,6 +70,14 @@ struct DevPlan {
   const int32_t* route_node;
   const int32_t* route_slot;
   int mode;                // 0 adjoint, 1 primal
+  // low-rank (H-matrix) storage of the boundary maps
+  double lr_eps;
+  int lr_kmax, lr_l;       // rank cap, sketch width (k_max + 8 <= 32)
+  const int32_t* lr_rows;  // position pools
+  const int32_t* lr_cols;
+  const int32_t* lr_blk;   // [n][5]: node (depth-local), row offset, p, col offset, q
+  const double* lr_omega;  // [q_max][32] fixed Gaussian test matrix
+  double* lr_scale;        // [max nodes per depth][bcap]  ||Psi||_F^2
   int64_t fac_elems, u_elems;
   int n_fslots;
   double* fac;             // [bcap][fac_elems]  W | L^T | v rows of every upper node
@@ -96,6 +104,8 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
                          int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s);
 size_t merge_m2_smem_bytes(int ngp, int ldp);
 size_t merge_l_smem_bytes();
+cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int blk0, int nblk, int B,
+                            int pmax, cudaStream_t s);
 cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_ng, cudaStream_t s);
 cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cudaStream_t s);
 size_t leaf_smem_bytes(int leaf_cols);

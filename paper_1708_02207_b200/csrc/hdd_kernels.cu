@@ -1278,6 +1278,261 @@ __global__ void __launch_bounds__(256) topdown_kernel(DevPlan p, const DevUpper*
   for (int g = tid; g < ng; g += 256) mine[k + g] = u[g];
 }
 
+// ---------------------------------------------------------------------------
+// K5: low-rank storage of Psi (lowrank.py:52-77 compress, :155-179 partition,
+// hdd.py:280-286).  For every admissible (disjoint-bbox) block A (p x q) of a
+// large node's Psi and every sample: randomized range finder Y = A Omega
+// (Omega q x l Gaussian, l = k_max + 8), Q = orth(Y) by shifted CholeskyQR2,
+// B = Q^T A, pivoted Cholesky of M = B B^T gives a rank-k A_k = (Q C)(L_SS^-1 B_S)
+// with EXACT error ||A - A_k||_F^2 = ||A||^2 - ||B||^2 + trace(Schur_k).  k is the
+// smallest rank meeting the reference's relative Frobenius criterion eps; the
+// block stays dense when k > k_max or k (p + q) >= p q (the reference's rule);
+// ||A|| <= 1e-14 ||Psi|| collapses the block to rank 0.  The node's maps are then
+// the re-densified compressed maps, as in the reference (hdd.py:227-228).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) psi_norm_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int n_nodes) {
+  const DevUpper& U = nodes[blockIdx.y];
+  const int s = blockIdx.x;
+  const double* psi = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
+  const int k = U.k;
+  const int n = tri(k);
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < n; t += 256) {
+    int a = int((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+    if (tri(a + 1) <= t) ++a;
+    if (tri(a) > t) --a;
+    const double v = psi[t];
+    acc += (t - tri(a) == a) ? v * v : 2.0 * v * v;
+  }
+  __shared__ double red[8];
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t2 = 0.0;
+    for (int w = 0; w < 8; ++w) t2 += red[w];
+    p.lr_scale[int64_t(blockIdx.y) * p.bcap + s] = t2;
+  }
+}
+
+__global__ void __launch_bounds__(256) compress_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int blk0) {
+  extern __shared__ __align__(16) double sm[];
+  const int32_t* bd = p.lr_blk + 5 * (blk0 + blockIdx.y);
+  const int ln = bd[0], roff = bd[1], P_ = bd[2], coff = bd[3], Q_ = bd[4];
+  const DevUpper& U = nodes[ln];
+  const int s = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int L = p.lr_l;
+  double* psi = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
+  const int32_t* R = p.lr_rows + roff;
+  const int32_t* Cc = p.lr_cols + coff;
+  double* Y = sm;                         // [P_][33]
+  double* G = Y + size_t(P_) * 33;        // [32][kLdd] gram / pivoted factor C
+  double* LiT = G + 32 * kLdd;            // [32][kLdd]
+  double* Bc = LiT + 32 * kLdd;           // [32][65] chunk of B (or D)
+  double* red = Bc + 32 * 65;             // [64]
+  __shared__ int s_bad, s_k, s_piv[32];
+  __shared__ double s_an2, s_bn2;
+  auto A = [&](int i, int j) { const int r = R[i], c = Cc[j]; return r >= c ? psi[tri(r) + c] : psi[tri(c) + r]; };
+  // ---- pass 1: Y = A Omega, ||A||^2 ----
+  double an = 0.0;
+  for (int i = tid; i < P_; i += 256) {
+    double y[32];
+#pragma unroll
+    for (int t = 0; t < 32; ++t) y[t] = 0.0;
+    for (int j = 0; j < Q_; ++j) {
+      const double a = A(i, j);
+      an = fma(a, a, an);
+      const double* om = p.lr_omega + j * 32;
+#pragma unroll
+      for (int t = 0; t < 32; ++t) y[t] = fma(a, om[t], y[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < 32; ++t) Y[i * 33 + t] = t < L ? y[t] : 0.0;
+  }
+  for (int off = 16; off > 0; off >>= 1) an += __shfl_xor_sync(0xffffffffu, an, off);
+  if (lane == 0) red[warp] = an;
+  __syncthreads();
+  if (tid == 0) {
+    double t2 = 0.0;
+    for (int w = 0; w < 8; ++w) t2 += red[w];
+    s_an2 = t2;
+  }
+  __syncthreads();
+  const double an2 = s_an2;
+  const double scale2 = p.lr_scale[int64_t(ln) * p.bcap + s];
+  if (an2 <= 1e-28 * scale2) {          // ||A|| <= 1e-14 ||Psi||: rank 0
+    for (int t = tid; t < P_ * Q_; t += 256) {
+      const int i = t / Q_, j = t - i * Q_;
+      const int r = R[i], c = Cc[j];
+      psi[r >= c ? tri(r) + c : tri(c) + r] = 0.0;
+    }
+    return;
+  }
+  // ---- shifted CholeskyQR2: Q = Y R^-1 (in place) ----
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int t = tid; t < 32 * 32; t += 256) {
+      const int a = t >> 5, b = t & 31;
+      double v = 0.0;
+      if (a < L && b < L)
+        for (int i = 0; i < P_; ++i) v = fma(Y[i * 33 + a], Y[i * 33 + b], v);
+      G[a * kLdd + b] = v;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double tr = 0.0;
+      for (int a = 0; a < L; ++a) tr += G[a * kLdd + a];
+      const double shift = 1e-13 * tr + 1e-300;
+      for (int a = 0; a < 32; ++a) G[a * kLdd + a] = a < L ? G[a * kLdd + a] + shift : 1.0;
+      s_bad = 0;
+    }
+    __syncthreads();
+    if (warp == 0) factor_diag_block<32>(G, kLdd, LiT, &s_bad);
+    __syncthreads();
+    for (int i = tid; i < P_; i += 256) {
+      double y[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) y[t] = Y[i * 33 + t];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        double v = 0.0;
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+          if (t <= c) v = fma(y[t], LiT[t * kLdd + c], v);
+        Y[i * 33 + c] = c < L ? v : 0.0;
+      }
+    }
+    __syncthreads();
+  }
+  // ---- pass 2: M = B B^T with B = Q^T A, in 64-column chunks ----
+  for (int t = tid; t < 32 * 32; t += 256) G[(t >> 5) * kLdd + (t & 31)] = 0.0;
+  double macc[4] = {0.0, 0.0, 0.0, 0.0};     // thread owns M entries tid + 256 u
+  for (int j0 = 0; j0 < Q_; j0 += 64) {
+    __syncthreads();
+    for (int t = tid; t < 32 * 64; t += 256) {
+      const int a = t >> 6, jj = t & 63, j = j0 + jj;
+      double v = 0.0;
+      if (a < L && j < Q_)
+        for (int i = 0; i < P_; ++i) v = fma(Y[i * 33 + a], A(i, j), v);
+      Bc[a * 65 + jj] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = tid + 256 * u, a = e >> 5, b = e & 31;
+      if (a < L && b < L)
+        for (int jj = 0; jj < 64; ++jj) macc[u] = fma(Bc[a * 65 + jj], Bc[b * 65 + jj], macc[u]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = tid + 256 * u;
+    G[(e >> 5) * kLdd + (e & 31)] = macc[u];
+  }
+  __syncthreads();
+  // ---- pivoted Cholesky of M (one warp): rank decision ----
+  if (warp == 0) {
+    double bn2 = 0.0;
+    for (int a = 0; a < L; ++a) bn2 += G[a * kLdd + a];
+    double dg = lane < L ? G[lane * kLdd + lane] : -1.0;   // residual diagonal
+    bool used = lane >= L;
+    const double budget = p.lr_eps * p.lr_eps * an2;
+    double resid = fmax(an2 - bn2, 0.0);
+    double trace = 0.0;
+    for (int a = 0; a < L; ++a) trace += G[a * kLdd + a];
+    int kk = 0;
+    // C column t stored in LiT[.][t] (LiT reused as the pivoted factor C, rows = original index)
+    while (kk < L && !(resid + trace <= budget)) {
+      double best = used ? -1.0 : dg;
+      int bi = lane;
+      for (int off = 16; off > 0; off >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (best <= 0.0) break;
+      const int piv = bi;
+      const double sq = sqrt(best);
+      double v = 0.0;
+      if (!used || lane == piv) {
+        v = G[lane * kLdd + piv];
+        for (int u = 0; u < kk; ++u) v = fma(-LiT[lane * kLdd + u], LiT[piv * kLdd + u], v);
+        v /= sq;
+      }
+      __syncwarp();
+      if (lane < 32) LiT[lane * kLdd + kk] = (lane == piv) ? sq : ((used && lane != piv) ? 0.0 : v);
+      if (lane == piv) used = true;
+      if (!used) dg -= v * v;
+      if (lane == 0) s_piv[kk] = piv;
+      trace = 0.0;
+      {
+        double mine = used ? 0.0 : fmax(dg, 0.0);
+        for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
+        trace = mine;
+      }
+      ++kk;
+      __syncwarp();
+    }
+    if (lane == 0) { s_k = kk; s_bn2 = bn2; }
+  }
+  __syncthreads();
+  const int kk = s_k;
+  if (kk > p.lr_kmax || int64_t(kk) * (P_ + Q_) >= int64_t(P_) * Q_) return;   // stays dense
+  // ---- pass 3: A_k = Q (C D) with D = L_SS^-1 B_S, per 64-column chunk ----
+  double* Ec = red + 64;                  // [32][65]
+  for (int j0 = 0; j0 < Q_; j0 += 64) {
+    for (int t = tid; t < 32 * 64; t += 256) {
+      const int u = t >> 6, jj = t & 63, j = j0 + jj;
+      double v = 0.0;
+      if (u < kk && j < Q_) {
+        const int a = s_piv[u];
+        for (int i = 0; i < P_; ++i) v = fma(Y[i * 33 + a], A(i, j), v);   // B[a][j]
+      }
+      Bc[u * 65 + jj] = v;
+    }
+    __syncthreads();
+    for (int jj = tid; jj < 64; jj += 256) {      // forward substitution with L_SS
+      for (int u = 0; u < kk; ++u) {
+        double v = Bc[u * 65 + jj];
+        for (int w = 0; w < u; ++w) v = fma(-LiT[s_piv[u] * kLdd + w], Bc[w * 65 + jj], v);
+        Bc[u * 65 + jj] = v / LiT[s_piv[u] * kLdd + u];
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < 32 * 64; t += 256) {    // E = C D  (L x 64)
+      const int a = t >> 6, jj = t & 63;
+      double v = 0.0;
+      if (a < L)
+        for (int u = 0; u < kk; ++u) v = fma(LiT[a * kLdd + u], Bc[u * 65 + jj], v);
+      Ec[a * 65 + jj] = v;
+    }
+    __syncthreads();
+    for (int t = tid; t < P_ * 64; t += 256) {
+      const int i = t >> 6, jj = t & 63, j = j0 + jj;
+      if (j >= Q_) continue;
+      double v = 0.0;
+      for (int a = 0; a < L; ++a) v = fma(Y[i * 33 + a], Ec[a * 65 + jj], v);
+      const int r = R[i], c = Cc[j];
+      psi[r >= c ? tri(r) + c : tri(c) + r] = v;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int blk0, int nblk, int B,
+                            int pmax, cudaStream_t s) {
+  psi_norm_kernel<<<dim3(B, n_nodes), 256, 0, s>>>(p, nodes_dev, n_nodes);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (nblk == 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * (size_t(pmax) * 33 + 2 * 32 * kLdd + 2 * 32 * 65 + 64) + 64;
+  e = cudaFuncSetAttribute(compress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  compress_kernel<<<dim3(B, nblk), 256, smem, s>>>(p, nodes_dev, blk0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_kng,
                            cudaStream_t s) {
   const size_t smem = sizeof(double) * (size_t(max_kng) + 32 * 33) + 64;

@@ -83,6 +83,67 @@ int find_pos(const std::vector<int64_t>& sorted, int64_t id) {
 
 int64_t subtree_size(int level, int depth) { return (int64_t(1) << (2 * level - depth + 1)) - 1; }
 
+// Geometric cluster tree over point positions (lowrank.py:101-115): split at the
+// bbox midpoint of the longer axis (x on ties), fall back to sorted halves.
+struct Cluster {
+  std::vector<int32_t> pos;
+  double bb[4];          // xmin, xmax, ymin, ymax
+  int child[2] = {-1, -1};
+};
+
+int build_cluster(std::vector<Cluster>& cl, std::vector<int32_t> pos, const std::vector<double>& x,
+                  const std::vector<double>& y, int n_min) {
+  Cluster c;
+  c.bb[0] = c.bb[2] = 1e300;
+  c.bb[1] = c.bb[3] = -1e300;
+  for (int p : pos) {
+    c.bb[0] = std::min(c.bb[0], x[p]); c.bb[1] = std::max(c.bb[1], x[p]);
+    c.bb[2] = std::min(c.bb[2], y[p]); c.bb[3] = std::max(c.bb[3], y[p]);
+  }
+  c.pos = pos;
+  const int me = int(cl.size());
+  cl.push_back(c);
+  if (int(pos.size()) <= n_min) return me;
+  const bool ax = (c.bb[1] - c.bb[0]) >= (c.bb[3] - c.bb[2]);
+  const double mid = ax ? 0.5 * (c.bb[0] + c.bb[1]) : 0.5 * (c.bb[2] + c.bb[3]);
+  std::vector<int32_t> l, r;
+  for (int p : pos) ((ax ? x[p] : y[p]) < mid ? l : r).push_back(p);
+  if (l.empty() || r.empty()) {
+    std::vector<int32_t> srt = pos;
+    std::stable_sort(srt.begin(), srt.end(), [&](int a, int b) { return (ax ? x[a] : y[a]) < (ax ? x[b] : y[b]); });
+    l.assign(srt.begin(), srt.begin() + srt.size() / 2);
+    r.assign(srt.begin() + srt.size() / 2, srt.end());
+    // keep the original relative order inside each half (reference uses pos[left])
+    std::vector<char> inl(x.size(), 0);
+    for (int p : l) inl[p] = 1;
+    l.clear(); r.clear();
+    for (int p : pos) (inl[p] ? l : r).push_back(p);
+  }
+  const int a = build_cluster(cl, l, x, y, n_min);
+  const int b = build_cluster(cl, r, x, y, n_min);
+  cl[me].child[0] = a;
+  cl[me].child[1] = b;
+  return me;
+}
+
+bool disjoint(const Cluster& a, const Cluster& b) {
+  return a.bb[1] < b.bb[0] || b.bb[1] < a.bb[0] || a.bb[3] < b.bb[2] || b.bb[3] < a.bb[2];
+}
+
+// Admissible (disjoint-bbox) block pairs of the partition (lowrank.py:166-179).
+void collect_blocks(const std::vector<Cluster>& cl, int rc, int cc, std::vector<std::pair<int, int>>& out) {
+  const Cluster& R = cl[rc];
+  const Cluster& Cc = cl[cc];
+  if (R.pos.empty() || Cc.pos.empty()) return;
+  if (disjoint(R, Cc)) { out.push_back({rc, cc}); return; }
+  const bool rl = R.child[0] < 0, cl_ = Cc.child[0] < 0;
+  if (rl && cl_) return;   // dense leaf block
+  std::vector<int> rch = rl ? std::vector<int>{rc} : std::vector<int>{R.child[0], R.child[1]};
+  std::vector<int> cch = cl_ ? std::vector<int>{cc} : std::vector<int>{Cc.child[0], Cc.child[1]};
+  for (int a : rch)
+    for (int b : cch) collect_blocks(cl, a, b, out);
+}
+
 }  // namespace
 
 int64_t postorder_id(int level, const std::vector<int>& path) {
@@ -418,6 +479,39 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     P.route[o] = ObsRoute{0, it->second, 0.0};
   }
   P.root_nc = dl > 0 ? P.upper[P.root].nc : int(P.leaves[0].cols.size());
+
+  // ---- low-rank block structure of every large Psi (hdd.py:280-286) -------
+  P.lr_eps = d->lr_eps > 0 ? d->lr_eps : 0.0;
+  P.lr_kmax = d->lr_kmax > 0 ? d->lr_kmax : 64;
+  P.lr_nmin = d->lr_nmin > 0 ? d->lr_nmin : 32;
+  if (P.lr_eps > 0) {
+    P.lr_kmax = std::min(P.lr_kmax, 24);   // device sketch width 32 = k_max + 8
+    for (UpperNode& U : P.upper) {
+      if (U.k <= P.lr_nmin) continue;
+      std::vector<double> x(U.k), y(U.k);
+      for (int i = 0; i < U.k; ++i) { x[i] = double(U.bnd[i] % m) * P.h; y[i] = double(U.bnd[i] / m) * P.h; }
+      std::vector<Cluster> cl;
+      std::vector<int32_t> all(U.k);
+      for (int i = 0; i < U.k; ++i) all[i] = i;
+      const int root = build_cluster(cl, all, x, y, P.lr_nmin);
+      std::vector<std::pair<int, int>> blocks;
+      collect_blocks(cl, root, root, blocks);
+      for (auto& b : blocks) {
+        const auto& R = cl[b.first].pos;
+        const auto& Cc = cl[b.second].pos;
+        // Psi is symmetric: keep one block of each transposed pair, rows = the smaller cluster
+        if (*std::min_element(R.begin(), R.end()) > *std::min_element(Cc.begin(), Cc.end())) continue;
+        const auto& rr = R.size() <= Cc.size() ? R : Cc;
+        const auto& cc = R.size() <= Cc.size() ? Cc : R;
+        U.lr_desc.push_back(int32_t(U.lr_rows.size()));
+        U.lr_desc.push_back(int32_t(rr.size()));
+        U.lr_desc.push_back(int32_t(U.lr_cols.size()));
+        U.lr_desc.push_back(int32_t(cc.size()));
+        U.lr_rows.insert(U.lr_rows.end(), rr.begin(), rr.end());
+        U.lr_cols.insert(U.lr_cols.end(), cc.begin(), cc.end());
+      }
+    }
+  }
 
   // ---- father links and child-boundary maps (primal top-down) -------------
   for (int u = 0; u < int(P.upper.size()); ++u) {

@@ -39,6 +39,9 @@ struct UpperNode {
   std::vector<double> ccoef;    // [nc][2]
   std::vector<int32_t> cbirth;  // [nc]
   std::vector<Col> cols;
+  // low-rank blocks of Psi (admissible pairs of the boundary cluster tree)
+  std::vector<int32_t> lr_rows, lr_cols;   // concatenated position lists
+  std::vector<int32_t> lr_desc;            // [n][4]: row offset, p, col offset, q
   // output layout (per sample): rows k, leading dim ld, then nc sigmas
   int out_ld = 0;
   int64_t out_elems = 0;
@@ -96,6 +99,8 @@ struct Plan {
   int root_nc = 0;
   int n_buffers = 2;
   int mode = 0;                               // 0 adjoint (functionals to the root), 1 primal top-down
+  double lr_eps = 0.0;                        // low-rank truncation (0 = dense maps)
+  int lr_kmax = 64, lr_nmin = 32;
   int n_fslots = 0;                           // leaf point functionals kept for the top-down pass
   int64_t fac_elems = 0, u_elems = 0;         // per-sample sizes of the primal buffers
   std::vector<int64_t> buf_elems_per_sample;  // per buffer
