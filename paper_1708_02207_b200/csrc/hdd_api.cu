@@ -214,6 +214,13 @@ static int setup_device(HddPlan* pl, int max_batch) {
     ccoef.insert(ccoef.end(), U.ccoef.begin(), U.ccoef.end());
     cbirth.insert(cbirth.end(), U.cbirth.begin(), U.cbirth.end());
     size_t sm = pl->depth_tier[U.depth] ? 0 : merge_m2_smem_bytes(ngp_u, d.ldp);
+    if (!pl->depth_tier[U.depth]) {
+      // stage the sons in smem when panel + sons still allow two CTAs per SM
+      const size_t sons = sizeof(double) * size_t(((d.son_elems[0] + 1) & ~1) + ((d.son_elems[1] + 1) & ~1));
+      // measured: pays off only on the first merge level (sons = kernel leaves)
+      d.stage = (U.son[0] < 0 && U.son[1] < 0 && sm + sons <= 110 * 1024) ? 1 : 0;
+      if (d.stage) sm += sons;
+    }
     pl->depth_smem[U.depth] = std::max(pl->depth_smem[U.depth], sm);
   }
   if ((rc = upload(pl, gmap, &D.gmap))) return rc;

@@ -11,7 +11,8 @@ constexpr int kMaxBuffers = 24;
 struct DevUpper {
   int k, ng, K, nc;
   int ldp;                 // panel leading dimension
-  int nb;                  // elimination block rows (16 or 32); panel rows = ng rounded up to nb
+  int nb;                  // elimination block rows (8 or 32); panel rows = ng rounded up to nb
+  int stage;               // tier M: stage both sons' outputs in shared memory
   int out_ld;
   int64_t out_elems, out_off;
   int buf;

@@ -1076,7 +1076,20 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
   double* P = sm;                          // [ngp][ldp]
   double* piv = P + size_t(ngp) * ldp;     // [NB] pivots of the current block
   __shared__ int s_bad;
-  const MergeCtx mc = merge_ctx(p, U, s);
+  MergeCtx mc = merge_ctx(p, U, s);
+  if (U.stage) {
+    // stage both sons' packed outputs in shared memory (coalesced 16-byte copies)
+    double* st = piv + 8;
+#pragma unroll
+    for (int sn = 0; sn < 2; ++sn) {
+      const int n = int(U.son_elems[sn]);
+      const double* src = mc.sv[sn].b;
+      for (int t = tid; t < n; t += NT) st[t] = __ldg(src + t);
+      mc.sv[sn].b = st;
+      st += (n + 1) & ~1;
+    }
+    __syncthreads();
+  }
   for (int g = warp; g < ngp; g += NWp) gather_panel_row(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   const int gq = lane & 3, gr = lane >> 2;
