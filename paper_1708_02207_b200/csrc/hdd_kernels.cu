@@ -108,6 +108,9 @@ struct LeafTmplDev {
 __constant__ LeafTmplDev c_tmpl;
 __constant__ int16_t c_map[2][256];
 __constant__ uint16_t c_orig[512];   // in-leaf node origin (x | y << 8), index 2^r - 1 + q
+// lower-triangle tile coordinates of tile index tt (row-major over the triangle)
+__constant__ uint8_t c_tile_i[64];
+__constant__ uint8_t c_tile_j[64];
 
 // Precomputed per-level gather programs of the leaf kernel (one set per column
 // class NC = 2, 4, 8): every panel / update item of level r knows its source
@@ -225,6 +228,13 @@ int upload_leaf_template() {
   if (cudaMemcpyToSymbol(c_tmpl, &t, sizeof(t)) != cudaSuccess) return -1;
   if (cudaMemcpyToSymbol(c_map, maps, sizeof(maps)) != cudaSuccess) return -1;
   if (cudaMemcpyToSymbol(c_orig, orig, sizeof(orig)) != cudaSuccess) return -1;
+  {
+    uint8_t ti[64] = {}, tj[64] = {};
+    for (int i = 0, t = 0; t < 64; ++i)
+      for (int j = 0; j <= i && t < 64; ++j, ++t) { ti[t] = uint8_t(i); tj[t] = uint8_t(j); }
+    if (cudaMemcpyToSymbol(c_tile_i, ti, sizeof(ti)) != cudaSuccess) return -1;
+    if (cudaMemcpyToSymbol(c_tile_j, tj, sizeof(tj)) != cudaSuccess) return -1;
+  }
   return 0;
 }
 
@@ -246,78 +256,82 @@ __device__ __forceinline__ double sym(const double* P, int i, int j) {
   return i >= j ? P[tri(i) + j] : P[tri(j) + i];
 }
 
-// Leaf smem layout (doubles): ints (maps 2x256 int16 + col info) [160] | bufA[bufd] |
-// bufB[bufd] (kappa[512] and f[296] alias its head until level 5 writes it) | panel[pand] |
-// staged gather programs of the current level [tabd]
-static void leaf_sizes(int ncl, int* bufd, int* pand, int* tabd = nullptr) {
+// Leaf smem layout (doubles): col info [32] | bufA[bufa] (even-level outputs) |
+// bufB[bufb] (odd-level outputs; kappa[512] and f[289] alias its head until level 5
+// writes it) | panel[pand] | gather programs: panel program of even levels [tp0] | of
+// odd levels [tp1] | update program [tu].  The panel program of level r-1 is
+// prefetched (cp.async) while level r eliminates; the update program of level r
+// streams in behind level r's gather and factorization.
+struct LeafSmem {
+  int bufa, bufb, pand, tp0, tp1, tu;
+};
+static LeafSmem leaf_sizes(int ncl) {
   const auto& T = leaf_template();
-  int mb = 808, mp = 0, mt = 0;
+  LeafSmem s{0, 808, 0, 0, 0, 0};
   for (int r = 0; r < kLeafLevels; ++r) {
-    int nf = 1 << r, k = T[r].k, K = T[r].K, ng = T[r].ng;
-    if (r >= 1 && r <= 6) mb = std::max(mb, nf * (k * (k + 1) / 2 + k * ncl + ncl + 2));
-    if (r <= 5) mp = std::max(mp, nf * ng * ((K + ncl) + (k + ncl) + 2 * ng));
-    if (r <= 5) mt = std::max(mt, ng * (K + ncl) + k * (k + 1) / 2 + k * ncl);
+    const int nf = 1 << r, k = T[r].k, K = T[r].K, ng = T[r].ng;
+    if (r >= 1 && r <= 6) {
+      int& b = (r & 1) ? s.bufb : s.bufa;
+      b = std::max(b, nf * (k * (k + 1) / 2 + k * ncl + ncl + 2));
+    }
+    if (r <= 5) {
+      s.pand = std::max(s.pand, nf * ng * (K + ncl));
+      int& tp = (r & 1) ? s.tp1 : s.tp0;
+      tp = std::max(tp, ng * (K + ncl));
+      s.tu = std::max(s.tu, k * (k + 1) / 2 + k * ncl);
+    }
   }
-  *bufd = (mb + 1) & ~1;
-  *pand = (mp + 1) & ~1;
-  if (tabd) *tabd = (mt + 1) & ~1;
+  for (int* v : {&s.bufa, &s.bufb, &s.pand, &s.tp0, &s.tp1, &s.tu}) *v = (*v + 1) & ~1;
+  return s;
 }
+constexpr int kLeafHdr = 32;
 
 size_t leaf_smem_bytes(int ncl) {
-  int bufd, pand, tabd;
-  leaf_sizes(ncl, &bufd, &pand, &tabd);
-  return sizeof(double) * (160 + 2 * size_t(bufd) + pand + tabd);
+  const LeafSmem s = leaf_sizes(ncl);
+  return sizeof(double) * (size_t(kLeafHdr) + s.bufa + s.bufb + s.pand + s.tp0 + s.tp1 + s.tu);
 }
 
-// Panel region layout per level: P [nf][ng][W] | X [nf][ng][k+NC] | Linv [nf][ng][ng]
-template <int R, int NC>
-__host__ __device__ constexpr int leaf_panel_doubles() {
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int R, int NC, int NTH>
+__device__ __forceinline__ void stage_panel_program(uint64_t* dst) {
   constexpr LeafLevelShape S = leaf_shape(R);
-  return (1 << R) * S.ng * ((S.K + NC) + (S.k + NC) + S.ng);
+  constexpr int CI = NC == 2 ? 0 : (NC == 4 ? 1 : 2);
+  constexpr int NPI = S.ng * (S.K + NC);
+  const LeafItemP* g = c_ltab.P[CI] + c_ltab.poff[CI][R];
+  for (int t = threadIdx.x; t < NPI; t += NTH) cp_async8(dst + t, g + t);
+  cp_async_commit();
 }
 
-// SPC samples of the same leaf are processed together, interleaved element by
-// element (double2 for SPC = 2): every index program, map lookup and barrier is
-// shared, every shared-memory access moves both samples.
-template <int SPC> struct LV;
-template <> struct LV<1> {
-  using T = double;
-  static __device__ __forceinline__ T zero() { return 0.0; }
-  static __device__ __forceinline__ T one() { return 1.0; }
-  static __device__ __forceinline__ T add(T a, T b) { return a + b; }
-  static __device__ __forceinline__ T fms(T a, T b, T c) { return fma(-a, b, c); }   // c - a b
-  static __device__ __forceinline__ T fma_(T a, T b, T c) { return fma(a, b, c); }
-  static __device__ __forceinline__ T mul(T a, T b) { return a * b; }
-  static __device__ __forceinline__ T scal(T a, double s) { return a * s; }
-  static __device__ __forceinline__ T rcp(T a) { return __drcp_rn(a); }
-  static __device__ __forceinline__ double get(T a, int j) { return a; }
-  static __device__ __forceinline__ bool bad(T a) { return !(a > 0.0); }
-};
-template <> struct LV<2> {
-  using T = double2;
-  static __device__ __forceinline__ T zero() { return make_double2(0.0, 0.0); }
-  static __device__ __forceinline__ T one() { return make_double2(1.0, 1.0); }
-  static __device__ __forceinline__ T add(T a, T b) { return make_double2(a.x + b.x, a.y + b.y); }
-  static __device__ __forceinline__ T fms(T a, T b, T c) { return make_double2(fma(-a.x, b.x, c.x), fma(-a.y, b.y, c.y)); }
-  static __device__ __forceinline__ T fma_(T a, T b, T c) { return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y)); }
-  static __device__ __forceinline__ T mul(T a, T b) { return make_double2(a.x * b.x, a.y * b.y); }
-  static __device__ __forceinline__ T scal(T a, double s) { return make_double2(a.x * s, a.y * s); }
-  static __device__ __forceinline__ T rcp(T a) { return make_double2(__drcp_rn(a.x), __drcp_rn(a.y)); }
-  static __device__ __forceinline__ double get(T a, int j) { return j ? a.y : a.x; }
-  static __device__ __forceinline__ bool bad(T a) { return !(a.x > 0.0) || !(a.y > 0.0); }
-};
+// 1/sqrt(d): MUFU seed + two Newton steps (full double precision for the
+// well-scaled pivots of the in-leaf factorizations)
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double hd = 0.5 * d;
+  y = y * fma(-hd * y, y, 1.5);
+  y = y * fma(-hd * y, y, 1.5);
+  return y;
+}
 
 // One in-leaf level: sons (level R+1, packed) in `in`, outputs (level R) to `out`
-// (or straight to the global leaf outputs at R = 0).  Element e of sample j lives
-// at ((double*)buf)[e * SPC + j].
-template <int R, int NC, int SPC, int NTH>
-__device__ __forceinline__ void leaf_level(const DevPlan& p, const typename LV<SPC>::T* __restrict__ in,
-                                           typename LV<SPC>::T* __restrict__ out,
-                                           typename LV<SPC>::T* __restrict__ pan, const int16_t* __restrict__ mp,
-                                           const int* __restrict__ cinfo, int leaf, int s0, int nvalid,
-                                           long long leaf_ref, uint64_t* __restrict__ tabs) {
-  using V = LV<SPC>;
-  using T = typename V::T;
+// (level 0: `out` is shared-memory staging, copied to the leaf's global block at the end).
+//   A  gather the interface panel [A21 | A22 | R_gamma] (all warps)
+//   B  Cholesky of A22 in registers (1-2 warps) || the other warps gather the
+//      sons' contributions A~ = Psi_s1 + Psi_s2 (and R_B) into `out`
+//   C  [W | V] = L^-1 [A21 | R_gamma] in place (thread per column)
+//   D  out -= W^T [W | V] on 8x8 DMMA tiles; sigma += V_0^T V
+template <int R, int NC, int NTH>
+__device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __restrict__ in, double* __restrict__ out,
+                                           double* __restrict__ pan, const int* __restrict__ cinfo, int leaf,
+                                           int s, long long leaf_ref, const uint64_t* __restrict__ tabP,
+                                           uint64_t* __restrict__ tabPnext, uint64_t* __restrict__ tabU) {
   constexpr LeafLevelShape S = leaf_shape(R);
   constexpr int K = S.K, k = S.k, ng = S.ng, ks = S.ks;
   constexpr int nf = 1 << R;
@@ -328,218 +342,272 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const typename LV<S
   constexpr int NT = NTH, NW = NTH / 32;
   constexpr int gsz = nf >= NW ? 1 : NW / nf;
   constexpr int qstep = NW / gsz;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int CI = NC == 2 ? 0 : (NC == 4 ? 1 : 2);
+  constexpr int NPI = ng * W, NUI = ctri(k) + k * NC;
+  constexpr int LPN = ng <= 1 ? 1 : (ng <= 4 ? 4 : (ng <= 8 ? 8 : 16));   // Cholesky lanes per node
+  constexpr int NPW = 32 / LPN;                                           // nodes per Cholesky warp
+  constexpr int NWB = (nf + NPW - 1) / NPW;                               // Cholesky warps
+  static_assert(NWB < NW, "the sons' gather needs free warps");
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // provably warp-uniform
   const int sub = warp % gsz;
   const int* ctype = cinfo;
   const int* br = cinfo + NC;
   const int* bq = cinfo + 2 * NC;
   const int* bg = cinfo + 3 * NC;
-  T* Pp = pan;
-  T* Xp = pan + nf * ng * W;
-  T* Lp = Xp + nf * ng * WX;
+  double* Pp = pan;
 
-  // ---- stage this level's gather programs into shared memory ----
-  constexpr int CI = NC == 2 ? 0 : (NC == 4 ? 1 : 2);
-  constexpr int NPI = ng * W, NUI = ctri(k) + k * NC;
-  {
-    const uint64_t* gp = reinterpret_cast<const uint64_t*>(c_ltab.P[CI] + c_ltab.poff[CI][R]);
-    const uint64_t* gu = reinterpret_cast<const uint64_t*>(c_ltab.U[CI] + c_ltab.uoff[CI][R]);
-    for (int t = tid; t < NPI + NUI; t += NT) tabs[t] = t < NPI ? __ldg(gp + t) : __ldg(gu + (t - NPI));
+  {   // this level's update program (the single U buffer is free: the previous level is done)
+    const LeafItemU* gu = c_ltab.U[CI] + c_ltab.uoff[CI][R];
+    for (int t = tid; t < NUI; t += NT) cp_async8(tabU + t, gu + t);
+    cp_async_commit();
   }
+  cp_async_wait<1>();   // this level's panel program (issued one level earlier) has landed
   __syncthreads();
-  // ---- A: gather the interface panel [A21 | A22 | R_gamma] (precomputed program) ----
+  // ---- A: gather the interface panel (precomputed program) ----
   {
-    const LeafItemP* prog = reinterpret_cast<const LeafItemP*>(tabs);
+    const LeafItemP* prog = reinterpret_cast<const LeafItemP*>(tabP);
+    constexpr int UA = 4;
+    const int stride = gsz * 32;
     for (int q = warp / gsz; q < nf; q += qstep) {
-      const T* s1 = in + (2 * q) * Sin;
-      const T* s2 = in + (2 * q + 1) * Sin;
-      T* P = Pp + q * ng * W;
-      for (int t = sub * 32 + lane; t < ng * W; t += gsz * 32) {
-        const LeafItemP it = prog[t];
-        T v = V::add(s1[it.o1], s2[it.o2]);
-        if (it.c >= 0 && br[it.c] == R && bq[it.c] == q && bg[it.c] == t / W) v = V::add(v, V::one());
-        P[t] = v;
+      const double* s1 = in + (2 * q) * Sin;
+      const double* s2 = in + (2 * q + 1) * Sin;
+      double* P = Pp + q * ng * W;
+      for (int t0 = sub * 32 + lane; t0 < NPI; t0 += UA * stride) {
+        LeafItemP it[UA];
+        double v[UA];
+#pragma unroll
+        for (int u = 0; u < UA; ++u) {
+          const int t = t0 + u * stride;
+          it[u] = t < NPI ? prog[t] : LeafItemP{int16_t(Sin - 2), int16_t(Sin - 2), -1, 0};
+        }
+#pragma unroll
+        for (int u = 0; u < UA; ++u) v[u] = s1[it[u].o1] + s2[it[u].o2];
+#pragma unroll
+        for (int u = 0; u < UA; ++u)
+          if (t0 + u * stride < NPI) P[t0 + u * stride] = v[u];
       }
     }
   }
+  cp_async_wait<0>();   // update program landed
   __syncthreads();
+  if constexpr (R > 0) stage_panel_program<R - 1, NC, NTH>(tabPnext);
   LEAF_TICK(10 + 8 * (5 - R) + 0);
-  // ---- B: M = A22^-1 for every node by in-place Gauss-Jordan, all threads ----
-  // (symmetric positive definite: no pivoting; a non-positive pivot is a
-  // NumericalError exactly like the reference's failed Cholesky)
-  {
-    T* M0 = Lp;                          // [nf][ng][ng] ping
-    T* M1 = Lp + nf * ng * ng;           // pong
-    constexpr int NE = nf * ng * ng;
-    for (int t = tid; t < NE; t += NT) {
-      const int q = t / (ng * ng), e = t - q * ng * ng;
-      const int i = e / ng, j = e - i * ng;
-      M0[t] = Pp[q * ng * W + i * W + k + j];
+  if (warp < NWB) {
+    // ---- B: Cholesky A22 = L L^T, a lane per row, LPN lanes per node, column
+    // broadcasts by shuffles; L back below the diagonal, 1/L_jj on it.  A
+    // non-positive pivot is a NumericalError, exactly like the reference's failed
+    // Cholesky (hdd.py:263-270 without the indefinite fallback).
+    const int i = lane % LPN;
+    const int q = warp * NPW + lane / LPN;
+    const bool act = q < nf && i < ng;
+    double* P = Pp + (act ? q : 0) * ng * W + k;     // A22[i][l] = P[i * W + l]
+    double a[ng];
+#pragma unroll
+    for (int l = 0; l < ng; ++l) a[l] = (act && l <= i) ? P[i * W + l] : (l == i ? 1.0 : 0.0);
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < ng; ++j) {
+      const double dj = __shfl_sync(0xffffffffu, a[j], j, LPN);
+      bad |= !(dj > 0.0);
+      const double il = rsqrt_nr(dj);
+      const double lij = a[j] * il;
+#pragma unroll
+      for (int l = j + 1; l < ng; ++l) a[l] = fma(-lij, __shfl_sync(0xffffffffu, lij, l, LPN), a[l]);
+      a[j] = i == j ? il : lij;
     }
-    __syncthreads();
-#pragma unroll 1
-    for (int pv = 0; pv < ng; ++pv) {
-      const T* Mi = (pv & 1) ? M1 : M0;
-      T* Mo = (pv & 1) ? M0 : M1;
-      for (int t = tid; t < NE; t += NT) {
-        const int q = t / (ng * ng), e = t - q * ng * ng;
-        const int i = e / ng, j = e - i * ng;
-        const T* m = Mi + q * ng * ng;
-        const T d = m[pv * ng + pv];
-        const T rd = V::rcp(d);
-        T v;
-        if (i == pv && j == pv) {
-          if (V::bad(d))
-            for (int jj = 0; jj < nvalid; ++jj)
-              if (!(V::get(d, jj) > 0.0)) record_error(p.err, HDD_ERR_NUMERICAL, s0 + jj, inleaf_ref_id(leaf_ref, R, q));
-          v = rd;
-        } else if (i == pv) {
-          v = V::mul(m[pv * ng + j], rd);
-        } else if (j == pv) {
-          v = V::scal(V::mul(m[i * ng + pv], rd), -1.0);
-        } else {
-          v = V::fms(m[i * ng + pv], V::mul(m[pv * ng + j], rd), m[i * ng + j]);
-        }
-        Mo[t] = v;
+    if (act) {
+#pragma unroll
+      for (int l = 0; l < ng; ++l)
+        if (l <= i) P[i * W + l] = a[l];
+      if (i == 0 && bad) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(leaf_ref, R, q));
+    }
+  } else {
+    // ---- B': sons' contributions to the outputs, A~ = Psi_s1 + Psi_s2 | R_s1 + R_s2 ----
+    const LeafItemU* uprog = reinterpret_cast<const LeafItemU*>(tabU);
+    constexpr int UB = 4;
+    const int wt = (warp - NWB) * 32 + lane, nth = (NW - NWB) * 32;
+    for (int i0 = wt; i0 < nf * NUI; i0 += UB * nth) {
+      double v[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int idx = i0 + u * nth;
+        const int q = idx < nf * NUI ? idx / NUI : 0;
+        const LeafItemU it = idx < nf * NUI ? uprog[idx - q * NUI] : LeafItemU{0, 0, int16_t(Sin - 2), int16_t(Sin - 2)};
+        v[u] = in[(2 * q) * Sin + it.o1] + in[(2 * q + 1) * Sin + it.o2];
       }
-      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int idx = i0 + u * nth;
+        if (idx < nf * NUI) {
+          const int q = idx / NUI;
+          out[q * Sout + (idx - q * NUI)] = v[u];
+        }
+      }
     }
-    if ((ng & 1) == 1) {   // result in M1: copy back to M0
-      for (int t = tid; t < NE; t += NT) M0[t] = M1[t];
-    }
+    // functional births at this level: +1 in the panel's R_gamma column
+    if (warp == NW - 1 && lane < NC && br[lane] == R)
+      Pp[bq[lane] * ng * W + bg[lane] * W + K + lane] += 1.0;
   }
   __syncthreads();
   LEAF_TICK(10 + 8 * (5 - R) + 1);
-  // ---- C: Y = M [A21 | R_gamma] ----
-  for (int q = warp / gsz; q < nf; q += qstep) {
-    const T* P = Pp + q * ng * W;
-    const T* Mq = Lp + q * ng * ng;
-    T* Y = Xp + q * ng * WX;
-    for (int t = sub * 32 + lane; t < ng * WX; t += gsz * 32) {
-      const int g = t / WX, jj = t - g * WX;
-      const int j = jj < k ? jj : K + (jj - k);
-      T v = V::zero();
+  // ---- C: [W | V] = L^-1 [A21 | R_gamma] in place, a thread per column ----
+  for (int t = tid; t < nf * WX; t += NT) {
+    const int q = t / WX, jj = t - (t / WX) * WX;
+    const int col = jj < k ? jj : K + (jj - k);
+    double* P = Pp + q * ng * W;
+    double w[ng];
 #pragma unroll
-      for (int h = 0; h < ng; ++h) v = V::fma_(Mq[g * ng + h], P[h * W + j], v);
-      Y[t] = v;
+    for (int g = 0; g < ng; ++g) {
+      double v = P[g * W + col];
+#pragma unroll
+      for (int h = 0; h < g; ++h) v = fma(-P[g * W + k + h], w[h], v);
+      w[g] = v * P[g * W + k + g];
+      P[g * W + col] = w[g];
     }
   }
   __syncthreads();
   LEAF_TICK(10 + 8 * (5 - R) + 2);
-  // ---- D: streamed Schur update out = A~ - A21^T Y; sigma += R_g0^T Y_R ----
-  constexpr int E = ctri(k) + k * NC;
-  const LeafItemU* uprog = reinterpret_cast<const LeafItemU*>(tabs + NPI);
-  constexpr int UN = SPC == 1 ? 4 : 2;    // independent items per thread per iteration (ILP)
-  const double inv_area = 1.0 / (double(kLeafCells * kLeafCells) * p.h * p.h);   // exact power of two
-  for (int q = warp / gsz; q < nf; q += qstep) {
-    const T* s1 = in + (2 * q) * Sin;
-    const T* s2 = in + (2 * q + 1) * Sin;
-    const T* P = Pp + q * ng * W;
-    const T* Y = Xp + q * ng * WX;
-    T* o = out + q * Sout;
-    const int stride = gsz * 32;
-    for (int t0 = sub * 32 + lane; t0 < E; t0 += UN * stride) {
-      LeafItemU it[UN];
-      T v[UN];
+  // ---- D: out -= W^T [W | V]; sigma += V_0^T V ----
+  if constexpr (ng >= 3) {
+    // 8x8 output tiles on FP64 DMMA (m8n8k4, interface dimension padded to 4):
+    // lower-triangle Psi tiles, then one tile column for the R columns
+    constexpr int nT = (k + 7) / 8, TPN = ctri(nT) + nT, KS = (ng + 3) / 4;
+    constexpr int NTILE = nf * TPN, TU = 2;     // TU tiles per warp in flight
+    const int lr = lane >> 2, lc = lane & 3;
+    for (int w0 = warp; w0 < NTILE; w0 += TU * NW) {
+      int qv[TU], ldA[TU], ldB[TU], ov[TU][2];
+      bool vA[TU], vB[TU];
+      double acc[TU][2], old[TU][2];
 #pragma unroll
-      for (int u = 0; u < UN; ++u) {
-        const int t = t0 + u * stride;
-        it[u] = t < E ? uprog[t] : LeafItemU{0, 0, int16_t(Sin - 2), int16_t(Sin - 2)};
-      }
+      for (int u = 0; u < TU; ++u) {
+        const int w = w0 + u * NW;
+        const bool live = w < NTILE;
+        const int q = live ? w / TPN : 0;
+        const int tt = live ? w - q * TPN : 0;
+        const bool rt = tt >= ctri(nT);
+        const int ti = rt ? tt - ctri(nT) : c_tile_i[tt];
+        const int tj = rt ? 0 : c_tile_j[tt];
+        qv[u] = q;
+        const int a = 8 * ti + lr;
+        ldA[u] = a;
+        ldB[u] = rt ? K + lr : 8 * tj + lr;
+        vA[u] = live && a < k;
+        vB[u] = live && (rt ? lr < NC : ldB[u] < k);
+        // output offsets of this lane's two accumulator elements (-1: not stored),
+        // old values fetched ahead of the DMMA chain
 #pragma unroll
-      for (int u = 0; u < UN; ++u) v[u] = V::add(s1[it[u].o1], s2[it[u].o2]);
-#pragma unroll
-      for (int g = 0; g < ng; ++g)
-#pragma unroll
-        for (int u = 0; u < UN; ++u) v[u] = V::fms(P[g * W + it[u].a], Y[g * WX + it[u].bx], v[u]);
-#pragma unroll
-      for (int u = 0; u < UN; ++u) {
-        const int t = t0 + u * stride;
-        if (t >= E) continue;
-        const int a = it[u].a, bx = it[u].bx;
-        if constexpr (R > 0) {
-          o[t] = v[u];
-        } else {
-          for (int jj = 0; jj < nvalid; ++jj) {
-            const int sj = s0 + jj;
-            double* gdst = p.buf[p.leaf_buf] + int64_t(leaf) * p.leaf_elems * p.bcap + int64_t(sj) * p.leaf_elems;
-            const double val = V::get(v[u], jj);
-            if (bx < k) {
-              gdst[t] = val;                       // packed lower: same order as the items
-            } else if (bx - k < p.leaf_cols) {
-              const double sc = ctype[bx - k] == 1 ? inv_area : 1.0;
-              gdst[ctri(kLeafPerim) + a * p.leaf_cols + (bx - k)] = val * sc;
-              const int fs = cinfo[4 * NC + (bx - k)];
-              if (fs >= 0) p.fbuf[(int64_t(sj) * p.n_fslots + fs) * 65 + a] = val;
-            }
+        for (int e = 0; e < 2; ++e) {
+          const int cc = 2 * lc + e;
+          int t = -1;
+          if (live && a < k) {
+            if (!rt) { if (8 * tj + cc <= a) t = ctri(a) + 8 * tj + cc; }
+            else if (cc < NC) t = ctri(k) + a * NC + cc;
           }
+          ov[u][e] = t < 0 ? -1 : q * Sout + t;
+          old[u][e] = t < 0 ? 0.0 : out[q * Sout + t];
+          acc[u][e] = 0.0;
         }
       }
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {
+        const int g = 4 * kk + lc;
+#pragma unroll
+        for (int u = 0; u < TU; ++u) {
+          const double* P = Pp + qv[u] * ng * W;
+          const double x = (vA[u] && g < ng) ? P[g * W + ldA[u]] : 0.0;
+          const double y = (vB[u] && g < ng) ? P[g * W + ldB[u]] : 0.0;
+          dmma884(acc[u], x, y);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < TU; ++u)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (ov[u][e] >= 0) out[ov[u][e]] = old[u][e] - acc[u][e];
     }
-    if (sub == 0 && lane < NC) {
+  } else {
+    // ng = 1: rank-1 update, a thread per output element
+    const double* P0 = Pp;
+    for (int idx = tid; idx < nf * NUI; idx += NT) {
+      const int q = idx / NUI, t = idx - q * NUI;
+      const LeafItemU it = reinterpret_cast<const LeafItemU*>(tabU)[t];
+      const int bx = it.bx;
+      const double* P = P0 + q * ng * W;
+      out[q * Sout + t] -= P[it.a] * P[bx < k ? bx : K + (bx - k)];
+    }
+  }
+  // sigma row: sigma_c = sigma_s1 + sigma_s2 + V_0^T V_c (column 0 is the load)
+  for (int q = warp; q < nf; q += NW) {
+    if (lane < NC) {
+      const double* P = Pp + q * ng * W;
       const int c = lane;
-      T sg = V::add(s1[ctri(ks) + ks * NC + c], s2[ctri(ks) + ks * NC + c]);
+      double sg = in[(2 * q) * Sin + ctri(ks) + ks * NC + c] + in[(2 * q + 1) * Sin + ctri(ks) + ks * NC + c];
       if (c >= 1)
 #pragma unroll
-        for (int g = 0; g < ng; ++g) sg = V::fma_(P[g * W + K], Y[g * WX + k + c], sg);
-      if constexpr (R > 0) {
-        o[ctri(k) + k * NC + c] = sg;
-        if (c < 2) o[Sout - 2 + c] = V::zero();    // zero slot
-      } else if (c < p.leaf_cols) {
-        for (int jj = 0; jj < nvalid; ++jj) {
-          const int sj = s0 + jj;
-          double* gdst = p.buf[p.leaf_buf] + int64_t(leaf) * p.leaf_elems * p.bcap + int64_t(sj) * p.leaf_elems;
-          gdst[ctri(kLeafPerim) + kLeafPerim * p.leaf_cols + c] = V::get(sg, jj) * (ctype[c] == 1 ? inv_area : 1.0);
-          const int fs = cinfo[4 * NC + c];
-          if (fs >= 0) p.fbuf[(int64_t(sj) * p.n_fslots + fs) * 65 + 64] = V::get(sg, jj);
-        }
-      }
+        for (int g = 0; g < ng; ++g) sg = fma(P[g * W + K], P[g * W + K + c], sg);
+      double* o = out + q * Sout;
+      o[ctri(k) + k * NC + c] = sg;
+      if (c < 2) o[Sout - 2 + c] = 0.0;    // zero slot
     }
   }
   __syncthreads();
+  if constexpr (R == 0) {
+    // leaf output: Psi packed lower, R [64][leaf_cols] (mean columns rescaled by
+    // 1/|leaf|, an exact power of two), sigma; primal-mode leaf functionals
+    const double inv_area = 1.0 / (double(kLeafCells * kLeafCells) * p.h * p.h);
+    double* gdst = p.buf[p.leaf_buf] + int64_t(leaf) * p.leaf_elems * p.bcap + int64_t(s) * p.leaf_elems;
+    const int lc = min(NC, p.leaf_cols);
+    for (int t = tid; t < ctri(k); t += NT) gdst[t] = out[t];
+    for (int t = tid; t < (k + 1) * lc; t += NT) {
+      const int a = t / lc, c = t - (t / lc) * lc;
+      const double val = out[ctri(k) + a * NC + c];
+      gdst[ctri(k) + a * p.leaf_cols + c] = val * (ctype[c] == 1 ? inv_area : 1.0);
+      const int fs = cinfo[4 * NC + c];
+      if (fs >= 0) p.fbuf[(int64_t(s) * p.n_fslots + fs) * 65 + a] = val;
+    }
+  }
   LEAF_TICK(10 + 8 * (5 - R) + 3);
 }
 
-// One CTA per (16x16-cell leaf, SPC samples).  Level 6 (2x2-cell blocks) is
-// built per thread in registers straight from the cells' kappa; levels 5..0
-// run level-synchronously in shared memory with lower-packed Schur
-// complements: gather the interface panel, Gauss-Jordan interface inverse,
-// Y = A22^-1 [A21 | R], then the streamed Schur update A11 - A21^T Y.
-template <int NC, int SPC, int NTH>
-__global__ void __launch_bounds__(NTH, NTH == 256 ? 2 : 1) leaf2_kernel(DevPlan p, const int* __restrict__ order,
-                                                                           int bufd, int pand, int B) {
-  using T = typename LV<SPC>::T;
+// One CTA per (16x16-cell leaf, sample).  Level 6 (2x2-cell blocks) is built per
+// thread in registers straight from the cells' kappa; levels 5..0 run
+// level-synchronously in shared memory with lower-packed Schur complements:
+// gather the interface panel, Gauss-Jordan interface inverse (warp per node),
+// Y = A22^-1 [A21 | R], then the Schur update A11 - A21^T Y on DMMA tiles.
+template <int NC, int NTH>
+__global__ void __launch_bounds__(NTH, 2) leaf2_kernel(DevPlan p, const int* __restrict__ order, LeafSmem ls,
+                                                       int B) {
   extern __shared__ __align__(16) double sm[];
   const int leaf = order[blockIdx.x];
-  const int s0 = blockIdx.y * SPC;
-  const int nvalid = min(SPC, B - s0);
+  const int s = blockIdx.y;
   LEAF_TICK(0);
   const int tid = threadIdx.x;
   constexpr int NT = NTH;
   const DevLeaf& L = p.leaves[leaf];
-  int16_t* mp = reinterpret_cast<int16_t*>(sm);                // [2][256]
-  int* cinfo = reinterpret_cast<int*>(sm + 128);                 // ctype, br, bq, bg, fslot
-  T* bufA = reinterpret_cast<T*>(sm + 160);
-  T* bufB = bufA + bufd;
-  T* pan = bufB + bufd;
-  uint64_t* tabs = reinterpret_cast<uint64_t*>(pan + pand);
-  double* kap = reinterpret_cast<double*>(bufB);      // [SPC][512], aliases bufB until level 5
-  double* fl = kap + 512 * SPC;                        // [289]
+  int* cinfo = reinterpret_cast<int*>(sm);                       // ctype, br, bq, bg, fslot
+  double* bufA = sm + kLeafHdr;
+  double* bufB = bufA + ls.bufa;
+  double* pan = bufB + ls.bufb;
+  uint64_t* tab0 = reinterpret_cast<uint64_t*>(pan + ls.pand);   // panel programs, even levels
+  uint64_t* tab1 = tab0 + ls.tp0;                                // odd levels
+  uint64_t* tabU = tab1 + ls.tp1;
+  double* kap = bufB;                                             // [512], aliases bufB until level 5
+  double* fl = kap + 512;                                         // [289]
   const int N = p.N;
   {
-    for (int t = tid; t < 512 * SPC; t += NT) {
-      const int j = t >> 9, tt = t & 511;
-      const int sj = s0 + min(j, nvalid - 1);
-      const double* kb = p.kappa + int64_t(sj) * 2 * N * N;
-      const int x = tt >> 5, r = tt & 31;
-      kap[t] = kb[2 * (int64_t(L.i0 + x) * N + L.j0) + r];
+    const double* kb = p.kappa + int64_t(s) * 2 * N * N;
+    for (int t = tid; t < 512; t += NT) {
+      const int x = t >> 5, r = t & 31;
+      cp_async8(kap + t, kb + 2 * (int64_t(L.i0 + x) * N + L.j0) + r);
     }
+    cp_async_commit();
+    stage_panel_program<5, NC, NTH>(tab1);
     if (p.f)
       for (int t = tid; t < 289; t += NT) {
         int y = t / 17, x = t - y * 17;
         fl[t] = p.f[int64_t(L.j0 + y) * p.m + L.i0 + x];
       }
-    for (int t = tid; t < 512; t += NT) mp[t] = c_map[t >> 8][t & 255];
     if (tid < NC) {
       cinfo[tid] = tid < L.ncols ? L.ctype[tid] : 3;     // 3 = unused column
       cinfo[NC + tid] = L.birth_r[tid];
@@ -547,6 +615,7 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 2 : 1) leaf2_kernel(DevPlan 
       cinfo[3 * NC + tid] = L.birth_g[tid];
       cinfo[4 * NC + tid] = tid < L.ncols ? L.fslot[tid] : -1;
     }
+    cp_async_wait<1>();
   }
   __syncthreads();
   const int* ctype = cinfo;
@@ -558,10 +627,7 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 2 : 1) leaf2_kernel(DevPlan 
   {
     constexpr int k6 = 8;
     const int S6 = tri(k6) + k6 * NC + NC + 2;
-    double* outd = reinterpret_cast<double*>(bufA);
-    for (int qq = tid; qq < 64 * SPC; qq += NT) {
-      const int q = qq & 63, j = qq >> 6;
-      const double* kj = kap + 512 * j;
+    for (int q = tid; q < 64; q += NT) {
       const int o = c_orig[63 + q];
       const int x0 = o & 255, y0 = o >> 8;
       double A[45];
@@ -574,8 +640,8 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 2 : 1) leaf2_kernel(DevPlan 
       for (int cy = 0; cy < 2; ++cy)
 #pragma unroll
         for (int cx = 0; cx < 2; ++cx) {
-          const double k0 = kj[(x0 + cx) * 32 + 2 * (y0 + cy)];
-          const double k1 = kj[(x0 + cx) * 32 + 2 * (y0 + cy) + 1];
+          const double k0 = kap[(x0 + cx) * 32 + 2 * (y0 + cy)];
+          const double k1 = kap[(x0 + cx) * 32 + 2 * (y0 + cy) + 1];
           const int a = cy * 3 + cx, b = a + 1, c = a + 3, d = a + 4;
           // P1 (a,b,d) and P2 (a,d,c) of fem.py:126-145
           A[tri(a) + a] += fma(k0, 0.5, k1 * 0.5);
@@ -602,17 +668,17 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 2 : 1) leaf2_kernel(DevPlan 
         }
       // eliminate the centre node 4
       const double dpiv = A[tri(4) + 4];
-      if (!(dpiv > 0.0) && j < nvalid) record_error(p.err, HDD_ERR_NUMERICAL, s0 + j, inleaf_ref_id(L.ref_id, 6, q));
+      if (!(dpiv > 0.0)) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, 6, q));
       const double inv = 1.0 / sqrt(dpiv);
       double xv[9];
 #pragma unroll
       for (int n = 0; n < 9; ++n) xv[n] = (n == 4) ? 0.0 : (n < 4 ? A[tri(4) + n] : A[tri(n) + 4]) * inv;
-      double* out = outd + (q * S6) * SPC + j;
+      double* out = bufA + q * S6;
       constexpr int P8[8] = {0, 1, 2, 3, 5, 6, 7, 8};
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int jj = 0; jj <= i; ++jj) out[(tri(i) + jj) * SPC] = fma(-xv[P8[i]], xv[P8[jj]], A[tri(P8[i]) + P8[jj]]);
+        for (int jj = 0; jj <= i; ++jj) out[tri(i) + jj] = fma(-xv[P8[i]], xv[P8[jj]], A[tri(P8[i]) + P8[jj]]);
       double v[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -627,31 +693,25 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 2 : 1) leaf2_kernel(DevPlan 
         for (int c = 0; c < NC; ++c) {
           const int ct = ctype[c];
           const double rb = ct == 0 ? rl[P8[i]] : (ct == 1 ? rm[P8[i]] : 0.0);
-          out[(tri(k6) + i * NC + c) * SPC] = fma(-xv[P8[i]], v[c], rb);
+          out[tri(k6) + i * NC + c] = fma(-xv[P8[i]], v[c], rb);
         }
 #pragma unroll
-      for (int c = 0; c < NC; ++c) out[(tri(k6) + k6 * NC + c) * SPC] = c == 0 ? 0.0 : v[0] * v[c];
-      out[(S6 - 2) * SPC] = 0.0;
-      out[(S6 - 1) * SPC] = 0.0;
+      for (int c = 0; c < NC; ++c) out[tri(k6) + k6 * NC + c] = c == 0 ? 0.0 : v[0] * v[c];
+      out[S6 - 2] = 0.0;
+      out[S6 - 1] = 0.0;
     }
   }
   __syncthreads();
 
   LEAF_TICK(1);
   // ---------------- levels 5..0 in shared memory ----------------
-  leaf_level<5, NC, SPC, NTH>(p, bufA, bufB, pan, mp, cinfo, leaf, s0, nvalid, L.ref_id, tabs);
-  leaf_level<4, NC, SPC, NTH>(p, bufB, bufA, pan, mp, cinfo, leaf, s0, nvalid, L.ref_id, tabs);
-  leaf_level<3, NC, SPC, NTH>(p, bufA, bufB, pan, mp, cinfo, leaf, s0, nvalid, L.ref_id, tabs);
-  leaf_level<2, NC, SPC, NTH>(p, bufB, bufA, pan, mp, cinfo, leaf, s0, nvalid, L.ref_id, tabs);
-  leaf_level<1, NC, SPC, NTH>(p, bufA, bufB, pan, mp, cinfo, leaf, s0, nvalid, L.ref_id, tabs);
-  leaf_level<0, NC, SPC, NTH>(p, bufB, bufA, pan, mp, cinfo, leaf, s0, nvalid, L.ref_id, tabs);
+  leaf_level<5, NC, NTH>(p, bufA, bufB, pan, cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
+  leaf_level<4, NC, NTH>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
+  leaf_level<3, NC, NTH>(p, bufA, bufB, pan, cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
+  leaf_level<2, NC, NTH>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
+  leaf_level<1, NC, NTH>(p, bufA, bufB, pan, cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
+  leaf_level<0, NC, NTH>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
   LEAF_TICK(63);
-}
-
-size_t leaf_smem_bytes_spc(int ncl, int spc) {
-  int bufd, pand, tabd;
-  leaf_sizes(ncl, &bufd, &pand, &tabd);
-  return sizeof(double) * (160 + size_t(spc) * (2 * size_t(bufd) + pand) + tabd);
 }
 
 cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_out) {
@@ -659,24 +719,19 @@ cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_ou
     const int cnt = p.leaf_class_count[cls];
     if (cnt == 0) continue;
     const int ncl = cls == 0 ? 2 : (cls == 1 ? 4 : 8);
-    int bufd, pand;
-    leaf_sizes(ncl, &bufd, &pand);
-    // SPC = 2 (two samples interleaved, 512 threads) measured: C2 -3 %, C3 +7 %, C4 +8 %
-    // leaf time against SPC = 1 (2 CTAs x 256 threads per SM) -> keep 1.
-    const int spc = 1;
-    const size_t smem = leaf_smem_bytes_spc(ncl, spc);
+    const LeafSmem ls = leaf_sizes(ncl);
+    const size_t smem = leaf_smem_bytes(ncl);
     if (smem_out) *smem_out = smem;
-    dim3 grid(cnt, (B + spc - 1) / spc);
+    dim3 grid(cnt, B);
     const int* ord = p.leaf_order + p.leaf_class_start[cls];
     cudaError_t e;
-#define HDD_LAUNCH_LEAF(NCV, SPCV)                                                                           \
-  e = cudaFuncSetAttribute(leaf2_kernel<NCV, SPCV, SPCV * 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                           int(smem));                                                                       \
-  if (e != cudaSuccess) return e;                                                                            \
-  leaf2_kernel<NCV, SPCV, SPCV * 256><<<grid, SPCV * 256, smem, s>>>(p, ord, bufd, pand, B);
-    if (ncl == 2) { if (spc == 2) { HDD_LAUNCH_LEAF(2, 2) } else { HDD_LAUNCH_LEAF(2, 1) } }
-    else if (ncl == 4) { if (spc == 2) { HDD_LAUNCH_LEAF(4, 2) } else { HDD_LAUNCH_LEAF(4, 1) } }
-    else { HDD_LAUNCH_LEAF(8, 1) }
+#define HDD_LAUNCH_LEAF(NCV)                                                                                   \
+  e = cudaFuncSetAttribute(leaf2_kernel<NCV, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));     \
+  if (e != cudaSuccess) return e;                                                                              \
+  leaf2_kernel<NCV, 256><<<grid, 256, smem, s>>>(p, ord, ls, B);
+    if (ncl == 2) { HDD_LAUNCH_LEAF(2) }
+    else if (ncl == 4) { HDD_LAUNCH_LEAF(4) }
+    else { HDD_LAUNCH_LEAF(8) }
 #undef HDD_LAUNCH_LEAF
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -951,13 +1006,6 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
   }
 }
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // Tier-L Schur update: 64 x 64 output tiles, X chunks of 32 interface rows
 // double-buffered HBM -> smem with cp.async, 8 warps as 2 x 4 of 32 x 16 DMMA tiles.
