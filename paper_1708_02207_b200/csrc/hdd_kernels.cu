@@ -256,6 +256,10 @@ __device__ __forceinline__ double sym(const double* P, int i, int j) {
   return i >= j ? P[tri(i) + j] : P[tri(j) + i];
 }
 
+// Panel row stride of level r: >= K + NC and = 4 (mod 8), so that the DMMA operand
+// fragments (4 rows x 8 consecutive doubles) hit distinct banks.
+__host__ __device__ constexpr int leaf_wpad(int w) { return w + ((12 - (w & 7)) & 7); }
+
 // Leaf smem layout (doubles): col info [32] | bufA[bufa] (even-level outputs) |
 // bufB[bufb] (odd-level outputs; kappa[512] and f[289] alias its head until level 5
 // writes it) | panel[pand] | gather programs: panel program of even levels [tp0] | of
@@ -275,7 +279,7 @@ static LeafSmem leaf_sizes(int ncl) {
       b = std::max(b, nf * (k * (k + 1) / 2 + k * ncl + ncl + 2));
     }
     if (r <= 5) {
-      s.pand = std::max(s.pand, nf * ng * (K + ncl));
+      s.pand = std::max(s.pand, nf * ng * leaf_wpad(K + ncl));
       int& tp = (r & 1) ? s.tp1 : s.tp0;
       tp = std::max(tp, ng * (K + ncl));
       s.tu = std::max(s.tu, k * (k + 1) / 2 + k * ncl);
@@ -337,13 +341,14 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
   constexpr int nf = 1 << R;
   constexpr int Sin = ctri(ks) + ks * NC + NC + 2;    // +2: zero slot at [Sin - 2] (even stride)
   constexpr int Sout = ctri(k) + k * NC + NC + 2;
-  constexpr int W = K + NC;
+  constexpr int WL = K + NC;                // logical panel row (program layout)
+  constexpr int W = leaf_wpad(WL);          // padded panel row stride
   constexpr int WX = k + NC;
   constexpr int NT = NTH, NW = NTH / 32;
   constexpr int gsz = nf >= NW ? 1 : NW / nf;
   constexpr int qstep = NW / gsz;
   constexpr int CI = NC == 2 ? 0 : (NC == 4 ? 1 : 2);
-  constexpr int NPI = ng * W, NUI = ctri(k) + k * NC;
+  constexpr int NPI = ng * WL, NUI = ctri(k) + k * NC;
   constexpr int LPN = ng <= 1 ? 1 : (ng <= 4 ? 4 : (ng <= 8 ? 8 : 16));   // Cholesky lanes per node
   constexpr int NPW = 32 / LPN;                                           // nodes per Cholesky warp
   constexpr int NWB = (nf + NPW - 1) / NPW;                               // Cholesky warps
@@ -384,8 +389,10 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 #pragma unroll
         for (int u = 0; u < UA; ++u) v[u] = s1[it[u].o1] + s2[it[u].o2];
 #pragma unroll
-        for (int u = 0; u < UA; ++u)
-          if (t0 + u * stride < NPI) P[t0 + u * stride] = v[u];
+        for (int u = 0; u < UA; ++u) {
+          const int t = t0 + u * stride;
+          if (t < NPI) P[(t / WL) * W + (t - (t / WL) * WL)] = v[u];
+        }
       }
     }
   }

@@ -36,5 +36,5 @@ for r in range(5, -1, -1):
     base = 10 + 8 * (5 - r)
     prev = c[1] if r == 5 else c[10 + 8 * (5 - (r + 1)) + 3]
     ph = [c[base + i] - (prev if i == 0 else c[base + i - 1]) for i in range(4)]
-    print(f"  level {r}: A {ph[0]}  B {ph[1]}  C {ph[2]}  D {ph[3]}")
+    print(f"  level {r}: A {ph[0]}  B {ph[1]} (chol {c[base + 4] - c[base]})  C {ph[2]}  D {ph[3]}")
 print("  total", c[63] - c[0])
