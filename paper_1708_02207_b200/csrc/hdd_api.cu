@@ -158,7 +158,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
     const UpperNode& U = P.upper[u];
     const int ngp32 = (U.ng + 31) / 32 * 32;
     const int ldp32 = (U.k + ngp32 + U.nc + 15) / 16 * 16 + 8;
-    if (merge_m2_smem_bytes(ngp32, ldp32) > 220 * 1024 || (force_l && force_l[0] == '1')) pl->depth_tier[U.depth] = 1;
+    if (merge_m2_smem_bytes(ngp32, ldp32, U.K, U.nc) > 220 * 1024 || (force_l && force_l[0] == '1')) pl->depth_tier[U.depth] = 1;
   }
   for (size_t u = 0; u < P.upper.size(); ++u) {
     const UpperNode& U = P.upper[u];
@@ -213,7 +213,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
     csrc.insert(csrc.end(), U.csrc.begin(), U.csrc.end());
     ccoef.insert(ccoef.end(), U.ccoef.begin(), U.ccoef.end());
     cbirth.insert(cbirth.end(), U.cbirth.begin(), U.cbirth.end());
-    size_t sm = pl->depth_tier[U.depth] ? 0 : merge_m2_smem_bytes(ngp_u, d.ldp);
+    size_t sm = pl->depth_tier[U.depth] ? 0 : merge_m2_smem_bytes(ngp_u, d.ldp, U.K, U.nc);
     if (!pl->depth_tier[U.depth]) {
       // stage the sons in smem when panel + sons still allow two CTAs per SM
       const size_t sons = sizeof(double) * size_t(((d.son_elems[0] + 1) & ~1) + ((d.son_elems[1] + 1) & ~1));

@@ -901,7 +901,8 @@ __device__ __forceinline__ double gather_sig(const MergeCtx& c, int col) {
   return v;
 }
 
-// panel row g of [A21 | A22 (padded) | R_gamma] -> dst (smem or HBM)
+// panel row g of [A21 | A22 (padded) | R_gamma] -> dst (smem or HBM); four entries
+// per thread in flight (the son reads are independent, predicated loads)
 __device__ __forceinline__ void gather_panel_row(const MergeCtx& c, int k, int ng, int Kp, int W, int g,
                                                  double* dst, int lane0, int step) {
   if (g >= ng) {
@@ -909,15 +910,32 @@ __device__ __forceinline__ void gather_panel_row(const MergeCtx& c, int k, int n
     return;
   }
   const int a = k + g;
-  for (int j = lane0; j < W; j += step) {
-    double v = 0.0;
-    if (j < k + ng) v = gather_A(c, a, j);
-    else if (j >= Kp) {
-      const int col = j - Kp;
-      v = gather_R(c, a, col);
-      if (c.cbirth[col] == g) v += 1.0;
+  const int pa0 = c.gm[a], pa1 = c.gm[c.K + a];
+  constexpr int U = 4;
+  for (int j0 = lane0; j0 < W; j0 += U * step) {
+    double v0[U], v1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * step;
+      v0[u] = 0.0;
+      v1[u] = 0.0;
+      if (j < k + ng) {
+        const int pb0 = c.gm[j], pb1 = c.gm[c.K + j];
+        if (pa0 >= 0 && pb0 >= 0) v0[u] = son_psi(c.sv[0], pa0, pb0);
+        if (pa1 >= 0 && pb1 >= 0) v1[u] = son_psi(c.sv[1], pa1, pb1);
+      } else if (j >= Kp && j < W) {
+        const int col = j - Kp;
+        const int s0 = c.csrc[2 * col], s1 = c.csrc[2 * col + 1];
+        if (pa0 >= 0 && s0 >= 0) v0[u] = c.ccoef[2 * col] * son_R(c.sv[0], pa0, s0);
+        if (pa1 >= 0 && s1 >= 0) v1[u] = c.ccoef[2 * col + 1] * son_R(c.sv[1], pa1, s1);
+        if (c.cbirth[col] == g) v0[u] += 1.0;
+      }
     }
-    dst[j] = v;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * step;
+      if (j < W) dst[j] = v0[u] + v1[u];
+    }
   }
 }
 
@@ -1115,7 +1133,12 @@ __device__ __forceinline__ void store_factors(const DevPlan& p, const DevUpper& 
 }
 
 // -- tier M: panel in shared memory ------------------------------------------
-size_t merge_m2_smem_bytes(int ngp, int ldp) { return sizeof(double) * (size_t(ngp) * ldp + 8) + 64; }
+// smem: panel [ngp][ldp] | scratch [8] + L, L^-1 of the diagonal block [2][64] | son maps [2][K] int | column plan (csrc
+// [nc][2], cbirth [nc]) int | ccoef [nc][2] | staged sons (optional)
+size_t merge_m2_smem_bytes(int ngp, int ldp, int K, int nc) {
+  const size_t ints = (size_t(2 * K + 3 * nc) + 1) & ~size_t(1);
+  return sizeof(double) * (size_t(ngp) * ldp + 8 + 128 + ints / 2 + 2 * size_t(nc)) + 64;
+}
 
 template <int NB, int NTH>
 __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes) {
@@ -1130,48 +1153,96 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
   const int W = Kp + nc;
   double* P = sm;                          // [ngp][ldp]
   double* piv = P + size_t(ngp) * ldp;     // [NB] pivots of the current block
+  int32_t* gms = reinterpret_cast<int32_t*>(piv + 8 + 128);
+  int32_t* cis = gms + 2 * U.K;
+  double* ccs = reinterpret_cast<double*>(gms + ((2 * U.K + 3 * nc + 1) & ~1));
+  double* st = ccs + 2 * nc;
   __shared__ int s_bad;
   MergeCtx mc = merge_ctx(p, U, s);
   if (U.stage) {
-    // stage both sons' packed outputs in shared memory (coalesced 16-byte copies)
-    double* st = piv + 8;
+    // stage both sons' packed outputs in shared memory (asynchronous 8-byte copies)
 #pragma unroll
     for (int sn = 0; sn < 2; ++sn) {
       const int n = int(U.son_elems[sn]);
       const double* src = mc.sv[sn].b;
-      for (int t = tid; t < n; t += NT) st[t] = __ldg(src + t);
+      for (int t = tid; t < n; t += NT) cp_async8(st + t, src + t);
       mc.sv[sn].b = st;
       st += (n + 1) & ~1;
     }
-    __syncthreads();
+    cp_async_commit();
   }
+  for (int t = tid; t < 2 * U.K; t += NT) gms[t] = __ldg(mc.gm + t);
+  for (int t = tid; t < 2 * nc; t += NT) {
+    cis[t] = __ldg(mc.csrc + t);
+    ccs[t] = __ldg(mc.ccoef + t);
+  }
+  for (int t = tid; t < nc; t += NT) cis[2 * nc + t] = __ldg(mc.cbirth + t);
+  mc.gm = gms;
+  mc.csrc = cis;
+  mc.cbirth = cis + 2 * nc;
+  mc.ccoef = ccs;
+  if (U.stage) cp_async_wait<0>();
+  __syncthreads();
   for (int g = warp; g < ngp; g += NWp) gather_panel_row(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   const int gq = lane & 3, gr = lane >> 2;
+  double* Ls = piv + 8;                    // [8][8] diagonal-block factor L
+  double* Li = Ls + 64;                    // [8][8] L^-1
   for (int r0 = 0; r0 < ngp; r0 += NB) {
-    // in-block elimination with unscaled pivot rows (one barrier per pivot):
-    // row r -= (P[r][k+c] / d_c) * P[c][.]; rows are scaled by 1/sqrt(d) afterwards
-    for (int c = r0; c < r0 + NB; ++c) {
-      const double* rc = P + c * ldp;
-      __syncthreads();                    // previous pivot's updates are complete
-      const double d = rc[k + c];
-      if (tid == 0) {
-        piv[c - r0] = d;
-        if (!(d > 0.0)) s_bad = 1;
+    static_assert(NB == 8, "8-row elimination blocks");
+    __syncthreads();                       // block rows final (gather / previous trailing update)
+    if (warp == 0) {
+      // Cholesky of the 8x8 diagonal block in registers (lane = row, shuffles), then
+      // L^-1 column by column (lane = column, L broadcast from smem)
+      const int i = lane & 7;
+      double a[8];
+#pragma unroll
+      for (int l = 0; l < 8; ++l) a[l] = l <= i ? P[(r0 + i) * ldp + k + r0 + l] : (l == i ? 1.0 : 0.0);
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double dj = __shfl_sync(0xffffffffu, a[j], j, 8);
+        bad |= !(dj > 0.0);
+        const double il = rsqrt_nr(dj);
+        const double lij = a[j] * il;
+#pragma unroll
+        for (int l = j + 1; l < 8; ++l) a[l] = fma(-lij, __shfl_sync(0xffffffffu, lij, l, 8), a[l]);
+        a[j] = i == j ? dj * il : lij;
       }
-      const double rd = 1.0 / d;
-      const int nr = r0 + NB - c - 1;
-      for (int t = warp; t < nr; t += NWp) {
-        double* rw = P + (c + 1 + t) * ldp;
-        const double lr = rw[k + c] * rd;
-        for (int j = lane; j < W; j += 32)
-          if (j != k + c) rw[j] = fma(-lr, rc[j], rw[j]);
+      if (lane < 8)
+#pragma unroll
+        for (int l = 0; l < 8; ++l) Ls[i * 8 + l] = l <= i ? a[l] : 0.0;
+      if (lane == 0 && bad) s_bad = 1;
+      __syncwarp();
+      if (lane < 8) {
+        double x[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          double v = m == lane ? 1.0 : 0.0;
+#pragma unroll
+          for (int q = 0; q < m; ++q) v = fma(-Ls[m * 8 + q], x[q], v);
+          x[m] = v / Ls[m * 8 + m];
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) Li[m * 8 + lane] = x[m];
       }
     }
     __syncthreads();
-    for (int t = tid; t < NB * W; t += NT) {
-      const int i = t / W, j = t - i * W;
-      if (j != k + r0 + i) P[(r0 + i) * ldp + j] *= rsqrt(piv[i]);
+    // block rows X = L^-1 P[r0:r0+8, :] in place, 8-column DMMA tiles across warps
+    for (int t = warp; t < (W + 7) / 8; t += NWp) {
+      const int c0 = 8 * t;
+      double acc[2] = {0.0, 0.0};
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const double av = Li[gr * 8 + 4 * kk + gq];
+        const double bv = c0 + gr < W ? P[(r0 + 4 * kk + gq) * ldp + c0 + gr] : 0.0;
+        dmma884(acc, av, bv);
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = c0 + 2 * gq + e;
+        if (col < W) P[(r0 + gr) * ldp + col] = acc[e];
+      }
     }
     __syncthreads();
     const int nrt = (ngp - r0 - NB) / 8;
@@ -1193,7 +1264,7 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
   }
   __syncthreads();
   if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
-  if (p.mode == 1) store_factors(p, U, s, P, ldp, Kp, true, tid, NT);
+  if (p.mode == 1) store_factors(p, U, s, P, ldp, Kp, false, tid, NT);
   double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
   const int tk = tri(k);
   for (int c = tid; c < nc; c += NT) {
