@@ -1132,6 +1132,51 @@ __device__ __forceinline__ void store_factors(const DevPlan& p, const DevUpper& 
   }
 }
 
+// Cholesky of an 8x8 SPD block D (row stride ld) by one warp: lane = row in
+// registers, column broadcasts by shuffles; L -> Ls (lower, zero upper), 1/L_ii ->
+// Ld, then L^-1 -> Li column by column (lane = column).  *bad = 1 on a
+// non-positive pivot.
+__device__ __forceinline__ void factor_block8(const double* D, int ld, double* Ls, double* Li, double* Ld,
+                                              int* bad) {
+  const int lane = threadIdx.x & 31, i = lane & 7;
+  double a[8];
+#pragma unroll
+  for (int l = 0; l < 8; ++l) a[l] = l <= i ? D[i * ld + l] : (l == i ? 1.0 : 0.0);
+  bool nb = false;
+  double ild = 1.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double dj = __shfl_sync(0xffffffffu, a[j], j, 8);
+    nb |= !(dj > 0.0);
+    const double il = rsqrt_nr(dj);
+    const double lij = a[j] * il;
+#pragma unroll
+    for (int l = j + 1; l < 8; ++l) a[l] = fma(-lij, __shfl_sync(0xffffffffu, lij, l, 8), a[l]);
+    if (i == j) ild = il;
+    a[j] = i == j ? dj * il : lij;
+  }
+  if (lane < 8) {
+#pragma unroll
+    for (int l = 0; l < 8; ++l) Ls[i * 8 + l] = l <= i ? a[l] : 0.0;
+    Ld[i] = ild;
+  }
+  if (lane == 0 && nb) *bad = 1;
+  __syncwarp();
+  if (lane < 8) {
+    double x[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      double v = m == lane ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = 0; q < m; ++q) v = fma(-Ls[m * 8 + q], x[q], v);
+      x[m] = v * Ld[m];
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) Li[m * 8 + lane] = x[m];
+  }
+  __syncwarp();
+}
+
 // -- tier M: panel in shared memory ------------------------------------------
 // smem: panel [ngp][ldp] | scratch [8] + L, L^-1 of the diagonal block [2][64] | son maps [2][K] int | column plan (csrc
 // [nc][2], cbirth [nc]) int | ccoef [nc][2] | staged sons (optional)
@@ -1186,48 +1231,16 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
   for (int g = warp; g < ngp; g += NWp) gather_panel_row(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   const int gq = lane & 3, gr = lane >> 2;
-  double* Ls = piv + 8;                    // [8][8] diagonal-block factor L
+  double* Ls = piv + 8;                    // [8][8] diagonal-block factor L (piv: 1/L_ii)
   double* Li = Ls + 64;                    // [8][8] L^-1
+  static_assert(NB == 8, "8-row elimination blocks");
+  // Right-looking blocked Cholesky of A22 on 8-row blocks with look-ahead: warp 0
+  // updates and factors the next diagonal block while warps 1.. apply the trailing
+  // update of the current block row (two barriers per block).
+  __syncthreads();                         // panel gathered
+  if (warp == 0) factor_block8(P + k, ldp, Ls, Li, piv, &s_bad);
+  __syncthreads();
   for (int r0 = 0; r0 < ngp; r0 += NB) {
-    static_assert(NB == 8, "8-row elimination blocks");
-    __syncthreads();                       // block rows final (gather / previous trailing update)
-    if (warp == 0) {
-      // Cholesky of the 8x8 diagonal block in registers (lane = row, shuffles), then
-      // L^-1 column by column (lane = column, L broadcast from smem)
-      const int i = lane & 7;
-      double a[8];
-#pragma unroll
-      for (int l = 0; l < 8; ++l) a[l] = l <= i ? P[(r0 + i) * ldp + k + r0 + l] : (l == i ? 1.0 : 0.0);
-      bool bad = false;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const double dj = __shfl_sync(0xffffffffu, a[j], j, 8);
-        bad |= !(dj > 0.0);
-        const double il = rsqrt_nr(dj);
-        const double lij = a[j] * il;
-#pragma unroll
-        for (int l = j + 1; l < 8; ++l) a[l] = fma(-lij, __shfl_sync(0xffffffffu, lij, l, 8), a[l]);
-        a[j] = i == j ? dj * il : lij;
-      }
-      if (lane < 8)
-#pragma unroll
-        for (int l = 0; l < 8; ++l) Ls[i * 8 + l] = l <= i ? a[l] : 0.0;
-      if (lane == 0 && bad) s_bad = 1;
-      __syncwarp();
-      if (lane < 8) {
-        double x[8];
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          double v = m == lane ? 1.0 : 0.0;
-#pragma unroll
-          for (int q = 0; q < m; ++q) v = fma(-Ls[m * 8 + q], x[q], v);
-          x[m] = v / Ls[m * 8 + m];
-        }
-#pragma unroll
-        for (int m = 0; m < 8; ++m) Li[m * 8 + lane] = x[m];
-      }
-    }
-    __syncthreads();
     // block rows X = L^-1 P[r0:r0+8, :] in place, 8-column DMMA tiles across warps
     for (int t = warp; t < (W + 7) / 8; t += NWp) {
       const int c0 = 8 * t;
@@ -1245,22 +1258,42 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
       }
     }
     __syncthreads();
-    const int nrt = (ngp - r0 - NB) / 8;
-    const int nct = (W + 31) / 32;
-    for (int t = warp; t < nrt * nct; t += NWp) {
-      const int rt = r0 + NB + (t / nct) * 8;
-      const int c0 = (t % nct) * 32;
-      if (c0 >= k && c0 + 32 <= k + rt) continue;     // A22 columns left of the tile rows: never read again
-      double acc[1][4][2] = {};
-      warp_gemm_tn<1, 4>(acc, P + r0 * ldp + k, ldp, rt, P + r0 * ldp, ldp, c0, NB);
+    const int rn = r0 + NB;                // next block
+    if (rn >= ngp) break;
+    if (warp == 0) {
+      // look-ahead: D_next -= X[:, next]^T X[:, next], then factor it
+      const double* X = P + r0 * ldp + k + rn;
+      double acc[2] = {0.0, 0.0};
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int kk = 0; kk < 2; ++kk) {
+        const double x = X[(4 * kk + gq) * ldp + gr];
+        dmma884(acc, x, x);
+      }
+      double* D = P + rn * ldp + k + rn;
+      D[gr * ldp + 2 * gq] -= acc[0];
+      D[gr * ldp + 2 * gq + 1] -= acc[1];
+      __syncwarp();
+      factor_block8(D, ldp, Ls, Li, piv, &s_bad);
+    } else {
+      const int nrt = (ngp - rn) / 8;
+      const int nct = (W + 31) / 32;
+      for (int t = warp - 1; t < nrt * nct; t += NWp - 1) {
+        const int rt = rn + (t / nct) * 8;
+        const int c0 = (t % nct) * 32;
+        if (c0 >= k && c0 + 32 <= k + rt) continue;     // A22 columns left of the tile rows: never read again
+        double acc[1][4][2] = {};
+        warp_gemm_tn<1, 4>(acc, P + r0 * ldp + k, ldp, rt, P + r0 * ldp, ldp, c0, NB);
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = c0 + 8 * j + 2 * gq + e;
-          if (col < W) P[(rt + gr) * ldp + col] -= acc[0][j][e];
-        }
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = c0 + 8 * j + 2 * gq + e;
+            const bool diag_next = rt == rn && col >= k + rn && col < k + rn + 8;   // warp 0's block
+            if (col < W && !diag_next) P[(rt + gr) * ldp + col] -= acc[0][j][e];
+          }
+      }
     }
+    __syncthreads();
   }
   __syncthreads();
   if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
