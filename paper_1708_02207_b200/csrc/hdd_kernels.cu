@@ -838,6 +838,75 @@ __device__ __forceinline__ void factor_diag_block(const double* src, int ld, dou
   }
 }
 
+// Cholesky of a 32x32 SPD block (rows from `src`, stride ld) by one warp: lane =
+// row in registers, column broadcasts by shuffles (fully unrolled); L goes to Ls
+// column-major (Ls[c * kLdd + r] = L[r][c], 1/L_cc on the diagonal), then L^-1 by
+// right-looking forward substitution, lane = column, into LiT[c * kLdd + r] =
+// (L^-1)[r][c].  Sets *bad on a non-positive pivot.
+__device__ __forceinline__ void factor_block32(const double* src, int ld, double* Ls, double* LiT, int* bad) {
+  const int lane = threadIdx.x & 31;
+  {
+    double a[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) a[l] = l <= lane ? src[lane * ld + l] : (l == lane ? 1.0 : 0.0);
+    bool nb = false;
+    double ild = 1.0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double dj = __shfl_sync(0xffffffffu, a[j], j);
+      nb |= !(dj > 0.0);
+      const double il = rsqrt_nr(dj);
+      const double lij = a[j] * il;
+#pragma unroll
+      for (int l = j + 1; l < 32; ++l) a[l] = fma(-lij, __shfl_sync(0xffffffffu, lij, l), a[l]);
+      if (lane == j) ild = il;
+      a[j] = lij;
+    }
+#pragma unroll
+    for (int l = 0; l < 32; ++l)
+      if (l <= lane) Ls[l * kLdd + lane] = l == lane ? ild : a[l];
+    if (lane == 0 && nb) *bad = 1;
+  }
+  __syncwarp();
+  // L^-1 = [L11^-1, 0; -L22^-1 L21 L11^-1, L22^-1] on 16x16 blocks (keeps 32 doubles live)
+  const int c = lane & 15, base = lane & 16;
+  double x[16];
+  {
+    double v[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = m == c ? 1.0 : 0.0;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      x[m] = v[m] * Ls[(base + m) * kLdd + base + m];
+      LiT[lane * kLdd + base + m] = x[m];
+#pragma unroll
+      for (int q = m + 1; q < 16; ++q) v[q] = fma(-Ls[(base + m) * kLdd + base + q], x[m], v[q]);
+    }
+    if (base)
+#pragma unroll
+      for (int m = 0; m < 16; ++m) LiT[lane * kLdd + m] = 0.0;    // upper-right block of L^-1
+  }
+  __syncwarp();
+  if (!base) {
+    double y[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double t = 0.0;
+#pragma unroll
+      for (int m = 0; m < 16; ++m) t = fma(Ls[m * kLdd + 16 + r], x[m], t);     // (L21 x)[r]
+      y[r] = t;
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q <= r; ++q) t = fma(LiT[(16 + q) * kLdd + 16 + r], y[q], t);   // (L22^-1 y)[r]
+      LiT[lane * kLdd + 16 + r] = -t;
+    }
+  }
+  __syncwarp();
+}
+
 // -- son views (packed-lower node outputs) ----------------------------------
 // A node output per sample is [Psi lower-packed tri(k) | R k x nc | sigma nc].
 struct SonView {
@@ -1337,7 +1406,7 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
   if (tid == 0) s_bad = 0;
   __syncthreads();
   for (int r0 = 0; r0 < ngp; r0 += kLB) {
-    if (warp == 0) factor_diag_block<32>(P + int64_t(r0) * ldp + k + r0, ldp, LiT, &s_bad);
+    if (warp == 0) factor_block32(P + int64_t(r0) * ldp + k + r0, ldp, sm, LiT, &s_bad);
     __syncthreads();
     // F2: X_b = L^-1 P_b in 64-column chunks (the block's own A22 columns give L_bb^T)
     for (int c0 = 0; c0 < W; c0 += kLC) {
