@@ -477,61 +477,76 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
   LEAF_TICK(10 + 8 * (5 - R) + 2);
   // ---- D: out -= W^T [W | V]; sigma += V_0^T V ----
   if constexpr (ng >= 3) {
-    // 8x8 output tiles on FP64 DMMA (m8n8k4, interface dimension padded to 4):
-    // lower-triangle Psi tiles, then one tile column for the R columns
-    constexpr int nT = (k + 7) / 8, TPN = ctri(nT) + nT, KS = (ng + 3) / 4;
-    constexpr int NTILE = nf * TPN, TU = 2;     // TU tiles per warp in flight
+    // 16x16 output blocks (2x2 DMMA m8n8k4 tiles; interface dimension padded to 4):
+    // lower-triangle Psi blocks, then 16x8 blocks for the R columns
+    constexpr int nB = (k + 15) / 16, TPN = ctri(nB) + nB, KS = (ng + 3) / 4;
+    constexpr int NBLK = nf * TPN;
     const int lr = lane >> 2, lc = lane & 3;
-    for (int w0 = warp; w0 < NTILE; w0 += TU * NW) {
-      int qv[TU], ldA[TU], ldB[TU], ov[TU][2];
-      bool vA[TU], vB[TU];
-      double acc[TU][2], old[TU][2];
+    for (int w = warp; w < NBLK; w += NW) {
+      const int q = w / TPN;
+      const int tt = w - q * TPN;
+      const bool rt = tt >= ctri(nB);
+      const int bi = rt ? tt - ctri(nB) : c_tile_i[tt];
+      const int bj = rt ? 0 : c_tile_j[tt];
+      const double* P = Pp + q * ng * W;
+      double* o = out + q * Sout;
+      // output offsets of this lane's accumulator elements (-1: not stored), old
+      // values (the sons' contributions, written by B') fetched ahead of the DMMAs
+      int ov[2][2][2];
+      double old[2][2][2], acc[2][2][2];
 #pragma unroll
-      for (int u = 0; u < TU; ++u) {
-        const int w = w0 + u * NW;
-        const bool live = w < NTILE;
-        const int q = live ? w / TPN : 0;
-        const int tt = live ? w - q * TPN : 0;
-        const bool rt = tt >= ctri(nT);
-        const int ti = rt ? tt - ctri(nT) : c_tile_i[tt];
-        const int tj = rt ? 0 : c_tile_j[tt];
-        qv[u] = q;
-        const int a = 8 * ti + lr;
-        ldA[u] = a;
-        ldB[u] = rt ? K + lr : 8 * tj + lr;
-        vA[u] = live && a < k;
-        vB[u] = live && (rt ? lr < NC : ldB[u] < k);
-        // output offsets of this lane's two accumulator elements (-1: not stored),
-        // old values fetched ahead of the DMMA chain
+      for (int i = 0; i < 2; ++i) {
+        const int a = 16 * bi + 8 * i + lr;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int cc = 2 * lc + e;
-          int t = -1;
-          if (live && a < k) {
-            if (!rt) { if (8 * tj + cc <= a) t = ctri(a) + 8 * tj + cc; }
-            else if (cc < NC) t = ctri(k) + a * NC + cc;
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            int t = -1;
+            if (a < k) {
+              if (!rt) {
+                const int b = 16 * bj + 8 * j + 2 * lc + e;
+                if (b <= a) t = ctri(a) + b;
+              } else if (j == 0 && 2 * lc + e < NC) {
+                t = ctri(k) + a * NC + 2 * lc + e;
+              }
+            }
+            ov[i][j][e] = t;
+            old[i][j][e] = t < 0 ? 0.0 : o[t];
+            acc[i][j][e] = 0.0;
           }
-          ov[u][e] = t < 0 ? -1 : q * Sout + t;
-          old[u][e] = t < 0 ? 0.0 : out[q * Sout + t];
-          acc[u][e] = 0.0;
-        }
+      }
+      int ca[2], cb[2];
+      bool vca[2], vcb[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        ca[i] = 16 * bi + 8 * i + lr;
+        vca[i] = ca[i] < k;
+        cb[i] = rt ? K + lr : 16 * bj + 8 * i + lr;
+        vcb[i] = rt ? (i == 0 && lr < NC) : cb[i] < k;
       }
 #pragma unroll
       for (int kk = 0; kk < KS; ++kk) {
         const int g = 4 * kk + lc;
+        const double* pr = P + g * W;
+        double x[2], y[2];
 #pragma unroll
-        for (int u = 0; u < TU; ++u) {
-          const double* P = Pp + qv[u] * ng * W;
-          const double x = (vA[u] && g < ng) ? P[g * W + ldA[u]] : 0.0;
-          const double y = (vB[u] && g < ng) ? P[g * W + ldB[u]] : 0.0;
-          dmma884(acc[u], x, y);
+        for (int i = 0; i < 2; ++i) {
+          x[i] = (vca[i] && g < ng) ? pr[ca[i]] : 0.0;
+          y[i] = (vcb[i] && g < ng) ? pr[cb[i]] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          dmma884(acc[i][0], x[i], y[0]);
+          if (!rt) dmma884(acc[i][1], x[i], y[1]);
         }
       }
 #pragma unroll
-      for (int u = 0; u < TU; ++u)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (ov[u][e] >= 0) out[ov[u][e]] = old[u][e] - acc[u][e];
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (ov[i][j][e] >= 0) o[ov[i][j][e]] = old[i][j][e] - acc[i][j][e];
     }
   } else {
     // ng = 1: rank-1 update, a thread per output element
