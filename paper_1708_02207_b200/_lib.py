@@ -7,12 +7,14 @@ fallback implementation: if the shared library is missing or fails to load,
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 from .errors import ConfigError, NumericalError, UsageError
 
-LIB_PATH = Path(__file__).resolve().parent / "libhdd_b200.so"
+# HDD_LIB_PATH: developer hook for A/B builds of the same sources (tools/ab_build.py)
+LIB_PATH = Path(os.environ.get("HDD_LIB_PATH") or Path(__file__).resolve().parent / "libhdd_b200.so")
 
 HDD_OK = 0
 HDD_ERR_CONFIG = -1

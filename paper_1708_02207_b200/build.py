@@ -30,20 +30,23 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+    """Build libhdd_b200.so in-tree (or `out`, with extra -D `defines`, for A/B runs)."""
+    target = Path(out) if out is not None else LIB
+    if out is None and not force and not needs_build():
         return LIB
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if verbose else "-O3", f"-I{ROOT / 'include'}", f"-I{CSRC}",
-           *map(str, sources()), "-o", str(LIB) + ".tmp", "-lcudart"]
+           *[f"-D{d}" for d in defines],
+           *map(str, sources()), "-o", str(target) + ".tmp", "-lcudart"]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         sys.stderr.write(proc.stdout + proc.stderr)
         raise RuntimeError("nvcc failed building libhdd_b200.so")
     if verbose:
         sys.stderr.write(proc.stderr)
-    os.replace(str(LIB) + ".tmp", LIB)
-    return LIB
+    os.replace(str(target) + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

@@ -429,7 +429,14 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
         if (l <= i) P[i * W + l] = a[l];
       if (i == 0 && bad) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(leaf_ref, R, q));
     }
+    LEAF_TICK(10 + 8 * (5 - R) + 4);
+#ifdef HDD_AB_SERIAL_B
+    if (R == 0) asm volatile("bar.arrive 1, %0;" ::"n"(NT));
+#endif
   } else {
+#ifdef HDD_AB_SERIAL_B
+    if (R == 0) asm volatile("bar.sync 1, %0;" ::"n"(NT));
+#endif
     // ---- B': sons' contributions to the outputs, A~ = Psi_s1 + Psi_s2 | R_s1 + R_s2 ----
     const LeafItemU* uprog = reinterpret_cast<const LeafItemU*>(tabU);
     constexpr int UB = 4;
