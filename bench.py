@@ -378,11 +378,16 @@ def main():
 
     launches = args.steps * info.n_kernels_per_batch * math.ceil(B / info.max_batch)
     # measured DRAM bytes per launch of the dominant kernel (ncu --set full capture,
-    # profiles/r01_ncu_full_leaf_C2.csv: 21.8 KB per leaf-sample) scaled to this launch
+    # profiles/r01_ncu_full_leaf_v4_C2.csv: 23.6 KB per leaf-sample) scaled to this launch;
+    # the leaf's binding resource is shared-memory bandwidth (same capture)
     traffic = None
+    binding = None
     if top == "leaf":
-        traffic = {"bytes": 21.8e3 * B * ((1 << cfg.level) // 16) ** 2,
-                   "source": "ncu dram__bytes_read+write, leaf2_kernel<4> C2, 268 MB / (12 leaves x 1024)"}
+        traffic = {"bytes": 23.6e3 * B * ((1 << cfg.level) // 16) ** 2,
+                   "source": "ncu dram__bytes_read+write, leaf2_kernel<2> C2: 1184 MB / (49 leaves x 1024)"}
+        binding = {"resource": "shared-memory wavefronts (l1tex lsu shared)", "util_pct": 66.6,
+                   "fp64_pipe_pct": 6.2, "issue_active_pct": 53.4,
+                   "source": "profiles/r01_ncu_full_leaf_v4_C2.csv"}
     line = {
         "metric": f"likelihood evals/s ({args.config}, {cfg.level}-level grid, n_z={cfg.n_z})",
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -397,6 +402,7 @@ def main():
                      "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "peak_source": FP64_PEAK_SRC,
                      "kernel_share_of_step": top_ms / sum(shares.values()),
+                     "binding_resource": binding,
                      "algorithmic_flops_per_launch": flops[top] * B},
         "step_roofline": {"achieved_tflops": total_fl * B / (ms_max * 1e-3) / 1e12,
                           "frac_fp64": total_fl * B / (ms_max * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
