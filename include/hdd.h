@@ -148,6 +148,19 @@ int hdd_forward_batch_timed(HddPlan* plan, const double* Z_dev, int64_t B,
 int hdd_forward_batch_host(HddPlan* plan, const double* Z_host, int64_t B,
                            double* S_host, double* ll_host);
 
+/* Full solution u at every mesh node for every row of Z: U_dev[B][n_nodes]
+ * (n_nodes = (2^level + 1)^2, node id j * (2^level + 1) + i).  The bottom-up
+ * sweep and the primal top-down sweep give u on every interface; each kernel
+ * leaf then solves for its interior nodes.  Requires a plan created with
+ * mode = 1 (primal: the factors are kept), else HDD_ERR_USAGE — the analogue of
+ * root_to_leaves requiring a store built with SolveMode.keep_all().
+ * Replaces root_to_leaves / forward_full_solve (reference hdd.py:397-432,
+ * bayes.py:201-208). */
+int hdd_solve_batch(HddPlan* plan, const double* Z_dev, int64_t B, double* U_dev, void* stream);
+
+/* Same call with HOST buffers. */
+int hdd_solve_batch_host(HddPlan* plan, const double* Z_host, int64_t B, double* U_host);
+
 /* Per-triangle kappa for a batch (parity hook for the assembly kernel). */
 int hdd_kappa_batch(HddPlan* plan, const double* Z_dev, int64_t B,
                     double* kappa_dev, void* stream);

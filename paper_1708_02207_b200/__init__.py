@@ -14,6 +14,7 @@ from .bayes import (  # noqa: F401
     SineKLField,
     ToleranceSpec,
     aligned_partition,
+    forward_full_solve,
     forward_functionals,
     forward_functionals_batch,
     gaussian_log_likelihood,
@@ -21,10 +22,16 @@ from .bayes import (  # noqa: F401
     log_likelihood,
     log_likelihood_batch,
     mean_observations,
+    mean_over_cells,
+    observe_solution,
     posterior_weights,
+    solve_batch,
+    solve_subdomain,
 )
 from .errors import ConfigError, GeometryError, NumericalError, UsageError  # noqa: F401
-from .geometry import DDTree, Mesh, Rect, boundary_nodes, build_mesh, build_tree, interior_nodes  # noqa: F401
+from .geometry import (  # noqa: F401
+    DDTree, Mesh, Rect, boundary_nodes, build_mesh, build_tree, interior_nodes, omega_nodes,
+)
 
 __version__ = "0.1.0"
 from . import configs, parallel  # noqa: E402,F401

@@ -320,6 +320,7 @@ class BayesProblem:
     max_batch: int = 0
     mode: int = -1          # -1 auto, 0 adjoint functionals, 1 primal top-down for points
     _plan: object = field(default=None, repr=False)
+    _solve_plan: object = field(default=None, repr=False)
 
     def __post_init__(self):
         mesh = self.tree.mesh
@@ -339,6 +340,16 @@ class BayesProblem:
         if self._plan is None:
             self._plan = _Plan(self, self.device, self.max_batch, mode=self.mode)
         return self._plan
+
+    def solve_plan(self) -> _Plan:
+        """A primal plan (factors kept) for the full-solution sweep; the likelihood
+        plan is reused when it already is one."""
+        info = self.plan().info()
+        if info.mode == 1 or info.leaf_depth == 0:
+            return self.plan()
+        if self._solve_plan is None:
+            self._solve_plan = _Plan(self, self.device, self.max_batch, mode=1)
+        return self._solve_plan
 
 
 def _as_batch(Z, n_z):
@@ -411,6 +422,84 @@ def forward_functionals(problem: BayesProblem, z) -> np.ndarray:
     if z.shape != (problem.param.n_z,):
         raise ConfigError(f"parameter vector must have length {problem.param.n_z}")
     return forward_functionals_batch(problem, z[None])[0]
+
+
+def solve_batch(problem: BayesProblem, Z):
+    """u at every mesh node for every row of Z: U[B, n_nodes] (node id j * m + i).
+
+    Bottom-up sweep, primal top-down sweep over the interfaces and the in-leaf
+    interior solves on the device — leaves_to_root(keep_all) + root_to_leaves
+    (hdd.py:289-432) for a batch.  numpy in -> numpy out; a CUDA torch tensor in ->
+    CUDA torch tensor out."""
+    plan = problem.solve_plan()
+    Zb = _as_batch(Z, plan.n_z)
+    B = Zb.shape[0]
+    n = problem.tree.mesh.n_nodes
+    if isinstance(Zb, np.ndarray):
+        U = np.empty((B, n))
+        plan.check(plan.lib.hdd_solve_batch_host(plan.handle, Zb.ctypes.data_as(_lib._f64p), B,
+                                                 U.ctypes.data_as(_lib._f64p)))
+        return U
+    import torch
+    if not Zb.is_cuda:
+        raise UsageError("torch inputs must live on the plan's CUDA device")
+    Zb = Zb.to(torch.float64).contiguous()
+    U = torch.empty((B, n), dtype=torch.float64, device=Zb.device)
+    stream = torch.cuda.current_stream(Zb.device).cuda_stream
+    plan.check(plan.lib.hdd_solve_batch(plan.handle, C.c_void_p(Zb.data_ptr()), B, C.c_void_p(U.data_ptr()),
+                                        C.c_void_p(stream)))
+    return U
+
+
+def mean_over_cells(mesh, u, cells) -> float:
+    """Mean of the P1 function u over a grid-aligned cell rectangle by the exact
+    per-triangle rule sum |t|/3 (u1+u2+u3) / |region| (oracle.py:74-83): per cell
+    (2 u_a + u_b + u_c + 2 u_d) / 6 for its triangles (a,b,d), (a,d,c)."""
+    i0, i1, j0, j1 = cells
+    if i1 <= i0 or j1 <= j0:
+        raise ConfigError("region contains no triangles")
+    m = mesh.m
+    u = np.asarray(u, dtype=float).reshape(m, m)     # [j][i]
+    a = u[j0:j1, i0:i1]
+    b = u[j0:j1, i0 + 1:i1 + 1]
+    c = u[j0 + 1:j1 + 1, i0:i1]
+    d = u[j0 + 1:j1 + 1, i0 + 1:i1 + 1]
+    return float((2.0 * a + b + c + 2.0 * d).sum() / (6.0 * a.size))
+
+
+def observe_solution(tree: DDTree, u, model: MeasurementModel) -> np.ndarray:
+    """Observation operators applied to an assembled solution (bayes.py:211-219)."""
+    out = np.empty(model.n_y)
+    u = np.asarray(u, dtype=float)
+    for k, (kind, ident) in enumerate(model.observations):
+        if kind == "mean":
+            out[k] = mean_over_cells(tree.mesh, u, tree.node(int(ident)).cells)
+        else:
+            out[k] = u[int(ident)]
+    return out
+
+
+def forward_full_solve(problem: BayesProblem, z) -> np.ndarray:
+    """Observation vector via the full solve plus the per-triangle mean rule — the
+    comparison route of the likelihood-equivalence checks (bayes.py:201-208)."""
+    z = np.asarray(z, dtype=float)
+    if z.shape != (problem.param.n_z,):
+        raise ConfigError(f"parameter vector must have length {problem.param.n_z}")
+    u = solve_batch(problem, z[None])[0]
+    return observe_solution(problem.tree, u, problem.model)
+
+
+def solve_subdomain(problem: BayesProblem, z, target_id: int) -> np.ndarray:
+    """Solution restricted to one tree node, aligned with its idx_omega (sorted
+    global node ids of the closed subdomain) — solve_subdomain, hdd.py:435-490.
+    The device sweep computes every interface anyway; the restriction is a gather."""
+    from .geometry import omega_nodes
+    target = problem.tree.node(int(target_id))
+    z = np.asarray(z, dtype=float)
+    if z.shape != (problem.param.n_z,):
+        raise ConfigError(f"parameter vector must have length {problem.param.n_z}")
+    u = solve_batch(problem, z[None])[0]
+    return u[omega_nodes(problem.tree.mesh, target.cells)]
 
 
 def gaussian_log_likelihood(y, s, sigma) -> float:

@@ -582,6 +582,55 @@ int hdd_forward_batch_host(HddPlan* pl, const double* Zh, int64_t B, double* Sh,
   return HDD_OK;
 }
 
+int hdd_solve_batch(HddPlan* pl, const double* Z, int64_t B, double* U, void* stream) {
+  if (!pl) return HDD_ERR_USAGE;
+  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan cannot run a solve");
+  if (pl->dev.mode != 1 && pl->plan.leaf_depth > 0)   // a single-leaf tree has no interfaces to sweep
+    return set_err(&pl->err, HDD_ERR_USAGE, "the full-solution sweep requires a primal plan (mode = 1 keeps the factors)");
+  if (B < 0 || (B > 0 && (!Z || !U))) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
+  const int nz = pl->plan.n_z;
+  const int64_t nn = int64_t(pl->plan.m) * pl->plan.m;
+  for (int64_t done = 0; done < B;) {
+    const int b = int(std::min<int64_t>(pl->bcap, B - done));
+    int rc = run_sub_batch(pl, Z + done * nz, b, nullptr, nullptr, st);
+    if (rc != HDD_OK) return rc;
+    CU(launch_leaf_solve(pl->dev, b, U + done * nn, nn, st));
+    done += b;
+  }
+  return check_device_error(pl, st, 0);
+}
+
+int hdd_solve_batch_host(HddPlan* pl, const double* Zh, int64_t B, double* Uh) {
+  if (!pl) return HDD_ERR_USAGE;
+  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan cannot run a solve");
+  if (B < 0 || (B > 0 && (!Zh || !Uh))) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  const int nz = pl->plan.n_z;
+  const int64_t nn = int64_t(pl->plan.m) * pl->plan.m;
+  double* dZ = nullptr;
+  double* dU = nullptr;
+  CU(cudaMalloc(&dZ, size_t(B) * nz * 8));
+  if (cudaMalloc(&dU, size_t(B) * nn * 8) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(dZ);
+    return set_err(&pl->err, HDD_ERR_NOMEM, "device allocation of the solution buffer failed");
+  }
+  cudaStream_t st = pl->stream;
+  int rc = HDD_OK;
+  if (cudaMemcpyAsync(dZ, Zh, size_t(B) * nz * 8, cudaMemcpyHostToDevice, st) != cudaSuccess) rc = HDD_ERR_CUDA;
+  if (rc == HDD_OK) rc = hdd_solve_batch(pl, dZ, B, dU, st);
+  if (rc == HDD_OK && cudaMemcpyAsync(Uh, dU, size_t(B) * nn * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    rc = HDD_ERR_CUDA;
+  if (rc == HDD_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = HDD_ERR_CUDA;
+  cudaFree(dZ);
+  cudaFree(dU);
+  return rc;
+}
+
 int hdd_kappa_batch(HddPlan* pl, const double* Z, int64_t B, double* kappa, void* stream) {
   if (!pl) return HDD_ERR_USAGE;
   if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan");

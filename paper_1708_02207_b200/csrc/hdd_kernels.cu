@@ -1915,3 +1915,131 @@ cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cuda
 }
 
 }  // namespace hdd
+
+namespace hdd {
+
+// ---------------------------------------------------------------------------
+// K6: full-solution path, the in-leaf part of root_to_leaves (hdd.py:397-432).
+// The upper interfaces come from the primal top-down sweep (u_K of every upper
+// node); each kernel leaf then solves for its 15 x 15 interior nodes from its 64
+// perimeter values: the exact P1 stiffness of the structured triangulation is the
+// variable-coefficient 5-point stencil, so the interior system is banded (half
+// bandwidth 15) and one warp factors it by a right-looking band Cholesky in
+// shared memory, then runs the two triangular solves.
+// ---------------------------------------------------------------------------
+constexpr int kIn = kLeafCells - 1;        // interior nodes per side
+constexpr int kNI = kIn * kIn;             // interior unknowns
+constexpr int kBW = kIn + 1;               // band width incl. the diagonal
+
+// perimeter index of local node (x, y) in the sorted-id perimeter order
+__device__ __forceinline__ int perim_index(int x, int y) {
+  return y == 0 ? x : (y == kLeafCells ? 3 * kLeafCells - 1 + x : kLeafCells + 1 + 2 * (y - 1) + (x == kLeafCells));
+}
+
+__global__ void __launch_bounds__(32) leaf_solve_kernel(DevPlan p, double* __restrict__ U, int64_t n_nodes) {
+  __shared__ double band[kNI * kBW];       // column j: rows j .. j+15 of L
+  __shared__ double rhs[kNI], invd[kNI];
+  __shared__ double kap[512];
+  __shared__ double ub[kLeafPerim];
+  const int leaf = blockIdx.x, s = blockIdx.y, lane = threadIdx.x;
+  const DevLeaf& L = p.leaves[leaf];
+  const int N = p.N, m = p.m;
+  const double* kb = p.kappa + int64_t(s) * 2 * N * N;
+  for (int t = lane; t < 512; t += 32) kap[t] = kb[2 * (int64_t(L.i0 + (t >> 5)) * N + L.j0) + (t & 31)];
+  for (int t = lane; t < kLeafPerim; t += 32) {
+    const int c = L.parent >= 0 ? p.leaf_cmap[int64_t(leaf) * kLeafPerim + t] : -1;
+    ub[t] = c >= 0 ? p.ubuf[int64_t(s) * p.u_elems + p.upper[L.parent].u_off + c] : 0.0;   // g = 0 on the domain boundary
+  }
+  __syncwarp();
+  auto k0 = [&](int cx, int cy) { return kap[cx * 32 + 2 * cy]; };
+  auto k1 = [&](int cx, int cy) { return kap[cx * 32 + 2 * cy + 1]; };
+  const double h2 = p.h * p.h;
+  for (int j = lane; j < kNI; j += 32) {
+    const int x = j % kIn + 1, y = j / kIn + 1;
+    // cell contributions of fem.py:126-145 (node = a of (x,y), b of (x-1,y), c of (x,y-1), d of (x-1,y-1))
+    const double D = 0.5 * (k0(x, y) + k1(x, y)) + k0(x - 1, y) + k1(x, y - 1) + 0.5 * (k0(x - 1, y - 1) + k1(x - 1, y - 1));
+    const double E = -0.5 * k0(x, y) - 0.5 * k1(x, y - 1);           // to (x+1, y)
+    const double Nn = -0.5 * k1(x, y) - 0.5 * k0(x - 1, y);          // to (x, y+1)
+    const double Wc = -0.5 * k0(x - 1, y) - 0.5 * k1(x - 1, y - 1);  // to (x-1, y)
+    const double Sc = -0.5 * k1(x, y - 1) - 0.5 * k0(x - 1, y - 1);  // to (x, y-1)
+    double* col = band + j * kBW;
+    col[0] = D;
+    col[1] = x < kIn ? E : 0.0;
+#pragma unroll
+    for (int i = 2; i < kBW - 1; ++i) col[i] = 0.0;
+    col[kBW - 1] = y < kIn ? Nn : 0.0;
+    // lumped load (psi_f = h^2/6 diag(2,1,1,2) per cell -> h^2 f at an interior node)
+    double r = h2 * (p.f ? p.f[int64_t(L.j0 + y) * m + L.i0 + x] : 1.0);
+    if (x == 1) r -= Wc * ub[perim_index(0, y)];
+    if (x == kIn) r -= E * ub[perim_index(kLeafCells, y)];
+    if (y == 1) r -= Sc * ub[perim_index(x, 0)];
+    if (y == kIn) r -= Nn * ub[perim_index(x, kLeafCells)];
+    rhs[j] = r;
+  }
+  // this lane's (i, m) pairs of the rank-1 band update, 1 <= m <= i <= 15 (120 pairs)
+  int pi[4], pm[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    int t = lane + 32 * u, i = 1;
+    while (t >= i) { t -= i; ++i; }
+    pi[u] = i;
+    pm[u] = t + 1;
+    if (lane + 32 * u >= 120) pi[u] = 0;
+  }
+  __syncwarp();
+  bool bad = false;
+  for (int j = 0; j < kNI; ++j) {
+    double* col = band + j * kBW;
+    const double d = col[0];
+    const double il = rsqrt_nr(d);
+    bad |= !(d > 0.0);
+    const double li = (lane >= 1 && lane < kBW) ? col[lane] * il : 0.0;
+    __syncwarp();
+    if (lane >= 1 && lane < kBW) col[lane] = li;
+    if (lane == 0) { col[0] = d * il; invd[j] = il; }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = pi[u], mm = pm[u];
+      if (i > 0 && j + i < kNI) band[(j + mm) * kBW + (i - mm)] -= col[i] * col[mm];
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && bad) record_error(p.err, HDD_ERR_NUMERICAL, s, L.ref_id);
+  // L y = rhs
+  for (int j = 0; j < kNI; ++j) {
+    if (lane == 0) rhs[j] *= invd[j];
+    __syncwarp();
+    const double yj = rhs[j];
+    if (lane >= 1 && lane < kBW && j + lane < kNI) rhs[j + lane] -= band[j * kBW + lane] * yj;
+    __syncwarp();
+  }
+  // L^T x = y
+  for (int j = kNI - 1; j >= 0; --j) {
+    if (lane == 0) rhs[j] *= invd[j];
+    __syncwarp();
+    const double xj = rhs[j];
+    if (lane >= 1 && lane < kBW && j - lane >= 0) rhs[j - lane] -= band[(j - lane) * kBW + lane] * xj;
+    __syncwarp();
+  }
+  double* Us = U + int64_t(s) * n_nodes;
+  for (int j = lane; j < kNI; j += 32) {
+    const int x = j % kIn + 1, y = j / kIn + 1;
+    Us[int64_t(L.j0 + y) * m + L.i0 + x] = rhs[j];
+  }
+  for (int t = lane; t < kLeafPerim; t += 32) {
+    int x, y;
+    if (t <= kLeafCells) { x = t; y = 0; }
+    else if (t >= 3 * kLeafCells - 1) { x = t - (3 * kLeafCells - 1); y = kLeafCells; }
+    else { y = (t - kLeafCells - 1) / 2 + 1; x = ((t - kLeafCells - 1) & 1) ? kLeafCells : 0; }
+    Us[int64_t(L.j0 + y) * m + L.i0 + x] = ub[t];
+  }
+}
+
+cudaError_t launch_leaf_solve(const DevPlan& p, int B, double* U, int64_t n_nodes, cudaStream_t s) {
+  dim3 grid(p.n_leaves, B);
+  leaf_solve_kernel<<<grid, 32, 0, s>>>(p, U, n_nodes);
+  return cudaGetLastError();
+}
+
+}  // namespace hdd

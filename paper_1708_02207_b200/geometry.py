@@ -107,6 +107,15 @@ def interior_nodes(mesh: Mesh, region: Rect) -> np.ndarray:
     return np.sort((jj[:, None] * mesh.m + ii[None, :]).ravel())
 
 
+def omega_nodes(mesh: Mesh, cells) -> np.ndarray:
+    """Sorted global ids of the mesh nodes of a closed cell rectangle (i0, i1, j0, j1):
+    the reference DDNode.idx_omega (ddtree.py:40-57)."""
+    i0, i1, j0, j1 = cells
+    ii = np.arange(i0, i1 + 1)
+    jj = np.arange(j0, j1 + 1)
+    return (jj[:, None] * mesh.m + ii[None, :]).ravel()
+
+
 def cell_centroid_tables(mesh: Mesh):
     """(cx[2N], cy[2N]): centroid coordinates of triangle type t in cell column
     i (cx[2i+t]) and cell row j (cy[2j+t]), computed as the float mean of the

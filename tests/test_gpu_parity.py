@@ -319,3 +319,67 @@ def test_c5_lowrank_config_matches_reference(torch_cuda, golden):
     assert abs(ll[0] - g["ll"][0]) <= 5e-4 * abs(g["ll"][0])
     dense = hb.forward_functionals_batch(configs.make_problem("C5"), g["Z"])
     assert rel(dense[0], g["S"][0]) <= TOL
+
+
+# ---- full-solution path (root_to_leaves / forward_full_solve /
+# solve_subdomain, hdd.py:397-490, bayes.py:201-208) ----------------------------------
+@pytest.mark.parametrize("level, n_z, nodal_f", [(4, 4, False), (5, 4, True), (7, 8, False)])
+def test_full_solution_matches_direct_solve(torch_cuda, level, n_z, nodal_f):
+    """u at every mesh node vs the oracle's sparse direct solve (level 4 = a single
+    kernel leaf, the root is a leaf)."""
+    mesh = hb.build_mesh(level)
+    tree = hb.build_tree(mesh)
+    f = np.random.default_rng(5).uniform(-1.0, 2.0, mesh.n_nodes) if nodal_f else np.ones(mesh.n_nodes)
+    obs = (("point", mesh.m * (mesh.m // 2) + mesh.m // 2),)
+    prob = hb.BayesProblem(tree, hb.SineKLField(tree, n_z), f, np.zeros(4 * mesh.n_cells),
+                           hb.MeasurementModel(obs, np.full(1, 0.01)))
+    grid = geometry.Grid(level)
+    fo = fields.SineKLField(grid, n_z)
+    Z = np.random.default_rng(6).standard_normal((3, n_z))
+    U = hb.solve_batch(prob, Z)
+    assert U.shape == (3, mesh.n_nodes)
+    for b in range(3):
+        u = direct.solve(grid, fo.kappa_values(Z[b]), f=f)
+        assert rel(U[b], u) <= TOL
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C4"])
+def test_forward_full_solve_equals_functional_path(torch_cuda, golden, name):
+    """The reference's likelihood-path equivalence (SPEC #10): S via the full
+    solution + observation operators = S via the functional sweep = goldens."""
+    prob = configs.make_problem(name)
+    g = golden(f"cfg_{name}")
+    Z = g["Z"][:2]
+    S_func = hb.forward_functionals_batch(prob, Z)
+    for b in range(Z.shape[0]):
+        S_full = hb.forward_full_solve(prob, Z[b])
+        assert rel(S_full, S_func[b]) <= TOL
+        assert rel(S_full, g["S"][b]) <= TOL
+
+
+def test_solve_subdomain_and_device_tensors(torch_cuda):
+    prob = configs.make_problem("C2")
+    Z = configs.draw_Z(configs.CONFIGS["C2"], batch=4)
+    U = hb.solve_batch(prob, Z)
+    Ud = hb.solve_batch(prob, torch_cuda.from_numpy(Z).cuda())
+    assert torch_cuda.equal(Ud.cpu(), torch_cuda.from_numpy(U))
+    tree = prob.tree
+    for nid in (tree.root_id, tree.nodes_at_depth(3)[5].id, tree.nodes_at_depth(9)[17].id):
+        node = tree.node(nid)
+        ut = hb.solve_subdomain(prob, Z[1], nid)
+        assert np.array_equal(ut, U[1][hb.omega_nodes(tree.mesh, node.cells)])
+        assert ut.size == (node.cells[1] - node.cells[0] + 1) * (node.cells[3] - node.cells[2] + 1)
+
+
+def test_solve_requires_primal_plan(torch_cuda):
+    """hdd_solve_batch on an adjoint plan is a UsageError, like root_to_leaves on a
+    store without kept maps (hdd.py:405-406)."""
+    prob = configs.make_problem("C2", mode=0)
+    plan = prob.plan()
+    assert plan.info().mode == 0
+    Z = torch_cuda.from_numpy(configs.draw_Z(configs.CONFIGS["C2"], batch=2)).cuda()
+    U = torch_cuda.empty((2, prob.tree.mesh.n_nodes), dtype=torch_cuda.float64, device="cuda")
+    with pytest.raises(hb.UsageError):
+        plan.check(plan.lib.hdd_solve_batch(plan.handle, C.c_void_p(Z.data_ptr()), 2, C.c_void_p(U.data_ptr()), None))
+    # the Python route builds a primal plan for the sweep on its own
+    assert np.isfinite(hb.solve_batch(prob, Z.cpu().numpy())).all()
