@@ -34,4 +34,5 @@ from .geometry import (  # noqa: F401
 )
 
 __version__ = "0.1.0"
-from . import configs, parallel  # noqa: E402,F401
+from . import configs, parallel, posterior  # noqa: E402,F401
+from .posterior import ChainSpec, GridSpec, PosteriorResult, posterior_grid, posterior_mcmc, posterior_mcmc_chains  # noqa: E402,F401
