@@ -30,7 +30,7 @@ from .bayes import (  # noqa: F401
 )
 from .errors import ConfigError, GeometryError, NumericalError, UsageError  # noqa: F401
 from .geometry import (  # noqa: F401
-    DDTree, Mesh, Rect, boundary_nodes, build_mesh, build_tree, interior_nodes, omega_nodes,
+    DDTree, Mesh, Rect, boundary_nodes, build_mesh, build_tree, dump_tree, interior_nodes, omega_nodes,
 )
 
 __version__ = "0.1.0"

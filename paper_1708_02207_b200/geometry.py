@@ -225,5 +225,28 @@ class DDTree:
         return out
 
 
+def dump_tree(tree: DDTree) -> str:
+    """Text lines `depth region |I(omega)| |I(boundary)| |I(gamma)|` for every node in
+    post-order — the reference regression format (ddtree.py:193-202)."""
+    h = tree.mesh.h
+    lines = []
+
+    def rec(r, depth):
+        i0, i1, j0, j1 = r
+        w, hh = i1 - i0, j1 - j0
+        gamma = 0
+        if w * hh > 1:
+            s1, s2 = _split(r, depth)
+            rec(s1, depth + 1)
+            rec(s2, depth + 1)
+            gamma = (hh - 1) if s1[1] != i1 else (w - 1)    # vertical cut: interior of the x line
+        region = f"[{i0 * h:g},{i1 * h:g}]x[{j0 * h:g},{j1 * h:g}]"
+        lines.append(f"{depth} {region} {(w + 1) * (hh + 1)} {2 * (w + hh)} {gamma}")
+
+    N = tree.mesh.n_cells
+    rec((0, N, 0, N), 0)
+    return "\n".join(lines) + "\n"
+
+
 def build_tree(mesh: Mesh) -> DDTree:
     return DDTree(mesh)

@@ -242,3 +242,12 @@ def test_primal_routing_auto_selection():
         c1 = configs.CONFIGS[name]
         p1 = host_problem(c1.level, c1.n_z, configs.observations(c1), mode=-1).plan()
         assert p1.info().mode == 0
+
+
+@pytest.mark.parametrize("level", [4, 5])
+def test_dump_tree_matches_reference_format(level):
+    """geometry.dump_tree reproduces the reference's regression dump line for line."""
+    from pathlib import Path
+    from paper_1708_02207_b200.geometry import dump_tree
+    ref = (Path(__file__).resolve().parent / "golden" / f"dump_tree_L{level}.txt").read_text()
+    assert dump_tree(hb.build_tree(hb.build_mesh(level))) == ref
