@@ -1655,21 +1655,25 @@ __global__ void __launch_bounds__(256) compress_kernel(DevPlan p, const DevUpper
   __shared__ int s_bad, s_k, s_piv[32];
   __shared__ double s_an2, s_bn2;
   auto A = [&](int i, int j) { const int r = R[i], c = Cc[j]; return r >= c ? psi[tri(r) + c] : psi[tri(c) + r]; };
-  // ---- pass 1: Y = A Omega, ||A||^2 ----
+  // ---- pass 1: Y = A Omega (thread per row and 4 sketch columns), ||A||^2 ----
   double an = 0.0;
-  for (int i = tid; i < P_; i += 256) {
-    double y[32];
-#pragma unroll
-    for (int t = 0; t < 32; ++t) y[t] = 0.0;
+  for (int w = tid; w < P_ * 8; w += 256) {
+    const int i = w >> 3, t0 = (w & 7) * 4;
+    double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
     for (int j = 0; j < Q_; ++j) {
       const double a = A(i, j);
-      an = fma(a, a, an);
-      const double* om = p.lr_omega + j * 32;
-#pragma unroll
-      for (int t = 0; t < 32; ++t) y[t] = fma(a, om[t], y[t]);
+      if (t0 == 0) an = fma(a, a, an);
+      const double4 om = *reinterpret_cast<const double4*>(p.lr_omega + j * 32 + t0);
+      y0 = fma(a, om.x, y0);
+      y1 = fma(a, om.y, y1);
+      y2 = fma(a, om.z, y2);
+      y3 = fma(a, om.w, y3);
     }
-#pragma unroll
-    for (int t = 0; t < 32; ++t) Y[i * 33 + t] = t < L ? y[t] : 0.0;
+    double* yr = Y + i * 33 + t0;
+    yr[0] = t0 < L ? y0 : 0.0;
+    yr[1] = t0 + 1 < L ? y1 : 0.0;
+    yr[2] = t0 + 2 < L ? y2 : 0.0;
+    yr[3] = t0 + 3 < L ? y3 : 0.0;
   }
   for (int off = 16; off > 0; off >>= 1) an += __shfl_xor_sync(0xffffffffu, an, off);
   if (lane == 0) red[warp] = an;
@@ -1708,7 +1712,7 @@ __global__ void __launch_bounds__(256) compress_kernel(DevPlan p, const DevUpper
       s_bad = 0;
     }
     __syncthreads();
-    if (warp == 0) factor_diag_block<32>(G, kLdd, LiT, &s_bad);
+    if (warp == 0) factor_block32(G, kLdd, G, LiT, &s_bad);   // G doubles as the L scratch
     __syncthreads();
     for (int i = tid; i < P_; i += 256) {
       double y[32];

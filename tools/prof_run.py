@@ -1,5 +1,5 @@
 """Minimal driver for ncu captures: one warm forward + one profiled forward.
-usage: python tools/prof_run.py CONFIG BATCH"""
+usage: python tools/prof_run.py CONFIG BATCH [lr]   (lr: the config's low-rank ToleranceSpec)"""
 import sys
 from pathlib import Path
 
@@ -15,7 +15,8 @@ from paper_1708_02207_b200 import _lib, configs  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 cfg = configs.CONFIGS[name]
-prob = configs.make_problem(name)
+lowrank = len(sys.argv) > 3 and sys.argv[3] == "lr"
+prob = configs.make_problem(name, compression=lowrank)
 plan = prob.plan()
 info = plan.info()
 Z = torch.from_numpy(configs.draw_Z(cfg, batch=max(B, cfg.batch))[:B].copy()).cuda()
