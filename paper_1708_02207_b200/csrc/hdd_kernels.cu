@@ -1636,7 +1636,7 @@ __global__ void __launch_bounds__(256) psi_norm_kernel(DevPlan p, const DevUpper
   }
 }
 
-__global__ void __launch_bounds__(256) compress_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int blk0) {
+__global__ void __launch_bounds__(256, 2) compress_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int blk0) {
   extern __shared__ __align__(16) double sm[];
   const int32_t* bd = p.lr_blk + 5 * (blk0 + blockIdx.y);
   const int ln = bd[0], roff = bd[1], P_ = bd[2], coff = bd[3], Q_ = bd[4];
@@ -1714,18 +1714,23 @@ __global__ void __launch_bounds__(256) compress_kernel(DevPlan p, const DevUpper
     __syncthreads();
     if (warp == 0) factor_block32(G, kLdd, G, LiT, &s_bad);   // G doubles as the L scratch
     __syncthreads();
-    for (int i = tid; i < P_; i += 256) {
-      double y[32];
+    // Y <- Y R^-1 in place, 32 rows x 8 column groups of 4 per chunk (compute, barrier, write)
+    for (int i0 = 0; i0 < P_; i0 += 32) {
+      const int i = i0 + (tid >> 3), c0 = (tid & 7) * 4;
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
+      if (i < P_) {
+        const double* yr = Y + i * 33;
+        for (int t = 0; t < c0 + 4; ++t) {
+          const double yt = yr[t];
 #pragma unroll
-      for (int t = 0; t < 32; ++t) y[t] = Y[i * 33 + t];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        double v = 0.0;
-#pragma unroll
-        for (int t = 0; t < 32; ++t)
-          if (t <= c) v = fma(y[t], LiT[t * kLdd + c], v);
-        Y[i * 33 + c] = c < L ? v : 0.0;
+          for (int u = 0; u < 4; ++u)
+            if (t <= c0 + u) v[u] = fma(yt, LiT[t * kLdd + c0 + u], v[u]);
+        }
       }
+      __syncthreads();
+      if (i < P_)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) Y[i * 33 + c0 + u] = c0 + u < L ? v[u] : 0.0;
     }
     __syncthreads();
   }
@@ -1734,14 +1739,18 @@ __global__ void __launch_bounds__(256) compress_kernel(DevPlan p, const DevUpper
   double macc[4] = {0.0, 0.0, 0.0, 0.0};     // thread owns M entries tid + 256 u
   for (int j0 = 0; j0 < Q_; j0 += 64) {
     __syncthreads();
-    for (int t = tid; t < 32 * 64; t += 256) {
-      const int a = t >> 6, jj = t & 63, j = j0 + jj;
-      double v = 0.0;
-      if (a < L && j < Q_)
-        for (int i = 0; i < P_; ++i) v = fma(Y[i * 33 + a], A(i, j), v);
-      Bc[a * 65 + jj] = v;
-    }
-    __syncthreads();
+    {   // B chunk: thread per (column, 8 rows of B); each A entry read by 4 threads
+      const int jj = tid & 63, a0 = (tid >> 6) * 8, j = j0 + jj;
+      double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      if (j < Q_)
+        for (int i = 0; i < P_; ++i) {
+          const double x = A(i, j);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = fma(Y[i * 33 + a0 + u], x, v[u]);
+        }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) Bc[(a0 + u) * 65 + jj] = (a0 + u < L) ? v[u] : 0.0;
+    }    __syncthreads();
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int e = tid + 256 * u, a = e >> 5, b = e & 31;
