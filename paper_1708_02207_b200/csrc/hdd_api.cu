@@ -213,7 +213,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
     csrc.insert(csrc.end(), U.csrc.begin(), U.csrc.end());
     ccoef.insert(ccoef.end(), U.ccoef.begin(), U.ccoef.end());
     cbirth.insert(cbirth.end(), U.cbirth.begin(), U.cbirth.end());
-    size_t sm = pl->depth_tier[U.depth] ? 0 : merge_m2_smem_bytes(ngp_u, d.ldp, U.K, U.nc);
+    size_t sm = pl->depth_tier[U.depth] ? merge_l_smem_bytes(U.K, U.nc) : merge_m2_smem_bytes(ngp_u, d.ldp, U.K, U.nc);
     if (!pl->depth_tier[U.depth]) {
       // stage the sons in smem when panel + sons still allow two CTAs per SM
       const size_t sons = sizeof(double) * size_t(((d.son_elems[0] + 1) & ~1) + ((d.son_elems[1] + 1) & ~1));

@@ -104,7 +104,7 @@ cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_ou
 cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
                          int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s);
 size_t merge_m2_smem_bytes(int ngp, int ldp, int K, int nc);
-size_t merge_l_smem_bytes();
+size_t merge_l_smem_bytes(int K, int nc);
 cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int blk0, int nblk, int B,
                             int pmax, cudaStream_t s);
 cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_ng, cudaStream_t s);

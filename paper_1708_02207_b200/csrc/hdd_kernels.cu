@@ -1401,11 +1401,13 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
 }
 
 // -- tier L: panel in HBM ----------------------------------------------------
-size_t merge_l_smem_bytes() {
-  // F phases: D/LiT/Xc/Lt; epilogue: 2 buffers x (A, B) chunks of 32 x kLds (reuses the same space)
-  const size_t f = 2 * 32 * kLdd + 32 * kLds + 32 * kLdd;
-  const size_t e = 4 * 32 * kLds;
-  return sizeof(double) * (f > e ? f : e) + 1024;
+// smem: F phases (L scratch / LiT / Xc / Lt) and the epilogue's 2 x (A, B) chunks of
+// 32 x kLds share the front region; the son maps and column plan follow it.
+constexpr size_t kLRegion = (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) > (4 * 32 * kLds)
+                                ? (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) : (4 * 32 * kLds);
+size_t merge_l_smem_bytes(int K, int nc) {
+  const size_t ints = (size_t(2 * K + 3 * nc) + 1) & ~size_t(1);
+  return sizeof(double) * (kLRegion + ints / 2 + 2 * size_t(nc)) + 1024;
 }
 
 __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
@@ -1423,7 +1425,23 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
   double* Xc = LiT + 32 * kLdd;           // [32][kLds]
   double* Lt = Xc + 32 * kLds;            // [32][kLdd]
   __shared__ int s_bad;
-  const MergeCtx mc = merge_ctx(p, U, s);
+  MergeCtx mc = merge_ctx(p, U, s);
+  {   // son maps and column plan in smem (the gathers' first hop)
+    int32_t* gms = reinterpret_cast<int32_t*>(sm + kLRegion);
+    int32_t* cis = gms + 2 * U.K;
+    double* ccs = reinterpret_cast<double*>(gms + ((2 * U.K + 3 * nc + 1) & ~1));
+    for (int t = tid; t < 2 * U.K; t += 256) gms[t] = __ldg(mc.gm + t);
+    for (int t = tid; t < 2 * nc; t += 256) {
+      cis[t] = __ldg(mc.csrc + t);
+      ccs[t] = __ldg(mc.ccoef + t);
+    }
+    for (int t = tid; t < nc; t += 256) cis[2 * nc + t] = __ldg(mc.cbirth + t);
+    mc.gm = gms;
+    mc.csrc = cis;
+    mc.cbirth = cis + 2 * nc;
+    mc.ccoef = ccs;
+    __syncthreads();
+  }
   for (int g = warp; g < ngp; g += 8) gather_panel_row(mc, k, ng, Kp, W, g, P + int64_t(g) * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   __syncthreads();
@@ -1519,10 +1537,9 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
       merge_m2_kernel<8, 256><<<grid, 256, smem, s>>>(p, nodes_dev);
     }
   } else {
-    const size_t sm = merge_l_smem_bytes();
-    e = cudaFuncSetAttribute(merge_l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    e = cudaFuncSetAttribute(merge_l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    merge_l_kernel<<<grid, 256, sm, s>>>(p, nodes_dev, ws, ws_stride);
+    merge_l_kernel<<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride);
   }
   return cudaGetLastError();
 }
