@@ -185,6 +185,10 @@ int hdd_debug_node_output(HddPlan* plan, int32_t idx, int32_t b,
 /* Profiling hook: clock64 stamps of leaf CTA (0,0) of the last launch
  * ([0] start, [1] after the register base, [10 + 8 (5-r) + phase] per level). */
 int hdd_debug_leaf_clocks(long long* out64);
+/* Per-phase clock64 stamps [32 depths][8] of CTA (sample 0, node 0) of each merge
+ * launch of the last batch (profiling hook): 0 start, 1 maps staged, 2 panel
+ * gathered, 3 eliminated, 4 sigma/factors written, 5 Schur update written. */
+int hdd_debug_merge_clocks(long long* out);
 
 const char* hdd_version(void);
 

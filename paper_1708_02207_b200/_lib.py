@@ -90,6 +90,7 @@ EXPORTS = {
     "hdd_leaf_template": (C.c_int, [C.c_int32, _i32p, _i32p, _i32p, C.POINTER(_i32p), C.POINTER(_i32p)]),
     "hdd_debug_node_output": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, _f64p, _f64p, _f64p]),
     "hdd_debug_leaf_clocks": (C.c_int, [C.POINTER(C.c_longlong)]),
+    "hdd_debug_merge_clocks": (C.c_int, [C.POINTER(C.c_longlong)]),
     "hdd_version": (C.c_char_p, []),
 }
 

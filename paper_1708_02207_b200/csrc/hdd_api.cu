@@ -406,6 +406,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
 extern "C" {
 
 int hdd_debug_leaf_clocks(long long* out) { return read_leaf_clocks(out); }
+int hdd_debug_merge_clocks(long long* out) { return read_merge_clocks(out); }
 
 const char* hdd_version(void) { return "hdd_b200 0.1 (sm_100a)"; }
 
@@ -470,7 +471,7 @@ static int run_sub_batch(HddPlan* pl, const double* Z, int B, double* S, double*
     const auto& ids = P.upper_by_depth[dep];
     if (!ids.empty()) {
       CU(launch_merge(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->ws, pl->depth_ws[dep],
-                      pl->depth_tier[dep], pl->depth_rows[dep], pl->depth_smem[dep], pl->depth_nb[dep], st));
+                      pl->depth_tier[dep], pl->depth_rows[dep], pl->depth_smem[dep], pl->depth_nb[dep], st, dep));
       if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0)
         CU(launch_compress(D, pl->d_upper + ids.front(), int(ids.size()), pl->lr_blk0[dep], pl->lr_nblk[dep], B,
                            pl->lr_pmax[dep], st));

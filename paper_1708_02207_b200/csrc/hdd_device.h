@@ -102,7 +102,7 @@ struct DevPlan {
 cudaError_t launch_kappa(const DevPlan& p, const double* Z, int B, double* kappa, cudaStream_t s);
 cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_out);
 cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
-                         int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s);
+                         int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s, int slot = -1);
 size_t merge_m2_smem_bytes(int ngp, int ldp, int K, int nc);
 size_t merge_l_smem_bytes(int K, int nc);
 cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int blk0, int nblk, int B,
@@ -113,5 +113,6 @@ cudaError_t launch_leaf_solve(const DevPlan& p, int B, double* U, int64_t n_node
 size_t leaf_smem_bytes(int leaf_cols);
 int upload_leaf_template();
 int read_leaf_clocks(long long* out);
+int read_merge_clocks(long long* out);
 
 }  // namespace hdd

@@ -132,6 +132,13 @@ __device__ long long g_leaf_clk[64];
 int read_leaf_clocks(long long* out) {
   return cudaMemcpyFromSymbol(out, g_leaf_clk, sizeof(long long) * 64) == cudaSuccess ? 0 : -1;
 }
+// per-phase clock64 stamps of CTA (sample 0, node 0) of every merge launch, by depth
+__device__ long long g_merge_clk[32][8];
+#define MERGE_TICK(i) \
+  do { if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && slot >= 0 && slot < 32) g_merge_clk[slot][i] = clock64(); } while (0)
+int read_merge_clocks(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_merge_clk, sizeof(long long) * 32 * 8) == cudaSuccess ? 0 : -1;
+}
 
 
 int upload_leaf_template() {
@@ -1277,8 +1284,9 @@ size_t merge_m2_smem_bytes(int ngp, int ldp, int K, int nc) {
 }
 
 template <int NB, int NTH>
-__global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes) {
+__global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int slot) {
   extern __shared__ __align__(16) double sm[];
+  MERGE_TICK(0);
   const DevUpper& U = nodes[blockIdx.y];
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1319,6 +1327,7 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
   mc.ccoef = ccs;
   if (U.stage) cp_async_wait<0>();
   __syncthreads();
+  MERGE_TICK(1);
   for (int g = warp; g < ngp; g += NWp) gather_panel_row(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   const int gq = lane & 3, gr = lane >> 2;
@@ -1329,6 +1338,7 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
   // updates and factors the next diagonal block while warps 1.. apply the trailing
   // update of the current block row (two barriers per block).
   __syncthreads();                         // panel gathered
+  MERGE_TICK(2);
   if (warp == 0) factor_block8(P + k, ldp, Ls, Li, piv, &s_bad);
   __syncthreads();
   for (int r0 = 0; r0 < ngp; r0 += NB) {
@@ -1387,6 +1397,7 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
     __syncthreads();
   }
   __syncthreads();
+  MERGE_TICK(3);
   if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
   if (p.mode == 1) store_factors(p, U, s, P, ldp, Kp, false, tid, NT);
   double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
@@ -1397,7 +1408,9 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
       for (int g = 0; g < ng; ++g) v = fma(P[g * ldp + Kp], P[g * ldp + Kp + c], v);
     out[tk + k * nc + c] = v;
   }
+  MERGE_TICK(4);
   schur_epilogue<true>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
+  MERGE_TICK(5);
 }
 
 // -- tier L: panel in HBM ----------------------------------------------------
@@ -1411,8 +1424,9 @@ size_t merge_l_smem_bytes(int K, int nc) {
 }
 
 __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
-                                                          double* __restrict__ ws, int64_t ws_stride) {
+                                                          double* __restrict__ ws, int64_t ws_stride, int slot) {
   extern __shared__ __align__(16) double sm[];
+  MERGE_TICK(0);
   const DevUpper& U = nodes[blockIdx.y];
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1442,9 +1456,11 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
     mc.ccoef = ccs;
     __syncthreads();
   }
+  MERGE_TICK(1);
   for (int g = warp; g < ngp; g += 8) gather_panel_row(mc, k, ng, Kp, W, g, P + int64_t(g) * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   __syncthreads();
+  MERGE_TICK(2);
   for (int r0 = 0; r0 < ngp; r0 += kLB) {
     if (warp == 0) factor_block32(P + int64_t(r0) * ldp + k + r0, ldp, sm, LiT, &s_bad);
     __syncthreads();
@@ -1507,6 +1523,7 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
     }
     __syncthreads();
   }
+  MERGE_TICK(3);
   if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
   if (p.mode == 1) store_factors(p, U, s, P, ldp, Kp, false, tid, 256);
   double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
@@ -1517,11 +1534,13 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
       for (int g = 0; g < ng; ++g) v = fma(P[int64_t(g) * ldp + Kp], P[int64_t(g) * ldp + Kp + c], v);
     out[tk + k * nc + c] = v;
   }
+  MERGE_TICK(4);
   schur_epilogue_l(mc, P, ldp, k, ngp, Kp, nc, out, sm);
+  MERGE_TICK(5);
 }
 
 cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
-                         int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s) {
+                         int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s, int slot) {
   (void)max_rows;
   (void)nb;
   cudaError_t e;
@@ -1530,16 +1549,16 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
     if (smem > 100 * 1024) {
       e = cudaFuncSetAttribute(merge_m2_kernel<8, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
-      merge_m2_kernel<8, 512><<<grid, 512, smem, s>>>(p, nodes_dev);
+      merge_m2_kernel<8, 512><<<grid, 512, smem, s>>>(p, nodes_dev, slot);
     } else {
       e = cudaFuncSetAttribute(merge_m2_kernel<8, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
-      merge_m2_kernel<8, 256><<<grid, 256, smem, s>>>(p, nodes_dev);
+      merge_m2_kernel<8, 256><<<grid, 256, smem, s>>>(p, nodes_dev, slot);
     }
   } else {
     e = cudaFuncSetAttribute(merge_l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    merge_l_kernel<<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride);
+    merge_l_kernel<<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride, slot);
   }
   return cudaGetLastError();
 }

@@ -39,3 +39,12 @@ for r in range(5, -1, -1):
     ph = [c[base + i] - (prev if i == 0 else c[base + i - 1]) for i in range(4)]
     print(f"  level {r}: A {ph[0]}  B {ph[1]} (chol {c[base + 4] - c[base]})  C {ph[2]}  D {ph[3]}")
 print("  total", c[63] - c[0])
+
+mc = (C.c_longlong * 256)()
+plan.lib.hdd_debug_merge_clocks(mc)
+print("merge CTA(0,0) phase cycles: maps / gather / eliminate / sigma+factors / Schur update")
+for d in range(info.leaf_depth - 1, -1, -1):
+    c = [int(mc[d * 8 + i]) for i in range(6)]
+    if c[0] == 0:
+        continue
+    print(f"  d{d}: " + "  ".join(str(c[i + 1] - c[i]) for i in range(5)) + f"   total {c[5] - c[0]}")
