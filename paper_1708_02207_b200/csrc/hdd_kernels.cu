@@ -320,6 +320,25 @@ __device__ __forceinline__ void stage_panel_program(uint64_t* dst) {
   cp_async_commit();
 }
 
+// TMA bulk copies (cp.async.bulk, global -> shared) completing on an mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n"
+               ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
 // 1/sqrt(d): MUFU seed + two Newton steps (full double precision for the
 // well-scaled pivots of the in-leaf factorizations)
 __device__ __forceinline__ double rsqrt_nr(double d) {
@@ -1280,7 +1299,7 @@ __device__ __forceinline__ void factor_block8(const double* D, int ld, double* L
 // [nc][2], cbirth [nc]) int | ccoef [nc][2] | staged sons (optional)
 size_t merge_m2_smem_bytes(int ngp, int ldp, int K, int nc) {
   const size_t ints = (size_t(2 * K + 3 * nc) + 1) & ~size_t(1);
-  return sizeof(double) * (size_t(ngp) * ldp + 8 + 128 + ints / 2 + 2 * size_t(nc)) + 64;
+  return sizeof(double) * (size_t(ngp) * ldp + 8 + 128 + ints / 2 + 2 * size_t(nc) + 2) + 64;   // +2: 16-byte alignment of the staged sons
 }
 
 template <int NB, int NTH>
@@ -1300,20 +1319,23 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
   int32_t* gms = reinterpret_cast<int32_t*>(piv + 8 + 128);
   int32_t* cis = gms + 2 * U.K;
   double* ccs = reinterpret_cast<double*>(gms + ((2 * U.K + 3 * nc + 1) & ~1));
-  double* st = ccs + 2 * nc;
+  double* st = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ccs + 2 * nc) + 15) & ~uintptr_t(15));
   __shared__ int s_bad;
+  __shared__ __align__(8) uint64_t s_bar;
   MergeCtx mc = merge_ctx(p, U, s);
   if (U.stage) {
-    // stage both sons' packed outputs in shared memory (asynchronous 8-byte copies)
-#pragma unroll
-    for (int sn = 0; sn < 2; ++sn) {
-      const int n = int(U.son_elems[sn]);
-      const double* src = mc.sv[sn].b;
-      for (int t = tid; t < n; t += NT) cp_async8(st + t, src + t);
-      mc.sv[sn].b = st;
-      st += (n + 1) & ~1;
+    // stage both sons' packed outputs in shared memory: two TMA bulk copies (the
+    // per-sample blocks are even-sized, hence 16-byte aligned) on one mbarrier
+    if (tid == 0) {
+      mbar_init(&s_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      const uint32_t b0 = uint32_t(U.son_elems[0]) * 8u, b1 = uint32_t(U.son_elems[1]) * 8u;
+      mbar_arrive_expect_tx(&s_bar, b0 + b1);
+      bulk_g2s(st, mc.sv[0].b, b0, &s_bar);
+      bulk_g2s(st + U.son_elems[0], mc.sv[1].b, b1, &s_bar);
     }
-    cp_async_commit();
+    mc.sv[0].b = st;
+    mc.sv[1].b = st + U.son_elems[0];
   }
   for (int t = tid; t < 2 * U.K; t += NT) gms[t] = __ldg(mc.gm + t);
   for (int t = tid; t < 2 * nc; t += NT) {
@@ -1325,8 +1347,8 @@ __global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPl
   mc.csrc = cis;
   mc.cbirth = cis + 2 * nc;
   mc.ccoef = ccs;
-  if (U.stage) cp_async_wait<0>();
-  __syncthreads();
+  __syncthreads();                         // maps staged; the mbarrier is initialised
+  if (U.stage) mbar_wait(&s_bar, 0);
   MERGE_TICK(1);
   for (int g = warp; g < ngp; g += NWp) gather_panel_row(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32);
   if (tid == 0) s_bad = 0;

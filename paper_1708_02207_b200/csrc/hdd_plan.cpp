@@ -549,7 +549,8 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
   // ---- output layouts -----------------------------------------------------
   // node outputs: [Psi lower-packed | R (k x nc) | sigma (nc)]; *_ld is the R row stride
   P.leaf_ld = P.leaf_cols;
-  P.leaf_elems = int64_t(kLeafPerim) * (kLeafPerim + 1) / 2 + int64_t(kLeafPerim) * P.leaf_cols + P.leaf_cols;
+  // per-sample blocks padded to an even number of doubles: 16-byte aligned bulk (TMA) copies
+  P.leaf_elems = (int64_t(kLeafPerim) * (kLeafPerim + 1) / 2 + int64_t(kLeafPerim) * P.leaf_cols + P.leaf_cols + 1) & ~int64_t(1);
   const bool keep = d->keep_nodes != 0;
   P.n_buffers = keep ? dl + 1 : 2;
   P.buf_elems_per_sample.assign(P.n_buffers, 0);
@@ -561,7 +562,7 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     for (int u : P.upper_by_depth[dep]) {
       UpperNode& U = P.upper[u];
       U.out_ld = U.nc;
-      U.out_elems = int64_t(U.k) * (U.k + 1) / 2 + int64_t(U.k) * U.nc + U.nc;
+      U.out_elems = (int64_t(U.k) * (U.k + 1) / 2 + int64_t(U.k) * U.nc + U.nc + 1) & ~int64_t(1);
       U.buf = b;
       U.out_off = acc;          // scaled by the sub-batch size at allocation
       acc += U.out_elems;
