@@ -1073,6 +1073,21 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
   for (int t = grp; t < na * nbt; t += ngrp) {
     const int a0 = (t / nbt) * 32, b0 = (t % nbt) * 64;
     if (b0 + 64 <= k && b0 > a0 + 31) continue;   // strictly upper Psi tile
+    // 8x8 DMMA blocks of this warp's 16x16 sub-tile that hold outputs (warp-uniform):
+    // rows < k, columns < k + nc, not strictly above the diagonal of Psi
+    bool live[2][2];
+    bool any = false;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int ar = a0 + m0 + 8 * i, bc = b0 + n0 + 8 * j;
+        live[i][j] = ar < k && bc < ow && !(bc + 8 <= k && bc > ar + 7);
+        any |= live[i][j];
+      }
+    if constexpr (SMEM) {
+      if (!any) continue;                          // no barriers in the smem-panel loop
+    }
     double acc[2][2][2] = {};
     int acol[2], bcol[2];
 #pragma unroll
@@ -1108,7 +1123,8 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int j = 0; j < 2; ++j) dmma884(acc[i][j], av[i], bv[j]);
+          for (int j = 0; j < 2; ++j)
+            if (live[i][j]) dmma884(acc[i][j], av[i], bv[j]);
       }
     } else {
       for (int g0 = 0; g0 < ngp; g0 += 32) {
