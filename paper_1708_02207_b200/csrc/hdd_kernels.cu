@@ -1020,6 +1020,7 @@ __device__ __forceinline__ double gather_sig(const MergeCtx& c, int col) {
 
 // panel row g of [A21 | A22 (padded) | R_gamma] -> dst (smem or HBM); four entries
 // per thread in flight (the son reads are independent, predicated loads)
+template <int U = 4>
 __device__ __forceinline__ void gather_panel_row(const MergeCtx& c, int k, int ng, int Kp, int W, int g,
                                                  double* dst, int lane0, int step) {
   if (g >= ng) {
@@ -1028,7 +1029,6 @@ __device__ __forceinline__ void gather_panel_row(const MergeCtx& c, int k, int n
   }
   const int a = k + g;
   const int pa0 = c.gm[a], pa1 = c.gm[c.K + a];
-  constexpr int U = 4;
   for (int j0 = lane0; j0 < W; j0 += U * step) {
     double v0[U], v1[U];
 #pragma unroll
@@ -1495,7 +1495,7 @@ __global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpp
     __syncthreads();
   }
   MERGE_TICK(1);
-  for (int g = warp; g < ngp; g += 8) gather_panel_row(mc, k, ng, Kp, W, g, P + int64_t(g) * ldp, lane, 32);
+  for (int g = warp; g < ngp; g += 8) gather_panel_row<8>(mc, k, ng, Kp, W, g, P + int64_t(g) * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   __syncthreads();
   MERGE_TICK(2);
