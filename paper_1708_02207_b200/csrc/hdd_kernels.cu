@@ -49,37 +49,47 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 // ---------------------------------------------------------------------------
 // K1: coefficient field
 // ---------------------------------------------------------------------------
-// grid: (ceil(N/128), N, B); block 128. Thread = cell (i = blockIdx.y, j).
+// grid: (ceil(N/128), N/8, B); block 128.  Thread = column j of 8 consecutive cell rows
+// i0..i0+7: each sy_k(j) pair is loaded once and feeds 8 cells; double2 stores.
+constexpr int kKappaRows = 8;
 __global__ void __launch_bounds__(128) kappa_kernel(DevPlan p, const double* __restrict__ Z, int B,
                                                     double* __restrict__ kappa) {
-  extern __shared__ double czx[];   // [n_z][2]: coef_k z_k sx_k(2i), coef_k z_k sx_k(2i+1)
+  extern __shared__ double czx[];   // [n_z][kKappaRows][2]: coef_k z_k sx_k(2i + type)
   const int N = p.N, nz = p.n_z;
-  const int i = blockIdx.y, s = blockIdx.z;
+  const int i0 = blockIdx.y * kKappaRows, s = blockIdx.z;
   const double* z = Z + int64_t(s) * nz;
-  for (int k = threadIdx.x; k < nz; k += blockDim.x) {
-    double cz = p.coef[k] * z[k];
-    czx[2 * k] = cz * p.sx[int64_t(k) * 2 * N + 2 * i];
-    czx[2 * k + 1] = cz * p.sx[int64_t(k) * 2 * N + 2 * i + 1];
+  for (int t = threadIdx.x; t < nz * kKappaRows * 2; t += blockDim.x) {
+    const int k = t / (kKappaRows * 2), r = t - k * (kKappaRows * 2);
+    czx[t] = p.coef[k] * z[k] * p.sx[int64_t(k) * 2 * N + 2 * i0 + r];
   }
   __syncthreads();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= N) return;
-  double q0 = 0.0, q1 = 0.0;
+  double q[kKappaRows][2] = {};
   const double2* sy2 = reinterpret_cast<const double2*>(p.sy);
   for (int k = 0; k < nz; ++k) {
-    double2 t = __ldg(sy2 + int64_t(k) * N + j);
-    q0 = fma(czx[2 * k], t.x, q0);
-    q1 = fma(czx[2 * k + 1], t.y, q1);
+    const double2 t = __ldg(sy2 + int64_t(k) * N + j);
+    const double* c = czx + k * kKappaRows * 2;
+#pragma unroll
+    for (int r = 0; r < kKappaRows; ++r) {
+      q[r][0] = fma(c[2 * r], t.x, q[r][0]);
+      q[r][1] = fma(c[2 * r + 1], t.y, q[r][1]);
+    }
   }
-  double2 out = make_double2(exp(q0), exp(q1));
-  if (!(out.x > 0.0) || !(out.y > 0.0) || !isfinite(out.x) || !isfinite(out.y))
-    record_error(p.err, HDD_ERR_CONFIG, s, -1);
-  reinterpret_cast<double2*>(kappa + int64_t(s) * 2 * N * N)[int64_t(i) * N + j] = out;
+  double2* out = reinterpret_cast<double2*>(kappa + int64_t(s) * 2 * N * N);
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < kKappaRows; ++r) {
+    const double2 v = make_double2(exp(q[r][0]), exp(q[r][1]));
+    bad |= !(v.x > 0.0) || !(v.y > 0.0) || !isfinite(v.x) || !isfinite(v.y);
+    out[int64_t(i0 + r) * N + j] = v;
+  }
+  if (bad) record_error(p.err, HDD_ERR_CONFIG, s, -1);
 }
 
 cudaError_t launch_kappa(const DevPlan& p, const double* Z, int B, double* kappa, cudaStream_t s) {
-  dim3 grid((p.N + 127) / 128, p.N, B);
-  kappa_kernel<<<grid, 128, size_t(2) * p.n_z * sizeof(double), s>>>(p, Z, B, kappa);
+  dim3 grid((p.N + 127) / 128, p.N / kKappaRows, B);
+  kappa_kernel<<<grid, 128, size_t(2) * kKappaRows * p.n_z * sizeof(double), s>>>(p, Z, B, kappa);
   return cudaGetLastError();
 }
 
