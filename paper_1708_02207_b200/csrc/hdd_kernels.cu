@@ -965,6 +965,53 @@ __device__ __forceinline__ void factor_block32(const double* src, int ld, double
   __syncwarp();
 }
 
+// Cholesky + L^-1 of an N x N SPD block (N <= 24) by one warp: lane = row, shuffles;
+// L^-1 right-looking, lane = column.  Same conventions as factor_block32.
+template <int N>
+__device__ __forceinline__ void factor_blockN(const double* src, int ld, double* Ls, double* LiT, int* bad) {
+  static_assert(N <= 24, "use factor_block32");
+  const int lane = threadIdx.x & 31;
+  const int row = lane < N ? lane : N - 1;
+  {
+    double a[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) a[l] = l <= row ? src[row * ld + l] : (l == row ? 1.0 : 0.0);
+    bool nb = false;
+    double ild = 1.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const double dj = __shfl_sync(0xffffffffu, a[j], j);
+      nb |= !(dj > 0.0);
+      const double il = rsqrt_nr(dj);
+      const double lij = a[j] * il;
+#pragma unroll
+      for (int l = j + 1; l < N; ++l) a[l] = fma(-lij, __shfl_sync(0xffffffffu, lij, l), a[l]);
+      if (row == j) ild = il;
+      a[j] = lij;
+    }
+    __syncwarp();
+    if (lane < N)
+#pragma unroll
+      for (int l = 0; l < N; ++l)
+        if (l <= lane) Ls[l * kLdd + lane] = l == lane ? ild : a[l];
+    if (lane == 0 && nb) *bad = 1;
+  }
+  __syncwarp();
+  if (lane < N) {
+    double v[N];
+#pragma unroll
+    for (int m = 0; m < N; ++m) v[m] = m == lane ? 1.0 : 0.0;
+#pragma unroll
+    for (int m = 0; m < N; ++m) {
+      const double x = v[m] * Ls[m * kLdd + m];
+      LiT[lane * kLdd + m] = x;
+#pragma unroll
+      for (int q = m + 1; q < N; ++q) v[q] = fma(-Ls[m * kLdd + q], x, v[q]);
+    }
+  }
+  __syncwarp();
+}
+
 // -- son views (packed-lower node outputs) ----------------------------------
 // A node output per sample is [Psi lower-packed tri(k) | R k x nc | sigma nc].
 struct SonView {
@@ -1744,14 +1791,22 @@ __global__ void __launch_bounds__(256, 2) compress_kernel(DevPlan p, const DevUp
   for (int w = tid; w < P_ * 8; w += 256) {
     const int i = w >> 3, t0 = (w & 7) * 4;
     double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
-    for (int j = 0; j < Q_; ++j) {
-      const double a = A(i, j);
-      if (t0 == 0) an = fma(a, a, an);
-      const double4 om = *reinterpret_cast<const double4*>(p.lr_omega + j * 32 + t0);
-      y0 = fma(a, om.x, y0);
-      y1 = fma(a, om.y, y1);
-      y2 = fma(a, om.z, y2);
-      y3 = fma(a, om.w, y3);
+    constexpr int UJ = 4;                       // Psi entries in flight per thread
+    for (int j0 = 0; j0 < Q_; j0 += UJ) {
+      double av[UJ];
+#pragma unroll
+      for (int u = 0; u < UJ; ++u) av[u] = j0 + u < Q_ ? A(i, j0 + u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < UJ; ++u) {
+        const int j = j0 + u < Q_ ? j0 + u : 0;
+        const double a = av[u];
+        if (t0 == 0) an = fma(a, a, an);
+        const double4 om = *reinterpret_cast<const double4*>(p.lr_omega + j * 32 + t0);
+        y0 = fma(a, om.x, y0);
+        y1 = fma(a, om.y, y1);
+        y2 = fma(a, om.z, y2);
+        y3 = fma(a, om.w, y3);
+      }
     }
     double* yr = Y + i * 33 + t0;
     yr[0] = t0 < L ? y0 : 0.0;
@@ -1796,7 +1851,11 @@ __global__ void __launch_bounds__(256, 2) compress_kernel(DevPlan p, const DevUp
       s_bad = 0;
     }
     __syncthreads();
-    if (warp == 0) factor_block32(G, kLdd, G, LiT, &s_bad);   // G doubles as the L scratch
+    if (warp == 0) {                                           // G doubles as the L scratch
+      if (L <= 16) factor_blockN<16>(G, kLdd, G, LiT, &s_bad);
+      else if (L <= 24) factor_blockN<24>(G, kLdd, G, LiT, &s_bad);
+      else factor_block32(G, kLdd, G, LiT, &s_bad);
+    }
     __syncthreads();
     // Y <- Y R^-1 in place, 32 rows x 8 column groups of 4 per chunk (compute, barrier, write)
     for (int i0 = 0; i0 < P_; i0 += 32) {
