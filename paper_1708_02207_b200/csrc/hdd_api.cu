@@ -90,9 +90,9 @@ static int setup_device(HddPlan* pl, int max_batch) {
   D.h = P.h;
   D.leaf_elems = P.leaf_elems;
   D.leaf_buf = P.leaf_buf;
-  if (P.leaf_cols > 8)
+  if (P.leaf_cols > kMaxLeafCols)
     return set_err(&pl->err, HDD_ERR_CONFIG,
-                   "more than 7 observations strictly inside one 16x16-cell leaf are not supported");
+                   "more than 63 observations strictly inside one 16x16-cell leaf are not supported");
   int rc;
   if ((rc = upload(pl, P.sx, &D.sx))) return rc;
   if ((rc = upload(pl, P.sy, &D.sy))) return rc;
@@ -109,7 +109,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
     d.j0 = L.j0;
     d.ncols = int(L.cols.size());
     d.ref_id = L.ref_id;
-    for (int c = 0; c < 16; ++c) {
+    for (int c = 0; c < kMaxLeafCols; ++c) {
       d.ctype[c] = 2; d.birth_r[c] = -1; d.birth_q[c] = -1; d.birth_g[c] = -1; d.fslot[c] = -1;
     }
     for (int c = 0; c < d.ncols; ++c) {
@@ -134,10 +134,14 @@ static int setup_device(HddPlan* pl, int max_batch) {
     std::vector<int32_t> order;
     for (int cls = 0; cls < 3; ++cls) {
       D.leaf_class_start[cls] = int(order.size());
-      const int lo = cls == 0 ? 0 : (cls == 1 ? 3 : 5), hi = cls == 0 ? 2 : (cls == 1 ? 4 : 8);
+      const int lo = cls == 0 ? 0 : (cls == 1 ? 3 : 5), hi = cls == 0 ? 2 : (cls == 1 ? 4 : kMaxLeafCols);
+      D.leaf_class_passes[cls] = 1;
       for (size_t l = 0; l < P.leaves.size(); ++l) {
         int nc = int(P.leaves[l].cols.size());
-        if (nc >= lo && nc <= hi) order.push_back(int32_t(l));
+        if (nc >= lo && nc <= hi) {
+          order.push_back(int32_t(l));
+          if (cls == 2) D.leaf_class_passes[cls] = std::max(D.leaf_class_passes[cls], nc <= 8 ? 1 : (nc - 1 + 6) / 7);
+        }
       }
       D.leaf_class_count[cls] = int(order.size()) - D.leaf_class_start[cls];
     }

@@ -29,15 +29,19 @@ struct DevUpper {
 };
 
 // One kernel leaf.
+// leaf columns (load + means + points strictly inside the leaf); the 8-column kernel
+// class runs ceil((ncols - 1) / 7) passes of (load + 7 columns) for wider leaves
+constexpr int kMaxLeafCols = 64;
+
 struct DevLeaf {
   int i0, j0;
   int ncols;
   int pad;
   int64_t ref_id;
   // per column: coefficient type (0 = load, 1 = mean, 2 = point) and birth
-  int ctype[16];
-  int birth_r[16], birth_q[16], birth_g[16];
-  int fslot[16];           // primal: functional slot of a point column, -1
+  int ctype[kMaxLeafCols];
+  int birth_r[kMaxLeafCols], birth_q[kMaxLeafCols], birth_g[kMaxLeafCols];
+  int fslot[kMaxLeafCols]; // primal: functional slot of a point column, -1
   int parent;              // upper index of the father (-1 when the leaf is the root)
 };
 
@@ -59,7 +63,7 @@ struct DevPlan {
   const double* f;         // nullptr = 1
   const DevLeaf* leaves;
   const int32_t* leaf_order;   // leaf indices grouped by column class (<=2, <=4, <=8)
-  int leaf_class_start[3], leaf_class_count[3];
+  int leaf_class_start[3], leaf_class_count[3], leaf_class_passes[3];
   const DevUpper* upper;
   const int32_t* gmap;
   const int32_t* csrc;

@@ -622,12 +622,14 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
     // 1/|leaf|, an exact power of two), sigma; primal-mode leaf functionals
     const double inv_area = 1.0 / (double(kLeafCells * kLeafCells) * p.h * p.h);
     double* gdst = p.buf[p.leaf_buf] + int64_t(leaf) * p.leaf_elems * p.bcap + int64_t(s) * p.leaf_elems;
-    const int lc = min(NC, p.leaf_cols);
-    for (int t = tid; t < ctri(k); t += NT) gdst[t] = out[t];
-    for (int t = tid; t < (k + 1) * lc; t += NT) {
-      const int a = t / lc, c = t - (t / lc) * lc;
+    if (blockIdx.z == 0)
+      for (int t = tid; t < ctri(k); t += NT) gdst[t] = out[t];
+    for (int t = tid; t < (k + 1) * NC; t += NT) {
+      const int a = t / NC, c = t - (t / NC) * NC;
+      const int col = cinfo[5 * NC + c];
+      if (col < 0) continue;
       const double val = out[ctri(k) + a * NC + c];
-      gdst[ctri(k) + a * p.leaf_cols + c] = val * (ctype[c] == 1 ? inv_area : 1.0);
+      gdst[ctri(k) + a * p.leaf_cols + col] = val * (ctype[c] == 1 ? inv_area : 1.0);
       const int fs = cinfo[4 * NC + c];
       if (fs >= 0) p.fbuf[(int64_t(s) * p.n_fslots + fs) * 65 + a] = val;
     }
@@ -646,10 +648,12 @@ __global__ void __launch_bounds__(NTH, 2) leaf2_kernel(DevPlan p, const int* __r
   extern __shared__ __align__(16) double sm[];
   const int leaf = order[blockIdx.x];
   const int s = blockIdx.y;
+  const int pass = blockIdx.z;
   LEAF_TICK(0);
   const int tid = threadIdx.x;
   constexpr int NT = NTH;
   const DevLeaf& L = p.leaves[leaf];
+  if (pass > 0 && 1 + (NC - 1) * pass >= L.ncols) return;   // no columns left for this pass
   int* cinfo = reinterpret_cast<int*>(sm);                       // ctype, br, bq, bg, fslot
   double* bufA = sm + kLeafHdr;
   double* bufB = bufA + ls.bufa;
@@ -674,11 +678,15 @@ __global__ void __launch_bounds__(NTH, 2) leaf2_kernel(DevPlan p, const int* __r
         fl[t] = p.f[int64_t(L.j0 + y) * p.m + L.i0 + x];
       }
     if (tid < NC) {
-      cinfo[tid] = tid < L.ncols ? L.ctype[tid] : 3;     // 3 = unused column
-      cinfo[NC + tid] = L.birth_r[tid];
-      cinfo[2 * NC + tid] = L.birth_q[tid];
-      cinfo[3 * NC + tid] = L.birth_g[tid];
-      cinfo[4 * NC + tid] = tid < L.ncols ? L.fslot[tid] : -1;
+      // local column tid of this pass -> leaf column lc (column 0 = the load, in every pass)
+      const int lc = tid == 0 ? 0 : 1 + (NC - 1) * pass + (tid - 1);
+      const bool ok = lc < L.ncols;
+      cinfo[tid] = ok ? L.ctype[lc] : 3;     // 3 = unused column
+      cinfo[NC + tid] = ok ? L.birth_r[lc] : -1;
+      cinfo[2 * NC + tid] = ok ? L.birth_q[lc] : -1;
+      cinfo[3 * NC + tid] = ok ? L.birth_g[lc] : -1;
+      cinfo[4 * NC + tid] = ok ? L.fslot[lc] : -1;
+      cinfo[5 * NC + tid] = ok && !(tid == 0 && pass > 0) ? lc : -1;   // output column
     }
     cp_async_wait<1>();
   }
@@ -787,7 +795,7 @@ cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_ou
     const LeafSmem ls = leaf_sizes(ncl);
     const size_t smem = leaf_smem_bytes(ncl);
     if (smem_out) *smem_out = smem;
-    dim3 grid(cnt, B);
+    dim3 grid(cnt, B, p.leaf_class_passes[cls]);
     const int* ord = p.leaf_order + p.leaf_class_start[cls];
     cudaError_t e;
 #define HDD_LAUNCH_LEAF(NCV)                                                                                   \
