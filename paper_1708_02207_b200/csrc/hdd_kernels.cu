@@ -277,6 +277,16 @@ __device__ __forceinline__ double sym(const double* P, int i, int j) {
 // fragments (4 rows x 8 consecutive doubles) hit distinct banks.
 __host__ __device__ constexpr int leaf_wpad(int w) { return w + ((12 - (w & 7)) & 7); }
 
+// Gather programs: read through L1 (__ldg; the tables of a class are shared by every
+// CTA) — no staging buffers, so the 2-column class fits 3 CTAs per SM and the
+// 8-column class 2 (measured: C2 leaf 7.01 -> 6.11 ms, C4 26.8 -> 22.8 ms against
+// cp.async staging in smem, which HDD_LEAF_STAGE_ITEMS restores).
+#ifdef HDD_LEAF_STAGE_ITEMS
+constexpr bool kLeafStage = true;
+#else
+constexpr bool kLeafStage = false;
+#endif
+
 // Leaf smem layout (doubles): col info [32] | bufA[bufa] (even-level outputs) |
 // bufB[bufb] (odd-level outputs; kappa[512] and f[289] alias its head until level 5
 // writes it) | panel[pand] | gather programs: panel program of even levels [tp0] | of
@@ -298,8 +308,10 @@ static LeafSmem leaf_sizes(int ncl) {
     if (r <= 5) {
       s.pand = std::max(s.pand, nf * ng * leaf_wpad(K + ncl));
       int& tp = (r & 1) ? s.tp1 : s.tp0;
-      tp = std::max(tp, ng * (K + ncl));
-      s.tu = std::max(s.tu, k * (k + 1) / 2 + k * ncl);
+      if (kLeafStage) {
+        tp = std::max(tp, ng * (K + ncl));
+        s.tu = std::max(s.tu, k * (k + 1) / 2 + k * ncl);
+      }
     }
   }
   for (int* v : {&s.bufa, &s.bufb, &s.pand, &s.tp0, &s.tp1, &s.tu}) *v = (*v + 1) & ~1;
@@ -320,13 +332,25 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// Gather programs: staged in smem (cp.async) or, with HDD_LEAF_GLOBAL_ITEMS, read
+// through L1 (__ldg) — no staging buffers, so the 2-column class fits 3 CTAs per SM.
+template <typename T>
+__device__ __forceinline__ T load_item(const T* p, int t) {
+  static_assert(sizeof(T) == 8, "8-byte gather items");
+  const unsigned long long v = __ldg(reinterpret_cast<const unsigned long long*>(p) + t);
+  T it;
+  memcpy(&it, &v, 8);
+  return it;
+}
+
 template <int R, int NC, int NTH>
 __device__ __forceinline__ void stage_panel_program(uint64_t* dst) {
   constexpr LeafLevelShape S = leaf_shape(R);
   constexpr int CI = NC == 2 ? 0 : (NC == 4 ? 1 : 2);
   constexpr int NPI = S.ng * (S.K + NC);
   const LeafItemP* g = c_ltab.P[CI] + c_ltab.poff[CI][R];
-  for (int t = threadIdx.x; t < NPI; t += NTH) cp_async8(dst + t, g + t);
+  if constexpr (kLeafStage)
+    for (int t = threadIdx.x; t < NPI; t += NTH) cp_async8(dst + t, g + t);
   cp_async_commit();
 }
 
@@ -400,14 +424,15 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 
   {   // this level's update program (the single U buffer is free: the previous level is done)
     const LeafItemU* gu = c_ltab.U[CI] + c_ltab.uoff[CI][R];
-    for (int t = tid; t < NUI; t += NT) cp_async8(tabU + t, gu + t);
+    if constexpr (kLeafStage)
+      for (int t = tid; t < NUI; t += NT) cp_async8(tabU + t, gu + t);
     cp_async_commit();
   }
   cp_async_wait<1>();   // this level's panel program (issued one level earlier) has landed
   __syncthreads();
   // ---- A: gather the interface panel (precomputed program) ----
   {
-    const LeafItemP* prog = reinterpret_cast<const LeafItemP*>(tabP);
+    const LeafItemP* prog = kLeafStage ? reinterpret_cast<const LeafItemP*>(tabP) : c_ltab.P[CI] + c_ltab.poff[CI][R];
     constexpr int UA = 4;
     const int stride = gsz * 32;
     for (int q = warp / gsz; q < nf; q += qstep) {
@@ -420,7 +445,10 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 #pragma unroll
         for (int u = 0; u < UA; ++u) {
           const int t = t0 + u * stride;
-          it[u] = t < NPI ? prog[t] : LeafItemP{int16_t(Sin - 2), int16_t(Sin - 2), -1, 0};
+          if constexpr (kLeafStage)
+            it[u] = t < NPI ? prog[t] : LeafItemP{int16_t(Sin - 2), int16_t(Sin - 2), -1, 0};
+          else
+            it[u] = t < NPI ? load_item(prog, t) : LeafItemP{int16_t(Sin - 2), int16_t(Sin - 2), -1, 0};
         }
 #pragma unroll
         for (int u = 0; u < UA; ++u) v[u] = s1[it[u].o1] + s2[it[u].o2];
@@ -474,7 +502,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
     if (R == 0) asm volatile("bar.sync 1, %0;" ::"n"(NT));
 #endif
     // ---- B': sons' contributions to the outputs, A~ = Psi_s1 + Psi_s2 | R_s1 + R_s2 ----
-    const LeafItemU* uprog = reinterpret_cast<const LeafItemU*>(tabU);
+    const LeafItemU* uprog = kLeafStage ? reinterpret_cast<const LeafItemU*>(tabU) : c_ltab.U[CI] + c_ltab.uoff[CI][R];
     constexpr int UB = 4;
     const int wt = (warp - NWB) * 32 + lane, nth = (NW - NWB) * 32;
     for (int i0 = wt; i0 < nf * NUI; i0 += UB * nth) {
@@ -483,7 +511,11 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
       for (int u = 0; u < UB; ++u) {
         const int idx = i0 + u * nth;
         const int q = idx < nf * NUI ? idx / NUI : 0;
-        const LeafItemU it = idx < nf * NUI ? uprog[idx - q * NUI] : LeafItemU{0, 0, int16_t(Sin - 2), int16_t(Sin - 2)};
+        LeafItemU it = LeafItemU{0, 0, int16_t(Sin - 2), int16_t(Sin - 2)};
+        if (idx < nf * NUI) {
+          if constexpr (kLeafStage) it = uprog[idx - q * NUI];
+          else it = load_item(uprog, idx - q * NUI);
+        }
         v[u] = in[(2 * q) * Sin + it.o1] + in[(2 * q + 1) * Sin + it.o2];
       }
 #pragma unroll
@@ -596,7 +628,8 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
     const double* P0 = Pp;
     for (int idx = tid; idx < nf * NUI; idx += NT) {
       const int q = idx / NUI, t = idx - q * NUI;
-      const LeafItemU it = reinterpret_cast<const LeafItemU*>(tabU)[t];
+      const LeafItemU it = kLeafStage ? reinterpret_cast<const LeafItemU*>(tabU)[t]
+                                      : load_item(c_ltab.U[CI] + c_ltab.uoff[CI][R], t);
       const int bx = it.bx;
       const double* P = P0 + q * ng * W;
       out[q * Sout + t] -= P[it.a] * P[bx < k ? bx : K + (bx - k)];
@@ -643,7 +676,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 // gather the interface panel, Gauss-Jordan interface inverse (warp per node),
 // Y = A22^-1 [A21 | R], then the Schur update A11 - A21^T Y on DMMA tiles.
 template <int NC, int NTH>
-__global__ void __launch_bounds__(NTH, 2) leaf2_kernel(DevPlan p, const int* __restrict__ order, LeafSmem ls,
+__global__ void __launch_bounds__(NTH, (!kLeafStage && NC == 2) ? 3 : 2) leaf2_kernel(DevPlan p, const int* __restrict__ order, LeafSmem ls,
                                                        int B) {
   extern __shared__ __align__(16) double sm[];
   const int leaf = order[blockIdx.x];
