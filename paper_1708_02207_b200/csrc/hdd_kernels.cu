@@ -1416,8 +1416,8 @@ size_t merge_m2_smem_bytes(int ngp, int ldp, int K, int nc) {
   return sizeof(double) * (size_t(ngp) * ldp + 8 + 128 + ints / 2 + 2 * size_t(nc) + 2) + 64;   // +2: 16-byte alignment of the staged sons
 }
 
-template <int NB, int NTH>
-__global__ void __launch_bounds__(NTH, NTH == 256 ? 3 : 1) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int slot) {
+template <int NB, int NTH, int MINB>
+__global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int slot) {
   extern __shared__ __align__(16) double sm[];
   MERGE_TICK(0);
   const DevUpper& U = nodes[blockIdx.y];
@@ -1682,14 +1682,20 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
   cudaError_t e;
   dim3 grid(B, n_nodes);
   if (tier == 0) {
+    // occupancy by panel size: 1 x 512 threads for big panels; 4 x 256 threads (64
+    // registers) when 4 panels fit an SM, else 3 x 256 (80 registers; measured)
     if (smem > 100 * 1024) {
-      e = cudaFuncSetAttribute(merge_m2_kernel<8, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      e = cudaFuncSetAttribute(merge_m2_kernel<8, 512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
-      merge_m2_kernel<8, 512><<<grid, 512, smem, s>>>(p, nodes_dev, slot);
+      merge_m2_kernel<8, 512, 1><<<grid, 512, smem, s>>>(p, nodes_dev, slot);
+    } else if (smem <= 55 * 1024) {
+      e = cudaFuncSetAttribute(merge_m2_kernel<8, 256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      merge_m2_kernel<8, 256, 4><<<grid, 256, smem, s>>>(p, nodes_dev, slot);
     } else {
-      e = cudaFuncSetAttribute(merge_m2_kernel<8, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      e = cudaFuncSetAttribute(merge_m2_kernel<8, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
-      merge_m2_kernel<8, 256><<<grid, 256, smem, s>>>(p, nodes_dev, slot);
+      merge_m2_kernel<8, 256, 3><<<grid, 256, smem, s>>>(p, nodes_dev, slot);
     }
   } else {
     e = cudaFuncSetAttribute(merge_l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
