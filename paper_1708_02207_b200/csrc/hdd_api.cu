@@ -78,7 +78,12 @@ static int setup_device(HddPlan* pl, int max_batch) {
   Plan& P = pl->plan;
   CU(cudaSetDevice(pl->device));
   CU(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking));
-  if (upload_leaf_template() != 0) return set_err(&pl->err, HDD_ERR_CUDA, "leaf template upload failed");
+  int up_rc;
+  {   // per-device leaf tables are built once per process; plans may be created concurrently
+    std::lock_guard<std::mutex> lk(g_mu);
+    up_rc = upload_leaf_template();
+  }
+  if (up_rc != 0) return set_err(&pl->err, HDD_ERR_CUDA, "leaf template upload failed");
   DevPlan& D = pl->dev;
   D.N = P.N;
   D.m = P.m;

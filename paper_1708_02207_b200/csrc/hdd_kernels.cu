@@ -183,8 +183,13 @@ int upload_leaf_template() {
     }
   }
   {
-    static bool built = false;
-    static LeafTabDev tab{};
+    // one set of tables per device (the __constant__ pointers are per device too)
+    static bool built_dev[64] = {};
+    static LeafTabDev tab_dev[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return -1;
+    bool& built = built_dev[dev];
+    LeafTabDev& tab = tab_dev[dev];
     if (!built) {
       for (int ci = 0; ci < 3; ++ci) {
         const int NC = ci == 0 ? 2 : (ci == 1 ? 4 : 8);
