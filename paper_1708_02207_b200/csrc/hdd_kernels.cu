@@ -282,6 +282,14 @@ __device__ __forceinline__ double sym(const double* P, int i, int j) {
 // fragments (4 rows x 8 consecutive doubles) hit distinct banks.
 __host__ __device__ constexpr int leaf_wpad(int w) { return w + ((12 - (w & 7)) & 7); }
 
+// Levels 6 and 5 of the leaf condensed directly per 2x4-cell node (HDD_LEAF_UNFUSED
+// restores the register 2x2 base + shared-memory level 5).
+#ifdef HDD_LEAF_UNFUSED
+constexpr bool kLeafFused56 = false;
+#else
+constexpr bool kLeafFused56 = true;
+#endif
+
 // Gather programs: read through L1 (__ldg; the tables of a class are shared by every
 // CTA) — no staging buffers, so the 2-column class fits 3 CTAs per SM and the
 // 8-column class 2 (measured: C2 leaf 7.01 -> 6.11 ms, C4 26.8 -> 22.8 ms against
@@ -303,10 +311,10 @@ struct LeafSmem {
 };
 static LeafSmem leaf_sizes(int ncl) {
   const auto& T = leaf_template();
-  LeafSmem s{0, 808, 0, 0, 0, 0};
+  LeafSmem s{kLeafFused56 ? 808 : 0, kLeafFused56 ? 0 : 808, 0, 0, 0, 0};   // kappa + f alias
   for (int r = 0; r < kLeafLevels; ++r) {
     const int nf = 1 << r, k = T[r].k, K = T[r].K, ng = T[r].ng;
-    if (r >= 1 && r <= 6) {
+    if (r >= 1 && r <= (kLeafFused56 ? 5 : 6)) {
       int& b = (r & 1) ? s.bufb : s.bufa;
       b = std::max(b, nf * (k * (k + 1) / 2 + k * ncl + ncl + 2));
     }
@@ -681,7 +689,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 // gather the interface panel, Gauss-Jordan interface inverse (warp per node),
 // Y = A22^-1 [A21 | R], then the Schur update A11 - A21^T Y on DMMA tiles.
 template <int NC, int NTH>
-__global__ void __launch_bounds__(NTH, (!kLeafStage && NC == 2) ? 3 : 2) leaf2_kernel(DevPlan p, const int* __restrict__ order, LeafSmem ls,
+__global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && kLeafFused56))) ? 3 : 2) leaf2_kernel(DevPlan p, const int* __restrict__ order, LeafSmem ls,
                                                        int B) {
   extern __shared__ __align__(16) double sm[];
   const int leaf = order[blockIdx.x];
@@ -699,7 +707,11 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && NC == 2) ? 3 : 2) leaf2_k
   uint64_t* tab0 = reinterpret_cast<uint64_t*>(pan + ls.pand);   // panel programs, even levels
   uint64_t* tab1 = tab0 + ls.tp0;                                // odd levels
   uint64_t* tabU = tab1 + ls.tp1;
+#ifdef HDD_LEAF_UNFUSED
   double* kap = bufB;                                             // [512], aliases bufB until level 5
+#else
+  double* kap = bufA;                                             // [512], aliases bufA until level 4
+#endif
   double* fl = kap + 512;                                         // [289]
   const int N = p.N;
   {
@@ -734,6 +746,7 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && NC == 2) ? 3 : 2) leaf2_k
   const int* bq = cinfo + 2 * NC;
   const double h2_6 = p.h * p.h / 6.0;
 
+#ifdef HDD_LEAF_UNFUSED
   // ---------------- level 6: 2x2-cell blocks in registers ----------------
   {
     constexpr int k6 = 8;
@@ -814,9 +827,153 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && NC == 2) ? 3 : 2) leaf2_k
   }
   __syncthreads();
 
+#else
+  // ---------------- levels 6 + 5 fused: 2x4-cell nodes condensed directly ----------------
+  // A level-5 node (2 x 4 cells, 3 x 5 nodes) has 12 boundary nodes and 3 interior ones
+  // (the 2x2-block centres c1 = (1,1), c2 = (1,3) and the level-5 interface node
+  // m = (1,2)); A_II is tridiagonal and every boundary node couples to at most one
+  // interior node, so  Psi = A_BB - v_a M(g_a, g_b) v_b,  R = r_B - v_a (M r_I)(g_a),
+  // sigma_c = r_0I^T M r_cI  with M = A_II^-1 in closed form: the block elimination of
+  // the level-6 and level-5 steps (fem.py:126-145 cell patterns), one warp per two nodes
+  // at a time, lane = boundary row (16 lanes per node).
+  {
+    constexpr int k5 = 12;
+    constexpr int S5 = ctri(k5) + k5 * NC + NC + 2;
+    const int lane = tid & 31, wid = tid >> 5;
+    const int half = lane >> 4, a = lane & 15;
+    const double h2 = p.h * p.h;
+    // boundary index <-> local node (sorted (y, x) like the leaf template); interior
+    // neighbour 0 = c1, 1 = m, 2 = c2, -1 none
+    auto bx_f = [](int i) { return i < 3 ? i : (i < 9 ? (((i - 3) & 1) ? 2 : 0) : i - 9); };
+    auto by_f = [](int i) { return i < 3 ? 0 : (i < 9 ? (i - 3) / 2 + 1 : 4); };
+    auto bg_f = [](int i) { return i == 1 || i == 3 || i == 4 ? 0 : (i == 5 || i == 6 ? 1 : (i == 7 || i == 8 || i == 10 ? 2 : -1)); };
+    for (int pass = 0; pass < 2; ++pass) {
+      const int q = wid * 4 + pass * 2 + half;
+      const int o = c_orig[31 + q];
+      const int ox = o & 255, oy = o >> 8;
+      auto k0 = [&](int cx, int cy) -> double { return kap[(ox + cx) * 32 + 2 * (oy + cy)]; };
+      auto k1 = [&](int cx, int cy) -> double { return kap[(ox + cx) * 32 + 2 * (oy + cy) + 1]; };
+      auto in_ = [](int cx, int cy) { return cx >= 0 && cx < 2 && cy >= 0 && cy < 4; };
+      auto Dl = [&](int x, int y) -> double {
+        double d = 0.0;
+        if (in_(x, y)) d += 0.5 * (k0(x, y) + k1(x, y));
+        if (in_(x - 1, y)) d += k0(x - 1, y);
+        if (in_(x, y - 1)) d += k1(x, y - 1);
+        if (in_(x - 1, y - 1)) d += 0.5 * (k0(x - 1, y - 1) + k1(x - 1, y - 1));
+        return d;
+      };
+      auto El = [&](int x, int y) -> double {      // (x,y)-(x+1,y)
+        double e = 0.0;
+        if (in_(x, y)) e -= 0.5 * k0(x, y);
+        if (in_(x, y - 1)) e -= 0.5 * k1(x, y - 1);
+        return e;
+      };
+      auto Nl = [&](int x, int y) -> double {      // (x,y)-(x,y+1)
+        double e = 0.0;
+        if (in_(x, y)) e -= 0.5 * k1(x, y);
+        if (in_(x - 1, y)) e -= 0.5 * k0(x - 1, y);
+        return e;
+      };
+      auto wl = [&](int x, int y) -> double {      // lumped load weight
+        double w = 0.0;
+        if (in_(x, y)) w += 2.0;
+        if (in_(x - 1, y)) w += 1.0;
+        if (in_(x, y - 1)) w += 1.0;
+        if (in_(x - 1, y - 1)) w += 2.0;
+        return w * h2_6;
+      };
+      auto fv = [&](int x, int y) -> double { return p.f ? fl[(oy + y) * 17 + ox + x] : 1.0; };
+      // interior block and its inverse (every lane of the node, broadcast loads)
+      const double ia = Dl(1, 1), ib = Nl(1, 1), ic = Dl(1, 2), idd = Nl(1, 2), ie = Dl(1, 3);
+      const double p1 = ia * ic - ib * ib;
+      const double det = p1 * ie - ia * idd * idd;
+      if (a == 0 && (!(ia > 0.0) || !(p1 > 0.0) || !(det > 0.0)))
+        record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, 5, q));
+      const double rdet = 1.0 / det;
+      const double M00 = (ic * ie - idd * idd) * rdet, M01 = -ib * ie * rdet, M02 = ib * idd * rdet;
+      const double M11 = ia * ie * rdet, M12 = -ia * idd * rdet, M22 = p1 * rdet;
+      auto Mrow = [&](int g, double& x0, double& x1, double& x2) {
+        x0 = g == 0 ? M00 : (g == 1 ? M01 : M02);
+        x1 = g == 0 ? M01 : (g == 1 ? M11 : M12);
+        x2 = g == 0 ? M02 : (g == 1 ? M12 : M22);
+      };
+      // boundary-interior couplings of every boundary node
+      double vb[12];
+      vb[0] = 0.0; vb[2] = 0.0; vb[9] = 0.0; vb[11] = 0.0;
+      vb[1] = Nl(1, 0);
+      vb[3] = El(0, 1);
+      vb[4] = El(1, 1);
+      vb[5] = El(0, 2);
+      vb[6] = El(1, 2);
+      vb[7] = El(0, 3);
+      vb[8] = El(1, 3);
+      vb[10] = Nl(1, 3);
+      if (a < k5) {
+        double* out = bufB + q * S5;
+        const int xa = bx_f(a), ya = by_f(a), ga = bg_f(a);
+        double va = 0.0;
+#pragma unroll
+        for (int b = 0; b < 12; ++b)
+          if (b == a) va = vb[b];
+        double ma0 = 0.0, ma1 = 0.0, ma2 = 0.0;      // row g_a of M, times v_a
+        if (ga >= 0) {
+          Mrow(ga, ma0, ma1, ma2);
+          ma0 *= va; ma1 *= va; ma2 *= va;
+        }
+        // Psi row a (packed lower): own diagonal and the couplings to the left / lower
+        // boundary neighbours computed once per lane, then a uniform loop over b
+        const double dself = Dl(xa, ya);
+        const int il = (xa >= 1 && (ya == 0 || ya == 4 || xa == 2)) ? (xa == 2 && ya >= 1 && ya <= 3 ? -1 : a - 1) : -1;
+        const int idn = (ya >= 1 && xa != 1) ? (ya == 1 ? (xa == 0 ? 0 : 2) : (ya == 4 ? (xa == 0 ? 7 : 8) : a - 2)) : -1;
+        const double eleft = il >= 0 ? El(xa - 1, ya) : 0.0;
+        const double ndown = idn >= 0 ? Nl(xa, ya - 1) : 0.0;
+#pragma unroll
+        for (int b = 0; b < 12; ++b) {
+          const int gb = bg_f(b);
+          double val = b == a ? dself : (b == il ? eleft : (b == idn ? ndown : 0.0));
+          if (gb >= 0) val -= (gb == 0 ? ma0 : (gb == 1 ? ma1 : ma2)) * vb[b];
+          if (b <= a) out[ctri(a) + b] = val;
+        }
+        // R row a and (lane 0) sigma: interior right-hand sides per column
+        const double wa = wl(xa, ya), fa = fv(xa, ya);
+        const double fI0 = fv(1, 1), fI1 = fv(1, 2), fI2 = fv(1, 3);
+        double r00 = 0.0, r01 = 0.0, r02 = 0.0;        // load column interior rhs
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const int ct = ctype[c];
+          double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+          if (ct == 0) { r0 = h2 * fI0; r1 = h2 * fI1; r2 = h2 * fI2; }
+          else if (ct == 1) { r0 = h2; r1 = h2; r2 = h2; }
+          if (br[c] == 6 && bq[c] == 2 * q) r0 += 1.0;
+          if (br[c] == 6 && bq[c] == 2 * q + 1) r2 += 1.0;
+          if (br[c] == 5 && bq[c] == q) r1 += 1.0;
+          if (c == 0) { r00 = r0; r01 = r1; r02 = r2; }
+          double val = ct == 0 ? wa * fa : (ct == 1 ? wa : 0.0);
+          if (ga >= 0) val -= ma0 * r0 + ma1 * r1 + ma2 * r2;
+          out[ctri(k5) + a * NC + c] = val;
+          if (a == 0) {
+            double sg = 0.0;
+            if (c >= 1) {
+              const double t0 = M00 * r0 + M01 * r1 + M02 * r2;
+              const double t1 = M01 * r0 + M11 * r1 + M12 * r2;
+              const double t2 = M02 * r0 + M12 * r1 + M22 * r2;
+              sg = r00 * t0 + r01 * t1 + r02 * t2;
+            }
+            out[ctri(k5) + k5 * NC + c] = sg;
+          }
+        }
+        if (a == 0) { out[S5 - 2] = 0.0; out[S5 - 1] = 0.0; }   // zero slot
+      }
+    }
+  }
+  __syncthreads();
+#endif
+
   LEAF_TICK(1);
   // ---------------- levels 5..0 in shared memory ----------------
+#ifdef HDD_LEAF_UNFUSED
   leaf_level<5, NC, NTH>(p, bufA, bufB, pan, cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
+#endif
   leaf_level<4, NC, NTH>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
   leaf_level<3, NC, NTH>(p, bufA, bufB, pan, cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
   leaf_level<2, NC, NTH>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
