@@ -1425,7 +1425,8 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
 }
 
 
-// Tier-L Schur update: 64 x 64 output tiles, X chunks of 32 interface rows
+constexpr int kEC = 16;     // tier-L epilogue: interface rows per staged chunk
+// Tier-L Schur update: 64 x 64 output tiles, X chunks of kEC interface rows
 // double-buffered HBM -> smem with cp.async, 8 warps as 2 x 4 of 32 x 16 DMMA tiles.
 // E: [2][2][32][kLds] smem (A chunk, B chunk) x double buffer.
 __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const double* __restrict__ P, int ldp, int k,
@@ -1435,15 +1436,15 @@ __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const doubl
   const int ow = k + nc;
   const int m0 = (warp >> 2) * 32, n0 = (warp & 3) * 16;
   const int na = (k + 63) / 64, nbt = (ow + 63) / 64;
-  const int nch = ngp / 32;
+  const int nch = ngp / kEC;
   for (int t = 0; t < na * nbt; ++t) {
     const int a0 = (t / nbt) * 64, b0 = (t % nbt) * 64;
     if (b0 + 64 <= k && b0 >= a0 + 64) continue;   // strictly upper Psi tile
     auto stage = [&](int c, int buf) {
-      double* Ea = E + buf * 2 * 32 * kLds;
-      double* Eb = Ea + 32 * kLds;
-      const int g0 = c * 32;
-      for (int tt = tid; tt < 32 * 64; tt += 256) {
+      double* Ea = E + buf * 2 * kEC * kLds;
+      double* Eb = Ea + kEC * kLds;
+      const int g0 = c * kEC;
+      for (int tt = tid; tt < kEC * 64; tt += 256) {
         const int g = tt >> 6, i = tt & 63;
         const int aa = a0 + i;
         if (aa < k) cp_async8(Ea + g * kLds + i, P + int64_t(g0 + g) * ldp + aa);
@@ -1483,8 +1484,8 @@ __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const doubl
         cp_async_wait<0>();
       }
       __syncthreads();
-      const double* Ea = E + (c & 1) * 2 * 32 * kLds;
-      warp_gemm_tn<4, 2>(acc, Ea, kLds, m0, Ea + 32 * kLds, kLds, n0, 32);
+      const double* Ea = E + (c & 1) * 2 * kEC * kLds;
+      warp_gemm_tn<4, 2>(acc, Ea, kLds, m0, Ea + kEC * kLds, kLds, n0, kEC);
       __syncthreads();
     }
 #pragma unroll
@@ -1714,14 +1715,15 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
 // -- tier L: panel in HBM ----------------------------------------------------
 // smem: F phases (L scratch / LiT / Xc / Lt) and the epilogue's 2 x (A, B) chunks of
 // 32 x kLds share the front region; the son maps and column plan follow it.
-constexpr size_t kLRegion = (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) > (4 * 32 * kLds)
-                                ? (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) : (4 * 32 * kLds);
+constexpr size_t kLRegion = (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) > (4 * kEC * kLds)
+                                ? (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) : (4 * kEC * kLds);
 size_t merge_l_smem_bytes(int K, int nc) {
   const size_t ints = (size_t(2 * K + 3 * nc) + 1) & ~size_t(1);
   return sizeof(double) * (kLRegion + ints / 2 + 2 * size_t(nc)) + 1024;
 }
 
-__global__ void __launch_bounds__(256, 2) merge_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
                                                           double* __restrict__ ws, int64_t ws_stride, int slot) {
   extern __shared__ __align__(16) double sm[];
   MERGE_TICK(0);
@@ -1860,9 +1862,17 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
       merge_m2_kernel<8, 256, 3><<<grid, 256, smem, s>>>(p, nodes_dev, slot);
     }
   } else {
-    e = cudaFuncSetAttribute(merge_l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    merge_l_kernel<<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride, slot);
+    // 3 CTAs/SM (80 registers, some spills) pays when the launch has enough CTAs to
+    // fill them and the panel region fits three per SM (measured: C4 depths 3-5 -12 %)
+    if (int64_t(n_nodes) * B >= 148 * 3 * 2 && smem <= 74 * 1024) {
+      e = cudaFuncSetAttribute(merge_l_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      merge_l_kernel<3><<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride, slot);
+    } else {
+      e = cudaFuncSetAttribute(merge_l_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      merge_l_kernel<2><<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride, slot);
+    }
   }
   return cudaGetLastError();
 }
