@@ -1986,7 +1986,7 @@ __global__ void __launch_bounds__(256) psi_norm_kernel(DevPlan p, const DevUpper
   }
 }
 
-__global__ void __launch_bounds__(256, 2) compress_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int blk0) {
+__global__ void __launch_bounds__(256, 3) compress_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int blk0) {
   extern __shared__ __align__(16) double sm[];
   const int32_t* bd = p.lr_blk + 5 * (blk0 + blockIdx.y);
   const int ln = bd[0], roff = bd[1], P_ = bd[2], coff = bd[3], Q_ = bd[4];
