@@ -74,6 +74,10 @@ static int upload(HddPlan* pl, const std::vector<T>& v, const T** out) {
   return 0;
 }
 
+// panel row stride: the smallest ld >= w with ld = 8 (mod 16) doubles (conflict-free
+// DMMA fragments of 4 rows x 8 columns)
+static int panel_ld(int w) { return w + ((24 - (w & 15)) & 15); }
+
 static int setup_device(HddPlan* pl, int max_batch) {
   Plan& P = pl->plan;
   CU(cudaSetDevice(pl->device));
@@ -166,14 +170,14 @@ static int setup_device(HddPlan* pl, int max_batch) {
   for (size_t u = 0; u < P.upper.size(); ++u) {
     const UpperNode& U = P.upper[u];
     const int ngp32 = (U.ng + 31) / 32 * 32;
-    const int ldp32 = (U.k + ngp32 + U.nc + 15) / 16 * 16 + 8;
+    const int ldp32 = panel_ld(U.k + ngp32 + U.nc);
     if (merge_m2_smem_bytes(ngp32, ldp32, U.K, U.nc) > 220 * 1024 || (force_l && force_l[0] == '1')) pl->depth_tier[U.depth] = 1;
   }
   for (size_t u = 0; u < P.upper.size(); ++u) {
     const UpperNode& U = P.upper[u];
     const int nbk = pl->depth_tier[U.depth] ? 32 : 8;
     const int ngp = (U.ng + nbk - 1) / nbk * nbk;
-    const int ldp = (U.k + ngp + U.nc + 15) / 16 * 16 + 8;
+    const int ldp = panel_ld(U.k + ngp + U.nc);
     pl->depth_nb[U.depth] = nbk;
     if (pl->depth_tier[U.depth]) pl->depth_ws[U.depth] = std::max<int64_t>(pl->depth_ws[U.depth], int64_t(ngp) * ldp);
     pl->depth_rows[U.depth] = std::max(pl->depth_rows[U.depth], U.k + ngp);
@@ -185,7 +189,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
     d.k = U.k; d.ng = U.ng; d.K = U.K; d.nc = U.nc;
     const int nbk = pl->depth_nb[U.depth];
     const int ngp_u = (U.ng + nbk - 1) / nbk * nbk;
-    d.ldp = (U.k + ngp_u + U.nc + 15) / 16 * 16 + 8;
+    d.ldp = panel_ld(U.k + ngp_u + U.nc);
     d.nb = nbk;
     d.out_ld = U.out_ld;
     d.out_elems = U.out_elems;

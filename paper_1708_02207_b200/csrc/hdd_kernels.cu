@@ -1848,7 +1848,11 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
   if (tier == 0) {
     // occupancy by panel size: 1 x 512 threads for big panels; 4 x 256 threads (64
     // registers) when 4 panels fit an SM, else 3 x 256 (80 registers; measured)
-    if (smem > 100 * 1024) {
+    if (smem > 100 * 1024 && smem <= 113 * 1024) {
+      e = cudaFuncSetAttribute(merge_m2_kernel<8, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      merge_m2_kernel<8, 256, 2><<<grid, 256, smem, s>>>(p, nodes_dev, slot);
+    } else if (smem > 100 * 1024) {
       e = cudaFuncSetAttribute(merge_m2_kernel<8, 512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
       merge_m2_kernel<8, 512, 1><<<grid, 512, smem, s>>>(p, nodes_dev, slot);
