@@ -1939,8 +1939,9 @@ __global__ void __launch_bounds__(256) topdown_kernel(DevPlan p, const DevUpper*
       const double* arow = dblk + lane * 33;
       double yv = lane < nb ? y[row_i] : 0.0;
       double uv = 0.0;
+      const double inv_own = lane < nb ? 1.0 / arow[lane] : 0.0;   // off the serial chain
       for (int r = nb - 1; r >= 0; --r) {
-        if (lane == r) uv = yv / arow[r];
+        if (lane == r) uv = yv * inv_own;
         const double v = __shfl_sync(0xffffffffu, uv, r);
         if (lane < r) yv = fma(-arow[r], v, yv);
       }
