@@ -553,13 +553,16 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
     double* P = Pp + q * ng * W;
     double w[ng];
 #pragma unroll
+    for (int g = 0; g < ng; ++g) w[g] = P[g * W + col];     // all loads ahead of the stores
+#pragma unroll
     for (int g = 0; g < ng; ++g) {
-      double v = P[g * W + col];
+      double v = w[g];
 #pragma unroll
       for (int h = 0; h < g; ++h) v = fma(-P[g * W + k + h], w[h], v);
       w[g] = v * P[g * W + k + g];
-      P[g * W + col] = w[g];
     }
+#pragma unroll
+    for (int g = 0; g < ng; ++g) P[g * W + col] = w[g];
   }
   __syncthreads();
   LEAF_TICK(10 + 8 * (5 - R) + 2);
