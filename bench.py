@@ -227,11 +227,13 @@ def run_reference(args):
         t_all += wall
     value = args.steps * per_step / t_all
     line = {
-        "impl": "reference", "metric": f"likelihood evals/s ({args.config}, {cfg.level}-level grid)",
+        "impl": "reference", "metric": f"likelihood evals/s ({args.config}, {cfg.level}-level grid, n_z={cfg.n_z})",
         "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * t_all / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "batch_per_step": per_step, "level": cfg.level, "n_z": cfg.n_z},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded protocol, DESIGN.md)",
+        "config": {"workload": args.config, "batch_per_step": per_step, "grid_nodes": (1 << cfg.level) + 1,
+                   "n_z": cfg.n_z, "n_obs": len(configs.observations(cfg)),
+                   "parallelism": "host cores (one forked worker per core, rank 0 only)"},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": min(per_step, cores), "kind": "port",
                          "sample": f"{per_step} Z rows per step of {args.config}, forked workers x 1 BLAS thread, "
                                    "oracle/hdd_port.py (restatement of the reference HDD functional path)"},
