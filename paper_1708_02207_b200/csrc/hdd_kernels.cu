@@ -1630,7 +1630,7 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
   __syncthreads();                         // maps staged; the mbarrier is initialised
   if (U.stage) mbar_wait(&s_bar, 0);
   MERGE_TICK(1);
-  for (int g = warp; g < ngp; g += NWp) gather_panel_row<MINB == 1 ? 8 : 4>(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32);
+  for (int g = warp; g < ngp; g += NWp) gather_panel_row<MINB <= 2 ? 8 : 4>(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   const int gq = lane & 3, gr = lane >> 2;
   double* Ls = piv + 8;                    // [8][8] diagonal-block factor L (piv: 1/L_ii)
