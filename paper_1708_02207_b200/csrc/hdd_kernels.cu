@@ -581,6 +581,43 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
       const int bj = rt ? 0 : c_tile_j[tt];
       const double* P = Pp + q * ng * W;
       double* o = out + q * Sout;
+      if (!rt && bj < bi && 16 * bi + 16 <= k) {
+        // strictly-lower 16x16 block with every row inside: no per-element predicates
+        const int a0 = 16 * bi + lr, b0 = 16 * bj + 2 * lc;
+        double* o0 = o + ctri(a0) + b0;
+        double* o1 = o + ctri(a0 + 8) + b0;
+        double old[2][2][2], acc[2][2][2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            old[0][j][e] = o0[8 * j + e];
+            old[1][j][e] = o1[8 * j + e];
+            acc[0][j][e] = 0.0;
+            acc[1][j][e] = 0.0;
+          }
+        const int ca0 = 16 * bi + lr, cb0 = 16 * bj + lr;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int g = 4 * kk + lc;
+          const bool gv = g < ng;
+          const double* pr = P + g * W;
+          const double x0 = gv ? pr[ca0] : 0.0, x1 = gv ? pr[ca0 + 8] : 0.0;
+          const double y0 = gv ? pr[cb0] : 0.0, y1 = gv ? pr[cb0 + 8] : 0.0;
+          dmma884(acc[0][0], x0, y0);
+          dmma884(acc[0][1], x0, y1);
+          dmma884(acc[1][0], x1, y0);
+          dmma884(acc[1][1], x1, y1);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            o0[8 * j + e] = old[0][j][e] - acc[0][j][e];
+            o1[8 * j + e] = old[1][j][e] - acc[1][j][e];
+          }
+        continue;
+      }
       // output offsets of this lane's accumulator elements (-1: not stored), old
       // values (the sons' contributions, written by B') fetched ahead of the DMMAs
       int ov[2][2][2];
