@@ -618,6 +618,40 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
           }
         continue;
       }
+      if (!rt && bj == bi && 16 * bi + 16 <= k) {
+        // diagonal 16x16 block: the upper-right 8x8 is never stored (no DMMA), the
+        // lower-left one always is, the two diagonal 8x8 keep b <= a
+        const int a0 = 16 * bi + lr, b0 = 16 * bi + 2 * lc;
+        double* o0 = o + ctri(a0) + b0;
+        double* o1 = o + ctri(a0 + 8) + b0;
+        double old00[2], old10[2], old11[2], acc00[2] = {0.0, 0.0}, acc10[2] = {0.0, 0.0}, acc11[2] = {0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool dg = 2 * lc + e <= lr;
+          old00[e] = dg ? o0[e] : 0.0;
+          old10[e] = o1[e];
+          old11[e] = dg ? o1[8 + e] : 0.0;
+        }
+        const int ca0 = 16 * bi + lr;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int g = 4 * kk + lc;
+          const bool gv = g < ng;
+          const double* pr = P + g * W;
+          const double x0 = gv ? pr[ca0] : 0.0, x1 = gv ? pr[ca0 + 8] : 0.0;
+          dmma884(acc00, x0, x0);
+          dmma884(acc10, x1, x0);
+          dmma884(acc11, x1, x1);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool dg = 2 * lc + e <= lr;
+          if (dg) o0[e] = old00[e] - acc00[e];
+          o1[e] = old10[e] - acc10[e];
+          if (dg) o1[8 + e] = old11[e] - acc11[e];
+        }
+        continue;
+      }
       // output offsets of this lane's accumulator elements (-1: not stored), old
       // values (the sons' contributions, written by B') fetched ahead of the DMMAs
       int ov[2][2][2];
