@@ -652,6 +652,31 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
         }
         continue;
       }
+      if (rt && 16 * bi + 16 <= k) {
+        // R block with every row inside: columns c = 2 lc + e < NC
+        const int a0 = 16 * bi + lr, c0 = 2 * lc;
+        double* o0 = o + ctri(k) + a0 * NC + c0;
+        double* o1 = o0 + 8 * NC;
+        const bool cv0 = c0 < NC, cv1 = c0 + 1 < NC;
+        double old0[2], old1[2], acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
+        old0[0] = cv0 ? o0[0] : 0.0; old0[1] = cv1 ? o0[1] : 0.0;
+        old1[0] = cv0 ? o1[0] : 0.0; old1[1] = cv1 ? o1[1] : 0.0;
+        const int ca0 = 16 * bi + lr;
+        const bool vy = lr < NC;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          const int g = 4 * kk + lc;
+          const bool gv = g < ng;
+          const double* pr = P + g * W;
+          const double x0 = gv ? pr[ca0] : 0.0, x1 = gv ? pr[ca0 + 8] : 0.0;
+          const double y0 = (gv && vy) ? pr[K + lr] : 0.0;
+          dmma884(acc0, x0, y0);
+          dmma884(acc1, x1, y0);
+        }
+        if (cv0) { o0[0] = old0[0] - acc0[0]; o1[0] = old1[0] - acc1[0]; }
+        if (cv1) { o0[1] = old0[1] - acc0[1]; o1[1] = old1[1] - acc1[1]; }
+        continue;
+      }
       // output offsets of this lane's accumulator elements (-1: not stored), old
       // values (the sons' contributions, written by B') fetched ahead of the DMMAs
       int ov[2][2][2];
