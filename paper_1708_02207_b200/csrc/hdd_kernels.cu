@@ -1418,7 +1418,7 @@ __device__ __forceinline__ void gather_panel_row(const MergeCtx& c, int k, int n
 // Schur-update epilogue on 32 x 64 output tiles (lower-triangle Psi tiles and
 // the R columns), the assembled A~ values gathered from the sons and issued
 // before the DMMA loop; output packed-lower.
-template <bool SMEM>
+template <bool SMEM, bool FAST = false>
 __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double* __restrict__ P, int ldp, int k,
                                                int ngp, int Kp, int nc, double* __restrict__ out, double* Ea,
                                                double* Eb) {
@@ -1446,6 +1446,39 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
       }
     if constexpr (SMEM) {
       if (!any) continue;                          // no barriers in the smem-panel loop
+      const int ar0 = a0 + m0, bc0 = b0 + n0;
+      if (FAST && ar0 + 16 <= k && bc0 + 16 <= k && bc0 + 15 < ar0) {
+        // this warp's 16x16 sub-tile is strictly lower and inside Psi: no per-element
+        // predicates (the common case on big nodes)
+        double pre[2][2][2], acc[2][2][2] = {};
+        int trow[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int aa = ar0 + 8 * i + gr;
+          trow[i] = tri(aa);
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) pre[i][j][e] = gather_A(mc, aa, bc0 + 8 * j + 2 * gq + e);
+        }
+        for (int g0 = 0; g0 < ngp; g0 += 4) {
+          const double* pr = P + size_t(g0 + gq) * ldp;
+          double av[2], bv[2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) { av[i] = pr[ar0 + 8 * i + gr]; bv[i] = pr[bc0 + 8 * i + gr]; }
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) dmma884(acc[i][j], av[i], bv[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) out[trow[i] + bc0 + 8 * j + 2 * gq + e] = pre[i][j][e] - acc[i][j][e];
+        continue;
+      }
     }
     double acc[2][2][2] = {};
     int acol[2], bcol[2];
@@ -1807,7 +1840,7 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
     out[tk + k * nc + c] = v;
   }
   MERGE_TICK(4);
-  schur_epilogue<true>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
+  schur_epilogue<true, MINB <= 2>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
   MERGE_TICK(5);
 }
 
