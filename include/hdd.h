@@ -117,6 +117,9 @@ typedef struct {
   int64_t ref_id;
   int32_t i0, j0, ncols, has_mean;
   const int32_t* birth;    /* [ncols][3]: in-leaf level, node, gamma pos     */
+  const int32_t* ccode;    /* [ncols] 0 load, 1 own mean, 2 point, or a mean
+                              over a sub-leaf node: (1 << 24) | i0 | i1 << 5 |
+                              j0 << 10 | j1 << 15 (leaf-local cell range)    */
 } HddLeafInfo;
 
 typedef struct {

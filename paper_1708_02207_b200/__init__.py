@@ -34,5 +34,6 @@ from .geometry import (  # noqa: F401
 )
 
 __version__ = "0.1.0"
-from . import configs, parallel, posterior  # noqa: E402,F401
+from . import configs, dumps, parallel, posterior  # noqa: E402,F401
+from .dumps import dump_functionals, dump_store_stats, functional_summaries, store_stats  # noqa: E402,F401
 from .posterior import ChainSpec, GridSpec, PosteriorResult, posterior_grid, posterior_mcmc, posterior_mcmc_chains  # noqa: E402,F401

@@ -63,7 +63,7 @@ class HddNodeInfo(C.Structure):
 
 class HddLeafInfo(C.Structure):
     _fields_ = [("ref_id", C.c_int64), ("i0", C.c_int32), ("j0", C.c_int32),
-                ("ncols", C.c_int32), ("has_mean", C.c_int32), ("birth", _i32p)]
+                ("ncols", C.c_int32), ("has_mean", C.c_int32), ("birth", _i32p), ("ccode", _i32p)]
 
 
 class HddObsInfo(C.Structure):

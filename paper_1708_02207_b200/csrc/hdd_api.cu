@@ -122,7 +122,8 @@ static int setup_device(HddPlan* pl, int max_batch) {
       d.ctype[c] = 2; d.birth_r[c] = -1; d.birth_q[c] = -1; d.birth_g[c] = -1; d.fslot[c] = -1;
     }
     for (int c = 0; c < d.ncols; ++c) {
-      d.ctype[c] = L.cols[c].kind == COL_LOAD ? 0 : (L.cols[c].kind == COL_MEAN ? 1 : 2);
+      d.ctype[c] = L.ccode[c];
+      if (L.ccode[c] >= kSubMeanTag) D.has_submean = 1;
       d.birth_r[c] = L.birth[3 * c];
       d.birth_q[c] = L.birth[3 * c + 1];
       d.birth_g[c] = L.birth[3 * c + 2];
@@ -712,6 +713,7 @@ int hdd_plan_leaf_info(const HddPlan* pl, int32_t idx, HddLeafInfo* out) {
   out->ncols = int(L.cols.size());
   out->has_mean = L.own_mean ? 1 : 0;
   out->birth = L.birth.data();
+  out->ccode = L.ccode.data();
   return HDD_OK;
 }
 

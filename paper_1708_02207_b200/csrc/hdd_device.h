@@ -53,6 +53,7 @@ struct DevError {
 
 struct DevPlan {
   int N, m, n_z, n_obs, n_leaves, leaf_cols, leaf_ld;
+  int has_submean;         // some leaf column is a mean over a sub-leaf node
   double h;
   int64_t leaf_elems;
   int leaf_buf;

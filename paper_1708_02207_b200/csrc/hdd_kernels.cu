@@ -282,6 +282,22 @@ __device__ __forceinline__ double sym(const double* P, int i, int j) {
 // fragments (4 rows x 8 consecutive doubles) hit distinct banks.
 __host__ __device__ constexpr int leaf_wpad(int w) { return w + ((12 - (w & 7)) & 7); }
 
+// Mean over a sub-leaf tree node (column code kSubMeanTag | i0 | i1 << 5 | j0 << 10 |
+// j1 << 15, leaf-local cells): the lumped mean weight of leaf-local node (X, Y) —
+// 2, 1, 1, 2 sixths of h^2 from the cells it is the (i,j), (i+1,j), (i,j+1), (i+1,j+1)
+// corner of (functionals.py:47-61: a third of each triangle's area per vertex) —
+// counting only the cells of the mean's node that lie in the block [bx0,bx1) x [by0,by1).
+constexpr int kSubMeanCode = 1 << 24;
+__device__ __forceinline__ double submean_weight(int code, int X, int Y, int bx0, int bx1, int by0, int by1) {
+  const int x0 = max(bx0, code & 31), x1 = min(bx1, (code >> 5) & 31);
+  const int y0 = max(by0, (code >> 10) & 31), y1 = min(by1, (code >> 15) & 31);
+  auto cin = [&](int cx, int cy) { return (cx >= x0 && cx < x1 && cy >= y0 && cy < y1) ? 1.0 : 0.0; };
+  return 2.0 * cin(X, Y) + cin(X - 1, Y) + cin(X, Y - 1) + 2.0 * cin(X - 1, Y - 1);
+}
+__device__ __forceinline__ double submean_inv_area(int code, double h) {
+  return 1.0 / (double((((code >> 5) & 31) - (code & 31)) * (((code >> 15) & 31) - ((code >> 10) & 31))) * h * h);
+}
+
 // Levels 6 and 5 of the leaf condensed directly per 2x4-cell node (HDD_LEAF_UNFUSED
 // restores the register 2x2 base + shared-memory level 5).
 #ifdef HDD_LEAF_UNFUSED
@@ -773,8 +789,10 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
       const int a = t / NC, c = t - (t / NC) * NC;
       const int col = cinfo[5 * NC + c];
       if (col < 0) continue;
-      const double val = out[ctri(k) + a * NC + c];
-      gdst[ctri(k) + a * p.leaf_cols + col] = val * (ctype[c] == 1 ? inv_area : 1.0);
+      const int ct = ctype[c];
+      const double val = out[ctri(k) + a * NC + c] *
+                         (ct == 1 ? inv_area : (ct >= kSubMeanCode ? submean_inv_area(ct, p.h) : 1.0));
+      gdst[ctri(k) + a * p.leaf_cols + col] = val;
       const int fs = cinfo[4 * NC + c];
       if (fs >= 0) p.fbuf[(int64_t(s) * p.n_fslots + fs) * 65 + a] = val;
     }
@@ -787,7 +805,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 // level-synchronously in shared memory with lower-packed Schur complements:
 // gather the interface panel, Gauss-Jordan interface inverse (warp per node),
 // Y = A22^-1 [A21 | R], then the Schur update A11 - A21^T Y on DMMA tiles.
-template <int NC, int NTH>
+template <int NC, int NTH, bool SUB>
 __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && kLeafFused56))) ? 3 : 2) leaf2_kernel(DevPlan p, const int* __restrict__ order, LeafSmem ls,
                                                        int B) {
   extern __shared__ __align__(16) double sm[];
@@ -907,6 +925,7 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
       for (int c = 0; c < NC; ++c) {
         const int ct = ctype[c];
         double rc4 = ct == 0 ? rl[4] : (ct == 1 ? rm[4] : 0.0);
+        if (SUB && ct >= kSubMeanCode) rc4 = h2_6 * submean_weight(ct, x0 + 1, y0 + 1, x0, x0 + 2, y0, y0 + 2);
         if (br[c] == 6 && bq[c] == q) rc4 += 1.0;
         v[c] = rc4 * inv;
       }
@@ -915,7 +934,9 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           const int ct = ctype[c];
-          const double rb = ct == 0 ? rl[P8[i]] : (ct == 1 ? rm[P8[i]] : 0.0);
+          double rb = ct == 0 ? rl[P8[i]] : (ct == 1 ? rm[P8[i]] : 0.0);
+          if (SUB && ct >= kSubMeanCode)
+            rb = h2_6 * submean_weight(ct, x0 + P8[i] % 3, y0 + P8[i] / 3, x0, x0 + 2, y0, y0 + 2);
           out[tri(k6) + i * NC + c] = fma(-xv[P8[i]], v[c], rb);
         }
 #pragma unroll
@@ -1043,11 +1064,17 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
           double r0 = 0.0, r1 = 0.0, r2 = 0.0;
           if (ct == 0) { r0 = h2 * fI0; r1 = h2 * fI1; r2 = h2 * fI2; }
           else if (ct == 1) { r0 = h2; r1 = h2; r2 = h2; }
+          else if (SUB && ct >= kSubMeanCode) {
+            r0 = h2_6 * submean_weight(ct, ox + 1, oy + 1, ox, ox + 2, oy, oy + 4);
+            r1 = h2_6 * submean_weight(ct, ox + 1, oy + 2, ox, ox + 2, oy, oy + 4);
+            r2 = h2_6 * submean_weight(ct, ox + 1, oy + 3, ox, ox + 2, oy, oy + 4);
+          }
           if (br[c] == 6 && bq[c] == 2 * q) r0 += 1.0;
           if (br[c] == 6 && bq[c] == 2 * q + 1) r2 += 1.0;
           if (br[c] == 5 && bq[c] == q) r1 += 1.0;
           if (c == 0) { r00 = r0; r01 = r1; r02 = r2; }
           double val = ct == 0 ? wa * fa : (ct == 1 ? wa : 0.0);
+          if (SUB && ct >= kSubMeanCode) val = h2_6 * submean_weight(ct, ox + xa, oy + ya, ox, ox + 2, oy, oy + 4);
           if (ga >= 0) val -= ma0 * r0 + ma1 * r1 + ma2 * r2;
           out[ctri(k5) + a * NC + c] = val;
           if (a == 0) {
@@ -1092,13 +1119,21 @@ cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_ou
     dim3 grid(cnt, B, p.leaf_class_passes[cls]);
     const int* ord = p.leaf_order + p.leaf_class_start[cls];
     cudaError_t e;
-#define HDD_LAUNCH_LEAF(NCV)                                                                                   \
-  e = cudaFuncSetAttribute(leaf2_kernel<NCV, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));     \
+#define HDD_LAUNCH_LEAF(NCV, SUBV)                                                                             \
+  e = cudaFuncSetAttribute(leaf2_kernel<NCV, 256, SUBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
   if (e != cudaSuccess) return e;                                                                              \
-  leaf2_kernel<NCV, 256><<<grid, 256, smem, s>>>(p, ord, ls, B);
-    if (ncl == 2) { HDD_LAUNCH_LEAF(2) }
-    else if (ncl == 4) { HDD_LAUNCH_LEAF(4) }
-    else { HDD_LAUNCH_LEAF(8) }
+  leaf2_kernel<NCV, 256, SUBV><<<grid, 256, smem, s>>>(p, ord, ls, B);
+    // sub-leaf mean columns only exist in plans that observe such means (separate
+    // instantiation: the likelihood configs never pay for the masked weights)
+    if (p.has_submean) {
+      if (ncl == 2) { HDD_LAUNCH_LEAF(2, true) }
+      else if (ncl == 4) { HDD_LAUNCH_LEAF(4, true) }
+      else { HDD_LAUNCH_LEAF(8, true) }
+    } else {
+      if (ncl == 2) { HDD_LAUNCH_LEAF(2, false) }
+      else if (ncl == 4) { HDD_LAUNCH_LEAF(4, false) }
+      else { HDD_LAUNCH_LEAF(8, false) }
+    }
 #undef HDD_LAUNCH_LEAF
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -1369,6 +1404,20 @@ __device__ __forceinline__ double gather_R(const MergeCtx& c, int a, int col) {
   if (pa1 >= 0 && s1 >= 0) v += c.ccoef[2 * col + 1] * son_R(c.sv[1], pa1, s1);
   return v;
 }
+// the two sons' contributions kept apart (the add is deferred past the DMMA chain so
+// the loads' latency overlaps it)
+__device__ __forceinline__ void gather_A2(const MergeCtx& c, int a, int j, double& v0, double& v1) {
+  const int pa0 = c.gm[a], pa1 = c.gm[c.K + a];
+  const int pb0 = c.gm[j], pb1 = c.gm[c.K + j];
+  v0 = (pa0 >= 0 && pb0 >= 0) ? son_psi(c.sv[0], pa0, pb0) : 0.0;
+  v1 = (pa1 >= 0 && pb1 >= 0) ? son_psi(c.sv[1], pa1, pb1) : 0.0;
+}
+__device__ __forceinline__ void gather_R2(const MergeCtx& c, int a, int col, double& v0, double& v1) {
+  const int pa0 = c.gm[a], pa1 = c.gm[c.K + a];
+  const int s0 = c.csrc[2 * col], s1 = c.csrc[2 * col + 1];
+  v0 = (pa0 >= 0 && s0 >= 0) ? c.ccoef[2 * col] * son_R(c.sv[0], pa0, s0) : 0.0;
+  v1 = (pa1 >= 0 && s1 >= 0) ? c.ccoef[2 * col + 1] * son_R(c.sv[1], pa1, s1) : 0.0;
+}
 __device__ __forceinline__ double gather_sig(const MergeCtx& c, int col) {
   double v = 0.0;
   const int s0 = c.csrc[2 * col], s1 = c.csrc[2 * col + 1];
@@ -1418,7 +1467,7 @@ __device__ __forceinline__ void gather_panel_row(const MergeCtx& c, int k, int n
 // Schur-update epilogue on 32 x 64 output tiles (lower-triangle Psi tiles and
 // the R columns), the assembled A~ values gathered from the sons and issued
 // before the DMMA loop; output packed-lower.
-template <bool SMEM, bool FAST = false>
+template <bool SMEM, bool FAST = false, bool SPLIT = false>
 __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double* __restrict__ P, int ldp, int k,
                                                int ngp, int Kp, int nc, double* __restrict__ out, double* Ea,
                                                double* Eb) {
@@ -1450,7 +1499,7 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
       if (FAST && ar0 + 16 <= k && bc0 + 16 <= k && bc0 + 15 < ar0) {
         // this warp's 16x16 sub-tile is strictly lower and inside Psi: no per-element
         // predicates (the common case on big nodes)
-        double pre[2][2][2], acc[2][2][2] = {};
+        double pre[2][2][2], pre1[2][2][2], acc[2][2][2] = {};
         int trow[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
@@ -1459,7 +1508,10 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
 #pragma unroll
           for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) pre[i][j][e] = gather_A(mc, aa, bc0 + 8 * j + 2 * gq + e);
+            for (int e = 0; e < 2; ++e) {
+              if constexpr (SPLIT) gather_A2(mc, aa, bc0 + 8 * j + 2 * gq + e, pre[i][j][e], pre1[i][j][e]);
+              else { pre[i][j][e] = gather_A(mc, aa, bc0 + 8 * j + 2 * gq + e); pre1[i][j][e] = 0.0; }
+            }
         }
         for (int g0 = 0; g0 < ngp; g0 += 4) {
           const double* pr = P + size_t(g0 + gq) * ldp;
@@ -1476,7 +1528,8 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
 #pragma unroll
           for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) out[trow[i] + bc0 + 8 * j + 2 * gq + e] = pre[i][j][e] - acc[i][j][e];
+            for (int e = 0; e < 2; ++e)
+              out[trow[i] + bc0 + 8 * j + 2 * gq + e] = (SPLIT ? pre[i][j][e] + pre1[i][j][e] : pre[i][j][e]) - acc[i][j][e];
         continue;
       }
     }
@@ -1489,7 +1542,7 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
       const int bb = b0 + n0 + 8 * i + gr;
       bcol[i] = bb < k ? bb : (bb < ow ? Kp + (bb - k) : 0);
     }
-    double pre[2][2][2];
+    double pre[2][2][2], pre1[2][2][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int aa = a0 + m0 + 8 * i + gr;
@@ -1498,12 +1551,18 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int bb = b0 + n0 + 8 * j + 2 * gq + e;
-          double v = 0.0;
+          double v = 0.0, v1 = 0.0;
           if (aa < k && bb < ow) {
-            if (bb < k) { if (bb <= aa) v = gather_A(mc, aa, bb); }
-            else v = gather_R(mc, aa, bb - k);
+            if constexpr (SPLIT) {
+              if (bb < k) { if (bb <= aa) gather_A2(mc, aa, bb, v, v1); }
+              else gather_R2(mc, aa, bb - k, v, v1);
+            } else {
+              if (bb < k) { if (bb <= aa) v = gather_A(mc, aa, bb); }
+              else v = gather_R(mc, aa, bb - k);
+            }
           }
           pre[i][j][e] = v;
+          pre1[i][j][e] = v1;
         }
     }
     if constexpr (SMEM) {
@@ -1547,9 +1606,9 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
           const int bb = b0 + n0 + 8 * j + 2 * gq + e;
           if (bb >= ow) continue;
           if (bb < k) {
-            if (bb <= aa) out[tri(aa) + bb] = pre[i][j][e] - acc[i][j][e];
+            if (bb <= aa) out[tri(aa) + bb] = (pre[i][j][e] + pre1[i][j][e]) - acc[i][j][e];
           } else {
-            out[tk + aa * nc + (bb - k)] = pre[i][j][e] - acc[i][j][e];
+            out[tk + aa * nc + (bb - k)] = (pre[i][j][e] + pre1[i][j][e]) - acc[i][j][e];
           }
         }
     }
@@ -1840,7 +1899,7 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
     out[tk + k * nc + c] = v;
   }
   MERGE_TICK(4);
-  schur_epilogue<true, MINB <= 2>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
+  schur_epilogue<true, MINB <= 2, MINB <= 2>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
   MERGE_TICK(5);
 }
 

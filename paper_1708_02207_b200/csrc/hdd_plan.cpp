@@ -301,6 +301,7 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
   struct Birth { int where; int node; int r; int q; int gpos; };   // where: 0 upper, 1 leaf
   std::vector<Birth> births(n_obs, Birth{-1, -1, -1, -1, -1});
   std::vector<int> mean_tmp(n_obs, -1);
+  std::vector<int> sub_code(n_obs, 0);      // sub-leaf means: device column code
   P.route.assign(n_obs, ObsRoute{1, -1, 0.0});
   std::map<int64_t, int> tmp_of_refid;
   for (int t = 0; t < int(all.size()); ++t) tmp_of_refid[postorder_id(P.level, all[t].path)] = t;
@@ -343,11 +344,32 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     } else if (P.obs_kind[o] == HDD_OBS_MEAN) {
       auto it = tmp_of_refid.find(id);
       if (it == tmp_of_refid.end()) {
-        if (id >= 0 && id < subtree_size(P.level, 0))
-          return "mean observation of tree node " + std::to_string(id) +
-                 " lies below the 16x16-cell kernel-leaf level (unsupported)";
-        *code = HDD_ERR_USAGE;
-        return "no tree node with id " + std::to_string(id);
+        if (id < 0 || id >= subtree_size(P.level, 0)) {
+          *code = HDD_ERR_USAGE;
+          return "no tree node with id " + std::to_string(id);
+        }
+        // a node below the kernel-leaf level: locate its cells by descending the
+        // post-order numbering, then the kernel leaf that contains them
+        Rect r{0, int(P.N), 0, int(P.N)};
+        int depth = 0;
+        int64_t lo = 0;
+        while (lo + subtree_size(P.level, depth) - 1 != id) {
+          Rect a, b;
+          split(r, depth, a, b, nullptr);
+          const int64_t half = subtree_size(P.level, depth + 1);
+          if (id < lo + half) r = a;
+          else { r = b; lo += half; }
+          ++depth;
+        }
+        int t = 0;
+        while (all[t].depth < dl) {
+          const Rect& s0 = all[all[t].son[0]].r;
+          t = (r.i0 >= s0.i0 && r.i1 <= s0.i1 && r.j0 >= s0.j0 && r.j1 <= s0.j1) ? all[t].son[0] : all[t].son[1];
+        }
+        const Rect& lr = all[t].r;
+        births[o] = {1, -1 - to_plan[t], -1, -1, -1};
+        sub_code[o] = submean_code(r.i0 - lr.i0, r.i1 - lr.i0, r.j0 - lr.j0, r.j1 - lr.j0);
+        continue;
       }
       mean_tmp[o] = it->second;
     } else {
@@ -402,11 +424,14 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
           colmap[t][o] = c;
           L.fslot.push_back(-1);
         }
-        L.cols.push_back({COL_OBS, o});
+        if (sub_code[o]) L.cols.push_back({COL_SUBMEAN, o, sub_code[o]});
+        else L.cols.push_back({COL_OBS, o});
         L.birth.insert(L.birth.end(), {births[o].r, births[o].q, births[o].gpos});
       }
       if (mean_tmp[o] == t) colmap[t][o] = mean_col;
     }
+    for (const Col& c : L.cols)
+      L.ccode.push_back(c.kind == COL_LOAD ? 0 : (c.kind == COL_MEAN ? 1 : (c.kind == COL_SUBMEAN ? c.code : 2)));
     P.leaf_cols = std::max(P.leaf_cols, int(L.cols.size()));
   }
   for (int dep = dl - 1; dep >= 0; --dep) {

@@ -20,11 +20,20 @@ constexpr int kLeafCells = 16;                 // kernel-leaf subdomain (cells p
 constexpr int kLeafPerim = 4 * kLeafCells;     // 64 perimeter nodes
 constexpr int kLeafLevels = 8;                 // in-leaf merge levels r = 0..7
 
-enum ColKind { COL_LOAD = 0, COL_MEAN = 1, COL_OBS = 2 };
+enum ColKind { COL_LOAD = 0, COL_MEAN = 1, COL_OBS = 2, COL_SUBMEAN = 3 };
+
+// Device column code of a mean over a sub-leaf tree node (functionals.py:47-61 mean
+// rule restricted to the node's cells): tag | i0 | i1 << 5 | j0 << 10 | j1 << 15, the
+// node's cell range in leaf-local coordinates.
+constexpr int kSubMeanTag = 1 << 24;
+inline int submean_code(int i0, int i1, int j0, int j1) {
+  return kSubMeanTag | i0 | (i1 << 5) | (j0 << 10) | (j1 << 15);
+}
 
 struct Col {
   int kind;      // ColKind
-  int obs;       // observation index for COL_OBS
+  int obs;       // observation index for COL_OBS / COL_SUBMEAN
+  int code = 0;  // COL_SUBMEAN: submean_code of the node's cells
 };
 
 struct UpperNode {
@@ -63,6 +72,7 @@ struct Leaf {
   int parent = -1;              // upper index of the father
   std::vector<int32_t> cmap;    // [64] father K-index of each perimeter node, -1 on the domain boundary
   std::vector<int32_t> fslot;   // [ncols] functional slot of a primal point column, -1
+  std::vector<int32_t> ccode;   // [ncols] device column code: 0 load, 1 own mean, 2 point, submean_code
 };
 
 struct ObsRoute {

@@ -88,10 +88,10 @@ def run(plan, level, kappa, f=None):
         assert L.hdd_plan_leaf_info(plan.handle, li, C.byref(lf)) == 0
         nc = lf.ncols
         birth = _arr(lf.birth, 3 * nc, int).reshape(nc, 3)
-        ctype = np.full(nc, 2)
-        ctype[0] = 0
-        if lf.has_mean:
-            ctype[1] = 1
+        ctype = _arr(lf.ccode, nc, int)
+        assert ctype[0] == 0 and (nc > 1 and ctype[1] == 1) == bool(lf.has_mean)
+        sub = [(c, ctype[c] & 31, (ctype[c] >> 5) & 31, (ctype[c] >> 10) & 31, (ctype[c] >> 15) & 31)
+               for c in range(nc) if ctype[c] >= 1 << 24]       # means over sub-leaf nodes
         coef = np.where(ctype == 1, 0.5, 1.0)
         # cells
         level_nodes = []
@@ -105,6 +105,9 @@ def run(plan, level, kappa, f=None):
             R[:, 0] = loadpat * f[nodes]
             if lf.has_mean:
                 R[:, 1] = meanpat
+            for c, i0, i1, j0, j1 in sub:
+                if i0 <= x < i1 and j0 <= y < j1:
+                    R[:, c] = loadpat
             level_nodes.append((psi, R, np.zeros(nc)))
         for r in range(7, -1, -1):
             K, k, ng, m1, m2 = tmpl[r]
@@ -123,7 +126,11 @@ def run(plan, level, kappa, f=None):
                         Rt[k + birth[c, 2], c] += 1.0
                 new.append(eliminate(At, Rt, sg, k))
             level_nodes = new
-        leaf_out.append(level_nodes[0])
+        psi, R, sg = level_nodes[0]
+        for c, i0, i1, j0, j1 in sub:
+            R[:, c] /= (i1 - i0) * (j1 - j0) * h * h
+            sg[c] /= (i1 - i0) * (j1 - j0) * h * h
+        leaf_out.append((psi, R, sg))
     upper_out = {}
 
     def son_out(s):

@@ -71,7 +71,7 @@ def test_leaf_template_shapes():
 
 
 @pytest.mark.parametrize("mode", [0, 1])
-@pytest.mark.parametrize("case", ["C1", "points6", "means6", "indicator5", "f_nodal5"])
+@pytest.mark.parametrize("case", ["C1", "points6", "means6", "submeans6", "indicator5", "f_nodal5"])
 def test_emulated_plan_matches_direct_solve(case, mode):
     rng = np.random.default_rng(5)
     f = None
@@ -87,6 +87,14 @@ def test_emulated_plan_matches_direct_solve(case, mode):
         obs = tuple(("mean", nid) for nid, _ in geometry.nodes_at_depth(6, 2)) + \
             tuple(("mean", nid) for nid, _ in geometry.nodes_at_depth(6, 4))[:6] + \
             (("mean", geometry.nodes_at_depth(6, 0)[0][0]), ("point", 65 * 30 + 33))
+    elif case == "submeans6":
+        # means of nodes below the 16x16-cell kernel leaves (depths 5..12, down to one
+        # cell), next to a leaf's own mean and in-leaf points, with a nodal f
+        level, n_z = 6, 8
+        obs = tuple(("mean", geometry.nodes_at_depth(6, d)[i][0])
+                    for d, i in ((5, 3), (6, 0), (6, 57), (7, 100), (8, 31), (9, 400), (11, 1500), (12, 4095),
+                                 (4, 9), (10, 1023))) + (("point", 65 * 30 + 33), ("point", 65 * 3 + 5))
+        f = rng.uniform(0.5, 2.0, (65 * 65))
     elif case == "indicator5":
         level, n_z = 5, 4
         param = "ind"
@@ -136,9 +144,10 @@ def test_plan_errors():
     p = hb.SineKLField(tree, 4)
     with pytest.raises(hb.ConfigError):
         hb.BayesProblem(tree, p, np.ones(mesh.n_nodes), np.ones(128), hb.MeasurementModel(obs, np.ones(1)))
-    deep = geometry.nodes_at_depth(5, 5)[0][0]
-    with pytest.raises(hb.ConfigError):
-        host_problem(5, 4, (("mean", deep),)).plan()
+    deep = geometry.nodes_at_depth(5, 10)[0][0]               # one cell inside a kernel leaf
+    host_problem(5, 4, (("mean", deep),)).plan()
+    with pytest.raises(hb.UsageError):
+        host_problem(5, 4, (("mean", -1),)).plan()
     with pytest.raises(hb.UsageError):
         host_problem(5, 4, (("mean", 10 ** 9),)).plan()
     with pytest.raises(hb.UsageError):
