@@ -83,6 +83,11 @@ typedef struct {
   double lr_eps;
   int32_t lr_kmax;
   int32_t lr_nmin;
+  /* Dirichlet data on the domain boundary, [4N] in increasing mesh-node order
+   * (the reference's root.idx_boundary order, bayes.py:162); NULL = 0.  Known
+   * boundary values are folded into the load and functional columns at the
+   * kernel-leaf outputs, so the upper merges never see them.                 */
+  const double* g;
 } HddPlanDesc;
 
 typedef struct {
@@ -120,6 +125,8 @@ typedef struct {
   const int32_t* ccode;    /* [ncols] 0 load, 1 own mean, 2 point, or a mean
                               over a sub-leaf node: (1 << 24) | i0 | i1 << 5 |
                               j0 << 10 | j1 << 15 (leaf-local cell range)    */
+  const double* gperim;    /* [64] Dirichlet value of each perimeter node on the
+                              domain boundary (NULL when g = 0)                */
 } HddLeafInfo;
 
 typedef struct {

@@ -38,6 +38,7 @@ class HddPlanDesc(C.Structure):
         ("sigma", _f64p), ("y", _f64p),
         ("max_batch", C.c_int32), ("device", C.c_int32), ("keep_nodes", C.c_int32),
         ("mode", C.c_int32), ("lr_eps", C.c_double), ("lr_kmax", C.c_int32), ("lr_nmin", C.c_int32),
+        ("g", _f64p),
     ]
 
 
@@ -63,7 +64,8 @@ class HddNodeInfo(C.Structure):
 
 class HddLeafInfo(C.Structure):
     _fields_ = [("ref_id", C.c_int64), ("i0", C.c_int32), ("j0", C.c_int32),
-                ("ncols", C.c_int32), ("has_mean", C.c_int32), ("birth", _i32p), ("ccode", _i32p)]
+                ("ncols", C.c_int32), ("has_mean", C.c_int32), ("birth", _i32p), ("ccode", _i32p),
+                ("gperim", _f64p)]
 
 
 class HddObsInfo(C.Structure):

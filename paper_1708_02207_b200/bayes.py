@@ -17,8 +17,9 @@ the B200 through libhdd_b200.so:
   (per-sample Python loop)                    forward_functionals_batch /
                                               log_likelihood_batch (one C call)
 
-Only f and g of the BASELINE problem class are supported on the device path:
-any nodal f, and g = 0 (the Dirichlet rows are pruned).
+Any nodal right-hand side f and any Dirichlet data g (over the boundary nodes in
+increasing id order, like the reference's root.idx_boundary) are supported; both are
+fixed per plan.
 """
 from __future__ import annotations
 
@@ -249,6 +250,7 @@ class _Plan:
             sy=np.ascontiguousarray(param.sy, dtype=np.float64),
             coef=np.ascontiguousarray(param.coef, dtype=np.float64),
             f=None if problem._f_is_one else np.ascontiguousarray(problem.f, dtype=np.float64),
+            g=np.ascontiguousarray(problem.g, dtype=np.float64) if np.any(problem.g != 0.0) else None,
             kind=kinds, ids=np.array([int(i) for _, i in obs], dtype=np.int64),
             sigma=np.ascontiguousarray(model.sigma, dtype=np.float64),
             y=None if model.y is None else np.ascontiguousarray(model.y, dtype=np.float64))
@@ -262,7 +264,8 @@ class _Plan:
             max_batch=int(max_batch), device=int(device), keep_nodes=int(keep_nodes), mode=int(mode),
             lr_eps=float(getattr(problem.compression, "eps", 0.0) or 0.0) if problem.compression is not None else 0.0,
             lr_kmax=int(getattr(problem.compression, "k_max", 64)) if problem.compression is not None else 0,
-            lr_nmin=int(getattr(problem.compression, "n_min", 32)) if problem.compression is not None else 0)
+            lr_nmin=int(getattr(problem.compression, "n_min", 32)) if problem.compression is not None else 0,
+            g=ptr(k["g"], _lib._f64p))
         h = C.c_void_p()
         rc = L.hdd_plan_create(C.byref(desc), C.byref(h))
         if rc != _lib.HDD_OK:
@@ -330,8 +333,8 @@ class BayesProblem:
             raise UsageError("data sizes do not match the mesh")
         if g.shape != (4 * mesh.n_cells,):
             raise UsageError("data sizes do not match the mesh")
-        if np.any(g != 0.0):
-            raise ConfigError("the device likelihood path supports g = 0 only (Dirichlet rows are pruned)")
+        if not np.all(np.isfinite(g)):
+            raise ConfigError("Dirichlet data g is not finite")
         self.f = f
         self.g = g
         self._f_is_one = bool(np.all(f == 1.0))

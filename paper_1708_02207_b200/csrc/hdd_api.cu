@@ -132,6 +132,12 @@ static int setup_device(HddPlan* pl, int max_batch) {
     d.parent = L.parent;
   }
   if ((rc = upload(pl, dl, &D.leaves))) return rc;
+  D.leaf_g = nullptr;
+  if (P.has_g) {
+    std::vector<double> lg;
+    for (const Leaf& L : P.leaves) lg.insert(lg.end(), L.gperim.begin(), L.gperim.end());
+    if ((rc = upload(pl, lg, &D.leaf_g))) return rc;
+  }
   {
     std::vector<int32_t> lc;
     for (const Leaf& L : P.leaves) {
@@ -714,6 +720,7 @@ int hdd_plan_leaf_info(const HddPlan* pl, int32_t idx, HddLeafInfo* out) {
   out->has_mean = L.own_mean ? 1 : 0;
   out->birth = L.birth.data();
   out->ccode = L.ccode.data();
+  out->gperim = pl->plan.has_g ? L.gperim.data() : nullptr;
   return HDD_OK;
 }
 

@@ -54,6 +54,7 @@ struct DevError {
 struct DevPlan {
   int N, m, n_z, n_obs, n_leaves, leaf_cols, leaf_ld;
   int has_submean;         // some leaf column is a mean over a sub-leaf node
+  const double* leaf_g;    // [n_leaves][64] Dirichlet values on the domain boundary, NULL = g = 0
   double h;
   int64_t leaf_elems;
   int leaf_buf;

@@ -420,7 +420,7 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
 //      sons' contributions A~ = Psi_s1 + Psi_s2 (and R_B) into `out`
 //   C  [W | V] = L^-1 [A21 | R_gamma] in place (thread per column)
 //   D  out -= W^T [W | V] on 8x8 DMMA tiles; sigma += V_0^T V
-template <int R, int NC, int NTH>
+template <int R, int NC, int NTH, bool EXT = false>
 __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __restrict__ in, double* __restrict__ out,
                                            double* __restrict__ pan, const int* __restrict__ cinfo, int leaf,
                                            int s, long long leaf_ref, const uint64_t* __restrict__ tabP,
@@ -785,13 +785,29 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
     double* gdst = p.buf[p.leaf_buf] + int64_t(leaf) * p.leaf_elems * p.bcap + int64_t(s) * p.leaf_elems;
     if (blockIdx.z == 0)
       for (int t = tid; t < ctri(k); t += NT) gdst[t] = out[t];
+    // Dirichlet data g on the domain boundary (known perimeter values u_D = g_D):
+    // load rows r_a -= Psi_aD g_D, functional columns sigma_c += R_c(D)^T g_D
+    const double* lg = (EXT && p.leaf_g) ? p.leaf_g + int64_t(leaf) * kLeafPerim : nullptr;
     for (int t = tid; t < (k + 1) * NC; t += NT) {
       const int a = t / NC, c = t - (t / NC) * NC;
       const int col = cinfo[5 * NC + c];
       if (col < 0) continue;
       const int ct = ctype[c];
-      const double val = out[ctri(k) + a * NC + c] *
-                         (ct == 1 ? inv_area : (ct >= kSubMeanCode ? submean_inv_area(ct, p.h) : 1.0));
+      double raw = out[ctri(k) + a * NC + c];
+      if (lg) {
+        if (ct == 0 && a < k) {
+          for (int d = 0; d < k; ++d) {
+            const double gd = lg[d];
+            if (gd != 0.0) raw -= out[a >= d ? tri(a) + d : tri(d) + a] * gd;
+          }
+        } else if (ct != 0 && a == k) {
+          for (int d = 0; d < k; ++d) {
+            const double gd = lg[d];
+            if (gd != 0.0) raw += out[ctri(k) + d * NC + c] * gd;
+          }
+        }
+      }
+      const double val = raw * (ct == 1 ? inv_area : ((EXT && ct >= kSubMeanCode) ? submean_inv_area(ct, p.h) : 1.0));
       gdst[ctri(k) + a * p.leaf_cols + col] = val;
       const int fs = cinfo[4 * NC + c];
       if (fs >= 0) p.fbuf[(int64_t(s) * p.n_fslots + fs) * 65 + a] = val;
@@ -805,7 +821,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 // level-synchronously in shared memory with lower-packed Schur complements:
 // gather the interface panel, Gauss-Jordan interface inverse (warp per node),
 // Y = A22^-1 [A21 | R], then the Schur update A11 - A21^T Y on DMMA tiles.
-template <int NC, int NTH, bool SUB>
+template <int NC, int NTH, bool SUB>   // SUB: sub-leaf mean columns or Dirichlet data present
 __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && kLeafFused56))) ? 3 : 2) leaf2_kernel(DevPlan p, const int* __restrict__ order, LeafSmem ls,
                                                        int B) {
   extern __shared__ __align__(16) double sm[];
@@ -1104,7 +1120,7 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
   leaf_level<3, NC, NTH>(p, bufA, bufB, pan, cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
   leaf_level<2, NC, NTH>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
   leaf_level<1, NC, NTH>(p, bufA, bufB, pan, cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
-  leaf_level<0, NC, NTH>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
+  leaf_level<0, NC, NTH, SUB>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
   LEAF_TICK(63);
 }
 
@@ -1123,9 +1139,9 @@ cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_ou
   e = cudaFuncSetAttribute(leaf2_kernel<NCV, 256, SUBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
   if (e != cudaSuccess) return e;                                                                              \
   leaf2_kernel<NCV, 256, SUBV><<<grid, 256, smem, s>>>(p, ord, ls, B);
-    // sub-leaf mean columns only exist in plans that observe such means (separate
-    // instantiation: the likelihood configs never pay for the masked weights)
-    if (p.has_submean) {
+    // sub-leaf mean columns and Dirichlet data only exist in plans that need them
+    // (separate instantiation: the likelihood configs never pay for them)
+    if (p.has_submean || p.leaf_g) {
       if (ncl == 2) { HDD_LAUNCH_LEAF(2, true) }
       else if (ncl == 4) { HDD_LAUNCH_LEAF(4, true) }
       else { HDD_LAUNCH_LEAF(8, true) }
@@ -2519,7 +2535,8 @@ __global__ void __launch_bounds__(32) leaf_solve_kernel(DevPlan p, double* __res
   for (int t = lane; t < 512; t += 32) kap[t] = kb[2 * (int64_t(L.i0 + (t >> 5)) * N + L.j0) + (t & 31)];
   for (int t = lane; t < kLeafPerim; t += 32) {
     const int c = L.parent >= 0 ? p.leaf_cmap[int64_t(leaf) * kLeafPerim + t] : -1;
-    ub[t] = c >= 0 ? p.ubuf[int64_t(s) * p.u_elems + p.upper[L.parent].u_off + c] : 0.0;   // g = 0 on the domain boundary
+    ub[t] = c >= 0 ? p.ubuf[int64_t(s) * p.u_elems + p.upper[L.parent].u_off + c]
+                   : (p.leaf_g ? p.leaf_g[int64_t(leaf) * kLeafPerim + t] : 0.0);   // u = g on the domain boundary
   }
   __syncwarp();
   auto k0 = [&](int cx, int cy) { return kap[cx * 32 + 2 * cy]; };

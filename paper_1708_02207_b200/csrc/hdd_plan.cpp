@@ -212,6 +212,13 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     P.f.assign(d->f, d->f + size_t(m) * m);
     for (double v : P.f) if (!std::isfinite(v)) return "right-hand side f is not finite";
   }
+  if (d->g) {
+    P.g.assign(d->g, d->g + size_t(4) * N);
+    for (double v : P.g) {
+      if (!std::isfinite(v)) return "Dirichlet data g is not finite";
+      if (v != 0.0) P.has_g = true;
+    }
+  }
   const int n_obs = d->n_obs;
   P.obs_kind.assign(d->obs_kind, d->obs_kind + n_obs);
   P.obs_id.assign(d->obs_id, d->obs_id + n_obs);
@@ -271,6 +278,14 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     int64_t i = id % m, j = id / m;
     return i == 0 || j == 0 || i == N || j == N;
   };
+  // position of a boundary node in increasing-id order: the bottom row (m), then two
+  // per interior row (left, right), then the top row
+  auto g_of = [&](int64_t id) -> double {
+    if (!P.has_g) return 0.0;
+    const int64_t i = id % m, j = id / m;
+    const int64_t pos = j == 0 ? i : (j == N ? m + 2 * (N - 1) + i : m + 2 * (j - 1) + (i == N ? 1 : 0));
+    return P.g[size_t(pos)];
+  };
   for (int t = 0; t < int(all.size()); ++t) {
     const Tmp& T = all[t];
     int64_t rid = postorder_id(P.level, T.path);
@@ -279,6 +294,12 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
       L.ref_id = rid;
       L.i0 = T.r.i0;
       L.j0 = T.r.j0;
+      L.gperim.assign(kLeafPerim, 0.0);
+      if (P.has_g) {
+        const std::vector<int64_t> per = perimeter(T.r, m);
+        for (int a = 0; a < kLeafPerim; ++a)
+          if (is_boundary(per[a])) L.gperim[a] = g_of(per[a]);
+      }
       continue;
     }
     UpperNode& U = P.upper[to_plan[t]];
@@ -309,7 +330,7 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     int64_t id = P.obs_id[o];
     if (P.obs_kind[o] == HDD_OBS_POINT) {
       if (id < 0 || id >= m * m) { *code = HDD_ERR_USAGE; return "mesh node " + std::to_string(id) + " not found on any interface"; }
-      if (is_boundary(id)) { P.route[o] = ObsRoute{1, -1, 0.0}; continue; }  // g = 0
+      if (is_boundary(id)) { P.route[o] = ObsRoute{1, -1, g_of(id)}; continue; }  // u = g there
       int64_t pi = id % m, pj = id / m;
       int t = 0;
       while (true) {

@@ -73,6 +73,7 @@ struct Leaf {
   std::vector<int32_t> cmap;    // [64] father K-index of each perimeter node, -1 on the domain boundary
   std::vector<int32_t> fslot;   // [ncols] functional slot of a primal point column, -1
   std::vector<int32_t> ccode;   // [ncols] device column code: 0 load, 1 own mean, 2 point, submean_code
+  std::vector<double> gperim;   // [64] Dirichlet value of each perimeter node on the domain boundary, else 0
 };
 
 struct ObsRoute {
@@ -93,6 +94,8 @@ struct Plan {
   double h = 0;
   std::vector<double> sx, sy, coef, f;
   bool f_is_one = true;
+  std::vector<double> g;        // [4N] Dirichlet data (sorted boundary ids), empty = 0
+  bool has_g = false;
   std::vector<int32_t> obs_kind;
   std::vector<int64_t> obs_id;
   std::vector<double> sigma, y;

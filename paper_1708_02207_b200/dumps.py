@@ -115,8 +115,8 @@ def functional_summaries(problem, z, forward=None) -> dict:
         forward = forward_functionals_batch
     mesh = problem.tree.mesh
     unit = problem
-    if not problem._f_is_one:
-        unit = BayesProblem(problem.tree, problem.param, np.ones(mesh.n_nodes), problem.g, problem.model,
+    if not problem._f_is_one or np.any(problem.g != 0.0):
+        unit = BayesProblem(problem.tree, problem.param, np.ones(mesh.n_nodes), np.zeros(4 * mesh.n_cells), problem.model,
                             compression=problem.compression, device=problem.device, mode=problem.mode)
     S = np.asarray(forward(unit, np.asarray(z, dtype=float)[None]), dtype=float).reshape(-1)
     root = problem.tree.root_id

@@ -127,6 +127,13 @@ def run(plan, level, kappa, f=None):
                 new.append(eliminate(At, Rt, sg, k))
             level_nodes = new
         psi, R, sg = level_nodes[0]
+        if lf.gperim:
+            # known boundary values: load rows r -= Psi_{.,D} g_D, functionals sigma += R_D^T g_D
+            gp = _arr(lf.gperim, 64, float)
+            R = R.copy()
+            sg = sg.copy()
+            R[:, 0] -= psi @ gp
+            sg[1:] += gp @ R[:, 1:]
         for c, i0, i1, j0, j1 in sub:
             R[:, c] /= (i1 - i0) * (j1 - j0) * h * h
             sg[c] /= (i1 - i0) * (j1 - j0) * h * h

@@ -1,7 +1,7 @@
 """Randomised parity sweep: random levels, parameter dimensions, observation sets
 (interior / interface / boundary points, subdomain means at every depth of the tree,
-down to single cells inside the kernel leaves),
-right-hand sides and evaluation modes against the oracle's sparse direct solve
+down to single cells inside the kernel leaves), right-hand sides f, Dirichlet data g
+and evaluation modes against the oracle's sparse direct solve
 (relative 1e-10, the BASELINE tolerance)."""
 import numpy as np
 import pytest
@@ -38,15 +38,16 @@ def test_random_problem_matches_direct_solve(cuda, seed):
     rng.shuffle(obs)
     obs = tuple(obs)
     f = rng.uniform(-1.0, 2.0, mesh.n_nodes) if rng.random() < 0.5 else np.ones(mesh.n_nodes)
+    g = rng.uniform(-1.0, 1.0, 4 * mesh.n_cells) if rng.random() < 0.5 else np.zeros(4 * mesh.n_cells)
     mode = int(rng.choice([-1, 0, 1]))
-    prob = hb.BayesProblem(tree, hb.SineKLField(tree, n_z), f, np.zeros(4 * mesh.n_cells),
+    prob = hb.BayesProblem(tree, hb.SineKLField(tree, n_z), f, g,
                            hb.MeasurementModel(obs, np.full(len(obs), 0.01)), mode=mode)
     grid = geometry.Grid(level)
     fo = fields.SineKLField(grid, n_z)
     Z = 1.5 * rng.standard_normal((3, n_z))
     S = hb.forward_functionals_batch(prob, Z)
     for b in range(Z.shape[0]):
-        u = direct.solve(grid, fo.kappa_values(Z[b]), f=f)
+        u = direct.solve(grid, fo.kappa_values(Z[b]), f=f, g=g)
         ref = ocfg.observe(grid, u, obs)
         assert np.max(np.abs(S[b] - ref)) <= TOL * max(np.max(np.abs(ref)), 1e-300), (level, n_z, mode, obs)
     assert m == grid.m

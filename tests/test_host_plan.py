@@ -17,13 +17,14 @@ from paper_1708_02207_b200 import _lib, parallel
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def host_problem(level, n_z, obs, param="kl", sigma=0.01, y=None, f=None, mode=0):
+def host_problem(level, n_z, obs, param="kl", sigma=0.01, y=None, f=None, mode=0, g=None):
     mesh = hb.build_mesh(level)
     tree = hb.build_tree(mesh)
     p = hb.SineKLField(tree, n_z) if param == "kl" else hb.ParamField.build(tree, n_z)
     model = hb.MeasurementModel(obs, np.full(len(obs), sigma), y)
     f = np.ones(mesh.n_nodes) if f is None else f
-    return hb.BayesProblem(tree, p, f, np.zeros(4 * mesh.n_cells), model, device=-1, mode=mode)
+    g = np.zeros(4 * mesh.n_cells) if g is None else g
+    return hb.BayesProblem(tree, p, f, g, model, device=-1, mode=mode)
 
 
 def test_library_exports_header_symbols():
@@ -71,10 +72,12 @@ def test_leaf_template_shapes():
 
 
 @pytest.mark.parametrize("mode", [0, 1])
-@pytest.mark.parametrize("case", ["C1", "points6", "means6", "submeans6", "indicator5", "f_nodal5"])
+@pytest.mark.parametrize("case", ["C1", "points6", "means6", "submeans6", "indicator5", "f_nodal5",
+                                  "dirichlet4", "dirichlet6"])
 def test_emulated_plan_matches_direct_solve(case, mode):
     rng = np.random.default_rng(5)
     f = None
+    g = None
     param = "kl"
     if case == "C1":
         level, n_z = 5, 4
@@ -95,6 +98,17 @@ def test_emulated_plan_matches_direct_solve(case, mode):
                     for d, i in ((5, 3), (6, 0), (6, 57), (7, 100), (8, 31), (9, 400), (11, 1500), (12, 4095),
                                  (4, 9), (10, 1023))) + (("point", 65 * 30 + 33), ("point", 65 * 3 + 5))
         f = rng.uniform(0.5, 2.0, (65 * 65))
+    elif case.startswith("dirichlet"):
+        # non-zero Dirichlet data: points on and next to the domain boundary, means
+        # touching it (whole domain, a boundary leaf, a sub-leaf corner node)
+        level, n_z = int(case[-1]), 5
+        m = 2 ** level + 1
+        obs = (("point", 0), ("point", 3), ("point", m + 1), ("point", m * (m // 2) + m // 2),
+               ("point", m * (m - 2) + m - 2), ("mean", geometry.nodes_at_depth(level, 0)[0][0]),
+               ("mean", geometry.nodes_at_depth(level, 2 * level - 8)[0][0]),
+               ("mean", geometry.nodes_at_depth(level, 2 * level)[-1][0]))
+        f = rng.uniform(0.5, 2.0, m * m)
+        g = rng.uniform(-1.0, 1.0, 4 * (m - 1))
     elif case == "indicator5":
         level, n_z = 5, 4
         param = "ind"
@@ -103,14 +117,14 @@ def test_emulated_plan_matches_direct_solve(case, mode):
         level, n_z = 5, 4
         obs = configs.observations(configs.CONFIGS["C1"])
         f = rng.uniform(0.5, 2.0, (33 * 33))
-    prob = host_problem(level, n_z, obs, param=param, f=f, mode=mode)
-    assert prob.plan().info().mode == mode
+    prob = host_problem(level, n_z, obs, param=param, f=f, mode=mode, g=g)
+    assert prob.plan().info().mode == (0 if level == 4 else mode)
     grid = geometry.Grid(level)
     fo = fields.SineKLField(grid, n_z) if param == "kl" else fields.IndicatorField(grid, n_z)
     for z in rng.standard_normal((2, n_z)):
         kap = fo.kappa_values(z)
         S, _, _ = pe.run(prob.plan(), level, kap, f)
-        u = direct.solve(grid, kap, f=f)
+        u = direct.solve(grid, kap, f=f, g=g)
         Sd = configs.observe(grid, u, obs)
         assert np.max(np.abs(S - Sd)) <= 1e-12 * np.max(np.abs(Sd))
 
@@ -142,8 +156,8 @@ def test_plan_errors():
     mesh = hb.build_mesh(5)
     tree = hb.build_tree(mesh)
     p = hb.SineKLField(tree, 4)
-    with pytest.raises(hb.ConfigError):
-        hb.BayesProblem(tree, p, np.ones(mesh.n_nodes), np.ones(128), hb.MeasurementModel(obs, np.ones(1)))
+    with pytest.raises(hb.UsageError):
+        hb.BayesProblem(tree, p, np.ones(mesh.n_nodes), np.ones(127), hb.MeasurementModel(obs, np.ones(1)))
     deep = geometry.nodes_at_depth(5, 10)[0][0]               # one cell inside a kernel leaf
     host_problem(5, 4, (("mean", deep),)).plan()
     with pytest.raises(hb.UsageError):
