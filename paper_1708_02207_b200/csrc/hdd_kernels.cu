@@ -397,6 +397,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// TMA bulk prefetch of a global range into L2 (no shared memory, no completion)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n"
                ::"r"(smem_u32(bar)), "r"(parity) : "memory");
@@ -1821,6 +1825,14 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
     mc.sv[0].b = st;
     mc.sv[1].b = st + U.son_elems[0];
   }
+#ifndef HDD_NO_L2_PREFETCH
+  else if (tid == 0) {
+    // the sons' packed outputs are read twice (panel gather now, A11 / R_B in the Schur
+    // epilogue after the elimination): pull them into L2 while the maps are staged
+    bulk_prefetch_l2(mc.sv[0].b, uint32_t(U.son_elems[0] * 8) & ~15u);
+    bulk_prefetch_l2(mc.sv[1].b, uint32_t(U.son_elems[1] * 8) & ~15u);
+  }
+#endif
   for (int t = tid; t < 2 * U.K; t += NT) gms[t] = __ldg(mc.gm + t);
   for (int t = tid; t < 2 * nc; t += NT) {
     cis[t] = __ldg(mc.csrc + t);
