@@ -49,47 +49,54 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 // ---------------------------------------------------------------------------
 // K1: coefficient field
 // ---------------------------------------------------------------------------
-// grid: (ceil(N/128), N/8, B); block 128.  Thread = column j of 8 consecutive cell rows
-// i0..i0+7: each sy_k(j) pair is loaded once and feeds 8 cells; double2 stores.
-constexpr int kKappaRows = 8;
+// grid: (ceil(N/128), ceil(N/32), B); block 128.  Thread = column j of 32 consecutive
+// cell rows, in groups of 8: each sy_k(j) pair is loaded once per group and feeds 8
+// cells; double2 stores (each warp writes 512 contiguous bytes per cell row).  32 rows
+// per CTA amortise the czx setup (dependent loads + barrier) over 32 KB of output.
+constexpr int kKappaRows = 8, kKappaGroups = 4;
 __global__ void __launch_bounds__(128) kappa_kernel(DevPlan p, const double* __restrict__ Z, int B,
                                                     double* __restrict__ kappa) {
-  extern __shared__ double czx[];   // [n_z][kKappaRows][2]: coef_k z_k sx_k(2i + type)
+  extern __shared__ double czx[];   // [n_z][kKappaGroups * kKappaRows][2]: coef_k z_k sx_k(2i + type)
+  constexpr int RB = kKappaRows * kKappaGroups;
   const int N = p.N, nz = p.n_z;
-  const int i0 = blockIdx.y * kKappaRows, s = blockIdx.z;
+  const int i0 = blockIdx.y * RB, s = blockIdx.z;
+  const int nrow = min(RB, N - i0);
   const double* z = Z + int64_t(s) * nz;
-  for (int t = threadIdx.x; t < nz * kKappaRows * 2; t += blockDim.x) {
-    const int k = t / (kKappaRows * 2), r = t - k * (kKappaRows * 2);
-    czx[t] = p.coef[k] * z[k] * p.sx[int64_t(k) * 2 * N + 2 * i0 + r];
+  for (int t = threadIdx.x; t < nz * RB * 2; t += blockDim.x) {
+    const int k = t / (RB * 2), r = t - k * (RB * 2);
+    czx[t] = r < 2 * nrow ? p.coef[k] * z[k] * p.sx[int64_t(k) * 2 * N + 2 * i0 + r] : 0.0;
   }
   __syncthreads();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= N) return;
-  double q[kKappaRows][2] = {};
   const double2* sy2 = reinterpret_cast<const double2*>(p.sy);
-  for (int k = 0; k < nz; ++k) {
-    const double2 t = __ldg(sy2 + int64_t(k) * N + j);
-    const double* c = czx + k * kKappaRows * 2;
-#pragma unroll
-    for (int r = 0; r < kKappaRows; ++r) {
-      q[r][0] = fma(c[2 * r], t.x, q[r][0]);
-      q[r][1] = fma(c[2 * r + 1], t.y, q[r][1]);
-    }
-  }
   double2* out = reinterpret_cast<double2*>(kappa + int64_t(s) * 2 * N * N);
   bool bad = false;
+  for (int g = 0; g < nrow; g += kKappaRows) {
+    double q[kKappaRows][2] = {};
+    for (int k = 0; k < nz; ++k) {
+      const double2 t = __ldg(sy2 + int64_t(k) * N + j);
+      const double* c = czx + k * RB * 2 + 2 * g;
 #pragma unroll
-  for (int r = 0; r < kKappaRows; ++r) {
-    const double2 v = make_double2(exp(q[r][0]), exp(q[r][1]));
-    bad |= !(v.x > 0.0) || !(v.y > 0.0) || !isfinite(v.x) || !isfinite(v.y);
-    out[int64_t(i0 + r) * N + j] = v;
+      for (int r = 0; r < kKappaRows; ++r) {
+        q[r][0] = fma(c[2 * r], t.x, q[r][0]);
+        q[r][1] = fma(c[2 * r + 1], t.y, q[r][1]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kKappaRows; ++r) {
+      const double2 v = make_double2(exp(q[r][0]), exp(q[r][1]));
+      bad |= !(v.x > 0.0) || !(v.y > 0.0) || !isfinite(v.x) || !isfinite(v.y);
+      if (g + r < nrow) out[int64_t(i0 + g + r) * N + j] = v;
+    }
   }
   if (bad) record_error(p.err, HDD_ERR_CONFIG, s, -1);
 }
 
 cudaError_t launch_kappa(const DevPlan& p, const double* Z, int B, double* kappa, cudaStream_t s) {
-  dim3 grid((p.N + 127) / 128, p.N / kKappaRows, B);
-  kappa_kernel<<<grid, 128, size_t(2) * kKappaRows * p.n_z * sizeof(double), s>>>(p, Z, B, kappa);
+  constexpr int RB = kKappaRows * kKappaGroups;
+  dim3 grid((p.N + 127) / 128, (p.N + RB - 1) / RB, B);
+  kappa_kernel<<<grid, 128, size_t(2) * RB * p.n_z * sizeof(double), s>>>(p, Z, B, kappa);
   return cudaGetLastError();
 }
 
