@@ -239,6 +239,9 @@ static int setup_device(HddPlan* pl, int max_batch) {
       const size_t sons = sizeof(double) * size_t(((d.son_elems[0] + 1) & ~1) + ((d.son_elems[1] + 1) & ~1));
       // measured: pays off only on the first merge level (sons = kernel leaves)
       d.stage = (U.son[0] < 0 && U.son[1] < 0 && sm + sons <= 110 * 1024) ? 1 : 0;
+#ifdef HDD_NO_STAGE
+      d.stage = 0;
+#endif
       if (d.stage) sm += sons;
     }
     pl->depth_smem[U.depth] = std::max(pl->depth_smem[U.depth], sm);

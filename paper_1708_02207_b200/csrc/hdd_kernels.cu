@@ -413,6 +413,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
                ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
+// 1/d: MUFU seed + two Newton steps (full double precision)
+__device__ __forceinline__ double rcp_nr(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  y = fma(y, fma(-d, y, 1.0), y);
+  y = fma(y, fma(-d, y, 1.0), y);
+  return y;
+}
+
 // 1/sqrt(d): MUFU seed + two Newton steps (full double precision for the
 // well-scaled pivots of the in-leaf factorizations)
 __device__ __forceinline__ double rsqrt_nr(double d) {
@@ -517,6 +526,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 #pragma unroll
     for (int l = 0; l < ng; ++l) a[l] = (act && l <= i) ? P[i * W + l] : (l == i ? 1.0 : 0.0);
     bool bad = false;
+#ifdef HDD_OLD_CHOL
 #pragma unroll
     for (int j = 0; j < ng; ++j) {
       const double dj = __shfl_sync(0xffffffffu, a[j], j, LPN);
@@ -527,6 +537,22 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
       for (int l = j + 1; l < ng; ++l) a[l] = fma(-lij, __shfl_sync(0xffffffffu, lij, l, LPN), a[l]);
       a[j] = i == j ? il : lij;
     }
+#else
+    // unscaled (LDL^T-ordered) elimination: a_il -= a_ij a_lj / d_j.  The column
+    // broadcast a_lj does not wait for the pivot's reciprocal, so the serial chain per
+    // step is shuffle -> rcp -> mul -> fma; the sqrt scaling of column j runs beside it
+#pragma unroll
+    for (int j = 0; j < ng; ++j) {
+      const double dj = __shfl_sync(0xffffffffu, a[j], j, LPN);
+      bad |= !(dj > 0.0);
+      const double rj = rcp_nr(dj);
+      const double sj = a[j] * rj;
+#pragma unroll
+      for (int l = j + 1; l < ng; ++l) a[l] = fma(-sj, __shfl_sync(0xffffffffu, a[j], l, LPN), a[l]);
+      const double il = rsqrt_nr(dj);
+      a[j] = i == j ? il : a[j] * il;
+    }
+#endif
     if (act) {
 #pragma unroll
       for (int l = 0; l < ng; ++l)
@@ -1505,8 +1531,13 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
   const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * 16;
   const int na = (k + 31) / 32, nbt = (ow + 63) / 64;
   const int tk = tri(k);
+  // tiles t = ta * nbt + tb, walked without integer division
+  int ta = 0, tb = grp;
+  while (tb >= nbt && nbt > 0) { tb -= nbt; ++ta; }
   for (int t = grp; t < na * nbt; t += ngrp) {
-    const int a0 = (t / nbt) * 32, b0 = (t % nbt) * 64;
+    const int a0 = ta * 32, b0 = tb * 64;
+    tb += ngrp;
+    while (tb >= nbt) { tb -= nbt; ++ta; }
     if (b0 + 64 <= k && b0 > a0 + 31) continue;   // strictly upper Psi tile
     // 8x8 DMMA blocks of this warp's 16x16 sub-tile that hold outputs (warp-uniform):
     // rows < k, columns < k + nc, not strictly above the diagonal of Psi
@@ -1934,15 +1965,27 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
     out[tk + k * nc + c] = v;
   }
   MERGE_TICK(4);
+  #ifdef HDD_FAST_ALL
+  schur_epilogue<true, true, MINB <= 2>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
+#else
   schur_epilogue<true, MINB <= 2, MINB <= 2>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
+#endif
   MERGE_TICK(5);
 }
 
 // -- tier L: panel in HBM ----------------------------------------------------
 // smem: F phases (L scratch / LiT / Xc / Lt) and the epilogue's 2 x (A, B) chunks of
 // 32 x kLds share the front region; the son maps and column plan follow it.
-constexpr size_t kLRegion = (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) > (4 * kEC * kLds)
-                                ? (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) : (4 * kEC * kLds);
+#ifndef HDD_LL_WIDTH
+#define HDD_LL_WIDTH 64
+#endif
+// left-looking elimination: column chunks of kLW, staged rows per step kLH
+constexpr int kLW = HDD_LL_WIDTH, kLWs = kLW + 8, kLH = 16;
+constexpr size_t kLLStream = 2 * size_t(kLH) * (kLdd + kLWs);          // 2 x (A chunk | B chunk)
+constexpr size_t kLLRegion = 2 * 32 * kLdd + (kLLStream > size_t(32 * kLWs) ? kLLStream : size_t(32 * kLWs));
+constexpr size_t kLRegion0 = (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) > (4 * kEC * kLds)
+                                 ? (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) : (4 * kEC * kLds);
+constexpr size_t kLRegion = kLRegion0 > kLLRegion ? kLRegion0 : kLLRegion;
 size_t merge_l_smem_bytes(int K, int nc) {
   const size_t ints = (size_t(2 * K + 3 * nc) + 1) & ~size_t(1);
   return sizeof(double) * (kLRegion + ints / 2 + 2 * size_t(nc)) + 1024;
@@ -1987,6 +2030,7 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
   if (tid == 0) s_bad = 0;
   __syncthreads();
   MERGE_TICK(2);
+#ifdef HDD_RIGHT_LOOKING
   for (int r0 = 0; r0 < ngp; r0 += kLB) {
     if (warp == 0) factor_block32(P + int64_t(r0) * ldp + k + r0, ldp, sm, LiT, &s_bad);
     __syncthreads();
@@ -2049,6 +2093,109 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
     }
     __syncthreads();
   }
+#else
+  // Left-looking blocked elimination.  For each 32-row block r0 and each chunk of
+  // kLW columns c of C(r0) = [k + r0, W) u [0, k) (the diagonal block's own A22
+  // columns first, then the rest of A22, R_gamma, then A21):
+  //   T = P[r0 rows][c] - sum_{h < r0} U[h][r0 rows]^T P[h][c]     (depth-r0 DMMA GEMM,
+  //       rows h streamed through smem in kLH-row chunks, double-buffered cp.async)
+  //   chunk 0 only: Cholesky of T's leading 32x32 block -> L_bb, L_bb^-1 (warp 0)
+  //   P[r0 rows][c] = L_bb^-1 T                                   (the row block of U / W / V)
+  // Every panel element is written once (no trailing read-modify-write sweeps); the
+  // accumulators stay in registers for the whole depth.
+  {
+    double* LsB = sm;                        // [32][kLdd] factor scratch
+    double* LiB = sm + 32 * kLdd;            // [32][kLdd] L_bb^-1 (transposed)
+    double* St = sm + 2 * 32 * kLdd;         // stream buffers / T tile [32][kLWs]
+    constexpr int SB = kLH * (kLdd + kLWs);
+    constexpr int FN = kLW / 32;
+    const int gq = lane & 3, gr = lane >> 2;
+    const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * (kLW / 4);
+    for (int r0 = 0; r0 < ngp; r0 += kLB) {
+      const int nseg = W - k - r0;           // [k + r0, W) first, then [0, k)
+      const int nv = nseg + k;
+      const double* Arow = P + k + r0;       // A operand columns of row h: Arow[h * ldp + i]
+      for (int v0 = 0; v0 < nv; v0 += kLW) {
+        auto phys = [&](int v) { return v < nseg ? k + r0 + v : v - nseg; };
+        auto stage = [&](int h0, int buf) {
+          double* Sa = St + buf * SB;
+          double* Sb = Sa + kLH * kLdd;
+          for (int t = tid; t < kLH * 32; t += 256) {
+            const int g = t >> 5, i = t & 31;
+            cp_async8(Sa + g * kLdd + i, Arow + int64_t(h0 + g) * ldp + i);
+          }
+          for (int t = tid; t < kLH * kLW; t += 256) {
+            const int g = t / kLW, j = t - (t / kLW) * kLW;
+            const int v = v0 + j;
+            if (v < nv) cp_async8(Sb + g * kLWs + j, P + int64_t(h0 + g) * ldp + phys(v));
+            else Sb[g * kLWs + j] = 0.0;
+          }
+          cp_async_commit();
+        };
+        // the block's own panel values, loaded ahead of the depth-r0 GEMM
+        double pv[2][FN][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int row = m0 + 8 * i + gr, v = v0 + n0 + 8 * j + 2 * gq + e;
+              pv[i][j][e] = v < nv ? P[int64_t(r0 + row) * ldp + phys(v)] : 0.0;
+            }
+        double acc[2][FN][2] = {};
+        const int nch = r0 / kLH;
+        if (nch > 0) {
+          __syncthreads();                   // previous users of the stream buffers are done
+          stage(0, 0);
+          for (int c = 0; c < nch; ++c) {
+            if (c + 1 < nch) {
+              stage((c + 1) * kLH, (c + 1) & 1);
+              cp_async_wait<1>();
+            } else {
+              cp_async_wait<0>();
+            }
+            __syncthreads();
+            const double* Sa = St + (c & 1) * SB;
+            warp_gemm_tn<2, FN>(acc, Sa, kLdd, m0, Sa + kLH * kLdd, kLWs, n0, kLH);
+            __syncthreads();
+          }
+        } else {
+          __syncthreads();
+        }
+        // T = P[r0 rows][chunk] - acc -> smem
+        double* T = St;
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int row = m0 + 8 * i + gr, cc = n0 + 8 * j + 2 * gq + e;
+              T[row * kLWs + cc] = pv[i][j][e] - acc[i][j][e];
+            }
+        __syncthreads();
+        if (v0 == 0) {
+          if (warp == 0) factor_block32(T, kLWs, LsB, LiB, &s_bad);
+          __syncthreads();
+        }
+        double x[2][FN][2] = {};
+        warp_gemm_tn<2, FN>(x, LiB, kLdd, m0, T, kLWs, n0, 32);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int row = m0 + 8 * i + gr, cc = n0 + 8 * j + 2 * gq + e;
+              const int v = v0 + cc;
+              if (v < nv) P[int64_t(r0 + row) * ldp + phys(v)] = x[i][j][e];
+            }
+      }
+    }
+    __syncthreads();
+  }
+#endif
   MERGE_TICK(3);
   if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
   if (p.mode == 1) store_factors(p, U, s, P, ldp, Kp, false, tid, 256);

@@ -22,7 +22,7 @@ import paper_1708_02207_b200 as hb  # noqa: E402
 from paper_1708_02207_b200 import configs  # noqa: E402
 
 CASES = [("C1", 64, False, "forward"), ("C2", 1024, False, "forward"), ("C3", 1024, False, "forward"),
-         ("C4", 256, False, "forward"), ("C5", 64, False, "forward"), ("C5", 64, True, "forward"),
+         ("C4", 1024, False, "forward"), ("C5", 512, False, "forward"), ("C5", 512, True, "forward"),
          ("C2", 1024, False, "solve")]
 
 
