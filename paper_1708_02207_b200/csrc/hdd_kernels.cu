@@ -364,6 +364,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -1693,6 +1697,7 @@ __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const doubl
       double* Ea = E + buf * 2 * kEC * kLds;
       double* Eb = Ea + kEC * kLds;
       const int g0 = c * kEC;
+#ifdef HDD_STAGE8
       for (int tt = tid; tt < kEC * 64; tt += 256) {
         const int g = tt >> 6, i = tt & 63;
         const int aa = a0 + i;
@@ -1703,6 +1708,36 @@ __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const doubl
         if (col >= 0) cp_async8(Eb + g * kLds + i, P + int64_t(g0 + g) * ldp + col);
         else Eb[g * kLds + i] = 0.0;
       }
+#else
+      // column pairs as 16-byte copies: the panel rows are 16-byte aligned (even ldp),
+      // A21 pairs start at even columns, and the R block's pairs at Kp + (even - k),
+      // Kp - k = ngp even; only the pair straddling k (odd k) goes element-wise
+      for (int tt = tid; tt < kEC * 32; tt += 256) {
+        const int g = tt >> 5, i = 2 * (tt & 31);
+        const double* src = P + int64_t(g0 + g) * ldp;
+        double* ea = Ea + g * kLds + i;
+        double* eb = Eb + g * kLds + i;
+        const int aa = a0 + i;
+        if (aa + 1 < k) cp_async16(ea, src + aa);
+        else {
+          if (aa < k) cp_async8(ea, src + aa);
+          else ea[0] = 0.0;
+          ea[1] = 0.0;
+        }
+        const int bb = b0 + i;
+        if (bb + 1 < k) cp_async16(eb, src + bb);
+        else if (bb >= k && bb + 1 < ow) cp_async16(eb, src + Kp + (bb - k));
+        else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int b = bb + e;
+            const int col = b < k ? b : (b < ow ? Kp + (b - k) : -1);
+            if (col >= 0) cp_async8(eb + e, src + col);
+            else eb[e] = 0.0;
+          }
+        }
+      }
+#endif
       cp_async_commit();
     };
     __syncthreads();
