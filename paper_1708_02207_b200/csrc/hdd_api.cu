@@ -281,6 +281,17 @@ static int setup_device(HddPlan* pl, int max_batch) {
         }
       }
       pl->lr_nblk[dep] = int(blk.size() / 5) - pl->lr_blk0[dep];
+      if (std::getenv("HDD_LR_STATS")) {   // diagnostics: admissible blocks per depth
+        long long area = 0, small = 0;
+        int qm = 0;
+        for (size_t t = size_t(pl->lr_blk0[dep]) * 5; t < blk.size(); t += 5) {
+          area += (long long)blk[t + 2] * blk[t + 4];
+          small += (blk[t + 2] <= 64 && blk[t + 4] <= 64);
+          qm = std::max(qm, int(blk[t + 4]));
+        }
+        std::fprintf(stderr, "lr depth %zu: nodes %zu blocks %d (<=64x64: %lld) pmax %d qmax %d area %lld\n", dep,
+                     ids.size(), pl->lr_nblk[dep], small, pl->lr_pmax[dep], qm, area);
+      }
       if (pl->lr_pmax[dep] > 760)
         return set_err(&pl->err, HDD_ERR_CONFIG, "low-rank block with more than 760 rows does not fit the device sketch");
     }

@@ -2399,7 +2399,12 @@ __global__ void __launch_bounds__(256) psi_norm_kernel(DevPlan p, const DevUpper
   }
 }
 
-__global__ void __launch_bounds__(256, 3) compress_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int blk0) {
+// LW: sketch width rounded up (16 / 24 / 32).  Every pass reads each entry of the
+// block once: a thread owns a row (pass 1) or a column (passes 2, 3) and keeps the LW
+// sketch / projection values of it in registers; partial sums over row or column
+// groups meet in shared memory.
+template <int LW, int MINB>
+__global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int blk0) {
   extern __shared__ __align__(16) double sm[];
   const int32_t* bd = p.lr_blk + 5 * (blk0 + blockIdx.y);
   const int ln = bd[0], roff = bd[1], P_ = bd[2], coff = bd[3], Q_ = bd[4];
@@ -2418,33 +2423,46 @@ __global__ void __launch_bounds__(256, 3) compress_kernel(DevPlan p, const DevUp
   __shared__ int s_bad, s_k, s_piv[32];
   __shared__ double s_an2, s_bn2;
   auto A = [&](int i, int j) { const int r = R[i], c = Cc[j]; return r >= c ? psi[tri(r) + c] : psi[tri(c) + r]; };
-  // ---- pass 1: Y = A Omega (thread per row and 4 sketch columns), ||A||^2 ----
+  // ---- pass 1: Y = A Omega (thread per row, all sketch columns), ||A||^2 ----
+  // JG thread groups split the columns when the block has few rows
+  const int JG = P_ >= 256 ? 1 : (P_ >= 128 ? 2 : (P_ >= 64 ? 4 : 8));
+  const int RS = 256 / JG;
+  if (JG > 1)
+    for (int t = tid; t < P_ * 33; t += 256) Y[t] = 0.0;
+  __syncthreads();
   double an = 0.0;
-  for (int w = tid; w < P_ * 8; w += 256) {
-    const int i = w >> 3, t0 = (w & 7) * 4;
-    double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
-    constexpr int UJ = 4;                       // Psi entries in flight per thread
-    for (int j0 = 0; j0 < Q_; j0 += UJ) {
-      double av[UJ];
+  {
+    const int jg = tid / RS, ir = tid - (tid / RS) * RS;
+    for (int i0 = 0; i0 < P_; i0 += RS) {
+      const int i = i0 + ir;
+      if (i >= P_) continue;
+      double acc[LW];
 #pragma unroll
-      for (int u = 0; u < UJ; ++u) av[u] = j0 + u < Q_ ? A(i, j0 + u) : 0.0;
+      for (int t = 0; t < LW; ++t) acc[t] = 0.0;
+      const int r = R[i];
+      const int tr = tri(r);
+      for (int j = jg; j < Q_; j += JG) {
+        const int c = Cc[j];
+        const double a = r >= c ? psi[tr + c] : psi[tri(c) + r];
+        an = fma(a, a, an);
+        const double2* om = reinterpret_cast<const double2*>(p.lr_omega + j * 32);
 #pragma unroll
-      for (int u = 0; u < UJ; ++u) {
-        const int j = j0 + u < Q_ ? j0 + u : 0;
-        const double a = av[u];
-        if (t0 == 0) an = fma(a, a, an);
-        const double4 om = *reinterpret_cast<const double4*>(p.lr_omega + j * 32 + t0);
-        y0 = fma(a, om.x, y0);
-        y1 = fma(a, om.y, y1);
-        y2 = fma(a, om.z, y2);
-        y3 = fma(a, om.w, y3);
+        for (int t = 0; t < LW; t += 2) {
+          const double2 o = __ldg(om + t / 2);
+          acc[t] = fma(a, o.x, acc[t]);
+          acc[t + 1] = fma(a, o.y, acc[t + 1]);
+        }
+      }
+      double* yr = Y + i * 33;
+      if (JG == 1) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) yr[t] = (t < LW && t < L) ? acc[t < LW ? t : 0] : 0.0;
+      } else {
+#pragma unroll
+        for (int t = 0; t < LW; ++t)
+          if (t < L) atomicAdd(yr + t, acc[t]);
       }
     }
-    double* yr = Y + i * 33 + t0;
-    yr[0] = t0 < L ? y0 : 0.0;
-    yr[1] = t0 + 1 < L ? y1 : 0.0;
-    yr[2] = t0 + 2 < L ? y2 : 0.0;
-    yr[3] = t0 + 3 < L ? y3 : 0.0;
   }
   for (int off = 16; off > 0; off >>= 1) an += __shfl_xor_sync(0xffffffffu, an, off);
   if (lane == 0) red[warp] = an;
@@ -2514,18 +2532,30 @@ __global__ void __launch_bounds__(256, 3) compress_kernel(DevPlan p, const DevUp
   double macc[4] = {0.0, 0.0, 0.0, 0.0};     // thread owns M entries tid + 256 u
   for (int j0 = 0; j0 < Q_; j0 += 64) {
     __syncthreads();
-    {   // B chunk: thread per (column, 8 rows of B); each A entry read by 4 threads
-      const int jj = tid & 63, a0 = (tid >> 6) * 8, j = j0 + jj;
-      double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      if (j < Q_)
-        for (int i = 0; i < P_; ++i) {
-          const double x = A(i, j);
+    {   // B chunk: thread per (column, quarter of the rows), all LW rows of B in
+        // registers; each A entry read once, the quarters summed in smem
+      for (int t = tid; t < 32 * 65; t += 256) Bc[t] = 0.0;
+      __syncthreads();
+      const int jj = tid & 63, ig = tid >> 6, j = j0 + jj;
+      if (j < Q_) {
+        double v[LW];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = fma(Y[i * 33 + a0 + u], x, v[u]);
+        for (int u = 0; u < LW; ++u) v[u] = 0.0;
+        const int c = Cc[j];
+        const int tc = tri(c);
+        for (int i = ig; i < P_; i += 4) {
+          const int r = R[i];
+          const double x = r >= c ? psi[tri(r) + c] : psi[tc + r];
+          const double* yr = Y + i * 33;
+#pragma unroll
+          for (int u = 0; u < LW; ++u) v[u] = fma(yr[u], x, v[u]);
         }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) Bc[(a0 + u) * 65 + jj] = (a0 + u < L) ? v[u] : 0.0;
-    }    __syncthreads();
+        for (int u = 0; u < LW; ++u)
+          if (u < L) atomicAdd(Bc + u * 65 + jj, v[u]);
+      }
+    }
+    __syncthreads();
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int e = tid + 256 * u, a = e >> 5, b = e & 31;
@@ -2591,14 +2621,31 @@ __global__ void __launch_bounds__(256, 3) compress_kernel(DevPlan p, const DevUp
   // ---- pass 3: A_k = Q (C D) with D = L_SS^-1 B_S, per 64-column chunk ----
   double* Ec = red + 64;                  // [32][65]
   for (int j0 = 0; j0 < Q_; j0 += 64) {
-    for (int t = tid; t < 32 * 64; t += 256) {
-      const int u = t >> 6, jj = t & 63, j = j0 + jj;
-      double v = 0.0;
-      if (u < kk && j < Q_) {
-        const int a = s_piv[u];
-        for (int i = 0; i < P_; ++i) v = fma(Y[i * 33 + a], A(i, j), v);   // B[a][j]
+    for (int t = tid; t < 32 * 65; t += 256) Bc[t] = 0.0;     // B_S rows (pivot order)
+    __syncthreads();
+    {
+      const int jj = tid & 63, ig = tid >> 6, j = j0 + jj;
+      if (j < Q_) {
+        double v[LW];
+#pragma unroll
+        for (int u = 0; u < LW; ++u) v[u] = 0.0;
+        const int c = Cc[j];
+        const int tc = tri(c);
+        int pvt[LW];
+#pragma unroll
+        for (int u = 0; u < LW; ++u) pvt[u] = u < kk ? s_piv[u] : 0;
+        for (int i = ig; i < P_; i += 4) {
+          const int r = R[i];
+          const double x = r >= c ? psi[tri(r) + c] : psi[tc + r];
+          const double* yr = Y + i * 33;
+#pragma unroll
+          for (int u = 0; u < LW; ++u)
+            if (u < kk) v[u] = fma(yr[pvt[u]], x, v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < LW; ++u)
+          if (u < kk) atomicAdd(Bc + u * 65 + jj, v[u]);
       }
-      Bc[u * 65 + jj] = v;
     }
     __syncthreads();
     for (int jj = tid; jj < 64; jj += 256) {      // forward substitution with L_SS
@@ -2636,10 +2683,22 @@ cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_n
   if (e != cudaSuccess) return e;
   if (nblk == 0) return cudaSuccess;
   const size_t smem = sizeof(double) * (size_t(pmax) * 33 + 2 * 32 * kLdd + 2 * 32 * 65 + 64) + 64;
-  e = cudaFuncSetAttribute(compress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
-  compress_kernel<<<dim3(B, nblk), 256, smem, s>>>(p, nodes_dev, blk0);
-  return cudaGetLastError();
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e2 != cudaSuccess) return e2;
+    kern<<<dim3(B, nblk), 256, smem, s>>>(p, nodes_dev, blk0);
+    return cudaGetLastError();
+  };
+  // levels of small blocks (<= 64 rows) are latency-bound: three CTAs per SM (80
+  // registers) beat the spill-free two (measured on C5 depths 10-11)
+  if (pmax <= 64) {
+    if (p.lr_l <= 16) return go(compress_kernel<16, 3>);
+    if (p.lr_l <= 24) return go(compress_kernel<24, 3>);
+    return go(compress_kernel<32, 3>);
+  }
+  if (p.lr_l <= 16) return go(compress_kernel<16, 2>);
+  if (p.lr_l <= 24) return go(compress_kernel<24, 2>);
+  return go(compress_kernel<32, 2>);
 }
 
 cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_kng,
