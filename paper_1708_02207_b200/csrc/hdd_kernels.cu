@@ -2011,22 +2011,24 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
 // -- tier L: panel in HBM ----------------------------------------------------
 // smem: F phases (L scratch / LiT / Xc / Lt) and the epilogue's 2 x (A, B) chunks of
 // 32 x kLds share the front region; the son maps and column plan follow it.
-#ifndef HDD_LL_WIDTH
-#define HDD_LL_WIDTH 64
-#endif
-// left-looking elimination: column chunks of kLW, staged rows per step kLH
-constexpr int kLW = HDD_LL_WIDTH, kLWs = kLW + 8, kLH = 16;
-constexpr size_t kLLStream = 2 * size_t(kLH) * (kLdd + kLWs);          // 2 x (A chunk | B chunk)
-constexpr size_t kLLRegion = 2 * 32 * kLdd + (kLLStream > size_t(32 * kLWs) ? kLLStream : size_t(32 * kLWs));
-constexpr size_t kLRegion0 = (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) > (4 * kEC * kLds)
-                                 ? (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) : (4 * kEC * kLds);
-constexpr size_t kLRegion = kLRegion0 > kLLRegion ? kLRegion0 : kLLRegion;
+// left-looking elimination: column chunks of LW (64, or 128 for the 2-CTA/SM variant),
+// staged rows per step kLH
+constexpr int kLH = 16;
+__host__ __device__ constexpr size_t l_region(int lw) {
+  const size_t lws = size_t(lw) + 8;
+  const size_t stream = 2 * size_t(kLH) * (kLdd + lws);                 // 2 x (A chunk | B chunk)
+  const size_t ll = 2 * 32 * kLdd + (stream > 32 * lws ? stream : 32 * lws);
+  const size_t r0 = (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) > (4 * kEC * kLds)
+                        ? (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) : (4 * kEC * kLds);
+  return r0 > ll ? r0 : ll;
+}
+constexpr size_t kLRegion = l_region(64);
 size_t merge_l_smem_bytes(int K, int nc) {
   const size_t ints = (size_t(2 * K + 3 * nc) + 1) & ~size_t(1);
   return sizeof(double) * (kLRegion + ints / 2 + 2 * size_t(nc)) + 1024;
 }
 
-template <int MINB>
+template <int MINB, int LW>
 __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
                                                           double* __restrict__ ws, int64_t ws_stride, int slot) {
   extern __shared__ __align__(16) double sm[];
@@ -2045,7 +2047,7 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
   __shared__ int s_bad;
   MergeCtx mc = merge_ctx(p, U, s);
   {   // son maps and column plan in smem (the gathers' first hop)
-    int32_t* gms = reinterpret_cast<int32_t*>(sm + kLRegion);
+    int32_t* gms = reinterpret_cast<int32_t*>(sm + l_region(LW));
     int32_t* cis = gms + 2 * U.K;
     double* ccs = reinterpret_cast<double*>(gms + ((2 * U.K + 3 * nc + 1) & ~1));
     for (int t = tid; t < 2 * U.K; t += 256) gms[t] = __ldg(mc.gm + t);
@@ -2142,6 +2144,7 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
     double* LsB = sm;                        // [32][kLdd] factor scratch
     double* LiB = sm + 32 * kLdd;            // [32][kLdd] L_bb^-1 (transposed)
     double* St = sm + 2 * 32 * kLdd;         // stream buffers / T tile [32][kLWs]
+    constexpr int kLW = LW, kLWs = LW + 8;
     constexpr int SB = kLH * (kLdd + kLWs);
     constexpr int FN = kLW / 32;
     const int gq = lane & 3, gr = lane >> 2;
@@ -2276,14 +2279,17 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
   } else {
     // 3 CTAs/SM (80 registers, some spills) pays when the launch has enough CTAs to
     // fill them and the panel region fits three per SM (measured: C4 depths 3-5 -12 %)
+    // (the 2-CTA/SM variant has the smem for 128-column elimination chunks: twice the
+    // DMMA work per staged A operand, measured -18 % on the C5 root)
     if (int64_t(n_nodes) * B >= 148 * 3 * 2 && smem <= 74 * 1024) {
-      e = cudaFuncSetAttribute(merge_l_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      e = cudaFuncSetAttribute(merge_l_kernel<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
-      merge_l_kernel<3><<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride, slot);
+      merge_l_kernel<3, 64><<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride, slot);
     } else {
-      e = cudaFuncSetAttribute(merge_l_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      const size_t sm2 = smem + sizeof(double) * (l_region(128) - kLRegion);
+      e = cudaFuncSetAttribute(merge_l_kernel<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2));
       if (e != cudaSuccess) return e;
-      merge_l_kernel<2><<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride, slot);
+      merge_l_kernel<2, 128><<<grid, 256, sm2, s>>>(p, nodes_dev, ws, ws_stride, slot);
     }
   }
   return cudaGetLastError();
