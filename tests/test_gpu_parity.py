@@ -306,6 +306,21 @@ def test_lowrank_storage_within_truncation_tolerance(torch_cuda, golden):
     assert errs[2] <= 1e-8
 
 
+@pytest.mark.parametrize("k_max", [8, 24])
+def test_lowrank_sketch_widths(torch_cuda, golden, k_max):
+    """The compress kernel is instantiated per sketch width l = k_max + 8 (16 / 24 / 32
+    columns); the other two widths against the dense path and the reference at
+    eps = 1e-6 (a tighter rank cap keeps more blocks dense, never less accurate)."""
+    g = golden("cfg_C3")
+    Z = g["Z"]
+    dense_S = hb.forward_functionals_batch(configs.make_problem("C3"), Z)
+    pr = configs.make_problem("C3", compression=hb.ToleranceSpec(1e-6, k_max, 32))
+    S = hb.forward_functionals_batch(pr, Z)
+    ll = hb.log_likelihood_batch(pr, Z)
+    assert 0.0 < rel(S, dense_S) <= 1e-5
+    assert np.max(np.abs(ll - g["ll"]) / np.abs(g["ll"])) <= 1e-4
+
+
 def test_c5_lowrank_config_matches_reference(torch_cuda, golden):
     """C5 with the BASELINE ToleranceSpec (eps 1e-6, k <= 16, leaf block 32).
     The truncation error grows with the level (reference: 9e-8 at L5 ... 1.6e-6
