@@ -430,9 +430,18 @@ static int setup_device(HddPlan* pl, int max_batch) {
   }
   pl->leaf_smem = leaf_smem_bytes(P.leaf_cols <= 2 ? 2 : (P.leaf_cols <= 4 ? 4 : 8));
   {
+    // kernels one forward sub-batch launches (run_sub_batch): kappa, one leaf launch per
+    // column class, per depth one merge (+ psi_norm and compress with low-rank blocks),
+    // per depth one top-down solve in primal mode, finalize
     int ncls = 0;
     for (int c = 0; c < 3; ++c) ncls += D.leaf_class_count[c] > 0;
-    pl->n_launches = 2 + ncls + (2 + P.mode) * int(P.upper_by_depth.size());
+    int n = 2 + ncls;
+    for (size_t dep = 0; dep < P.upper_by_depth.size(); ++dep) {
+      if (P.upper_by_depth[dep].empty()) continue;
+      n += 1 + (D.mode == 1 ? 1 : 0);
+      if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0) n += 2;
+    }
+    pl->n_launches = n;
   }
   return HDD_OK;
 }
