@@ -43,6 +43,13 @@ struct HddPlan {
   double* d_ll = nullptr;
   int64_t io_cap = 0;
   int n_launches = 0;
+  // CUDA graph of one forward sub-batch (captured on the plan's stream, replayed on the
+  // caller's); keyed by the batch size and the caller's buffers
+  cudaGraphExec_t graph = nullptr;
+  const double* g_Z = nullptr;
+  double* g_S = nullptr;
+  double* g_ll = nullptr;
+  int g_B = 0;
 };
 
 static HddError g_create_err{};
@@ -494,6 +501,7 @@ int hdd_plan_destroy(HddPlan* pl) {
     if (pl->d_Z) cudaFree(pl->d_Z);
     if (pl->d_S) cudaFree(pl->d_S);
     if (pl->d_ll) cudaFree(pl->d_ll);
+    if (pl->graph) cudaGraphExecDestroy(pl->graph);
     if (pl->stream) cudaStreamDestroy(pl->stream);
   }
   delete pl;
@@ -559,6 +567,35 @@ int hdd_forward_batch(HddPlan* pl, const double* Z, int64_t B, double* S, double
   CU(cudaSetDevice(pl->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
   const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
+  static const bool no_graph = [] { const char* v = std::getenv("HDD_NO_GRAPH"); return v && v[0] == '1'; }();
+  if (B <= pl->bcap && !no_graph) {
+    // one sub-batch: replay the captured launch sequence (kappa, leaf classes, one merge
+    // per depth, ..., finalize) as a single graph launch
+    if (!(pl->graph && pl->g_Z == Z && pl->g_S == S && pl->g_ll == ll && pl->g_B == int(B))) {
+      if (pl->graph) {
+        cudaGraphExecDestroy(pl->graph);
+        pl->graph = nullptr;
+      }
+      CU(cudaStreamBeginCapture(pl->stream, cudaStreamCaptureModeThreadLocal));
+      const int rc = run_sub_batch(pl, Z, int(B), S, ll, pl->stream);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(pl->stream, &g);
+      if (rc != HDD_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      CU(ce);
+      const cudaError_t ie = cudaGraphInstantiate(&pl->graph, g, 0);
+      cudaGraphDestroy(g);
+      CU(ie);
+      pl->g_Z = Z;
+      pl->g_S = S;
+      pl->g_ll = ll;
+      pl->g_B = int(B);
+    }
+    CU(cudaGraphLaunch(pl->graph, st));
+    return check_device_error(pl, st, 0);
+  }
   int64_t done = 0;
   while (done < B) {
     int b = int(std::min<int64_t>(pl->bcap, B - done));

@@ -200,6 +200,24 @@ def test_determinism_and_batch_invariance(torch_cuda):
     assert np.array_equal(a[::9], d)
 
 
+def test_graph_replay_matches_stream_launches(torch_cuda):
+    """A batch that fits one sub-batch replays a captured CUDA graph of the launch
+    sequence (re-captured when the batch size or the caller's buffers change); it is
+    bitwise identical to the per-sub-batch stream launches of a smaller-capacity plan."""
+    import torch
+    cfg = configs.CONFIGS["C2"]
+    Z = torch.from_numpy(configs.draw_Z(cfg)[:24].copy()).cuda()
+    p_graph = configs.make_problem("C2")
+    p_stream = configs.make_problem("C2", max_batch=5)
+    ref = hb.log_likelihood_batch(p_stream, Z).cpu().numpy()
+    for _ in range(2):                       # fresh output tensors: new pointers each call
+        assert np.array_equal(hb.log_likelihood_batch(p_graph, Z).cpu().numpy(), ref)
+    assert np.array_equal(hb.log_likelihood_batch(p_graph, Z[:11]).cpu().numpy(), ref[:11])
+    S_g = hb.forward_functionals_batch(p_graph, Z).cpu().numpy()
+    S_s = hb.forward_functionals_batch(p_stream, Z).cpu().numpy()
+    assert np.array_equal(S_g, S_s)
+
+
 def test_full_c2_batch_properties(torch_cuda):
     """Full BASELINE C2 batch: finite ll, spot rows against the direct solve."""
     torch = torch_cuda
