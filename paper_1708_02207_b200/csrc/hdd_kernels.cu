@@ -530,18 +530,6 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 #pragma unroll
     for (int l = 0; l < ng; ++l) a[l] = (act && l <= i) ? P[i * W + l] : (l == i ? 1.0 : 0.0);
     bool bad = false;
-#ifdef HDD_OLD_CHOL
-#pragma unroll
-    for (int j = 0; j < ng; ++j) {
-      const double dj = __shfl_sync(0xffffffffu, a[j], j, LPN);
-      bad |= !(dj > 0.0);
-      const double il = rsqrt_nr(dj);
-      const double lij = a[j] * il;
-#pragma unroll
-      for (int l = j + 1; l < ng; ++l) a[l] = fma(-lij, __shfl_sync(0xffffffffu, lij, l, LPN), a[l]);
-      a[j] = i == j ? il : lij;
-    }
-#else
     // unscaled (LDL^T-ordered) elimination: a_il -= a_ij a_lj / d_j.  The column
     // broadcast a_lj does not wait for the pivot's reciprocal, so the serial chain per
     // step is shuffle -> rcp -> mul -> fma; the sqrt scaling of column j runs beside it
@@ -556,7 +544,6 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
       const double il = rsqrt_nr(dj);
       a[j] = i == j ? il : a[j] * il;
     }
-#endif
     if (act) {
 #pragma unroll
       for (int l = 0; l < ng; ++l)
@@ -1229,7 +1216,6 @@ __device__ __forceinline__ void warp_gemm_tn(double (&acc)[FM][FN][2], const dou
 }
 
 constexpr int kLB = 32;     // elimination block (rows)
-constexpr int kLC = 64;     // column chunk
 constexpr int kLds = 72;    // smem leading dim for 64-wide tiles (= 8 mod 16)
 constexpr int kLdd = 40;    // smem leading dim for 32-wide tiles (= 8 mod 16)
 
@@ -1697,18 +1683,6 @@ __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const doubl
       double* Ea = E + buf * 2 * kEC * kLds;
       double* Eb = Ea + kEC * kLds;
       const int g0 = c * kEC;
-#ifdef HDD_STAGE8
-      for (int tt = tid; tt < kEC * 64; tt += 256) {
-        const int g = tt >> 6, i = tt & 63;
-        const int aa = a0 + i;
-        if (aa < k) cp_async8(Ea + g * kLds + i, P + int64_t(g0 + g) * ldp + aa);
-        else Ea[g * kLds + i] = 0.0;
-        const int bb = b0 + i;
-        const int col = bb < k ? bb : (bb < ow ? Kp + (bb - k) : -1);
-        if (col >= 0) cp_async8(Eb + g * kLds + i, P + int64_t(g0 + g) * ldp + col);
-        else Eb[g * kLds + i] = 0.0;
-      }
-#else
       // column pairs as 16-byte copies: the panel rows are 16-byte aligned (even ldp),
       // A21 pairs start at even columns, and the R block's pairs at Kp + (even - k),
       // Kp - k = ngp even; only the pair straddling k (odd k) goes element-wise
@@ -1737,7 +1711,6 @@ __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const doubl
           }
         }
       }
-#endif
       cp_async_commit();
     };
     __syncthreads();
@@ -2000,11 +1973,7 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
     out[tk + k * nc + c] = v;
   }
   MERGE_TICK(4);
-  #ifdef HDD_FAST_ALL
-  schur_epilogue<true, true, MINB <= 2>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
-#else
   schur_epilogue<true, MINB <= 2, MINB <= 2>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
-#endif
   MERGE_TICK(5);
 }
 
@@ -2018,9 +1987,8 @@ __host__ __device__ constexpr size_t l_region(int lw) {
   const size_t lws = size_t(lw) + 8;
   const size_t stream = 2 * size_t(kLH) * (kLdd + lws);                 // 2 x (A chunk | B chunk)
   const size_t ll = 2 * 32 * kLdd + (stream > 32 * lws ? stream : 32 * lws);
-  const size_t r0 = (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) > (4 * kEC * kLds)
-                        ? (2 * 32 * kLdd + 32 * kLds + 32 * kLdd) : (4 * kEC * kLds);
-  return r0 > ll ? r0 : ll;
+  const size_t epi = 4 * kEC * kLds;                                     // Schur epilogue chunks
+  return epi > ll ? epi : ll;
 }
 constexpr size_t kLRegion = l_region(64);
 size_t merge_l_smem_bytes(int K, int nc) {
@@ -2041,9 +2009,6 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
   const int Kp = k + ngp;
   const int W = Kp + nc;
   double* P = ws + int64_t(blockIdx.y) * ws_stride * p.bcap + int64_t(s) * ws_stride;
-  double* LiT = sm + 32 * kLdd;           // [32][kLdd]
-  double* Xc = LiT + 32 * kLdd;           // [32][kLds]
-  double* Lt = Xc + 32 * kLds;            // [32][kLdd]
   __shared__ int s_bad;
   MergeCtx mc = merge_ctx(p, U, s);
   {   // son maps and column plan in smem (the gathers' first hop)
@@ -2067,70 +2032,6 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
   if (tid == 0) s_bad = 0;
   __syncthreads();
   MERGE_TICK(2);
-#ifdef HDD_RIGHT_LOOKING
-  for (int r0 = 0; r0 < ngp; r0 += kLB) {
-    if (warp == 0) factor_block32(P + int64_t(r0) * ldp + k + r0, ldp, sm, LiT, &s_bad);
-    __syncthreads();
-    // F2: X_b = L^-1 P_b in 64-column chunks (the block's own A22 columns give L_bb^T)
-    for (int c0 = 0; c0 < W; c0 += kLC) {
-      if (c0 >= k && c0 + kLC <= k + r0) continue;
-      for (int t = tid; t < 32 * kLC; t += 256) {
-        const int i = t >> 6, j = t & 63;
-        const int col = c0 + j;
-        Xc[i * kLds + j] = col < W ? P[int64_t(r0 + i) * ldp + col] : 0.0;
-      }
-      __syncthreads();
-      const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * 16;
-      double acc[2][2][2] = {};
-      warp_gemm_tn<2, 2>(acc, LiT, kLdd, m0, Xc, kLds, n0, 32);
-      const int gq = lane & 3, gr = lane >> 2;
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int row = m0 + 8 * i + gr, col = c0 + n0 + 8 * j + 2 * gq + e;
-            if (col < W) P[int64_t(r0 + row) * ldp + col] = acc[i][j][e];
-          }
-      __syncthreads();
-    }
-    // F3: trailing rows
-    if (r0 + kLB < ngp) {
-      for (int c0 = 0; c0 < W; c0 += kLC) {
-        if (c0 >= k && c0 + kLC <= k + r0 + kLB) continue;
-        for (int t = tid; t < 32 * kLC; t += 256) {
-          const int i = t >> 6, j = t & 63;
-          const int col = c0 + j;
-          Xc[i * kLds + j] = col < W ? P[int64_t(r0 + i) * ldp + col] : 0.0;
-        }
-        for (int rt = r0 + kLB; rt < ngp; rt += kLB) {
-          if (c0 >= k && c0 + kLC <= k + rt) continue;   // A22 columns left of the tile rows
-          for (int t = tid; t < 32 * 32; t += 256) {
-            const int h = t >> 5, r = t & 31;
-            Lt[h * kLdd + r] = P[int64_t(r0 + h) * ldp + k + rt + r];
-          }
-          __syncthreads();
-          const int m0 = (warp >> 2) * 16, n0 = (warp & 3) * 16;
-          double acc[2][2][2] = {};
-          warp_gemm_tn<2, 2>(acc, Lt, kLdd, m0, Xc, kLds, n0, 32);
-          const int gq = lane & 3, gr = lane >> 2;
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int row = rt + m0 + 8 * i + gr, col = c0 + n0 + 8 * j + 2 * gq + e;
-                if (col < W) P[int64_t(row) * ldp + col] -= acc[i][j][e];
-              }
-          __syncthreads();
-        }
-      }
-    }
-    __syncthreads();
-  }
-#else
   // Left-looking blocked elimination.  For each 32-row block r0 and each chunk of
   // kLW columns c of C(r0) = [k + r0, W) u [0, k) (the diagonal block's own A22
   // columns first, then the rest of A22, R_gamma, then A21):
@@ -2233,7 +2134,6 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
     }
     __syncthreads();
   }
-#endif
   MERGE_TICK(3);
   if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
   if (p.mode == 1) store_factors(p, U, s, P, ldp, Kp, false, tid, 256);
