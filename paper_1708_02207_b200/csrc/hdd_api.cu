@@ -44,12 +44,15 @@ struct HddPlan {
   int64_t io_cap = 0;
   int n_launches = 0;
   // CUDA graph of one forward sub-batch (captured on the plan's stream, replayed on the
-  // caller's); keyed by the batch size and the caller's buffers
+  // caller's), keyed by the batch size and the caller's buffers; captured once the same
+  // key is seen on two consecutive calls (callers that allocate fresh buffers per call
+  // keep the direct launches and never pay a capture)
   cudaGraphExec_t graph = nullptr;
   const double* g_Z = nullptr;
   double* g_S = nullptr;
   double* g_ll = nullptr;
   int g_B = 0;
+  bool g_seen = false;
 };
 
 static HddError g_create_err{};
@@ -569,13 +572,25 @@ int hdd_forward_batch(HddPlan* pl, const double* Z, int64_t B, double* S, double
   const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
   static const bool no_graph = [] { const char* v = std::getenv("HDD_NO_GRAPH"); return v && v[0] == '1'; }();
   if (B <= pl->bcap && !no_graph) {
-    // one sub-batch: replay the captured launch sequence (kappa, leaf classes, one merge
-    // per depth, ..., finalize) as a single graph launch
-    if (!(pl->graph && pl->g_Z == Z && pl->g_S == S && pl->g_ll == ll && pl->g_B == int(B))) {
+    const bool same = pl->g_seen && pl->g_Z == Z && pl->g_S == S && pl->g_ll == ll && pl->g_B == int(B);
+    if (!same) {
+      // new key: direct launches this time, remember the key
       if (pl->graph) {
         cudaGraphExecDestroy(pl->graph);
         pl->graph = nullptr;
       }
+      pl->g_Z = Z;
+      pl->g_S = S;
+      pl->g_ll = ll;
+      pl->g_B = int(B);
+      pl->g_seen = true;
+      const int rc = run_sub_batch(pl, Z, int(B), S, ll, st);
+      if (rc != HDD_OK) return rc;
+      return check_device_error(pl, st, 0);
+    }
+    if (!pl->graph) {
+      // second call with the same buffers: capture the launch sequence (kappa, leaf
+      // classes, one merge per depth, ..., finalize) once, replay it from now on
       CU(cudaStreamBeginCapture(pl->stream, cudaStreamCaptureModeThreadLocal));
       const int rc = run_sub_batch(pl, Z, int(B), S, ll, pl->stream);
       cudaGraph_t g = nullptr;
@@ -588,10 +603,6 @@ int hdd_forward_batch(HddPlan* pl, const double* Z, int64_t B, double* S, double
       const cudaError_t ie = cudaGraphInstantiate(&pl->graph, g, 0);
       cudaGraphDestroy(g);
       CU(ie);
-      pl->g_Z = Z;
-      pl->g_S = S;
-      pl->g_ll = ll;
-      pl->g_B = int(B);
     }
     CU(cudaGraphLaunch(pl->graph, st));
     return check_device_error(pl, st, 0);

@@ -201,17 +201,25 @@ def test_determinism_and_batch_invariance(torch_cuda):
 
 
 def test_graph_replay_matches_stream_launches(torch_cuda):
-    """A batch that fits one sub-batch replays a captured CUDA graph of the launch
-    sequence (re-captured when the batch size or the caller's buffers change); it is
-    bitwise identical to the per-sub-batch stream launches of a smaller-capacity plan."""
+    """A batch that fits one sub-batch is captured as a CUDA graph of the launch
+    sequence once the same batch size and buffers come twice in a row, and replayed
+    after that; direct launches, the capture call and the replays are all bitwise
+    identical to the per-sub-batch stream launches of a smaller-capacity plan."""
     import torch
     cfg = configs.CONFIGS["C2"]
     Z = torch.from_numpy(configs.draw_Z(cfg)[:24].copy()).cuda()
     p_graph = configs.make_problem("C2")
     p_stream = configs.make_problem("C2", max_batch=5)
     ref = hb.log_likelihood_batch(p_stream, Z).cpu().numpy()
-    for _ in range(2):                       # fresh output tensors: new pointers each call
+    for _ in range(2):                       # fresh output tensors (pointers may or may not repeat)
         assert np.array_equal(hb.log_likelihood_batch(p_graph, Z).cpu().numpy(), ref)
+    ll = torch.empty(24, dtype=torch.float64, device="cuda")
+    for _ in range(4):                       # fixed buffers: direct, capture, replay, replay
+        ll.fill_(0.0)
+        p_graph.plan().check(p_graph.plan().lib.hdd_forward_batch(
+            p_graph.plan().handle, C.c_void_p(Z.data_ptr()), 24, None, C.c_void_p(ll.data_ptr()), None))
+        torch.cuda.synchronize()
+        assert np.array_equal(ll.cpu().numpy(), ref)
     assert np.array_equal(hb.log_likelihood_batch(p_graph, Z[:11]).cpu().numpy(), ref[:11])
     S_g = hb.forward_functionals_batch(p_graph, Z).cpu().numpy()
     S_s = hb.forward_functionals_batch(p_stream, Z).cpu().numpy()
