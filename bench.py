@@ -378,7 +378,8 @@ def main():
                          "excluded), forked workers x 1 BLAS thread, oracle/hdd_port.py",
                "max_rel_ll_diff_vs_gpu": float(np.max(np.abs(ll_cpu - ll_gpu) / np.abs(ll_cpu)))}
 
-    launches = args.steps * info.n_kernels_per_batch * math.ceil(B / info.max_batch)
+    # forward kernels per sub-batch + the posterior-weights kernel per step
+    launches = args.steps * (info.n_kernels_per_batch * math.ceil(B / info.max_batch) + 1)
     # measured DRAM bytes per launch of the dominant kernel (ncu --set full capture,
     # profiles/r01_ncu_full_leaf_v4_C2.csv: 23.6 KB per leaf-sample) scaled to this launch;
     # the leaf's binding resource is shared-memory bandwidth (same capture)

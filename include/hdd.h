@@ -175,6 +175,16 @@ int hdd_solve_batch_host(HddPlan* plan, const double* Z_host, int64_t B, double*
 int hdd_kappa_batch(HddPlan* plan, const double* Z_dev, int64_t B,
                     double* kappa_dev, void* stream);
 
+/* Posterior weights of a batch of log-likelihoods, on the device (the pieces of the
+ * reference posterior_grid, bayes.py:325-330, for prior draws): joint = ll (+ log_prior
+ * when non-NULL), lse = logsumexp(joint), w = exp(joint - lse), idx = the first index
+ * of max(joint) (numpy argmax tie rule).  Device pointers on the current device; one
+ * kernel launch on `stream`, deterministic (fixed reduction order), so every rank of an
+ * all-gathered batch gets bitwise-identical weights.  HDD_ERR_USAGE for n <= 0 or NULL
+ * ll / w / idx / lse. */
+int hdd_posterior_weights(const double* ll_dev, const double* log_prior_dev, int64_t n, double* w_dev,
+                          int64_t* idx_dev, double* lse_dev, void* stream);
+
 int hdd_last_error(const HddPlan* plan, HddError* out);
 /* Error of the last failed hdd_plan_create (no plan exists then). */
 int hdd_create_error(HddError* out);

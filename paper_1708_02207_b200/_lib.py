@@ -83,6 +83,8 @@ EXPORTS = {
     "hdd_solve_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "hdd_solve_batch_host": (C.c_int, [C.c_void_p, _f64p, C.c_int64, _f64p]),
     "hdd_kappa_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "hdd_posterior_weights": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p]),
     "hdd_last_error": (C.c_int, [C.c_void_p, C.POINTER(HddError)]),
     "hdd_create_error": (C.c_int, [C.POINTER(HddError)]),
     "hdd_plan_info": (C.c_int, [C.c_void_p, C.POINTER(HddPlanInfo)]),

@@ -723,6 +723,14 @@ int hdd_solve_batch_host(HddPlan* pl, const double* Zh, int64_t B, double* Uh) {
   return rc;
 }
 
+int hdd_posterior_weights(const double* ll, const double* lp, int64_t n, double* w, int64_t* idx, double* lse,
+                          void* stream) {
+  if (n <= 0 || !ll || !w || !idx || !lse) return HDD_ERR_USAGE;
+  if (launch_posterior(ll, lp, n, w, idx, lse, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return HDD_ERR_CUDA;
+  return HDD_OK;
+}
+
 int hdd_kappa_batch(HddPlan* pl, const double* Z, int64_t B, double* kappa, void* stream) {
   if (!pl) return HDD_ERR_USAGE;
   if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan");

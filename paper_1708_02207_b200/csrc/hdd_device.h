@@ -115,6 +115,8 @@ cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_n
                             int pmax, cudaStream_t s);
 cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_ng, cudaStream_t s);
 cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cudaStream_t s);
+cudaError_t launch_posterior(const double* ll, const double* lp, int64_t n, double* w, int64_t* idx, double* lse,
+                             cudaStream_t s);
 cudaError_t launch_leaf_solve(const DevPlan& p, int B, double* U, int64_t n_nodes, cudaStream_t s);
 size_t leaf_smem_bytes(int leaf_cols);
 int upload_leaf_template();

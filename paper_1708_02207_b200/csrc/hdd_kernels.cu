@@ -2662,6 +2662,65 @@ __global__ void finalize_kernel(DevPlan p, int B, double* __restrict__ S, double
   if (lane == 0 && ll) ll[s] = p.y ? (-0.5 * acc - p.ll_const) : 0.0;
 }
 
+// ---------------------------------------------------------------------------
+// Posterior weights of a gathered batch (a13): one CTA, two passes over the batch
+// (max / first argmax, then sum exp(joint - max)), fixed reduction order.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) posterior_kernel(const double* __restrict__ ll,
+                                                         const double* __restrict__ lp, int64_t n,
+                                                         double* __restrict__ w, int64_t* __restrict__ idx,
+                                                         double* __restrict__ lse) {
+  __shared__ double s_v[32];
+  __shared__ int64_t s_i[32];
+  __shared__ double s_mx, s_lse;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  auto joint = [&](int64_t t) { return lp ? ll[t] + lp[t] : ll[t]; };
+  double mx = -INFINITY;
+  int64_t mi = INT64_MAX;
+  for (int64_t t = tid; t < n; t += blockDim.x) {
+    const double v = joint(t);
+    if (v > mx || (v == mx && t < mi)) { mx = v; mi = t; }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, mx, off);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, mi, off);
+    if (ov > mx || (ov == mx && oi < mi)) { mx = ov; mi = oi; }
+  }
+  if (lane == 0) { s_v[warp] = mx; s_i[warp] = mi; }
+  __syncthreads();
+  if (tid == 0) {
+    double m = s_v[0];
+    int64_t i = s_i[0];
+    for (int q = 1; q < nw; ++q)
+      if (s_v[q] > m || (s_v[q] == m && s_i[q] < i)) { m = s_v[q]; i = s_i[q]; }
+    s_mx = m;
+    *idx = i;
+  }
+  __syncthreads();
+  const double m = s_mx;
+  double sum = 0.0;
+  for (int64_t t = tid; t < n; t += blockDim.x) sum += exp(joint(t) - m);
+  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+  __syncthreads();
+  if (lane == 0) s_v[warp] = sum;
+  __syncthreads();
+  if (tid == 0) {
+    double tot = 0.0;
+    for (int q = 0; q < nw; ++q) tot += s_v[q];
+    s_lse = m + log(tot);
+    *lse = s_lse;
+  }
+  __syncthreads();
+  const double l = s_lse;
+  for (int64_t t = tid; t < n; t += blockDim.x) w[t] = exp(joint(t) - l);
+}
+
+cudaError_t launch_posterior(const double* ll, const double* lp, int64_t n, double* w, int64_t* idx, double* lse,
+                             cudaStream_t s) {
+  posterior_kernel<<<1, 1024, 0, s>>>(ll, lp, n, w, idx, lse);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cudaStream_t s) {
   finalize_kernel<<<(B + 7) / 8, 256, 0, s>>>(p, B, S, ll);
   return cudaGetLastError();

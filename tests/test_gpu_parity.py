@@ -226,6 +226,30 @@ def test_graph_replay_matches_stream_launches(torch_cuda):
     assert np.array_equal(S_g, S_s)
 
 
+def test_posterior_weights_kernel_matches_host(torch_cuda):
+    """Native posterior weights (hdd_posterior_weights) against the host formulas of
+    the reference posterior_grid (bayes.py:325-330): weights and logsumexp to 1e-12,
+    argmax bit-exact with numpy's first-occurrence rule (ties planted), with and
+    without a log prior, at a size that spans many threads per lane."""
+    import torch
+    from paper_1708_02207_b200 import parallel
+    rng = np.random.default_rng(7)
+    for n in (1, 37, 70001):
+        ll = rng.normal(-50.0, 20.0, n)
+        if n > 40:
+            ll[[11, 29, n - 3]] = ll.max() + 1.5      # three-way tie: first index wins
+        for lp in (None, rng.normal(0.0, 1.0, n)):
+            w_h, i_h, lse_h = hb.posterior_weights(ll, lp)
+            w_d, i_d, lse_d = parallel.posterior_weights_device(
+                torch.from_numpy(ll).cuda(), None if lp is None else torch.from_numpy(lp).cuda())
+            assert int(i_d) == i_h
+            assert abs(float(lse_d) - lse_h) <= 1e-12 * abs(lse_h)
+            assert np.max(np.abs(w_d.cpu().numpy() - w_h)) <= 1e-12
+    a = parallel.posterior_weights_device(torch.from_numpy(ll).cuda())
+    b = parallel.posterior_weights_device(torch.from_numpy(ll).cuda())
+    assert torch.equal(a[0], b[0]) and float(a[2]) == float(b[2])     # deterministic
+
+
 def test_full_c2_batch_properties(torch_cuda):
     """Full BASELINE C2 batch: finite ll, spot rows against the direct solve."""
     torch = torch_cuda
