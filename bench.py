@@ -389,8 +389,8 @@ def main():
         traffic = {"bytes": 23.6e3 * B * ((1 << cfg.level) // 16) ** 2,
                    "source": "ncu dram__bytes_read+write, leaf2_kernel<2> C2: 1184 MB / (49 leaves x 1024)"}
         binding = {"resource": "instruction issue + shared-memory wavefronts (3 CTAs/SM, latency-bound per CTA)",
-                   "issue_active_pct": 59.0, "smem_wavefront_util_pct": 68.6, "dmma_pipe_pct": 11.7,
-                   "source": "profiles/r01_ncu_full_leaf_v10_C2.csv"}
+                   "issue_active_pct": 59.3, "smem_wavefront_util_pct": 68.7, "dmma_pipe_pct": 11.7,
+                   "source": "profiles/r01_ncu_full_leaf_v13_C2.csv"}
     line = {
         "metric": f"likelihood evals/s ({args.config}, {cfg.level}-level grid, n_z={cfg.n_z})",
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
