@@ -41,8 +41,15 @@ def timed(fn, reps):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--full", action="store_true",
+                    help="the BASELINE batch of every config (C3 8192, C4 65536, C5 16384; sub-batched), 1 rep")
     args = ap.parse_args()
-    for name, B, lowrank, kind in CASES:
+    cases = CASES
+    if args.full:
+        cases = [(n, configs.CONFIGS[n].batch, lr, "forward") for n, lr in
+                 (("C1", False), ("C2", False), ("C3", False), ("C4", False), ("C5", False), ("C5", True))]
+        args.reps = 1
+    for name, B, lowrank, kind in cases:
         cfg = configs.CONFIGS[name]
         prob = configs.make_problem(name, compression=lowrank)
         Z = torch.from_numpy(configs.draw_Z(cfg, batch=max(B, 1))[:B].copy()).cuda()
