@@ -1,23 +1,33 @@
 """Benchmark of the batched HDD likelihood (one JSON line on rank 0).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
-A step = one batched likelihood evaluation of the config's Z batch (C2:
-1024 samples of the 129x129-node problem) per GPU, followed by the NCCL
-all-gather of the log-likelihoods and the global posterior weights / argmax
-(weak scaling: every rank evaluates its own B rows).
+Workload (default C4, the BASELINE flagship): the 513x513-node problem, n_z = 32, 16
+subdomain means, the FIXED global batch of 65,536 Z rows sharded over the N GPUs
+(strong scaling: rank r evaluates rows parallel.shard_rows(65536, N, r)).  A step =
+one batched likelihood evaluation of every rank's rows, the NCCL all-gather of the
+log-likelihoods and the global posterior weights / argmax.
 
-* value      samples/s over all ranks, Z resident in HBM, CUDA events around
-             each step on the launching stream, L2 flushed (256 MiB memset)
-             between steps, max over ranks;
-* e2e        the same through the public Python API with pinned host Z:
-             H2D of Z and D2H of ll inside every timed step;
-* roofline   dominant kernel (largest share of the step): algorithmic FP64
-             flops / its average CUDA-event time,
-             against the measured FP64 DGEMM peak (profiles/fp64_peaks_r01.jsonl);
-* cpu_baseline  the oracle port of the reference HDD path (oracle/hdd_port.py)
-             on the host cores, forked workers x 1 BLAS thread, bounded sample.
-`--impl reference` times that same CPU path as the reference arm.
+* value      samples/s of the whole job (65,536 / the max-over-ranks step time), Z
+             resident in HBM, CUDA events around each step on the launching stream,
+             L2 flushed (256 MiB memset) between steps;
+* e2e        the same through the public API with HOST buffers (pinned numpy Z ->
+             log_likelihood_batch -> hdd_forward_batch_host: H2D of Z, D2H of ll
+             inside every timed step; sub-batch copies overlap compute);
+* roofline   the dominant kernel stage (largest share of the step, CUDA events per
+             stage over a timed pass): algorithmic FP64 flops (DESIGN.md "flop
+             accounting") / its time, against the measured FP64 DGEMM peak; `traffic`
+             comes from a committed ncu --set full capture of the same config and
+             stage (profiles/traffic.json) or is null;
+* per_config the other BASELINE configs on this GPU (C1, C2, C3 whole batches; C5 dense
+             and low-rank on bounded prefixes), CUDA-event timed;
+* cpu_baseline  the reference's CPU path on the host cores (rank 0, N = 1): the
+             installed reference `hddsolve` under baseline/_ref (C1-C3: its HDD
+             likelihood `bayes.log_likelihood`; C4/C5: its `oracle.direct_solve`,
+             the only reference path that reaches levels 9/10 in seconds — its HDD caps
+             the mesh at level 8), one forked worker per core x 1 BLAS thread; the
+             oracle port when baseline/_ref is absent.
+`--impl reference` times that CPU path as the reference arm.
 """
 from __future__ import annotations
 
@@ -37,6 +47,7 @@ sys.path.insert(0, str(ROOT))
 
 FP64_PEAK_TFLOPS = 35.46       # cuBLAS DGEMM 8192^3 sustained, profiles/fp64_peaks_r01.jsonl
 FP64_PEAK_SRC = "measured cuBLAS DGEMM sustained on this pool's B200 (profiles/fp64_peaks_r01.jsonl)"
+REF_DIR = ROOT / "baseline" / "_ref"
 
 
 def hbm_peak():
@@ -87,7 +98,7 @@ def node_flops(r, depth, N):
 def flops_split(level):
     """(leaf-kernel flops, merge flops per depth) per sample, 16x16 leaves."""
     N = 1 << level
-    dl = 2 * (level - 4)
+    dl = max(0, 2 * (level - 4))
     leaf = 0.0
     merge = {}
 
@@ -166,47 +177,96 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------
-def cpu_port_worker(args):
-    """Forked worker: oracle port of the reference HDD path on a few samples."""
-    idx, Z, level, obs, y, sigma, n_z = args
-    from threadpoolctl import threadpool_limits
-    from oracle import hdd_port
-    threadpool_limits(1)
-    port = _PORT["port"]
-    fo = _PORT["field"]
-    out = []
-    for z in Z:
-        s = port.forward(fo.kappa_values(z))
-        out.append(hdd_port.gaussian_ll(y, s, sigma))
-    return idx, out
+# the reference's CPU path (reported baseline and the --impl reference arm)
+# --------------------------------------------------------------------------
+_CPU = {}
 
 
-_PORT = {}
-
-
-def time_cpu_port(cfg_name, n_samples, n_workers):
-    """Returns (samples/s, cores, wall seconds, build seconds, ll)."""
-    import multiprocessing as mp
+def _cpu_setup(cfg_name):
+    """Build (once, before forking) the CPU evaluator of one config.  Returns a
+    description of the path."""
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    from oracle import fields, geometry, hdd_port
     from paper_1708_02207_b200 import configs
     cfg = configs.CONFIGS[cfg_name]
     obs = configs.observations(cfg)
     y, sigma = configs.observed_data(cfg)
+    _CPU.update(cfg=cfg, obs=obs, y=y, sigma=sigma)
+    if (REF_DIR / "hddsolve").is_dir():
+        sys.path.insert(0, str(REF_DIR))
+        import hddsolve as hs
+        from hddsolve import bayes as rb, oracle as ro
+        from oracle import fields, geometry
+        if cfg.level > hs.mesh.MAX_LEVEL:
+            hs.mesh.MAX_LEVEL = cfg.level          # the reference caps the mesh at level 8
+        mesh = hs.build_mesh(cfg.level)
+        fo = fields.SineKLField(geometry.Grid(cfg.level), cfg.n_z)
+
+        class KL:                                    # duck-typed param (bayes.py:183)
+            n_z = cfg.n_z
+
+            def kappa(self, z):
+                return hs.CoefficientField(fo.kappa_values(z))
+
+        if cfg.level <= 8:
+            tree = hs.build_tree(mesh)
+            model = rb.MeasurementModel(obs, sigma, y)
+            prob = rb.BayesProblem(tree, KL(), np.ones(mesh.n_nodes), np.zeros(4 * (mesh.m - 1)), model)
+            _CPU["fn"] = lambda z: rb.log_likelihood(prob, z)
+            return "reference", "hddsolve.bayes.log_likelihood (reference HDD functional path, baseline/_ref)"
+        param = KL()
+        rects = {}
+        from oracle.geometry import rect_of_node_id
+        for kind, ident in obs:
+            if kind == "mean":
+                r, _ = rect_of_node_id(cfg.level, ident)
+                h = mesh.h
+                rects[ident] = hs.Rect(r[0] * h, r[1] * h, r[2] * h, r[3] * h)
+        f1, g0 = np.ones(mesh.n_nodes), np.zeros(4 * (mesh.m - 1))
+
+        def fn(z):
+            u = ro.direct_solve(mesh, param.kappa(z), f1, g0)
+            s = np.array([ro.direct_mean(mesh, u, rects[i]) if k == "mean" else u[i] for k, i in obs])
+            return rb.gaussian_log_likelihood(y, s, sigma)
+
+        _CPU["fn"] = fn
+        return "reference", ("hddsolve.oracle.direct_solve + direct_mean (baseline/_ref; the reference HDD caps the "
+                             f"mesh at level 8 — MAX_LEVEL raised to {cfg.level} at run time — and takes ~136 s per "
+                             "level-9 sample, so its sparse-LU truth path is the fastest reference CPU path here)")
+    from oracle import direct, fields, geometry, hdd_port
+    grid = geometry.Grid(cfg.level)
+    fo = fields.SineKLField(grid, cfg.n_z)
+    if cfg.level <= 8:
+        port = hdd_port.HDDPort(cfg.level, obs)
+        _CPU["fn"] = lambda z: hdd_port.gaussian_ll(y, port.forward(fo.kappa_values(z)), sigma)
+        return "port", "oracle/hdd_port.py (restatement of the reference HDD functional path)"
+    from oracle import configs as ocfg
+
+    def fn(z):
+        return hdd_port.gaussian_ll(y, ocfg.observe(grid, direct.solve(grid, fo.kappa_values(z)), obs), sigma)
+
+    _CPU["fn"] = fn
+    return "port", "oracle/direct.py (restatement of reference oracle.direct_solve)"
+
+
+def _cpu_worker(Z):
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+    return [float(_CPU["fn"](z)) for z in Z]
+
+
+def time_cpu(Z, n_workers):
+    """(samples/s, wall s, ll) of the prepared CPU path on the rows of Z."""
+    import multiprocessing as mp
+    chunks = [c for c in np.array_split(np.arange(Z.shape[0]), n_workers) if len(c)]
     t0 = time.time()
-    _PORT["port"] = hdd_port.HDDPort(cfg.level, obs)
-    _PORT["field"] = fields.SineKLField(geometry.Grid(cfg.level), cfg.n_z)
-    build_s = time.time() - t0
-    Z = configs.draw_Z(cfg)[:n_samples]
-    chunks = np.array_split(np.arange(n_samples), n_workers)
-    ctx = mp.get_context("fork")
-    t0 = time.time()
-    with ctx.Pool(n_workers) as pool:
-        res = pool.map(cpu_port_worker, [(i, Z[c], cfg.level, obs, y, sigma, cfg.n_z)
-                                         for i, c in enumerate(chunks) if len(c)])
+    with mp.get_context("fork").Pool(len(chunks)) as pool:
+        res = pool.map(_cpu_worker, [Z[c] for c in chunks])
     wall = time.time() - t0
-    ll = np.concatenate([np.array(r[1]) for r in sorted(res)])
-    return n_samples / wall, n_workers, wall, build_s, ll
+    return Z.shape[0] / wall, wall, np.concatenate([np.array(r) for r in res])
+
+
+def cpu_rows_per_step(cfg_name, cores):
+    return {"C1": 64, "C2": cores, "C3": cores}.get(cfg_name, cores)
 
 
 def run_reference(args):
@@ -216,46 +276,89 @@ def run_reference(args):
     cores = len(os.sched_getaffinity(0))
     from paper_1708_02207_b200 import configs
     cfg = configs.CONFIGS[args.config]
-    per_step = {"C1": 64, "C2": cores, "C3": cores}.get(args.config, cores)
-    for _ in range(args.warmup):
-        time_cpu_port(args.config, min(per_step, cores), min(per_step, cores))
-    vals = []
+    kind, path = _cpu_setup(args.config)
+    per_step = cpu_rows_per_step(args.config, cores)
+    Zall = configs.draw_Z(cfg)
+    rows = lambda i: Zall[(i * per_step + np.arange(per_step)) % Zall.shape[0]]  # noqa: E731
+    for w in range(args.warmup):
+        time_cpu(rows(w), min(per_step, cores))
     t_all = 0.0
-    for _ in range(args.steps):
-        v, c, wall, build_s, _ = time_cpu_port(args.config, per_step, min(per_step, cores))
-        vals.append(v)
+    for s in range(args.steps):
+        _, wall, _ = time_cpu(rows(args.warmup + s), min(per_step, cores))
         t_all += wall
     value = args.steps * per_step / t_all
     line = {
         "impl": "reference", "metric": f"likelihood evals/s ({args.config}, {cfg.level}-level grid, n_z={cfg.n_z})",
         "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * t_all / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * t_all / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded protocol, DESIGN.md)",
-        "config": {"workload": args.config, "batch_per_step": per_step, "grid_nodes": (1 << cfg.level) + 1,
-                   "n_z": cfg.n_z, "n_obs": len(configs.observations(cfg)),
+        "config": {"workload": args.config, "global_batch": cfg.batch, "batch_per_step": per_step,
+                   "grid_nodes": (1 << cfg.level) + 1, "n_z": cfg.n_z, "n_obs": len(configs.observations(cfg)),
                    "parallelism": "host cores (one forked worker per core, rank 0 only)"},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": min(per_step, cores), "kind": "port",
-                         "sample": f"{per_step} Z rows per step of {args.config}, forked workers x 1 BLAS thread, "
-                                   "oracle/hdd_port.py (restatement of the reference HDD functional path)"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": min(per_step, cores), "kind": kind,
+                         "sample": f"{per_step} distinct Z rows of {args.config} per step, forked workers x 1 BLAS "
+                                   f"thread: {path}"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------------
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
-    if args.impl == "reference":
-        run_reference(args)
-        return
+def traffic_from_capture(cfg_name, stage, launches_per_stage):
+    """DRAM bytes per launch of `stage` from a committed ncu --set full capture of the
+    same config (profiles/traffic.json), or None."""
+    try:
+        with open(ROOT / "profiles" / "traffic.json") as f:
+            rec = json.load(f).get(cfg_name, {}).get(stage)
+    except Exception:
+        return None
+    if not rec:
+        return None
+    return {"bytes_per_launch": rec["dram_bytes_per_launch"], "launches_per_stage_per_step": launches_per_stage,
+            "source": rec["source"], "binding": rec.get("binding")}
 
+
+def per_config_measurements(dev):
+    """Samples/s of the other BASELINE configs on this GPU (device-resident Z,
+    CUDA events, median of 3 after one warm-up)."""
+    import torch
+    import paper_1708_02207_b200 as hb
+    from paper_1708_02207_b200 import configs
+    cases = [("C1", 64, False), ("C2", 1024, False), ("C3", 8192, False), ("C5", 1088, False), ("C5", 544, True)]
+    out = {}
+    for name, B, lowrank in cases:
+        cfg = configs.CONFIGS[name]
+        prob = configs.make_problem(name, device=dev.index, compression=lowrank)
+        Z = torch.from_numpy(configs.draw_Z(cfg, batch=max(B, cfg.batch))[:B].copy()).to(dev)
+        hb.log_likelihood_batch(prob, Z)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            hb.log_likelihood_batch(prob, Z, sync=False)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        from paper_1708_02207_b200.bayes import synchronize
+        synchronize(prob)
+        ms = float(np.median(ts))
+        leaf_fl, merge_fl = flops_split(cfg.level)
+        fl = leaf_fl + sum(merge_fl.values())
+        key = name + ("_lowrank" if lowrank else "")
+        out[key] = {"samples_per_s": B / (ms * 1e-3), "batch": B, "ms": ms,
+                    "batch_note": "whole BASELINE batch" if B == cfg.batch else f"first {B} rows of {cfg.batch}",
+                    "step_fp64_frac": fl * B / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                    "compression": list(cfg.compression) if lowrank else None}
+        prob._plan = None
+        del prob, Z
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+    return out
+
+
+def main_rank(args):
     import torch
     import torch.distributed as dist
 
@@ -270,15 +373,18 @@ def main():
 
     import ctypes as C
     from paper_1708_02207_b200 import _lib, bayes, configs
-    from paper_1708_02207_b200.parallel import gather_log_likelihood, posterior_weights_device
+    from paper_1708_02207_b200.parallel import gather_ragged, posterior_weights_device, shard_rows
 
     cfg = configs.CONFIGS[args.config]
-    B = cfg.batch
+    G = cfg.batch if args.batch <= 0 else args.batch          # fixed global batch (strong scaling)
+    lo, hi = shard_rows(G, world, rank)
+    B = hi - lo
+    counts = [shard_rows(G, world, r)[1] - shard_rows(G, world, r)[0] for r in range(world)]
     problem = configs.make_problem(args.config, device=local)
     plan = problem.plan()
     info = plan.info()
-    Zall = configs.draw_Z(cfg, batch=B * world)
-    Zl = np.ascontiguousarray(Zall[rank * B:(rank + 1) * B])
+    Zall = configs.draw_Z(cfg, batch=max(G, cfg.batch))[:G]
+    Zl = np.ascontiguousarray(Zall[lo:hi])
     Zd = torch.from_numpy(Zl).to(dev)
     ll = torch.empty(B, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -286,65 +392,62 @@ def main():
     stage = np.zeros(n_stages)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step(timed_stages):
-        if timed_stages is not None:
-            rc = plan.lib.hdd_forward_batch_timed(plan.handle, C.c_void_p(Zd.data_ptr()), B, None,
-                                                  C.c_void_p(ll.data_ptr()), C.c_void_p(stream.cuda_stream),
-                                                  timed_stages.ctypes.data_as(_lib._f64p), n_stages)
-        else:
-            rc = plan.lib.hdd_forward_batch(plan.handle, C.c_void_p(Zd.data_ptr()), B, None,
-                                            C.c_void_p(ll.data_ptr()), C.c_void_p(stream.cuda_stream))
-        plan.check(rc)
-        return gather_log_likelihood(ll, world)
+    def step():
+        plan.check(plan.lib.hdd_forward_batch(plan.handle, C.c_void_p(Zd.data_ptr()), B, None,
+                                              C.c_void_p(ll.data_ptr()), C.c_void_p(stream.cuda_stream)))
+        ll_all = gather_ragged(ll, counts) if world > 1 else ll
+        return posterior_weights_device(ll_all)
 
     for _ in range(args.warmup):
-        posterior_weights_device(step(None))
+        step()
+    plan.check(plan.lib.hdd_sync(plan.handle, C.c_void_p(stream.cuda_stream)))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record(stream)
-            ll_all = step(None)
-            w, idx_t, lse_t = posterior_weights_device(ll_all)
+            w, idx_t, lse_t = step()
             ev[i][1].record(stream)
         torch.cuda.synchronize()
+    plan.check(plan.lib.hdd_sync(plan.handle, C.c_void_p(stream.cuda_stream)))
+    if world > 1:
+        dist.barrier()
     idx, lse, n_w = int(idx_t.item()), float(lse_t.item()), int(w.numel())
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    ms = float(np.mean(step_ms))
-    # per-stage (kernel) times: separate pass, same stream, CUDA events between launches
-    for _ in range(args.steps):
-        flush.zero_()
-        step(stage)
-    stage /= args.steps
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = world * B / (ms_max * 1e-3)
+    value = G / (ms_max * 1e-3)
+
+    # per-stage (kernel) times: one timed pass, same stream, CUDA events between launches
+    flush.zero_()
+    plan.check(plan.lib.hdd_forward_batch_timed(plan.handle, C.c_void_p(Zd.data_ptr()), B, None,
+                                                C.c_void_p(ll.data_ptr()), C.c_void_p(stream.cuda_stream),
+                                                stage.ctypes.data_as(_lib._f64p), n_stages))
 
     # ---- e2e through the public API: pinned host Z -> device -> ll -> host ----
     Zh = torch.from_numpy(Zl).pin_memory()
-    llh = torch.empty(B, dtype=torch.float64).pin_memory()
-    for _ in range(2):
-        bayes.log_likelihood_batch(problem, Zh.to(dev, non_blocking=True))
-    torch.cuda.synchronize()
-    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for i in range(args.steps):
+    Zh_np = Zh.numpy()
+    n_e2e = 3
+    e2e_ms = []
+    if world > 1:
+        dist.barrier()
+    for _ in range(n_e2e):
         flush.zero_()
-        e2e_ev[i][0].record(stream)
-        Zs = Zh.to(dev, non_blocking=True)
-        out = bayes.log_likelihood_batch(problem, Zs)
-        llh.copy_(out, non_blocking=True)
-        e2e_ev[i][1].record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = float(np.mean([a.elapsed_time(b) for a, b in e2e_ev]))
-    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = bayes.log_likelihood_batch(problem, Zh_np)      # hdd_forward_batch_host: H2D, compute, D2H
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    assert np.array_equal(out, ll.cpu().numpy())              # same numbers as the device-resident path
+    t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t.item())
+    e2e_max = float(t.item())
 
     if rank != 0:
         if world > 1:
@@ -352,7 +455,7 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel ----
+    # ---- roofline of the dominant kernel stage ----
     leaf_fl, merge_fl = flops_split(cfg.level)
     dl = info.leaf_depth
     names = ["kappa", "leaf"] + [f"merge_d{d}" for d in range(dl - 1, -1, -1)] + ["finalize"]
@@ -362,69 +465,116 @@ def main():
     shares = {n: float(stage[i]) for i, n in enumerate(names)}
     top = max(shares, key=shares.get)
     top_ms = shares[top]
+    n_sub = math.ceil(B / info.max_batch)
     achieved = flops[top] * B / (top_ms * 1e-3) / 1e12
     total_fl = leaf_fl + sum(merge_fl.values())
     hbm_gbs, hbm_src = hbm_peak()
     kappa_bytes = (2 * (1 << cfg.level) ** 2 * 8 + cfg.n_z * 8) * B
+    tr = traffic_from_capture(args.config, top, n_sub)
+    algo_per_launch = flops[top] * B / n_sub
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cores = len(os.sched_getaffinity(0))
-        n_s = {"C1": 64, "C2": 2 * cores, "C3": cores}.get(args.config, cores)
-        v, c, wall, build_s, ll_cpu = time_cpu_port(args.config, n_s, min(cores, n_s))
+        kind, path = _cpu_setup(args.config)
+        n_s = cpu_rows_per_step(args.config, cores)
+        v, wall, ll_cpu = time_cpu(Zl[:n_s], min(cores, n_s))
         ll_gpu = ll.cpu().numpy()[:n_s]
-        cpu = {"value": v, "unit": "samples/s", "cores": c, "kind": "port",
-               "sample": f"first {n_s} Z rows of {args.config} ({wall:.1f} s wall, tree build {build_s:.1f} s "
-                         "excluded), forked workers x 1 BLAS thread, oracle/hdd_port.py",
+        cpu = {"value": v, "unit": "samples/s", "cores": min(cores, n_s), "kind": kind,
+               "sample": f"first {n_s} Z rows of {args.config} ({wall:.1f} s wall, setup excluded), forked workers x "
+                         f"1 BLAS thread: {path}",
                "max_rel_ll_diff_vs_gpu": float(np.max(np.abs(ll_cpu - ll_gpu) / np.abs(ll_cpu)))}
 
+    per_cfg = None
+    if world == 1 and not args.no_per_config:
+        ll_host = ll.cpu().numpy()
+        plan = None                      # release the flagship plan's workspace first
+        problem._plan = None
+        del Zd, ll, flush
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        per_cfg = per_config_measurements(dev)
+        del ll_host
+
     # forward kernels per sub-batch + the posterior-weights kernel per step
-    launches = args.steps * (info.n_kernels_per_batch * math.ceil(B / info.max_batch) + 1)
-    # measured DRAM bytes per launch of the dominant kernel (ncu --set full capture,
-    # profiles/r01_ncu_full_leaf_v4_C2.csv: 23.6 KB per leaf-sample) scaled to this launch;
-    # the leaf's binding resource is shared-memory bandwidth (same capture)
-    traffic = None
-    binding = None
-    if top == "leaf":
-        traffic = {"bytes": 23.6e3 * B * ((1 << cfg.level) // 16) ** 2,
-                   "source": "ncu dram__bytes_read+write, leaf2_kernel<2> C2: 1184 MB / (49 leaves x 1024)"}
-        binding = {"resource": "instruction issue + shared-memory wavefronts (3 CTAs/SM, latency-bound per CTA)",
-                   "issue_active_pct": 59.3, "smem_wavefront_util_pct": 68.7, "dmma_pipe_pct": 11.7,
-                   "source": "profiles/r01_ncu_full_leaf_v13_C2.csv"}
+    launches = args.steps * (info.n_kernels_per_batch * n_sub + 1)
     line = {
         "metric": f"likelihood evals/s ({args.config}, {cfg.level}-level grid, n_z={cfg.n_z})",
         "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded protocol, DESIGN.md)",
-        "config": {"workload": args.config, "batch_per_gpu": B, "global_batch": B * world,
+        "config": {"workload": args.config, "global_batch": G, "batch_per_gpu": B, "sub_batches_per_gpu": n_sub,
                    "grid_nodes": (1 << cfg.level) + 1, "n_z": cfg.n_z, "n_obs": info.n_obs,
-                   "parallelism": f"dp{world} (Z rows sharded, NCCL all-gather of ll)",
+                   "parallelism": f"dp{world} (fixed global batch, Z rows sharded, NCCL all-gather of ll)",
                    "l2": "flushed between steps (256 MiB memset); per-step working set "
                          f"{info.workspace_bytes / 2**30:.2f} GiB > L2"},
         "roofline": {"bound": "tensor", "kernel": top, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                     "traffic": None if tr is None else tr["bytes_per_launch"],
+                     "traffic_source": None if tr is None else tr,
+                     "algorithmic_flops_per_launch": algo_per_launch,
+                     "launches_per_step": n_sub,
                      "peak_source": FP64_PEAK_SRC,
-                     "kernel_share_of_step": top_ms / sum(shares.values()),
-                     "binding_resource": binding,
-                     "algorithmic_flops_per_launch": flops[top] * B},
-        "step_roofline": {"achieved_tflops": total_fl * B / (ms_max * 1e-3) / 1e12,
-                          "frac_fp64": total_fl * B / (ms_max * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                     "kernel_share_of_step": top_ms / sum(shares.values())},
+        "step_roofline": {"achieved_tflops": total_fl * G / (ms_max * 1e-3) / 1e12,
+                          "frac_fp64": total_fl * G / (ms_max * 1e-3) / 1e12 / FP64_PEAK_TFLOPS / world,
                           "flops_per_sample": total_fl},
         "stage_ms": shares,
         "kappa_hbm": {"achieved_gbs": kappa_bytes / (shares["kappa"] * 1e-3) / 1e9, "peak": hbm_gbs,
                       "peak_source": hbm_src},
-        "e2e": {"value": world * B / (e2e_ms * 1e-3), "unit": "samples/s",
+        "e2e": {"value": G / (e2e_max * 1e-3), "unit": "samples/s",
                 "h2d_bytes_per_step": int(B * cfg.n_z * 8), "d2h_bytes_per_step": int(B * 8),
-                "ms_per_step": e2e_ms},
+                "ms_per_step": e2e_max, "steps": n_e2e,
+                "path": "bayes.log_likelihood_batch(numpy pinned Z) -> hdd_forward_batch_host"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "posterior": {"argmax": idx, "log_evidence_minus_logB": lse - math.log(n_w)},
         "cpu_baseline": cpu,
+        "per_config": per_cfg,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _spawned(local_rank, args, world, port):
+    os.environ.update(RANK=str(local_rank), LOCAL_RANK=str(local_rank), WORLD_SIZE=str(world),
+                      LOCAL_WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    main_rank(args)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--batch", type=int, default=0, help="global batch (default: the config's BASELINE batch)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # launched without torchrun: form the N-rank NCCL job ourselves
+        import socket
+        import torch
+        import torch.multiprocessing as mp
+        n_dev = torch.cuda.device_count()
+        if n_dev < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {n_dev} CUDA devices visible")
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        mp.start_processes(_spawned, args=(args, args.gpus, port), nprocs=args.gpus, start_method="spawn")
+        return
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
+    main_rank(args)
 
 
 if __name__ == "__main__":

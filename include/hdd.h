@@ -55,13 +55,16 @@ enum { HDD_OBS_POINT = 0, HDD_OBS_MEAN = 1 };
 typedef struct HddPlan HddPlan;
 
 typedef struct {
-  int32_t level;           /* mesh level L: 2^L cells per side (4 <= L <= 11) */
+  int32_t level;           /* mesh level L: 2^L cells per side (1 <= L <= 11);
+                              levels 1-3 are solved by one warp per sample   */
   int32_t n_z;             /* parameter dimension                             */
   /* separable log-coefficient: for triangle t = 2(i N + j) + type,
    *   log kappa_t = sum_k coef[k] z[k] sx[k][2 i + type] sy[k][2 j + type]
    * (sine-KL: sin(pi a_k cx), sin(pi b_k cy), coef 0.5/k; reference
    *  indicator ParamField: 0/1 interval masks, coef 1).  Row-major
-   *  [n_z][2N] host arrays.                                                   */
+   *  [n_z][2N] host arrays.  All three NULL: no parametrization, the plan
+   *  evaluates caller-supplied fields (hdd_forward_batch_kappa; the
+   *  reference's duck-typed param.kappa(z), bayes.py:183).                  */
   const double* sx;
   const double* sy;
   const double* coef;
@@ -88,6 +91,11 @@ typedef struct {
    * boundary values are folded into the load and functional columns at the
    * kernel-leaf outputs, so the upper merges never see them.                 */
   const double* g;
+  /* 1 = keep the primal factors of EVERY upper node (required by
+   * hdd_solve_batch, the root_to_leaves analogue of SolveMode.keep_all(),
+   * hdd.py:120-138); 0 = likelihood plans keep them only on the
+   * root-to-observation paths the top-down sweep visits.                      */
+  int32_t full_solve;
 } HddPlanDesc;
 
 typedef struct {
@@ -103,6 +111,10 @@ typedef struct {
   int32_t max_batch, n_kernels_per_batch;
   int64_t workspace_bytes;
   int32_t mode;
+  int32_t n_topdown;       /* primal: upper nodes the top-down sweep visits   */
+  int32_t tiny;            /* 1: level <= 3, one warp per sample (no tree)    */
+  int32_t separable;       /* 1: Z entry points (K1); 0: kappa entry points   */
+  int32_t full_solve;      /* 1: factors of every node kept (hdd_solve_batch) */
 } HddPlanInfo;
 
 typedef struct {
@@ -141,9 +153,28 @@ typedef struct {
 int hdd_plan_create(const HddPlanDesc* desc, HddPlan** out);
 int hdd_plan_destroy(HddPlan* plan);
 
-/* Z_dev [B][n_z], S_dev [B][n_obs] (nullable), ll_dev [B] (nullable). */
+/* Z_dev [B][n_z], S_dev [B][n_obs] (nullable), ll_dev [B] (nullable).
+ * ASYNCHRONOUS: returns once the launches are queued on `stream`.  Failures
+ * (non-SPD interface, non-finite S, invalid kappa) are recorded on the device
+ * and reported by hdd_sync, by the synchronous (_host) calls, or by the next
+ * call on the plan once the record has reached the host; the HddError then
+ * names the lowest failing sample of that call. */
 int hdd_forward_batch(HddPlan* plan, const double* Z_dev, int64_t B,
                       double* S_dev, double* ll_dev, void* stream);
+
+/* Waits for `stream` and returns the status of the calls queued since the last
+ * check: HDD_OK, or the recorded failure (hdd_last_error has the details). */
+int hdd_sync(HddPlan* plan, void* stream);
+
+/* Same as hdd_forward_batch with caller-supplied coefficient fields instead of
+ * Z: K_dev [B][2 N^2], triangle order t = 2(i N + j) + type (the reference's
+ * CoefficientField.values, fem.py:23-43) — the drop-in for a duck-typed
+ * problem.param whose .kappa(z) is arbitrary host code (bayes.py:183, :204,
+ * :242).  Values are checked positive and finite on the device (ConfigError). */
+int hdd_forward_batch_kappa(HddPlan* plan, const double* K_dev, int64_t B,
+                            double* S_dev, double* ll_dev, void* stream);
+int hdd_forward_batch_kappa_host(HddPlan* plan, const double* K_host, int64_t B,
+                                 double* S_host, double* ll_host);
 
 /* Same as hdd_forward_batch, plus per-stage device time (CUDA events on the
  * launching stream), accumulated over the internal sub-batches into
@@ -154,7 +185,9 @@ int hdd_forward_batch_timed(HddPlan* plan, const double* Z_dev, int64_t B,
                             double* S_dev, double* ll_dev, void* stream,
                             double* stage_ms, int32_t n_stages);
 
-/* Same call with HOST buffers: copies in, runs, copies out (pinned staging). */
+/* Same call with HOST buffers (synchronous): sub-batch i+1's H2D copy and
+ * sub-batch i-1's D2H copy run on two copy streams beside sub-batch i's
+ * compute; returns when the results are in host memory. */
 int hdd_forward_batch_host(HddPlan* plan, const double* Z_host, int64_t B,
                            double* S_host, double* ll_host);
 
@@ -162,14 +195,18 @@ int hdd_forward_batch_host(HddPlan* plan, const double* Z_host, int64_t B,
  * (n_nodes = (2^level + 1)^2, node id j * (2^level + 1) + i).  The bottom-up
  * sweep and the primal top-down sweep give u on every interface; each kernel
  * leaf then solves for its interior nodes.  Requires a plan created with
- * mode = 1 (primal: the factors are kept), else HDD_ERR_USAGE — the analogue of
- * root_to_leaves requiring a store built with SolveMode.keep_all().
+ * mode = 1 and full_solve = 1 (every factor kept), else HDD_ERR_USAGE — the
+ * analogue of root_to_leaves requiring a store built with SolveMode.keep_all().
+ * Asynchronous like hdd_forward_batch.
  * Replaces root_to_leaves / forward_full_solve (reference hdd.py:397-432,
  * bayes.py:201-208). */
 int hdd_solve_batch(HddPlan* plan, const double* Z_dev, int64_t B, double* U_dev, void* stream);
 
 /* Same call with HOST buffers. */
 int hdd_solve_batch_host(HddPlan* plan, const double* Z_host, int64_t B, double* U_host);
+/* Full solution from caller-supplied coefficient fields K [B][2 N^2]. */
+int hdd_solve_batch_kappa(HddPlan* plan, const double* K_dev, int64_t B, double* U_dev, void* stream);
+int hdd_solve_batch_kappa_host(HddPlan* plan, const double* K_host, int64_t B, double* U_host);
 
 /* Per-triangle kappa for a batch (parity hook for the assembly kernel). */
 int hdd_kappa_batch(HddPlan* plan, const double* Z_dev, int64_t B,

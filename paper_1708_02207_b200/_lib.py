@@ -38,7 +38,7 @@ class HddPlanDesc(C.Structure):
         ("sigma", _f64p), ("y", _f64p),
         ("max_batch", C.c_int32), ("device", C.c_int32), ("keep_nodes", C.c_int32),
         ("mode", C.c_int32), ("lr_eps", C.c_double), ("lr_kmax", C.c_int32), ("lr_nmin", C.c_int32),
-        ("g", _f64p),
+        ("g", _f64p), ("full_solve", C.c_int32),
     ]
 
 
@@ -51,7 +51,8 @@ class HddPlanInfo(C.Structure):
     _fields_ = [("level", C.c_int32), ("n_cells", C.c_int32), ("leaf_cells", C.c_int32),
                 ("leaf_depth", C.c_int32), ("n_upper", C.c_int32), ("n_leaves", C.c_int32),
                 ("n_obs", C.c_int32), ("leaf_cols", C.c_int32), ("max_batch", C.c_int32),
-                ("n_kernels_per_batch", C.c_int32), ("workspace_bytes", C.c_int64), ("mode", C.c_int32)]
+                ("n_kernels_per_batch", C.c_int32), ("workspace_bytes", C.c_int64), ("mode", C.c_int32),
+                ("n_topdown", C.c_int32), ("tiny", C.c_int32), ("separable", C.c_int32), ("full_solve", C.c_int32)]
 
 
 class HddNodeInfo(C.Structure):
@@ -80,6 +81,11 @@ EXPORTS = {
     "hdd_forward_batch_timed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                           _f64p, C.c_int32]),
     "hdd_forward_batch_host": (C.c_int, [C.c_void_p, _f64p, C.c_int64, _f64p, _f64p]),
+    "hdd_sync": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "hdd_forward_batch_kappa": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hdd_forward_batch_kappa_host": (C.c_int, [C.c_void_p, _f64p, C.c_int64, _f64p, _f64p]),
+    "hdd_solve_batch_kappa": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "hdd_solve_batch_kappa_host": (C.c_int, [C.c_void_p, _f64p, C.c_int64, _f64p]),
     "hdd_solve_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "hdd_solve_batch_host": (C.c_int, [C.c_void_p, _f64p, C.c_int64, _f64p]),
     "hdd_kappa_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),

@@ -36,7 +36,7 @@ from .geometry import DDTree, Mesh, Rect, cell_centroid_tables
 __all__ = [
     "ParamField", "SineKLField", "Prior", "ToleranceSpec", "MeasurementModel", "BayesProblem", "mean_observations",
     "aligned_partition", "kl_pairs", "forward_functionals", "forward_functionals_batch", "log_likelihood",
-    "log_likelihood_batch", "gaussian_log_likelihood", "posterior_weights",
+    "log_likelihood_batch", "gaussian_log_likelihood", "posterior_weights", "synchronize",
 ]
 
 
@@ -234,7 +234,7 @@ class _Plan:
     """Owns one HddPlan* (device tables + workspace)."""
 
     def __init__(self, problem: "BayesProblem", device: int, max_batch: int, keep_nodes: bool = False,
-                 mode: int = -1):
+                 mode: int = -1, full_solve: bool = False):
         L = _lib.lib()
         mesh = problem.tree.mesh
         param = problem.param
@@ -245,10 +245,14 @@ class _Plan:
         if (kinds < 0).any():
             bad = [k for k, _ in obs if k not in ("point", "mean")][0]
             raise ConfigError(f"unknown observation kind {bad!r}")
+        # separable fields are evaluated on the device (K1); any other duck-typed
+        # param (only .kappa(z) is used, bayes.py:183) hands its fields to the plan
+        self.separable = all(hasattr(param, a) for a in ("sx", "sy", "coef"))
+        sep = self.separable
         self._keep = dict(
-            sx=np.ascontiguousarray(param.sx, dtype=np.float64),
-            sy=np.ascontiguousarray(param.sy, dtype=np.float64),
-            coef=np.ascontiguousarray(param.coef, dtype=np.float64),
+            sx=np.ascontiguousarray(param.sx, dtype=np.float64) if sep else None,
+            sy=np.ascontiguousarray(param.sy, dtype=np.float64) if sep else None,
+            coef=np.ascontiguousarray(param.coef, dtype=np.float64) if sep else None,
             f=None if problem._f_is_one else np.ascontiguousarray(problem.f, dtype=np.float64),
             g=np.ascontiguousarray(problem.g, dtype=np.float64) if np.any(problem.g != 0.0) else None,
             kind=kinds, ids=np.array([int(i) for _, i in obs], dtype=np.int64),
@@ -257,7 +261,7 @@ class _Plan:
         k = self._keep
         ptr = lambda a, t: None if a is None else a.ctypes.data_as(t)  # noqa: E731
         desc = _lib.HddPlanDesc(
-            level=mesh.level, n_z=param.n_z,
+            level=mesh.level, n_z=int(getattr(param, "n_z", 0)),
             sx=ptr(k["sx"], _lib._f64p), sy=ptr(k["sy"], _lib._f64p), coef=ptr(k["coef"], _lib._f64p),
             f=ptr(k["f"], _lib._f64p), n_obs=len(obs), obs_kind=ptr(k["kind"], _lib._i32p),
             obs_id=ptr(k["ids"], _lib._i64p), sigma=ptr(k["sigma"], _lib._f64p), y=ptr(k["y"], _lib._f64p),
@@ -265,7 +269,7 @@ class _Plan:
             lr_eps=float(getattr(problem.compression, "eps", 0.0) or 0.0) if problem.compression is not None else 0.0,
             lr_kmax=int(getattr(problem.compression, "k_max", 64)) if problem.compression is not None else 0,
             lr_nmin=int(getattr(problem.compression, "n_min", 32)) if problem.compression is not None else 0,
-            g=ptr(k["g"], _lib._f64p))
+            g=ptr(k["g"], _lib._f64p), full_solve=int(full_solve))
         h = C.c_void_p()
         rc = L.hdd_plan_create(C.byref(desc), C.byref(h))
         if rc != _lib.HDD_OK:
@@ -274,9 +278,10 @@ class _Plan:
             _lib.raise_for(rc, e)
         self.handle = h
         self.lib = L
-        self.n_z = param.n_z
+        self.n_z = int(getattr(param, "n_z", 0))
         self.n_obs = len(obs)
         self.device = device
+        self.n_tri = mesh.n_triangles
 
     def check(self, rc):
         if rc != _lib.HDD_OK:
@@ -345,13 +350,13 @@ class BayesProblem:
         return self._plan
 
     def solve_plan(self) -> _Plan:
-        """A primal plan (factors kept) for the full-solution sweep; the likelihood
-        plan is reused when it already is one."""
+        """A full-solution plan (primal, every factor kept) for the full-solution
+        sweep; a single-leaf or sub-leaf mesh reuses the likelihood plan."""
         info = self.plan().info()
-        if info.mode == 1 or info.leaf_depth == 0:
+        if info.leaf_depth == 0:
             return self.plan()
         if self._solve_plan is None:
-            self._solve_plan = _Plan(self, self.device, self.max_batch, mode=1)
+            self._solve_plan = _Plan(self, self.device, self.max_batch, mode=1, full_solve=True)
         return self._solve_plan
 
 
@@ -363,8 +368,10 @@ def _as_batch(Z, n_z):
     if torch is not None and isinstance(Z, torch.Tensor):
         if Z.dim() == 1:
             Z = Z[None]
-        if Z.shape[-1] != n_z:
+        if Z.dim() != 2 or Z.shape[-1] != n_z:
             raise ConfigError(f"parameter vector must have length {n_z}")
+        if not Z.is_cuda:     # host tensors (pinned or not) take the host entry point
+            return np.ascontiguousarray(Z.detach().to(torch.float64).numpy())
         return Z
     Z = np.asarray(Z, dtype=np.float64)
     if Z.ndim == 1:
@@ -374,14 +381,49 @@ def _as_batch(Z, n_z):
     return np.ascontiguousarray(Z)
 
 
-def _run(problem: BayesProblem, Z, want_S: bool, want_ll: bool):
+def _kappa_rows(problem: BayesProblem, Z) -> np.ndarray:
+    """Coefficient fields of a duck-typed param (only .kappa(z) is used, bayes.py:183),
+    evaluated by the caller's own host code, one row per sample: [B, 2 N^2]."""
+    if not isinstance(Z, np.ndarray):
+        Z = Z.detach().cpu().numpy()
+    n_tri = problem.tree.mesh.n_triangles
+    K = np.empty((Z.shape[0], n_tri))
+    for b, z in enumerate(Z):
+        kap = problem.param.kappa(z)
+        v = np.asarray(getattr(kap, "values", kap), dtype=np.float64).reshape(-1)
+        if v.shape != (n_tri,):
+            raise ConfigError(f"coefficient field must have {n_tri} triangle values, got {v.size}")
+        K[b] = v
+    return K
+
+
+def _device_check(plan: _Plan, Zb):
+    if Zb.device.index != plan.device:
+        raise UsageError(f"torch inputs must live on the plan's CUDA device cuda:{plan.device}, got {Zb.device}")
+
+
+def _run(problem: BayesProblem, Z, want_S: bool, want_ll: bool, sync: bool = True):
     plan = problem.plan()
-    Zb = _as_batch(Z, plan.n_z)
+    n_z = plan.n_z if plan.separable else int(getattr(problem.param, "n_z", np.asarray(Z).shape[-1]))
+    Zb = _as_batch(Z, n_z)
     B = Zb.shape[0]
+    f64 = _lib._f64p
+    if not plan.separable:
+        # host-evaluated fields; device Z comes back as device tensors
+        K = _kappa_rows(problem, Zb)
+        S = np.empty((B, plan.n_obs)) if want_S else None
+        ll = np.empty(B) if want_ll else None
+        plan.check(plan.lib.hdd_forward_batch_kappa_host(
+            plan.handle, K.ctypes.data_as(f64), B, S.ctypes.data_as(f64) if S is not None else None,
+            ll.ctypes.data_as(f64) if ll is not None else None))
+        if not isinstance(Zb, np.ndarray):
+            import torch
+            S = None if S is None else torch.from_numpy(S).to(Zb.device)
+            ll = None if ll is None else torch.from_numpy(ll).to(Zb.device)
+        return S, ll
     if isinstance(Zb, np.ndarray):
         S = np.empty((B, plan.n_obs)) if want_S else None
         ll = np.empty(B) if want_ll else None
-        f64 = _lib._f64p
         rc = plan.lib.hdd_forward_batch_host(
             plan.handle, Zb.ctypes.data_as(f64), B,
             S.ctypes.data_as(f64) if S is not None else None,
@@ -389,41 +431,55 @@ def _run(problem: BayesProblem, Z, want_S: bool, want_ll: bool):
         plan.check(rc)
         return S, ll
     import torch
-    if not Zb.is_cuda:
-        raise UsageError("torch inputs must live on the plan's CUDA device")
+    _device_check(plan, Zb)
     Zb = Zb.to(torch.float64).contiguous()
     S = torch.empty((B, plan.n_obs), dtype=torch.float64, device=Zb.device) if want_S else None
     ll = torch.empty(B, dtype=torch.float64, device=Zb.device) if want_ll else None
-    stream = torch.cuda.current_stream(Zb.device).cuda_stream
+    stream = C.c_void_p(torch.cuda.current_stream(Zb.device).cuda_stream)
     rc = plan.lib.hdd_forward_batch(plan.handle, C.c_void_p(Zb.data_ptr()), B,
                                     C.c_void_p(S.data_ptr()) if S is not None else None,
-                                    C.c_void_p(ll.data_ptr()) if ll is not None else None,
-                                    C.c_void_p(stream))
+                                    C.c_void_p(ll.data_ptr()) if ll is not None else None, stream)
     plan.check(rc)
+    if sync:
+        plan.check(plan.lib.hdd_sync(plan.handle, stream))
     return S, ll
 
 
-def forward_functionals_batch(problem: BayesProblem, Z):
-    """S[B, n_y] for every row of Z (numpy host array or CUDA torch tensor)."""
-    S, _ = _run(problem, Z, True, False)
+def forward_functionals_batch(problem: BayesProblem, Z, sync: bool = True):
+    """S[B, n_y] for every row of Z (numpy / host torch -> numpy; CUDA torch tensor ->
+    CUDA torch tensor).  With CUDA tensors and sync=False the call returns as soon as
+    the work is queued on the current stream; failures then surface at the next call
+    on the problem or at `synchronize(problem)`."""
+    S, _ = _run(problem, Z, True, False, sync)
     problem.forward_calls += int(S.shape[0])
     return S
 
 
-def log_likelihood_batch(problem: BayesProblem, Z):
-    """ll[B] for every row of Z; raises UsageError without data (bayes.py:228-229)."""
+def log_likelihood_batch(problem: BayesProblem, Z, sync: bool = True):
+    """ll[B] for every row of Z; raises UsageError without data (bayes.py:228-229).
+    `sync` as in forward_functionals_batch."""
     if problem.model.y is None:
         raise UsageError("measurement model carries no data")
-    _, ll = _run(problem, Z, False, True)
+    _, ll = _run(problem, Z, False, True, sync)
     problem.forward_calls += int(ll.shape[0])
     return ll
+
+
+def synchronize(problem: BayesProblem, stream=None):
+    """Wait for the problem's queued device work and raise its recorded failure
+    (ConfigError / NumericalError naming the lowest failing sample), if any."""
+    import torch
+    plan = problem.plan()
+    st = stream if stream is not None else torch.cuda.current_stream(plan.device)
+    plan.check(plan.lib.hdd_sync(plan.handle, C.c_void_p(st.cuda_stream)))
 
 
 def forward_functionals(problem: BayesProblem, z) -> np.ndarray:
     """Observation vector S(z) (bayes.py:180-198), one sample."""
     z = np.asarray(z, dtype=float)
-    if z.shape != (problem.param.n_z,):
-        raise ConfigError(f"parameter vector must have length {problem.param.n_z}")
+    n_z = getattr(problem.param, "n_z", z.shape[-1] if z.ndim else 0)
+    if z.shape != (n_z,):
+        raise ConfigError(f"parameter vector must have length {n_z}")
     return forward_functionals_batch(problem, z[None])[0]
 
 
@@ -435,22 +491,30 @@ def solve_batch(problem: BayesProblem, Z):
     (hdd.py:289-432) for a batch.  numpy in -> numpy out; a CUDA torch tensor in ->
     CUDA torch tensor out."""
     plan = problem.solve_plan()
-    Zb = _as_batch(Z, plan.n_z)
+    n_z = plan.n_z if plan.separable else int(getattr(problem.param, "n_z", np.asarray(Z).shape[-1]))
+    Zb = _as_batch(Z, n_z)
     B = Zb.shape[0]
     n = problem.tree.mesh.n_nodes
+    f64 = _lib._f64p
+    if not plan.separable:
+        K = _kappa_rows(problem, Zb)
+        U = np.empty((B, n))
+        plan.check(plan.lib.hdd_solve_batch_kappa_host(plan.handle, K.ctypes.data_as(f64), B, U.ctypes.data_as(f64)))
+        if not isinstance(Zb, np.ndarray):
+            import torch
+            return torch.from_numpy(U).to(Zb.device)
+        return U
     if isinstance(Zb, np.ndarray):
         U = np.empty((B, n))
-        plan.check(plan.lib.hdd_solve_batch_host(plan.handle, Zb.ctypes.data_as(_lib._f64p), B,
-                                                 U.ctypes.data_as(_lib._f64p)))
+        plan.check(plan.lib.hdd_solve_batch_host(plan.handle, Zb.ctypes.data_as(f64), B, U.ctypes.data_as(f64)))
         return U
     import torch
-    if not Zb.is_cuda:
-        raise UsageError("torch inputs must live on the plan's CUDA device")
+    _device_check(plan, Zb)
     Zb = Zb.to(torch.float64).contiguous()
     U = torch.empty((B, n), dtype=torch.float64, device=Zb.device)
-    stream = torch.cuda.current_stream(Zb.device).cuda_stream
-    plan.check(plan.lib.hdd_solve_batch(plan.handle, C.c_void_p(Zb.data_ptr()), B, C.c_void_p(U.data_ptr()),
-                                        C.c_void_p(stream)))
+    stream = C.c_void_p(torch.cuda.current_stream(Zb.device).cuda_stream)
+    plan.check(plan.lib.hdd_solve_batch(plan.handle, C.c_void_p(Zb.data_ptr()), B, C.c_void_p(U.data_ptr()), stream))
+    plan.check(plan.lib.hdd_sync(plan.handle, stream))
     return U
 
 
@@ -486,8 +550,8 @@ def forward_full_solve(problem: BayesProblem, z) -> np.ndarray:
     """Observation vector via the full solve plus the per-triangle mean rule — the
     comparison route of the likelihood-equivalence checks (bayes.py:201-208)."""
     z = np.asarray(z, dtype=float)
-    if z.shape != (problem.param.n_z,):
-        raise ConfigError(f"parameter vector must have length {problem.param.n_z}")
+    if z.ndim != 1:
+        raise ConfigError("parameter vector must be one-dimensional")
     u = solve_batch(problem, z[None])[0]
     return observe_solution(problem.tree, u, problem.model)
 
@@ -499,8 +563,8 @@ def solve_subdomain(problem: BayesProblem, z, target_id: int) -> np.ndarray:
     from .geometry import omega_nodes
     target = problem.tree.node(int(target_id))
     z = np.asarray(z, dtype=float)
-    if z.shape != (problem.param.n_z,):
-        raise ConfigError(f"parameter vector must have length {problem.param.n_z}")
+    if z.ndim != 1:
+        raise ConfigError("parameter vector must be one-dimensional")
     u = solve_batch(problem, z[None])[0]
     return u[omega_nodes(problem.tree.mesh, target.cells)]
 
@@ -516,8 +580,9 @@ def log_likelihood(problem: BayesProblem, z, forward=None) -> float:
         raise UsageError("measurement model carries no data")
     if forward is None:
         z = np.asarray(z, dtype=float)
-        if z.shape != (problem.param.n_z,):
-            raise ConfigError(f"parameter vector must have length {problem.param.n_z}")
+        n_z = getattr(problem.param, "n_z", z.shape[-1] if z.ndim else 0)
+        if z.shape != (n_z,):
+            raise ConfigError(f"parameter vector must have length {n_z}")
         return float(log_likelihood_batch(problem, z[None])[0])
     s = forward(problem, z)
     return gaussian_log_likelihood(problem.model.y, s, problem.model.sigma)

@@ -53,6 +53,15 @@ struct HddPlan {
   double* g_ll = nullptr;
   int g_B = 0;
   bool g_seen = false;
+  // asynchronous failure reporting: pinned mirror of the device record
+  unsigned long long* h_err = nullptr;
+  // pipelined host entry points: copy streams, per-sub-batch events
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  std::vector<cudaEvent_t> pipe_ev;
+  bool io_kappa = false;
+  // primal top-down: DevUpper copies of the visited nodes, grouped by depth
+  DevUpper* d_td = nullptr;
+  std::vector<int> td_first, td_count;
 };
 
 static HddError g_create_err{};
@@ -92,6 +101,10 @@ static int setup_device(HddPlan* pl, int max_batch) {
   Plan& P = pl->plan;
   CU(cudaSetDevice(pl->device));
   CU(cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&pl->cs_in, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&pl->cs_out, cudaStreamNonBlocking));
+  CU(cudaHostAlloc(reinterpret_cast<void**>(&pl->h_err), sizeof(DevError), cudaHostAllocDefault));
+  *pl->h_err = kNoError;
   int up_rc;
   {   // per-device leaf tables are built once per process; plans may be created concurrently
     std::lock_guard<std::mutex> lk(g_mu);
@@ -332,6 +345,24 @@ static int setup_device(HddPlan* pl, int max_batch) {
     pl->d_upper = const_cast<DevUpper*>(du);
     D.upper = du;
   }
+  pl->td_first.assign(P.upper_by_depth.size(), -1);
+  pl->td_count.assign(P.upper_by_depth.size(), 0);
+  if (P.mode == 1) {
+    std::vector<DevUpper> td;
+    for (size_t dep = 0; dep < P.td_by_depth.size(); ++dep) {
+      if (P.td_by_depth[dep].empty()) continue;
+      pl->td_first[dep] = int(td.size());
+      pl->td_count[dep] = int(P.td_by_depth[dep].size());
+      for (int u : P.td_by_depth[dep]) td.push_back(pl->h_upper[u]);
+    }
+    const DevUpper* dt = nullptr;
+    if ((rc = upload(pl, td, &dt))) return rc;
+    pl->d_td = const_cast<DevUpper*>(dt);
+  }
+  D.tiny = P.tiny ? 1 : 0;
+  D.root_ref = P.root_ref;
+  D.gfull = nullptr;
+  if (P.tiny && P.has_g && (rc = upload(pl, P.gfull, &D.gfull))) return rc;
   // observations
   std::vector<int32_t> rk, rcol, rnode, rslot;
   std::vector<double> rv;
@@ -424,7 +455,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
     CU(cudaMalloc(&p, sizeof(DevError)));
     pl->allocs.push_back(p);
     D.err = static_cast<DevError*>(p);
-    CU(cudaMemset(p, 0, sizeof(DevError)));
+    CU(cudaMemset(p, 0xff, sizeof(DevError)));     // kNoError
   }
   if (P.root >= 0) {
     const UpperNode& R = P.upper[P.root];
@@ -448,7 +479,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
     int n = 2 + ncls;
     for (size_t dep = 0; dep < P.upper_by_depth.size(); ++dep) {
       if (P.upper_by_depth[dep].empty()) continue;
-      n += 1 + (D.mode == 1 ? 1 : 0);
+      n += 1 + (D.mode == 1 && pl->td_count[dep] > 0 ? 1 : 0);
       if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0) n += 2;
     }
     pl->n_launches = n;
@@ -499,28 +530,50 @@ int hdd_plan_destroy(HddPlan* pl) {
   if (!pl) return HDD_OK;
   if (pl->device >= 0) {
     cudaSetDevice(pl->device);
-    if (pl->stream) cudaStreamSynchronize(pl->stream);
+    cudaDeviceSynchronize();
     for (void* p : pl->allocs) cudaFree(p);
     if (pl->d_Z) cudaFree(pl->d_Z);
     if (pl->d_S) cudaFree(pl->d_S);
     if (pl->d_ll) cudaFree(pl->d_ll);
     if (pl->graph) cudaGraphExecDestroy(pl->graph);
+    for (cudaEvent_t e : pl->pipe_ev) cudaEventDestroy(e);
+    if (pl->cs_in) cudaStreamDestroy(pl->cs_in);
+    if (pl->cs_out) cudaStreamDestroy(pl->cs_out);
+    if (pl->h_err) cudaFreeHost(pl->h_err);
     if (pl->stream) cudaStreamDestroy(pl->stream);
   }
   delete pl;
   return HDD_OK;
 }
 
-static int run_sub_batch(HddPlan* pl, const double* Z, int B, double* S, double* ll, cudaStream_t st,
-                         cudaEvent_t* ev = nullptr) {
+// One sub-batch through the whole launch sequence.  Z (n_z per row) or, when Kin is
+// given, caller-supplied coefficient fields Kin [B][2N^2] (K1 replaced by a check
+// kernel); U non-NULL: the full-solution path (primal sweep + in-leaf solves).
+// sample0 = global index of the sub-batch's first row (failure records).
+static int run_sub_batch(HddPlan* pl, const double* Z, const double* Kin, int B, double* S, double* ll, double* U,
+                         cudaStream_t st, int64_t sample0, cudaEvent_t* ev = nullptr) {
   Plan& P = pl->plan;
-  DevPlan& D = pl->dev;
+  DevPlan D = pl->dev;                 // by-value copy: per-sub-batch fields
+  D.sample0 = sample0;
+  if (Kin) D.kappa = const_cast<double*>(Kin);
+  const int64_t nn = int64_t(P.m) * P.m;
   int e = 0;
-  if (ev) CU(cudaEventRecord(ev[e++], st));
-  CU(launch_kappa(D, Z, B, D.kappa, st));
-  if (ev) CU(cudaEventRecord(ev[e++], st));
+  auto mark = [&]() -> int {
+    if (ev) CU(cudaEventRecord(ev[e++], st));
+    return HDD_OK;
+  };
+  int rc;
+  if ((rc = mark())) return rc;
+  if (Kin) CU(launch_kappa_check(D, Kin, B, st));
+  else CU(launch_kappa(D, Z, B, D.kappa, st));
+  if ((rc = mark())) return rc;
+  if (P.tiny) {
+    CU(launch_tiny(D, B, S, ll, U, nn, st));
+    if ((rc = mark())) return rc;
+    return mark();                     // empty finalize stage
+  }
   CU(launch_leaf(D, B, st, nullptr));
-  if (ev) CU(cudaEventRecord(ev[e++], st));
+  if ((rc = mark())) return rc;
   for (int dep = int(P.upper_by_depth.size()) - 1; dep >= 0; --dep) {
     const auto& ids = P.upper_by_depth[dep];
     if (!ids.empty()) {
@@ -530,46 +583,94 @@ static int run_sub_batch(HddPlan* pl, const double* Z, int B, double* S, double*
         CU(launch_compress(D, pl->d_upper + ids.front(), int(ids.size()), pl->lr_blk0[dep], pl->lr_nblk[dep], B,
                            pl->lr_pmax[dep], st));
     }
-    if (ev) CU(cudaEventRecord(ev[e++], st));
+    if ((rc = mark())) return rc;
   }
   if (D.mode == 1) {
-    for (int dep = 0; dep < int(P.upper_by_depth.size()); ++dep) {
-      const auto& ids = P.upper_by_depth[dep];
-      if (!ids.empty())
-        CU(launch_topdown(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->depth_kng[dep], st));
-    }
+    // only the nodes on root-to-observation paths (every node in a full-solution plan)
+    for (int dep = 0; dep < int(P.upper_by_depth.size()); ++dep)
+      if (pl->td_count[dep] > 0)
+        CU(launch_topdown(D, pl->d_td + pl->td_first[dep], pl->td_count[dep], B, pl->depth_kng[dep], st));
   }
-  CU(launch_finalize(D, B, S, ll, st));
-  if (ev) CU(cudaEventRecord(ev[e++], st));
+  if (U) CU(launch_leaf_solve(D, B, U, nn, st));
+  else CU(launch_finalize(D, B, S, ll, st));
+  return mark();
+}
+
+// Failures are recorded on the device (sticky atomicMin key, DevError) and copied
+// to a pinned host word at the end of every call, on the call's stream: a call
+// returns as soon as its work is queued.  take_error() turns a recorded failure
+// into the plan's HddError (lowest failing sample of the call that failed) and
+// resets the record; it is reached from hdd_sync, from the synchronous entry
+// points, and at the start of the next call when the copy has already landed.
+static int enqueue_error_copy(HddPlan* pl, cudaStream_t st) {
+  CU(cudaMemcpyAsync(pl->h_err, pl->dev.err, sizeof(DevError), cudaMemcpyDeviceToHost, st));
   return HDD_OK;
 }
 
-static int check_device_error(HddPlan* pl, cudaStream_t st, int64_t b0) {
-  DevError e{};
-  CU(cudaMemcpyAsync(&e, pl->dev.err, sizeof(e), cudaMemcpyDeviceToHost, st));
+static int take_error(HddPlan* pl) {
+  const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(pl->h_err);
+  if (key == kNoError) return HDD_OK;
+  CU(cudaDeviceSynchronize());          // error path: drain every queued copy first
+  const unsigned long long k2 = *reinterpret_cast<volatile unsigned long long*>(pl->h_err);
+  CU(cudaMemset(pl->dev.err, 0xff, sizeof(DevError)));
+  *pl->h_err = kNoError;
+  int code;
+  long long sample, node;
+  dev_error_decode(std::min(key, k2), &code, &sample, &node);
+  std::string msg;
+  if (code == HDD_ERR_NUMERICAL)
+    msg = node >= 0 ? "interface block at node " + std::to_string(node) + " is not positive definite"
+                    : "non-finite forward observation";
+  else
+    msg = "coefficient values must be positive finite reals";
+  return set_err(&pl->err, code, msg, int(sample), node);
+}
+
+static int sync_and_check(HddPlan* pl, cudaStream_t st) {
   CU(cudaStreamSynchronize(st));
-  if (e.code != 0) {
-    CU(cudaMemsetAsync(pl->dev.err, 0, sizeof(DevError), st));
-    CU(cudaStreamSynchronize(st));
-    std::string msg;
-    if (e.code == HDD_ERR_NUMERICAL)
-      msg = e.node >= 0 ? "interface block at node " + std::to_string(e.node) + " is not positive definite"
-                        : "non-finite forward observation";
-    else
-      msg = "coefficient values must be positive finite reals";
-    return set_err(&pl->err, e.code, msg, int(b0 + e.sample), e.node);
-  }
+  return take_error(pl);
+}
+
+static int check_call(HddPlan* pl, int64_t B, const void* in, bool want_separable) {
+  if (!pl) return HDD_ERR_USAGE;
+  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan cannot run a forward batch");
+  if (B < 0 || (B > 0 && !in)) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  if (want_separable && !pl->plan.separable)
+    return set_err(&pl->err, HDD_ERR_USAGE,
+                   "plan has no separable parametrization: pass coefficient fields (hdd_forward_batch_kappa)");
   return HDD_OK;
+}
+
+// Sub-batched launch of a whole batch on `st` (asynchronous).
+static int run_batch(HddPlan* pl, const double* Z, const double* Kin, int64_t B, double* S, double* ll, double* U,
+                     cudaStream_t st) {
+  const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
+  const int64_t nt = int64_t(2) * pl->plan.N * pl->plan.N, nn = int64_t(pl->plan.m) * pl->plan.m;
+  for (int64_t done = 0; done < B;) {
+    const int b = int(std::min<int64_t>(pl->bcap, B - done));
+    const int rc = run_sub_batch(pl, Z ? Z + done * nz : nullptr, Kin ? Kin + done * nt : nullptr, b,
+                                 S ? S + done * no : nullptr, ll ? ll + done : nullptr, U ? U + done * nn : nullptr, st,
+                                 done);
+    if (rc != HDD_OK) return rc;
+    done += b;
+  }
+  return enqueue_error_copy(pl, st);
+}
+
+int hdd_sync(HddPlan* pl, void* stream) {
+  if (!pl) return HDD_ERR_USAGE;
+  if (pl->device < 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  return sync_and_check(pl, static_cast<cudaStream_t>(stream));
 }
 
 int hdd_forward_batch(HddPlan* pl, const double* Z, int64_t B, double* S, double* ll, void* stream) {
-  if (!pl) return HDD_ERR_USAGE;
-  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan cannot run a forward batch");
-  if (B < 0 || (B > 0 && !Z)) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  int rc = check_call(pl, B, Z, true);
+  if (rc != HDD_OK) return rc;
   if (B == 0) return HDD_OK;
   CU(cudaSetDevice(pl->device));
+  if ((rc = take_error(pl)) != HDD_OK) return rc;     // an earlier call's failure has landed
   cudaStream_t st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
-  const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
   static const bool no_graph = [] { const char* v = std::getenv("HDD_NO_GRAPH"); return v && v[0] == '1'; }();
   if (B <= pl->bcap && !no_graph) {
     const bool same = pl->g_seen && pl->g_Z == Z && pl->g_S == S && pl->g_ll == ll && pl->g_B == int(B);
@@ -584,15 +685,13 @@ int hdd_forward_batch(HddPlan* pl, const double* Z, int64_t B, double* S, double
       pl->g_ll = ll;
       pl->g_B = int(B);
       pl->g_seen = true;
-      const int rc = run_sub_batch(pl, Z, int(B), S, ll, st);
-      if (rc != HDD_OK) return rc;
-      return check_device_error(pl, st, 0);
+      return run_batch(pl, Z, nullptr, B, S, ll, nullptr, st);
     }
     if (!pl->graph) {
       // second call with the same buffers: capture the launch sequence (kappa, leaf
       // classes, one merge per depth, ..., finalize) once, replay it from now on
       CU(cudaStreamBeginCapture(pl->stream, cudaStreamCaptureModeThreadLocal));
-      const int rc = run_sub_batch(pl, Z, int(B), S, ll, pl->stream);
+      rc = run_sub_batch(pl, Z, nullptr, int(B), S, ll, nullptr, pl->stream, 0);
       cudaGraph_t g = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(pl->stream, &g);
       if (rc != HDD_OK) {
@@ -605,35 +704,38 @@ int hdd_forward_batch(HddPlan* pl, const double* Z, int64_t B, double* S, double
       CU(ie);
     }
     CU(cudaGraphLaunch(pl->graph, st));
-    return check_device_error(pl, st, 0);
+    return enqueue_error_copy(pl, st);
   }
-  int64_t done = 0;
-  while (done < B) {
-    int b = int(std::min<int64_t>(pl->bcap, B - done));
-    int rc = run_sub_batch(pl, Z + done * nz, b, S ? S + done * no : nullptr, ll ? ll + done : nullptr, st);
-    if (rc != HDD_OK) return rc;
-    done += b;
-  }
-  return check_device_error(pl, st, 0);
+  return run_batch(pl, Z, nullptr, B, S, ll, nullptr, st);
+}
+
+int hdd_forward_batch_kappa(HddPlan* pl, const double* K, int64_t B, double* S, double* ll, void* stream) {
+  int rc = check_call(pl, B, K, false);
+  if (rc != HDD_OK) return rc;
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  if ((rc = take_error(pl)) != HDD_OK) return rc;
+  return run_batch(pl, nullptr, K, B, S, ll, nullptr, static_cast<cudaStream_t>(stream));
 }
 
 int hdd_forward_batch_timed(HddPlan* pl, const double* Z, int64_t B, double* S, double* ll, void* stream,
                             double* stage_ms, int32_t n_stages) {
-  if (!pl) return HDD_ERR_USAGE;
-  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan cannot run a forward batch");
+  int rc = check_call(pl, B, Z, true);
+  if (rc != HDD_OK) return rc;
   const int ns = pl->plan.leaf_depth + 3;
   if (n_stages != ns || !stage_ms) return set_err(&pl->err, HDD_ERR_USAGE, "stage_ms must hold leaf_depth + 3 entries");
-  if (B <= 0 || !Z) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  if (B <= 0) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
   CU(cudaSetDevice(pl->device));
+  if ((rc = take_error(pl)) != HDD_OK) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
   std::vector<cudaEvent_t> ev(ns + 1);
   for (auto& e : ev) CU(cudaEventCreate(&e));
   const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
   int64_t done = 0;
-  int rc = HDD_OK;
   while (done < B && rc == HDD_OK) {
     int b = int(std::min<int64_t>(pl->bcap, B - done));
-    rc = run_sub_batch(pl, Z + done * nz, b, S ? S + done * no : nullptr, ll ? ll + done : nullptr, st, ev.data());
+    rc = run_sub_batch(pl, Z + done * nz, nullptr, b, S ? S + done * no : nullptr, ll ? ll + done : nullptr, nullptr,
+                       st, done, ev.data());
     if (rc == HDD_OK) {
       CU(cudaEventSynchronize(ev[ns]));
       for (int i = 0; i < ns; ++i) {
@@ -646,81 +748,143 @@ int hdd_forward_batch_timed(HddPlan* pl, const double* Z, int64_t B, double* S, 
   }
   for (auto& e : ev) cudaEventDestroy(e);
   if (rc != HDD_OK) return rc;
-  return check_device_error(pl, st, 0);
+  if ((rc = enqueue_error_copy(pl, st)) != HDD_OK) return rc;
+  return sync_and_check(pl, st);
 }
 
-int hdd_forward_batch_host(HddPlan* pl, const double* Zh, int64_t B, double* Sh, double* llh) {
-  if (!pl) return HDD_ERR_USAGE;
-  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan cannot run a forward batch");
-  if (B <= 0) return B == 0 ? HDD_OK : set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
-  CU(cudaSetDevice(pl->device));
-  const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
-  if (B > pl->io_cap) {
+// Host buffers: the batch is cut into sub-batches; the H2D copy of sub-batch i+1 (copy
+// stream in) and the D2H copy of sub-batch i-1's results (copy stream out) overlap
+// the compute of sub-batch i on the plan's stream.  Returns when the results are in
+// host memory.  `in_w` doubles per input row (n_z for Z, 2N^2 for kappa fields).
+static int run_host(HddPlan* pl, const double* Xh, int in_w, bool is_kappa, int64_t B, double* Sh, double* llh) {
+  const int no = int(pl->plan.obs_kind.size());
+  const int64_t nb = (B + pl->bcap - 1) / pl->bcap;
+  if (B > pl->io_cap || (is_kappa && !pl->io_kappa) || (!is_kappa && pl->io_kappa)) {
     if (pl->d_Z) cudaFree(pl->d_Z);
     if (pl->d_S) cudaFree(pl->d_S);
     if (pl->d_ll) cudaFree(pl->d_ll);
-    CU(cudaMalloc(&pl->d_Z, size_t(B) * nz * 8));
+    pl->d_Z = pl->d_S = pl->d_ll = nullptr;
+    pl->io_cap = 0;
+    CU(cudaMalloc(&pl->d_Z, size_t(B) * std::max(in_w, 1) * 8));
     CU(cudaMalloc(&pl->d_S, size_t(B) * no * 8));
     CU(cudaMalloc(&pl->d_ll, size_t(B) * 8));
     pl->io_cap = B;
+    pl->io_kappa = is_kappa;
   }
   cudaStream_t st = pl->stream;
-  CU(cudaMemcpyAsync(pl->d_Z, Zh, size_t(B) * nz * 8, cudaMemcpyHostToDevice, st));
-  int rc = hdd_forward_batch(pl, pl->d_Z, B, Sh ? pl->d_S : nullptr, llh ? pl->d_ll : nullptr, st);
+  while (int64_t(pl->pipe_ev.size()) < 2 * nb) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    pl->pipe_ev.push_back(e);
+  }
+  auto rows = [&](int64_t i) { return std::min<int64_t>(pl->bcap, B - i * pl->bcap); };
+  auto h2d = [&](int64_t i) -> int {
+    const int64_t r0 = i * pl->bcap;
+    CU(cudaMemcpyAsync(pl->d_Z + r0 * in_w, Xh + r0 * in_w, size_t(rows(i)) * in_w * 8, cudaMemcpyHostToDevice,
+                       pl->cs_in));
+    CU(cudaEventRecord(pl->pipe_ev[2 * i], pl->cs_in));
+    return HDD_OK;
+  };
+  int rc;
+  if ((rc = h2d(0))) return rc;
+  for (int64_t i = 0; i < nb; ++i) {
+    const int64_t r0 = i * pl->bcap;
+    const int b = int(rows(i));
+    CU(cudaStreamWaitEvent(st, pl->pipe_ev[2 * i], 0));
+    const double* x = pl->d_Z + r0 * in_w;
+    rc = run_sub_batch(pl, is_kappa ? nullptr : x, is_kappa ? x : nullptr, b, Sh ? pl->d_S + r0 * no : nullptr,
+                       llh ? pl->d_ll + r0 : nullptr, nullptr, st, r0);
+    if (rc != HDD_OK) return rc;
+    CU(cudaEventRecord(pl->pipe_ev[2 * i + 1], st));
+    if (i + 1 < nb && (rc = h2d(i + 1))) return rc;
+    CU(cudaStreamWaitEvent(pl->cs_out, pl->pipe_ev[2 * i + 1], 0));
+    if (Sh) CU(cudaMemcpyAsync(Sh + r0 * no, pl->d_S + r0 * no, size_t(b) * no * 8, cudaMemcpyDeviceToHost, pl->cs_out));
+    if (llh) CU(cudaMemcpyAsync(llh + r0, pl->d_ll + r0, size_t(b) * 8, cudaMemcpyDeviceToHost, pl->cs_out));
+  }
+  if ((rc = enqueue_error_copy(pl, st)) != HDD_OK) return rc;
+  CU(cudaStreamSynchronize(pl->cs_out));
+  return sync_and_check(pl, st);
+}
+
+int hdd_forward_batch_host(HddPlan* pl, const double* Zh, int64_t B, double* Sh, double* llh) {
+  int rc = check_call(pl, B, Zh, true);
   if (rc != HDD_OK) return rc;
-  if (Sh) CU(cudaMemcpyAsync(Sh, pl->d_S, size_t(B) * no * 8, cudaMemcpyDeviceToHost, st));
-  if (llh) CU(cudaMemcpyAsync(llh, pl->d_ll, size_t(B) * 8, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  return HDD_OK;
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  if ((rc = take_error(pl)) != HDD_OK) return rc;
+  return run_host(pl, Zh, pl->plan.n_z, false, B, Sh, llh);
+}
+
+int hdd_forward_batch_kappa_host(HddPlan* pl, const double* Kh, int64_t B, double* Sh, double* llh) {
+  int rc = check_call(pl, B, Kh, false);
+  if (rc != HDD_OK) return rc;
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  if ((rc = take_error(pl)) != HDD_OK) return rc;
+  return run_host(pl, Kh, 2 * pl->plan.N * pl->plan.N, true, B, Sh, llh);
+}
+
+static int solve_common(HddPlan* pl, const double* Z, const double* K, int64_t B, double* U, void* stream) {
+  if ((pl->dev.mode != 1 || !pl->plan.full_solve) && pl->plan.leaf_depth > 0)   // a single-leaf tree has no interfaces
+    return set_err(&pl->err, HDD_ERR_USAGE,
+                   "the full-solution sweep requires a full-solution plan (mode = 1, full_solve = 1 keeps every factor)");
+  if (B > 0 && !U) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  int rc = take_error(pl);
+  if (rc != HDD_OK) return rc;
+  return run_batch(pl, Z, K, B, nullptr, nullptr, U, static_cast<cudaStream_t>(stream));
 }
 
 int hdd_solve_batch(HddPlan* pl, const double* Z, int64_t B, double* U, void* stream) {
-  if (!pl) return HDD_ERR_USAGE;
-  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan cannot run a solve");
-  if (pl->dev.mode != 1 && pl->plan.leaf_depth > 0)   // a single-leaf tree has no interfaces to sweep
-    return set_err(&pl->err, HDD_ERR_USAGE, "the full-solution sweep requires a primal plan (mode = 1 keeps the factors)");
-  if (B < 0 || (B > 0 && (!Z || !U))) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
-  if (B == 0) return HDD_OK;
-  CU(cudaSetDevice(pl->device));
-  cudaStream_t st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
-  const int nz = pl->plan.n_z;
-  const int64_t nn = int64_t(pl->plan.m) * pl->plan.m;
-  for (int64_t done = 0; done < B;) {
-    const int b = int(std::min<int64_t>(pl->bcap, B - done));
-    int rc = run_sub_batch(pl, Z + done * nz, b, nullptr, nullptr, st);
-    if (rc != HDD_OK) return rc;
-    CU(launch_leaf_solve(pl->dev, b, U + done * nn, nn, st));
-    done += b;
-  }
-  return check_device_error(pl, st, 0);
+  int rc = check_call(pl, B, Z, true);
+  if (rc != HDD_OK) return rc;
+  return solve_common(pl, Z, nullptr, B, U, stream);
 }
 
-int hdd_solve_batch_host(HddPlan* pl, const double* Zh, int64_t B, double* Uh) {
-  if (!pl) return HDD_ERR_USAGE;
-  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan cannot run a solve");
-  if (B < 0 || (B > 0 && (!Zh || !Uh))) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+int hdd_solve_batch_kappa(HddPlan* pl, const double* K, int64_t B, double* U, void* stream) {
+  int rc = check_call(pl, B, K, false);
+  if (rc != HDD_OK) return rc;
+  return solve_common(pl, nullptr, K, B, U, stream);
+}
+
+static int solve_host(HddPlan* pl, const double* Xh, bool is_kappa, int64_t B, double* Uh) {
   if (B == 0) return HDD_OK;
   CU(cudaSetDevice(pl->device));
-  const int nz = pl->plan.n_z;
+  const int64_t in_w = is_kappa ? int64_t(2) * pl->plan.N * pl->plan.N : pl->plan.n_z;
   const int64_t nn = int64_t(pl->plan.m) * pl->plan.m;
-  double* dZ = nullptr;
+  double* dX = nullptr;
   double* dU = nullptr;
-  CU(cudaMalloc(&dZ, size_t(B) * nz * 8));
+  CU(cudaMalloc(&dX, size_t(B) * std::max<int64_t>(in_w, 1) * 8));
   if (cudaMalloc(&dU, size_t(B) * nn * 8) != cudaSuccess) {
     cudaGetLastError();
-    cudaFree(dZ);
+    cudaFree(dX);
     return set_err(&pl->err, HDD_ERR_NOMEM, "device allocation of the solution buffer failed");
   }
   cudaStream_t st = pl->stream;
   int rc = HDD_OK;
-  if (cudaMemcpyAsync(dZ, Zh, size_t(B) * nz * 8, cudaMemcpyHostToDevice, st) != cudaSuccess) rc = HDD_ERR_CUDA;
-  if (rc == HDD_OK) rc = hdd_solve_batch(pl, dZ, B, dU, st);
+  if (cudaMemcpyAsync(dX, Xh, size_t(B) * in_w * 8, cudaMemcpyHostToDevice, st) != cudaSuccess) rc = HDD_ERR_CUDA;
+  if (rc == HDD_OK) rc = solve_common(pl, is_kappa ? nullptr : dX, is_kappa ? dX : nullptr, B, dU, st);
   if (rc == HDD_OK && cudaMemcpyAsync(Uh, dU, size_t(B) * nn * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
     rc = HDD_ERR_CUDA;
-  if (rc == HDD_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = HDD_ERR_CUDA;
-  cudaFree(dZ);
+  if (rc == HDD_OK) rc = sync_and_check(pl, st);
+  cudaFree(dX);
   cudaFree(dU);
   return rc;
+}
+
+int hdd_solve_batch_host(HddPlan* pl, const double* Zh, int64_t B, double* Uh) {
+  int rc = check_call(pl, B, Zh, true);
+  if (rc != HDD_OK) return rc;
+  if (B > 0 && !Uh) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  return solve_host(pl, Zh, false, B, Uh);
+}
+
+int hdd_solve_batch_kappa_host(HddPlan* pl, const double* Kh, int64_t B, double* Uh) {
+  int rc = check_call(pl, B, Kh, false);
+  if (rc != HDD_OK) return rc;
+  if (B > 0 && !Uh) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  return solve_host(pl, Kh, true, B, Uh);
 }
 
 int hdd_posterior_weights(const double* ll, const double* lp, int64_t n, double* w, int64_t* idx, double* lse,
@@ -732,17 +896,22 @@ int hdd_posterior_weights(const double* ll, const double* lp, int64_t n, double*
 }
 
 int hdd_kappa_batch(HddPlan* pl, const double* Z, int64_t B, double* kappa, void* stream) {
-  if (!pl) return HDD_ERR_USAGE;
-  if (pl->device < 0) return set_err(&pl->err, HDD_ERR_USAGE, "host-only plan");
+  int rc = check_call(pl, B, Z, true);
+  if (rc != HDD_OK) return rc;
+  if (B > 0 && !kappa) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
   CU(cudaSetDevice(pl->device));
+  if ((rc = take_error(pl)) != HDD_OK) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);   // NULL = legacy default stream
   const int64_t nt = int64_t(2) * pl->plan.N * pl->plan.N;
   for (int64_t done = 0; done < B;) {
     int b = int(std::min<int64_t>(pl->bcap, B - done));
-    CU(launch_kappa(pl->dev, Z + done * pl->plan.n_z, b, kappa + done * nt, st));
+    DevPlan D = pl->dev;
+    D.sample0 = done;
+    CU(launch_kappa(D, Z + done * pl->plan.n_z, b, kappa + done * nt, st));
     done += b;
   }
-  return check_device_error(pl, st, 0);
+  if ((rc = enqueue_error_copy(pl, st)) != HDD_OK) return rc;
+  return sync_and_check(pl, st);
 }
 
 int hdd_last_error(const HddPlan* pl, HddError* out) {
@@ -768,6 +937,12 @@ int hdd_plan_info(const HddPlan* pl, HddPlanInfo* out) {
   for (int64_t e : P.buf_elems_per_sample) ws += e;
   out->workspace_bytes = ws * 8 * std::max(1, pl->bcap);
   out->mode = P.mode;
+  int ntd = 0;
+  for (const auto& v : P.td_by_depth) ntd += int(v.size());
+  out->n_topdown = ntd;
+  out->tiny = P.tiny ? 1 : 0;
+  out->separable = P.separable ? 1 : 0;
+  out->full_solve = P.full_solve ? 1 : 0;
   return HDD_OK;
 }
 

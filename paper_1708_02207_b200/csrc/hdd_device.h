@@ -45,11 +45,21 @@ struct DevLeaf {
   int parent;              // upper index of the father (-1 when the leaf is the root)
 };
 
+// Device failure record: key = sample << 33 | (code == NUMERICAL) << 32 | (node + 1),
+// ~0 = no failure (reset value).  Reference node ids < 2^31 (level <= 11).
 struct DevError {
-  int code;                // 0 ok, else HDD_ERR_*
-  int sample;
-  long long node;          // reference node id
+  unsigned long long key;
 };
+constexpr unsigned long long kNoError = ~0ull;
+__host__ __device__ inline unsigned long long dev_error_key(long long sample, int code, long long node) {
+  return (static_cast<unsigned long long>(sample) << 33) | (static_cast<unsigned long long>(code != -1) << 32) |
+         static_cast<unsigned long long>((node + 1) & 0xffffffffll);
+}
+inline void dev_error_decode(unsigned long long key, int* code, long long* sample, long long* node) {
+  *sample = static_cast<long long>(key >> 33);
+  *code = ((key >> 32) & 1) ? -3 : -1;     // HDD_ERR_NUMERICAL : HDD_ERR_CONFIG
+  *node = static_cast<long long>(key & 0xffffffffull) - 1;
+}
 
 struct DevPlan {
   int N, m, n_z, n_obs, n_leaves, leaf_cols, leaf_ld;
@@ -102,6 +112,11 @@ struct DevPlan {
   double* buf[kMaxBuffers];
   double* kappa;           // [bcap][2 N^2]
   DevError* err;
+  int64_t sample0;         // global index of the sub-batch's first sample (error records)
+  // meshes below one kernel leaf (levels 1-3): tiny_kernel
+  int tiny;
+  const double* gfull;     // [m*m] Dirichlet value at every boundary node (interior 0), NULL = g = 0
+  long long root_ref;      // reference id of the root (error records)
 };
 
 // launchers (hdd_kernels.cu); all return cudaError_t of the launch
@@ -118,6 +133,8 @@ cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cuda
 cudaError_t launch_posterior(const double* ll, const double* lp, int64_t n, double* w, int64_t* idx, double* lse,
                              cudaStream_t s);
 cudaError_t launch_leaf_solve(const DevPlan& p, int B, double* U, int64_t n_nodes, cudaStream_t s);
+cudaError_t launch_kappa_check(const DevPlan& p, const double* kappa, int B, cudaStream_t s);
+cudaError_t launch_tiny(const DevPlan& p, int B, double* S, double* ll, double* U, int64_t n_nodes, cudaStream_t s);
 size_t leaf_smem_bytes(int leaf_cols);
 int upload_leaf_template();
 int read_leaf_clocks(long long* out);

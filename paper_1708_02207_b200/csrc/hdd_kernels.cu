@@ -33,11 +33,11 @@ namespace hdd {
 // ---------------------------------------------------------------------------
 // shared helpers
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void record_error(DevError* e, int code, int sample, long long node) {
-  if (atomicCAS(&e->code, 0, code) == 0) {
-    e->sample = sample;
-    e->node = node;
-  }
+// Failure record: one 64-bit key, atomicMin over (global sample, kind, node) so the
+// reported failure is the lowest failing sample of the batch — the one the reference's
+// per-sample loop would raise on — independent of CTA scheduling and sub-batching.
+__device__ __forceinline__ void record_error(const DevPlan& p, int code, int sample, long long node) {
+  atomicMin(&p.err->key, dev_error_key(p.sample0 + sample, code, node));
 }
 
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(128) kappa_kernel(DevPlan p, const double* __r
       if (g + r < nrow) out[int64_t(i0 + g + r) * N + j] = v;
     }
   }
-  if (bad) record_error(p.err, HDD_ERR_CONFIG, s, -1);
+  if (bad) record_error(p, HDD_ERR_CONFIG, s, -1);
 }
 
 cudaError_t launch_kappa(const DevPlan& p, const double* Z, int B, double* kappa, cudaStream_t s) {
@@ -548,7 +548,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 #pragma unroll
       for (int l = 0; l < ng; ++l)
         if (l <= i) P[i * W + l] = a[l];
-      if (i == 0 && bad) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(leaf_ref, R, q));
+      if (i == 0 && bad) record_error(p, HDD_ERR_NUMERICAL, s, inleaf_ref_id(leaf_ref, R, q));
     }
     LEAF_TICK(10 + 8 * (5 - R) + 4);
 #ifdef HDD_AB_SERIAL_B
@@ -953,7 +953,7 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
         }
       // eliminate the centre node 4
       const double dpiv = A[tri(4) + 4];
-      if (!(dpiv > 0.0)) record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, 6, q));
+      if (!(dpiv > 0.0)) record_error(p, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, 6, q));
       const double inv = 1.0 / sqrt(dpiv);
       double xv[9];
 #pragma unroll
@@ -1052,7 +1052,7 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
       const double p1 = ia * ic - ib * ib;
       const double det = p1 * ie - ia * idd * idd;
       if (a == 0 && (!(ia > 0.0) || !(p1 > 0.0) || !(det > 0.0)))
-        record_error(p.err, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, 5, q));
+        record_error(p, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, 5, q));
       const double rdet = 1.0 / det;
       const double M00 = (ic * ie - idd * idd) * rdet, M01 = -ib * ie * rdet, M02 = ib * idd * rdet;
       const double M11 = ia * ie * rdet, M12 = -ia * idd * rdet, M22 = p1 * rdet;
@@ -1962,8 +1962,8 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
   }
   __syncthreads();
   MERGE_TICK(3);
-  if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
-  if (p.mode == 1) store_factors(p, U, s, P, ldp, Kp, false, tid, NT);
+  if (s_bad && tid == 0) record_error(p, HDD_ERR_NUMERICAL, s, U.ref_id);
+  if (p.mode == 1 && U.fac_off >= 0) store_factors(p, U, s, P, ldp, Kp, false, tid, NT);
   double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
   const int tk = tri(k);
   for (int c = tid; c < nc; c += NT) {
@@ -2135,8 +2135,8 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
     __syncthreads();
   }
   MERGE_TICK(3);
-  if (s_bad && tid == 0) record_error(p.err, HDD_ERR_NUMERICAL, s, U.ref_id);
-  if (p.mode == 1) store_factors(p, U, s, P, ldp, Kp, false, tid, 256);
+  if (s_bad && tid == 0) record_error(p, HDD_ERR_NUMERICAL, s, U.ref_id);
+  if (p.mode == 1 && U.fac_off >= 0) store_factors(p, U, s, P, ldp, Kp, false, tid, 256);
   double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
   const int tk = tri(k);
   for (int c = tid; c < nc; c += 256) {
@@ -2196,9 +2196,11 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
 }
 
 // ---------------------------------------------------------------------------
-// K4 (primal): top-down interface back-solve restricted to what F needs
-// (root_to_leaves, hdd.py:397-432): u_gamma = L^-T (v - W u_B), one CTA per
-// (node, sample), depth by depth from the root.
+// K4 (primal): top-down interface back-solve (root_to_leaves, hdd.py:397-432):
+// u_gamma = L^-T (v - W u_B), one CTA per (node, sample), depth by depth from the
+// root.  The likelihood sweep launches it only on the nodes of the plan's td lists
+// (ancestors of the observation owners, hdd_plan.cpp); the merges store factors
+// only for those nodes.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) topdown_kernel(DevPlan p, const DevUpper* __restrict__ nodes) {
   extern __shared__ __align__(16) double sm[];
@@ -2333,40 +2335,43 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
   // JG thread groups split the columns when the block has few rows
   const int JG = P_ >= 256 ? 1 : (P_ >= 128 ? 2 : (P_ >= 64 ? 4 : 8));
   const int RS = 256 / JG;
-  if (JG > 1)
-    for (int t = tid; t < P_ * 33; t += 256) Y[t] = 0.0;
-  __syncthreads();
   double an = 0.0;
   {
+    // the JG column groups of a row meet in smem in a fixed order (group 0 stores,
+    // groups 1.. add one after another): bitwise reproducible, no atomics
     const int jg = tid / RS, ir = tid - (tid / RS) * RS;
-    for (int i0 = 0; i0 < P_; i0 += RS) {
+    for (int i0 = 0; i0 < P_; i0 += RS) {     // uniform trip count (barriers below)
       const int i = i0 + ir;
-      if (i >= P_) continue;
+      const bool live = i < P_;
       double acc[LW];
 #pragma unroll
       for (int t = 0; t < LW; ++t) acc[t] = 0.0;
-      const int r = R[i];
-      const int tr = tri(r);
-      for (int j = jg; j < Q_; j += JG) {
-        const int c = Cc[j];
-        const double a = r >= c ? psi[tr + c] : psi[tri(c) + r];
-        an = fma(a, a, an);
-        const double2* om = reinterpret_cast<const double2*>(p.lr_omega + j * 32);
+      if (live) {
+        const int r = R[i];
+        const int tr = tri(r);
+        for (int j = jg; j < Q_; j += JG) {
+          const int c = Cc[j];
+          const double a = r >= c ? psi[tr + c] : psi[tri(c) + r];
+          an = fma(a, a, an);
+          const double2* om = reinterpret_cast<const double2*>(p.lr_omega + j * 32);
 #pragma unroll
-        for (int t = 0; t < LW; t += 2) {
-          const double2 o = __ldg(om + t / 2);
-          acc[t] = fma(a, o.x, acc[t]);
-          acc[t + 1] = fma(a, o.y, acc[t + 1]);
+          for (int t = 0; t < LW; t += 2) {
+            const double2 o = __ldg(om + t / 2);
+            acc[t] = fma(a, o.x, acc[t]);
+            acc[t + 1] = fma(a, o.y, acc[t + 1]);
+          }
         }
       }
       double* yr = Y + i * 33;
-      if (JG == 1) {
+      for (int g = 0; g < JG; ++g) {
+        if (live && jg == g) {
 #pragma unroll
-        for (int t = 0; t < 32; ++t) yr[t] = (t < LW && t < L) ? acc[t < LW ? t : 0] : 0.0;
-      } else {
-#pragma unroll
-        for (int t = 0; t < LW; ++t)
-          if (t < L) atomicAdd(yr + t, acc[t]);
+          for (int t = 0; t < 32; ++t) {
+            const double v = (t < LW && t < L) ? acc[t < LW ? t : 0] : 0.0;
+            yr[t] = g == 0 ? v : yr[t] + v;
+          }
+        }
+        if (JG > 1) __syncthreads();
       }
     }
   }
@@ -2439,14 +2444,15 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
   for (int j0 = 0; j0 < Q_; j0 += 64) {
     __syncthreads();
     {   // B chunk: thread per (column, quarter of the rows), all LW rows of B in
-        // registers; each A entry read once, the quarters summed in smem
+        // registers; each A entry read once, the quarters summed in smem in a fixed
+        // order (quarter 0 stores, 1..3 add in turn: bitwise reproducible)
       for (int t = tid; t < 32 * 65; t += 256) Bc[t] = 0.0;
       __syncthreads();
       const int jj = tid & 63, ig = tid >> 6, j = j0 + jj;
-      if (j < Q_) {
-        double v[LW];
+      double v[LW];
 #pragma unroll
-        for (int u = 0; u < LW; ++u) v[u] = 0.0;
+      for (int u = 0; u < LW; ++u) v[u] = 0.0;
+      if (j < Q_) {
         const int c = Cc[j];
         const int tc = tri(c);
         for (int i = ig; i < P_; i += 4) {
@@ -2456,9 +2462,13 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
 #pragma unroll
           for (int u = 0; u < LW; ++u) v[u] = fma(yr[u], x, v[u]);
         }
+      }
+      for (int g = 0; g < 4; ++g) {
+        if (ig == g && j < Q_)
 #pragma unroll
-        for (int u = 0; u < LW; ++u)
-          if (u < L) atomicAdd(Bc + u * 65 + jj, v[u]);
+          for (int u = 0; u < LW; ++u)
+            if (u < L) Bc[u * 65 + jj] += v[u];
+        __syncthreads();
       }
     }
     __syncthreads();
@@ -2531,10 +2541,10 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
     __syncthreads();
     {
       const int jj = tid & 63, ig = tid >> 6, j = j0 + jj;
-      if (j < Q_) {
-        double v[LW];
+      double v[LW];
 #pragma unroll
-        for (int u = 0; u < LW; ++u) v[u] = 0.0;
+      for (int u = 0; u < LW; ++u) v[u] = 0.0;
+      if (j < Q_) {
         const int c = Cc[j];
         const int tc = tri(c);
         int pvt[LW];
@@ -2548,9 +2558,13 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
           for (int u = 0; u < LW; ++u)
             if (u < kk) v[u] = fma(yr[pvt[u]], x, v[u]);
         }
+      }
+      for (int g = 0; g < 4; ++g) {     // fixed-order sum of the row quarters
+        if (ig == g && j < Q_)
 #pragma unroll
-        for (int u = 0; u < LW; ++u)
-          if (u < kk) atomicAdd(Bc + u * 65 + jj, v[u]);
+          for (int u = 0; u < LW; ++u)
+            if (u < kk) Bc[u * 65 + jj] += v[u];
+        __syncthreads();
       }
     }
     __syncthreads();
@@ -2651,7 +2665,7 @@ __global__ void finalize_kernel(DevPlan p, int B, double* __restrict__ S, double
       const DevUpper& U = p.upper[p.route_node[o]];
       v = ub[U.u_off + U.k + p.route_col[o]];
     }
-    if (!isfinite(v)) record_error(p.err, HDD_ERR_NUMERICAL, s, -1);
+    if (!isfinite(v)) record_error(p, HDD_ERR_NUMERICAL, s, -1);
     if (S) S[int64_t(s) * p.n_obs + o] = v;
     if (p.y) {
       const double r = (p.y[o] - v) / p.sigma[o];
@@ -2675,16 +2689,23 @@ __global__ void __launch_bounds__(1024) posterior_kernel(const double* __restric
   __shared__ double s_mx, s_lse;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   auto joint = [&](int64_t t) { return lp ? ll[t] + lp[t] : ll[t]; };
+  // numpy argmax order: NaN ranks above every number (the first NaN wins), then the
+  // largest value, ties to the first index
+  auto better = [](double v, int64_t i, double m, int64_t mi_) {
+    const bool vn = isnan(v), mn = isnan(m);
+    if (vn != mn) return vn;
+    return (vn || v == m) ? i < mi_ : v > m;
+  };
   double mx = -INFINITY;
   int64_t mi = INT64_MAX;
   for (int64_t t = tid; t < n; t += blockDim.x) {
     const double v = joint(t);
-    if (v > mx || (v == mx && t < mi)) { mx = v; mi = t; }
+    if (better(v, t, mx, mi)) { mx = v; mi = t; }
   }
   for (int off = 16; off > 0; off >>= 1) {
     const double ov = __shfl_xor_sync(0xffffffffu, mx, off);
     const int64_t oi = __shfl_xor_sync(0xffffffffu, mi, off);
-    if (ov > mx || (ov == mx && oi < mi)) { mx = ov; mi = oi; }
+    if (better(ov, oi, mx, mi)) { mx = ov; mi = oi; }
   }
   if (lane == 0) { s_v[warp] = mx; s_i[warp] = mi; }
   __syncthreads();
@@ -2692,7 +2713,7 @@ __global__ void __launch_bounds__(1024) posterior_kernel(const double* __restric
     double m = s_v[0];
     int64_t i = s_i[0];
     for (int q = 1; q < nw; ++q)
-      if (s_v[q] > m || (s_v[q] == m && s_i[q] < i)) { m = s_v[q]; i = s_i[q]; }
+      if (better(s_v[q], s_i[q], m, i)) { m = s_v[q]; i = s_i[q]; }
     s_mx = m;
     *idx = i;
   }
@@ -2818,7 +2839,7 @@ __global__ void __launch_bounds__(32) leaf_solve_kernel(DevPlan p, double* __res
     }
     __syncwarp();
   }
-  if (lane == 0 && bad) record_error(p.err, HDD_ERR_NUMERICAL, s, L.ref_id);
+  if (lane == 0 && bad) record_error(p, HDD_ERR_NUMERICAL, s, L.ref_id);
   // L y = rhs
   for (int j = 0; j < kNI; ++j) {
     if (lane == 0) rhs[j] *= invd[j];
@@ -2852,6 +2873,143 @@ __global__ void __launch_bounds__(32) leaf_solve_kernel(DevPlan p, double* __res
 cudaError_t launch_leaf_solve(const DevPlan& p, int B, double* U, int64_t n_nodes, cudaStream_t s) {
   dim3 grid(p.n_leaves, B);
   leaf_solve_kernel<<<grid, 32, 0, s>>>(p, U, n_nodes);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Caller-supplied coefficient fields (hdd_forward_batch_kappa): the check of
+// CoefficientField (fem.py:31-32) — every value positive and finite — on the device.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) kappa_check_kernel(DevPlan p, const double* __restrict__ kappa, int64_t nt) {
+  const int s = blockIdx.y;
+  const double* kb = kappa + int64_t(s) * nt;
+  bool bad = false;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < nt; t += int64_t(gridDim.x) * blockDim.x) {
+    const double v = kb[t];
+    bad |= !(v > 0.0) || !isfinite(v);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) record_error(p, HDD_ERR_CONFIG, s, -1);
+}
+
+cudaError_t launch_kappa_check(const DevPlan& p, const double* kappa, int B, cudaStream_t s) {
+  const int64_t nt = int64_t(2) * p.N * p.N;
+  const int gx = int(std::min<int64_t>(64, (nt + 255) / 256));
+  kappa_check_kernel<<<dim3(gx, B), 256, 0, s>>>(p, kappa, nt);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Meshes below one kernel leaf (levels 1-3, N <= 8 cells per side): the whole
+// tree's Schur recursion collapses to the elimination of the (N-1)^2 interior
+// unknowns at the root (the reference's leaves_to_root on such a mesh ends in the
+// same SPD system).  One warp per sample: 5-point P1 stiffness from the cell
+// patterns (fem.py:126-145), lumped load h^2 f (psi_f = h^2/6 diag(2,1,1,2) per
+// cell), Dirichlet data moved to the right-hand side, dense Cholesky in shared
+// memory, then the observations (points, per-triangle means, oracle.py:74-83 /
+// functionals.py:47-61) and the Gaussian log-likelihood (bayes.py:222-224).
+// ---------------------------------------------------------------------------
+constexpr int kTinyN = 8, kTinyI = kTinyN - 1, kTinyNI = kTinyI * kTinyI;
+
+__global__ void __launch_bounds__(32) tiny_kernel(DevPlan p, int B, double* __restrict__ S, double* __restrict__ ll,
+                                                  double* __restrict__ U, int64_t n_nodes) {
+  __shared__ double kap[2 * kTinyN * kTinyN];
+  __shared__ double A[kTinyNI * kTinyNI];
+  __shared__ double rhs[kTinyNI];
+  __shared__ double u[(kTinyN + 1) * (kTinyN + 1)];
+  const int s = blockIdx.x, lane = threadIdx.x;
+  const int N = p.N, m = p.m, ni = N - 1, n = ni * ni;
+  const double* kb = p.kappa + int64_t(s) * 2 * N * N;
+  for (int t = lane; t < 2 * N * N; t += 32) kap[t] = kb[t];
+  for (int t = lane; t < m * m; t += 32) u[t] = p.gfull ? p.gfull[t] : 0.0;
+  for (int t = lane; t < n * n; t += 32) A[t] = 0.0;
+  __syncwarp();
+  auto k0 = [&](int cx, int cy) { return kap[2 * (cx * N + cy)]; };
+  auto k1 = [&](int cx, int cy) { return kap[2 * (cx * N + cy) + 1]; };
+  const double h2 = p.h * p.h;
+  // row j = interior node (x, y), x, y in 1..N-1; cells (x-1..x, y-1..y) all exist
+  for (int j = lane; j < n; j += 32) {
+    const int x = j % ni + 1, y = j / ni + 1;
+    const double Dg = 0.5 * (k0(x, y) + k1(x, y)) + k0(x - 1, y) + k1(x, y - 1) + 0.5 * (k0(x - 1, y - 1) + k1(x - 1, y - 1));
+    const double E = -0.5 * k0(x, y) - 0.5 * k1(x, y - 1);           // to (x+1, y)
+    const double Nn = -0.5 * k1(x, y) - 0.5 * k0(x - 1, y);          // to (x, y+1)
+    const double Wc = -0.5 * k0(x - 1, y) - 0.5 * k1(x - 1, y - 1);  // to (x-1, y)
+    const double Sc = -0.5 * k1(x, y - 1) - 0.5 * k0(x - 1, y - 1);  // to (x, y-1)
+    A[j * n + j] = Dg;
+    if (x < ni) A[(j + 1) * n + j] = E;
+    if (y < ni) A[(j + ni) * n + j] = Nn;
+    double r = h2 * (p.f ? p.f[y * m + x] : 1.0);
+    if (x == 1) r -= Wc * u[y * m];
+    if (x == ni) r -= E * u[y * m + N];
+    if (y == 1) r -= Sc * u[x];
+    if (y == ni) r -= Nn * u[N * m + x];
+    rhs[j] = r;
+  }
+  __syncwarp();
+  bool bad = false;
+  for (int j = 0; j < n; ++j) {            // right-looking Cholesky, lower triangle
+    const double d = A[j * n + j];
+    bad |= !(d > 0.0);
+    const double sq = sqrt(d), il = 1.0 / sq;
+    __syncwarp();
+    for (int i = j + 1 + lane; i < n; i += 32) A[i * n + j] *= il;
+    if (lane == 0) A[j * n + j] = sq;
+    __syncwarp();
+    const int w = n - j - 1;
+    for (int t = lane; t < w * w; t += 32) {
+      const int i = j + 1 + t / w, c = j + 1 + t % w;
+      if (c <= i) A[i * n + c] = fma(-A[i * n + j], A[c * n + j], A[i * n + c]);
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && bad) record_error(p, HDD_ERR_NUMERICAL, s, p.root_ref);
+  for (int j = 0; j < n; ++j) {            // L y = rhs
+    if (lane == 0) rhs[j] /= A[j * n + j];
+    __syncwarp();
+    const double yj = rhs[j];
+    for (int i = j + 1 + lane; i < n; i += 32) rhs[i] = fma(-A[i * n + j], yj, rhs[i]);
+    __syncwarp();
+  }
+  for (int j = n - 1; j >= 0; --j) {       // L^T x = y
+    if (lane == 0) rhs[j] /= A[j * n + j];
+    __syncwarp();
+    const double xj = rhs[j];
+    for (int i = lane; i < j; i += 32) rhs[i] = fma(-A[j * n + i], xj, rhs[i]);
+    __syncwarp();
+  }
+  for (int j = lane; j < n; j += 32) u[(j / ni + 1) * m + j % ni + 1] = rhs[j];
+  __syncwarp();
+  if (U)
+    for (int t = lane; t < m * m; t += 32) U[int64_t(s) * n_nodes + t] = u[t];
+  double acc = 0.0;
+  for (int o = lane; o < p.n_obs; o += 32) {
+    const int kind = p.route_kind[o];
+    double v;
+    if (kind == 1) {
+      v = p.route_val[o];
+    } else if (kind == 4) {
+      v = u[p.route_col[o]];
+    } else {                                // kind 5: mean over the node's cells
+      const int c = p.route_col[o];
+      const int i0 = c & 31, i1 = (c >> 5) & 31, j0 = (c >> 10) & 31, j1 = (c >> 15) & 31;
+      double t = 0.0;
+      for (int cy = j0; cy < j1; ++cy)
+        for (int cx = i0; cx < i1; ++cx)
+          t += 2.0 * u[cy * m + cx] + u[cy * m + cx + 1] + u[(cy + 1) * m + cx] + 2.0 * u[(cy + 1) * m + cx + 1];
+      v = t / (6.0 * (i1 - i0) * (j1 - j0));
+    }
+    if (!isfinite(v)) record_error(p, HDD_ERR_NUMERICAL, s, -1);
+    if (S) S[int64_t(s) * p.n_obs + o] = v;
+    if (p.y) {
+      const double r = (p.y[o] - v) / p.sigma[o];
+      acc = fma(r, r, acc);
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0 && ll) ll[s] = p.y ? (-0.5 * acc - p.ll_const) : 0.0;
+}
+
+cudaError_t launch_tiny(const DevPlan& p, int B, double* S, double* ll, double* U, int64_t n_nodes, cudaStream_t s) {
+  tiny_kernel<<<B, 32, 0, s>>>(p, B, S, ll, U, n_nodes);
   return cudaGetLastError();
 }
 

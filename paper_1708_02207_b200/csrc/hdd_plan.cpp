@@ -186,13 +186,82 @@ const std::vector<LeafLevel>& leaf_template() {
   return tmpl;
 }
 
+namespace {
+// Cell rectangle of a reference post-order tree node id (ddtree.py:152-173): descend
+// from the root, the first son's subtree holds the smaller ids.
+bool rect_of_id(int level, int64_t id, Rect* out) {
+  if (id < 0 || id >= subtree_size(level, 0)) return false;
+  const int N = 1 << level;
+  Rect r{0, N, 0, N};
+  int depth = 0;
+  int64_t lo = 0;
+  while (lo + subtree_size(level, depth) - 1 != id) {
+    Rect a, b;
+    split(r, depth, a, b, nullptr);
+    const int64_t half = subtree_size(level, depth + 1);
+    if (id < lo + half) r = a;
+    else { r = b; lo += half; }
+    ++depth;
+  }
+  *out = r;
+  return true;
+}
+}  // namespace
+
+// Levels 1-3: the whole mesh is smaller than one kernel leaf; one warp per sample
+// eliminates the interior directly (tiny_kernel).  Observation routes: 1 constant
+// (boundary point: g there), 4 interior point (col = node id), 5 mean (col = packed cells).
+std::string build_tiny_plan(const HddPlanDesc* d, Plan& P, int* code) {
+  P.tiny = true;
+  P.leaf_depth = 0;
+  P.mode = 0;
+  P.root = -1;
+  P.root_ref = subtree_size(P.level, 0) - 1;
+  P.leaf_cols = 1;
+  P.n_buffers = 0;
+  const int N = P.N;
+  const int64_t m = P.m;
+  auto is_boundary = [&](int64_t id) {
+    const int64_t i = id % m, j = id / m;
+    return i == 0 || j == 0 || i == N || j == N;
+  };
+  P.gfull.assign(size_t(m) * m, 0.0);
+  if (P.has_g) {
+    size_t pos = 0;   // boundary nodes in increasing id order (root.idx_boundary)
+    for (int64_t id = 0; id < m * m; ++id)
+      if (is_boundary(id)) P.gfull[size_t(id)] = P.g[pos++];
+  }
+  P.route.assign(P.obs_kind.size(), ObsRoute{1, -1, 0.0});
+  for (size_t o = 0; o < P.obs_kind.size(); ++o) {
+    const int64_t id = P.obs_id[o];
+    if (P.obs_kind[o] == HDD_OBS_POINT) {
+      if (id < 0 || id >= m * m) { *code = HDD_ERR_USAGE; return "mesh node " + std::to_string(id) + " not found on any interface"; }
+      P.route[o] = is_boundary(id) ? ObsRoute{1, -1, P.gfull[size_t(id)]} : ObsRoute{4, int(id), 0.0};
+    } else if (P.obs_kind[o] == HDD_OBS_MEAN) {
+      Rect r;
+      if (!rect_of_id(P.level, id, &r)) { *code = HDD_ERR_USAGE; return "no tree node with id " + std::to_string(id); }
+      P.route[o] = ObsRoute{5, r.i0 | (r.i1 << 5) | (r.j0 << 10) | (r.j1 << 15), 0.0};
+    } else {
+      return "unknown observation kind " + std::to_string(P.obs_kind[o]);
+    }
+  }
+  P.lr_eps = d->lr_eps > 0 ? d->lr_eps : 0.0;   // no map is larger than n_min: nothing to compress
+  *code = HDD_OK;
+  return "";
+}
+
 std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
   *code = HDD_ERR_CONFIG;
   if (!d) { *code = HDD_ERR_USAGE; return "null plan descriptor"; }
-  if (d->level < 4 || d->level > 11)
-    return "mesh level must be an integer in [4, 11] (16x16-cell kernel leaves), got " + std::to_string(d->level);
-  if (d->n_z < 1 || d->n_z > 256) return "parameter dimension n_z must be in [1, 256]";
-  if (!d->sx || !d->sy || !d->coef) return "separable parametrization tables are required";
+  if (d->level < 1 || d->level > 11)
+    return "mesh level must be an integer in [1, 11], got " + std::to_string(d->level);
+  // separable tables are optional: without them the plan evaluates caller-supplied
+  // coefficient fields only (hdd_forward_batch_kappa; the reference's duck-typed
+  // param.kappa(z), bayes.py:183)
+  P.separable = d->sx && d->sy && d->coef;
+  if ((d->sx || d->sy || d->coef) && !P.separable) return "separable parametrization needs all of sx, sy, coef";
+  if (P.separable && (d->n_z < 1 || d->n_z > 256)) return "parameter dimension n_z must be in [1, 256]";
+  if (!P.separable && (d->n_z < 0 || d->n_z > 256)) return "parameter dimension n_z must be in [0, 256]";
   if (d->n_obs < 1) return "at least one observation is required";
   if (!d->obs_kind || !d->obs_id || !d->sigma) return "observation arrays are required";
   P.level = d->level;
@@ -202,9 +271,11 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
   P.n_z = d->n_z;
   const int N = P.N;
   const int64_t m = P.m;
-  P.sx.assign(d->sx, d->sx + size_t(d->n_z) * 2 * N);
-  P.sy.assign(d->sy, d->sy + size_t(d->n_z) * 2 * N);
-  P.coef.assign(d->coef, d->coef + d->n_z);
+  if (P.separable) {
+    P.sx.assign(d->sx, d->sx + size_t(d->n_z) * 2 * N);
+    P.sy.assign(d->sy, d->sy + size_t(d->n_z) * 2 * N);
+    P.coef.assign(d->coef, d->coef + d->n_z);
+  }
   for (double v : P.sx) if (!std::isfinite(v)) return "parametrization table sx is not finite";
   for (double v : P.sy) if (!std::isfinite(v)) return "parametrization table sy is not finite";
   P.f_is_one = (d->f == nullptr);
@@ -230,6 +301,8 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     P.y.assign(d->y, d->y + n_obs);
     for (double v : P.y) if (!std::isfinite(v)) return "data vector y is not finite";
   }
+  P.root_ref = subtree_size(P.level, 0) - 1;
+  if (P.level < 4) return build_tiny_plan(d, P, code);
   const int dl = 2 * (P.level - 4);   // depth of the 16x16-cell kernel leaves
   P.leaf_depth = dl;
 
@@ -581,13 +654,30 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     }
   }
   if (primal) {
-    int64_t fo = 0, uo = 0;
-    for (UpperNode& U : P.upper) {
-      U.fac_off = fo;
-      fo += int64_t(U.ng) * (U.k + U.ng + 1);
-      U.u_off = uo;
-      uo += U.K;
+    // nodes the top-down sweep must visit: the ancestors of every observation's
+    // owner (north_star item 4: restricted to what F needs); a full-solution plan
+    // (hdd_solve_batch) visits every node
+    P.full_solve = d->full_solve != 0;
+    std::vector<char> need(P.upper.size(), P.full_solve ? 1 : 0);
+    auto mark_up = [&](int u) {
+      while (u >= 0 && !need[u]) { need[u] = 1; u = P.upper[u].parent; }
+    };
+    for (const ObsRoute& r : P.route) {
+      if (r.kind == 2) mark_up(P.leaves[r.node].parent);
+      else if (r.kind == 3) mark_up(r.node);
     }
+    int64_t fo = 0, uo = 0;
+    P.td_by_depth.assign(P.upper_by_depth.size(), {});
+    for (size_t dep = 0; dep < P.upper_by_depth.size(); ++dep)
+      for (int u : P.upper_by_depth[dep]) {
+        UpperNode& U = P.upper[u];
+        if (!need[u]) { U.fac_off = -1; U.u_off = -1; continue; }
+        P.td_by_depth[dep].push_back(u);
+        U.fac_off = fo;
+        fo += int64_t(U.ng) * (U.k + U.ng + 1);
+        U.u_off = uo;
+        uo += U.K;
+      }
     P.fac_elems = fo;
     P.u_elems = uo;
   }

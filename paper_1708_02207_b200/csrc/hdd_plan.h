@@ -117,11 +117,18 @@ struct Plan {
   int n_fslots = 0;                           // leaf point functionals kept for the top-down pass
   int64_t fac_elems = 0, u_elems = 0;         // per-sample sizes of the primal buffers
   std::vector<int64_t> buf_elems_per_sample;  // per buffer
+  bool full_solve = false;                    // primal factors kept for every node
+  std::vector<std::vector<int>> td_by_depth;  // primal: upper nodes the top-down sweep visits
+  bool separable = true;                      // sx/sy/coef given (else kappa per call)
+  bool tiny = false;                          // level <= 3: tiny_kernel, no tree sweep
+  std::vector<double> gfull;                  // tiny: [m*m] boundary values
+  int64_t root_ref = 0;
 };
 
 // Build the plan; returns empty string on success, else the ConfigError /
 // UsageError message (code in *code).
 std::string build_plan(const HddPlanDesc* desc, Plan& plan, int* code);
+std::string build_tiny_plan(const HddPlanDesc* desc, Plan& plan, int* code);
 
 const std::vector<LeafLevel>& leaf_template();
 int64_t postorder_id(int level, const std::vector<int>& path);

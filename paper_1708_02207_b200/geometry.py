@@ -19,7 +19,7 @@ import numpy as np
 from .errors import ConfigError, GeometryError, UsageError
 
 MAX_LEVEL = 11
-MIN_LEVEL = 4
+MIN_LEVEL = 1
 
 
 @dataclass(frozen=True)

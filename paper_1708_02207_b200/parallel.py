@@ -50,24 +50,31 @@ def gather_ragged(x_local, counts, group=None):
 
 def posterior_weights_device(ll_all, log_prior=None):
     """(weights, argmax, logsumexp) on the device — one launch of the native
-    posterior kernel (hdd_posterior_weights); argmax takes the first maximal index
-    like numpy.  CPU tensors (gloo tests) use the same formulas in torch."""
+    posterior kernel (hdd_posterior_weights) on ll's device and current stream;
+    argmax follows numpy (first NaN if any, else the first maximal index).  CPU
+    tensors (gloo tests) use the same formulas in torch."""
     import torch
     if not ll_all.is_cuda:
         joint = ll_all if log_prior is None else ll_all + log_prior
         lse = torch.logsumexp(joint, dim=0)
         return torch.exp(joint - lse), torch.argmax(joint), lse
     from . import _lib
-    ll = ll_all.to(torch.float64).contiguous()
-    lp = None if log_prior is None else torch.as_tensor(log_prior, dtype=torch.float64, device=ll.device).contiguous()
+    from .errors import UsageError
+    ll = ll_all.to(torch.float64).reshape(-1).contiguous()
     n = int(ll.numel())
-    w = torch.empty_like(ll)
-    idx = torch.empty((), dtype=torch.int64, device=ll.device)
-    lse = torch.empty((), dtype=torch.float64, device=ll.device)
-    rc = _lib.lib().hdd_posterior_weights(
-        C.c_void_p(ll.data_ptr()), None if lp is None else C.c_void_p(lp.data_ptr()), n,
-        C.c_void_p(w.data_ptr()), C.c_void_p(idx.data_ptr()), C.c_void_p(lse.data_ptr()),
-        C.c_void_p(torch.cuda.current_stream(ll.device).cuda_stream))
+    lp = None if log_prior is None else torch.as_tensor(log_prior, dtype=torch.float64, device=ll.device).reshape(-1).contiguous()
+    if lp is not None and int(lp.numel()) != n:
+        raise UsageError(f"log_prior has {int(lp.numel())} entries for {n} log-likelihoods")
+    if n == 0:
+        raise UsageError("posterior weights of an empty batch")
+    with torch.cuda.device(ll.device):
+        w = torch.empty_like(ll)
+        idx = torch.empty((), dtype=torch.int64, device=ll.device)
+        lse = torch.empty((), dtype=torch.float64, device=ll.device)
+        rc = _lib.lib().hdd_posterior_weights(
+            C.c_void_p(ll.data_ptr()), None if lp is None else C.c_void_p(lp.data_ptr()), n,
+            C.c_void_p(w.data_ptr()), C.c_void_p(idx.data_ptr()), C.c_void_p(lse.data_ptr()),
+            C.c_void_p(torch.cuda.current_stream(ll.device).cuda_stream))
     _lib.raise_for(rc)
     return w, idx, lse
 

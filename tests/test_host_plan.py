@@ -150,7 +150,9 @@ def test_emulated_leaf_maps_match_reference_nodes(golden):
 def test_plan_errors():
     obs = (("point", 100),)
     with pytest.raises(hb.ConfigError):
-        hb.build_mesh(3)
+        hb.build_mesh(0)                                    # the reference accepts levels >= 1 (mesh.py:92-93)
+    with pytest.raises(hb.ConfigError):
+        hb.build_mesh(12)
     with pytest.raises(hb.ConfigError):
         hb.MeasurementModel(obs, np.array([0.0]))
     mesh = hb.build_mesh(5)
