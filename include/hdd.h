@@ -222,6 +222,33 @@ int hdd_kappa_batch(HddPlan* plan, const double* Z_dev, int64_t B,
 int hdd_posterior_weights(const double* ll_dev, const double* log_prior_dev, int64_t n, double* w_dev,
                           int64_t* idx_dev, double* lse_dev, void* stream);
 
+/* Per-call right-hand sides: the general maps Psi^f / Phi^f (hdd.py:58-105,
+ * PsiMap.residual / PhiMap.apply) applied to new data without a new plan — a
+ * batch row may carry its own f and g ("multiple right-hand sides and multiple
+ * Dirichlet data").  f rows hold n_nodes values (mesh-node order),
+ * g rows 4N values (boundary nodes in increasing id order, the reference's
+ * root.idx_boundary); stride 0 = one row shared by the whole batch; NULL = the
+ * plan's f / g.  Host variants take host rows (stride 0 or the row length). */
+typedef struct {
+  const double* f;
+  int64_t f_stride;
+  const double* g;
+  int64_t g_stride;
+} HddRhs;
+
+/* Forward / likelihood with exactly one of Z_dev [B][n_z] and K_dev [B][2N^2]
+ * (caller fields) and optional per-call rows (asynchronous, like
+ * hdd_forward_batch). */
+int hdd_forward_batch_ex(HddPlan* plan, const double* Z_dev, const double* K_dev, int64_t B, const HddRhs* rhs,
+                         double* S_dev, double* ll_dev, void* stream);
+int hdd_forward_batch_ex_host(HddPlan* plan, const double* Z_host, const double* K_host, int64_t B,
+                              const HddRhs* rhs_host, double* S_host, double* ll_host);
+/* Full solution u with per-call rows (full-solution plans). */
+int hdd_solve_batch_ex(HddPlan* plan, const double* Z_dev, const double* K_dev, int64_t B, const HddRhs* rhs,
+                       double* U_dev, void* stream);
+int hdd_solve_batch_ex_host(HddPlan* plan, const double* Z_host, const double* K_host, int64_t B,
+                            const HddRhs* rhs_host, double* U_host);
+
 int hdd_last_error(const HddPlan* plan, HddError* out);
 /* Error of the last failed hdd_plan_create (no plan exists then). */
 int hdd_create_error(HddError* out);
@@ -246,6 +273,9 @@ int hdd_debug_leaf_clocks(long long* out64);
  * launch of the last batch (profiling hook): 0 start, 1 maps staged, 2 panel
  * gathered, 3 eliminated, 4 sigma/factors written, 5 Schur update written. */
 int hdd_debug_merge_clocks(long long* out);
+/* Low-rank plans with k_max > 24: number of (block, sample) pairs handed to the
+ * 72-column wide sketch since the plan was created (0 otherwise). */
+int hdd_debug_lowrank_wide(HddPlan* plan, int64_t* total);
 
 const char* hdd_version(void);
 

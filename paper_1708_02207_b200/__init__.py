@@ -25,6 +25,7 @@ from .bayes import (  # noqa: F401
     mean_over_cells,
     observe_solution,
     posterior_weights,
+    prolong_rhs,
     solve_batch,
     solve_subdomain,
 )

@@ -42,6 +42,10 @@ class HddPlanDesc(C.Structure):
     ]
 
 
+class HddRhs(C.Structure):
+    _fields_ = [("f", C.c_void_p), ("f_stride", C.c_int64), ("g", C.c_void_p), ("g_stride", C.c_int64)]
+
+
 class HddError(C.Structure):
     _fields_ = [("code", C.c_int32), ("sample", C.c_int32), ("node_id", C.c_int64),
                 ("message", C.c_char * 256)]
@@ -85,6 +89,14 @@ EXPORTS = {
     "hdd_forward_batch_kappa": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hdd_forward_batch_kappa_host": (C.c_int, [C.c_void_p, _f64p, C.c_int64, _f64p, _f64p]),
     "hdd_solve_batch_kappa": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "hdd_forward_batch_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(HddRhs), C.c_void_p,
+                                       C.c_void_p, C.c_void_p]),
+    "hdd_forward_batch_ex_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(HddRhs),
+                                            C.c_void_p, C.c_void_p]),
+    "hdd_solve_batch_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(HddRhs), C.c_void_p,
+                                     C.c_void_p]),
+    "hdd_solve_batch_ex_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(HddRhs),
+                                          C.c_void_p]),
     "hdd_solve_batch_kappa_host": (C.c_int, [C.c_void_p, _f64p, C.c_int64, _f64p]),
     "hdd_solve_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "hdd_solve_batch_host": (C.c_int, [C.c_void_p, _f64p, C.c_int64, _f64p]),
@@ -101,6 +113,7 @@ EXPORTS = {
     "hdd_debug_node_output": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, _f64p, _f64p, _f64p]),
     "hdd_debug_leaf_clocks": (C.c_int, [C.POINTER(C.c_longlong)]),
     "hdd_debug_merge_clocks": (C.c_int, [C.POINTER(C.c_longlong)]),
+    "hdd_debug_lowrank_wide": (C.c_int, [C.c_void_p, _i64p]),
     "hdd_version": (C.c_char_p, []),
 }
 

@@ -36,7 +36,7 @@ from .geometry import DDTree, Mesh, Rect, cell_centroid_tables
 __all__ = [
     "ParamField", "SineKLField", "Prior", "ToleranceSpec", "MeasurementModel", "BayesProblem", "mean_observations",
     "aligned_partition", "kl_pairs", "forward_functionals", "forward_functionals_batch", "log_likelihood",
-    "log_likelihood_batch", "gaussian_log_likelihood", "posterior_weights", "synchronize",
+    "log_likelihood_batch", "gaussian_log_likelihood", "posterior_weights", "synchronize", "prolong_rhs",
 ]
 
 
@@ -147,8 +147,10 @@ class ParamField(_Separable):
 @dataclass(frozen=True)
 class ToleranceSpec:
     """Truncation tolerance (relative Frobenius), rank cap and dense-block size
-    of the low-rank map storage (lowrank.py:20-30).  The device path caps the
-    rank at 24 (sketch width 32)."""
+    of the low-rank map storage (lowrank.py:20-30).  The device sketches each
+    admissible block with k_max + 8 random columns (k_max <= 24: one 16/24/32-column
+    pass; 25..64: blocks needing a rank above 24 are re-sketched with 72 columns);
+    k_max > 64 is a ConfigError naming the device limit."""
 
     eps: float = 1e-6
     k_max: int = 64
@@ -402,20 +404,55 @@ def _device_check(plan: _Plan, Zb):
         raise UsageError(f"torch inputs must live on the plan's CUDA device cuda:{plan.device}, got {Zb.device}")
 
 
-def _run(problem: BayesProblem, Z, want_S: bool, want_ll: bool, sync: bool = True):
+class _Rows:
+    """Per-call right-hand sides (f rows [n_nodes], g rows [4N]; one shared row or one
+    per sample) as an HddRhs: the general Psi^f / Phi^f maps applied to new data
+    (hdd.py:58-105) without rebuilding the plan."""
+
+    def __init__(self, problem: BayesProblem, B: int, f, g, device=None):
+        mesh = problem.tree.mesh
+        self.keep = []
+        self.rhs = _lib.HddRhs()
+        for name, arr, width in (("f", f, mesh.n_nodes), ("g", g, 4 * mesh.n_cells)):
+            if arr is None:
+                continue
+            if device is not None:
+                import torch
+                t = torch.as_tensor(arr, dtype=torch.float64).to(device).contiguous()
+                shape, ptr = tuple(t.shape), t.data_ptr()
+                self.keep.append(t)
+            else:
+                t = np.ascontiguousarray(np.asarray(arr, dtype=np.float64))
+                shape, ptr = t.shape, t.ctypes.data
+                self.keep.append(t)
+            if shape == (width,):
+                stride = 0
+            elif shape == (B, width):
+                stride = width
+            else:
+                raise UsageError(f"{name} must have shape ({width},) or ({B}, {width}), got {shape}")
+            setattr(self.rhs, name, ptr)
+            setattr(self.rhs, f"{name}_stride", stride)
+
+
+def _run(problem: BayesProblem, Z, want_S: bool, want_ll: bool, sync: bool = True, f=None, g=None):
     plan = problem.plan()
     n_z = plan.n_z if plan.separable else int(getattr(problem.param, "n_z", np.asarray(Z).shape[-1]))
     Zb = _as_batch(Z, n_z)
     B = Zb.shape[0]
     f64 = _lib._f64p
-    if not plan.separable:
-        # host-evaluated fields; device Z comes back as device tensors
-        K = _kappa_rows(problem, Zb)
+    general = f is not None or g is not None
+    if not plan.separable or (general and isinstance(Zb, np.ndarray)):
+        # host entry point: caller-evaluated fields and/or per-call right-hand sides
+        K = None if plan.separable else _kappa_rows(problem, Zb)
+        Zh = None if K is not None else (Zb if isinstance(Zb, np.ndarray) else Zb.detach().cpu().numpy())
         S = np.empty((B, plan.n_obs)) if want_S else None
         ll = np.empty(B) if want_ll else None
-        plan.check(plan.lib.hdd_forward_batch_kappa_host(
-            plan.handle, K.ctypes.data_as(f64), B, S.ctypes.data_as(f64) if S is not None else None,
-            ll.ctypes.data_as(f64) if ll is not None else None))
+        rows = _Rows(problem, B, f, g) if general else None
+        plan.check(plan.lib.hdd_forward_batch_ex_host(
+            plan.handle, None if Zh is None else Zh.ctypes.data, None if K is None else K.ctypes.data, B,
+            None if rows is None else C.byref(rows.rhs),
+            None if S is None else S.ctypes.data, None if ll is None else ll.ctypes.data))
         if not isinstance(Zb, np.ndarray):
             import torch
             S = None if S is None else torch.from_numpy(S).to(Zb.device)
@@ -436,6 +473,14 @@ def _run(problem: BayesProblem, Z, want_S: bool, want_ll: bool, sync: bool = Tru
     S = torch.empty((B, plan.n_obs), dtype=torch.float64, device=Zb.device) if want_S else None
     ll = torch.empty(B, dtype=torch.float64, device=Zb.device) if want_ll else None
     stream = C.c_void_p(torch.cuda.current_stream(Zb.device).cuda_stream)
+    if general:
+        rows = _Rows(problem, B, f, g, device=Zb.device)
+        rc = plan.lib.hdd_forward_batch_ex(plan.handle, C.c_void_p(Zb.data_ptr()), None, B, C.byref(rows.rhs),
+                                           C.c_void_p(S.data_ptr()) if S is not None else None,
+                                           C.c_void_p(ll.data_ptr()) if ll is not None else None, stream)
+        plan.check(rc)
+        plan.check(plan.lib.hdd_sync(plan.handle, stream))     # rows must outlive the launches
+        return S, ll
     rc = plan.lib.hdd_forward_batch(plan.handle, C.c_void_p(Zb.data_ptr()), B,
                                     C.c_void_p(S.data_ptr()) if S is not None else None,
                                     C.c_void_p(ll.data_ptr()) if ll is not None else None, stream)
@@ -445,22 +490,27 @@ def _run(problem: BayesProblem, Z, want_S: bool, want_ll: bool, sync: bool = Tru
     return S, ll
 
 
-def forward_functionals_batch(problem: BayesProblem, Z, sync: bool = True):
+def forward_functionals_batch(problem: BayesProblem, Z, sync: bool = True, f=None, g=None):
     """S[B, n_y] for every row of Z (numpy / host torch -> numpy; CUDA torch tensor ->
     CUDA torch tensor).  With CUDA tensors and sync=False the call returns as soon as
     the work is queued on the current stream; failures then surface at the next call
-    on the problem or at `synchronize(problem)`."""
-    S, _ = _run(problem, Z, True, False, sync)
+    on the problem or at `synchronize(problem)`.
+
+    `f` ([n_nodes] or [B, n_nodes]) and `g` ([4N] or [B, 4N], boundary nodes in
+    increasing id order) replace the problem's right-hand side / Dirichlet data for
+    this call only — one shared row or one row per sample (the general maps of
+    hdd.py:58-105 applied to new data, "multiple right-hand sides")."""
+    S, _ = _run(problem, Z, True, False, sync, f, g)
     problem.forward_calls += int(S.shape[0])
     return S
 
 
-def log_likelihood_batch(problem: BayesProblem, Z, sync: bool = True):
+def log_likelihood_batch(problem: BayesProblem, Z, sync: bool = True, f=None, g=None):
     """ll[B] for every row of Z; raises UsageError without data (bayes.py:228-229).
-    `sync` as in forward_functionals_batch."""
+    `sync`, `f`, `g` as in forward_functionals_batch."""
     if problem.model.y is None:
         raise UsageError("measurement model carries no data")
-    _, ll = _run(problem, Z, False, True, sync)
+    _, ll = _run(problem, Z, False, True, sync, f, g)
     problem.forward_calls += int(ll.shape[0])
     return ll
 
@@ -483,39 +533,64 @@ def forward_functionals(problem: BayesProblem, z) -> np.ndarray:
     return forward_functionals_batch(problem, z[None])[0]
 
 
-def solve_batch(problem: BayesProblem, Z):
+def solve_batch(problem: BayesProblem, Z, f=None, g=None):
     """u at every mesh node for every row of Z: U[B, n_nodes] (node id j * m + i).
 
     Bottom-up sweep, primal top-down sweep over the interfaces and the in-leaf
     interior solves on the device — leaves_to_root(keep_all) + root_to_leaves
     (hdd.py:289-432) for a batch.  numpy in -> numpy out; a CUDA torch tensor in ->
-    CUDA torch tensor out."""
+    CUDA torch tensor out.  `f` / `g`: per-call right-hand sides as in
+    forward_functionals_batch (root_to_leaves(store, f, g) for new data)."""
     plan = problem.solve_plan()
     n_z = plan.n_z if plan.separable else int(getattr(problem.param, "n_z", np.asarray(Z).shape[-1]))
     Zb = _as_batch(Z, n_z)
     B = Zb.shape[0]
     n = problem.tree.mesh.n_nodes
-    f64 = _lib._f64p
-    if not plan.separable:
-        K = _kappa_rows(problem, Zb)
+    general = f is not None or g is not None
+    if not plan.separable or isinstance(Zb, np.ndarray):
+        K = None if plan.separable else _kappa_rows(problem, Zb)
+        Zh = None if K is not None else (Zb if isinstance(Zb, np.ndarray) else Zb.detach().cpu().numpy())
+        rows = _Rows(problem, B, f, g) if general else None
         U = np.empty((B, n))
-        plan.check(plan.lib.hdd_solve_batch_kappa_host(plan.handle, K.ctypes.data_as(f64), B, U.ctypes.data_as(f64)))
+        plan.check(plan.lib.hdd_solve_batch_ex_host(
+            plan.handle, None if Zh is None else Zh.ctypes.data, None if K is None else K.ctypes.data, B,
+            None if rows is None else C.byref(rows.rhs), U.ctypes.data))
         if not isinstance(Zb, np.ndarray):
             import torch
             return torch.from_numpy(U).to(Zb.device)
-        return U
-    if isinstance(Zb, np.ndarray):
-        U = np.empty((B, n))
-        plan.check(plan.lib.hdd_solve_batch_host(plan.handle, Zb.ctypes.data_as(f64), B, U.ctypes.data_as(f64)))
         return U
     import torch
     _device_check(plan, Zb)
     Zb = Zb.to(torch.float64).contiguous()
     U = torch.empty((B, n), dtype=torch.float64, device=Zb.device)
     stream = C.c_void_p(torch.cuda.current_stream(Zb.device).cuda_stream)
-    plan.check(plan.lib.hdd_solve_batch(plan.handle, C.c_void_p(Zb.data_ptr()), B, C.c_void_p(U.data_ptr()), stream))
+    rows = _Rows(problem, B, f, g, device=Zb.device) if general else None
+    plan.check(plan.lib.hdd_solve_batch_ex(plan.handle, C.c_void_p(Zb.data_ptr()), None, B,
+                                           None if rows is None else C.byref(rows.rhs), C.c_void_p(U.data_ptr()),
+                                           stream))
     plan.check(plan.lib.hdd_sync(plan.handle, stream))
     return U
+
+
+def prolong_rhs(f_coarse, level_coarse: int, level_fine: int) -> np.ndarray:
+    """Two-grid right-hand side: nodal values on the level_coarse grid prolonged to the
+    level_fine grid by bilinear interpolation (the reference SPEC's "coarse RHS given
+    on a coarser grid injected to fine nodes", PAPER.md:286 / :319 property 1, f_h in
+    V_H subset V_h).  Node ids j * m + i on both grids."""
+    if not (1 <= level_coarse <= level_fine):
+        raise ConfigError("two-grid right-hand side needs 1 <= level_coarse <= level_fine")
+    mc = (1 << level_coarse) + 1
+    fc = np.asarray(f_coarse, dtype=float)
+    if fc.shape != (mc * mc,):
+        raise ConfigError(f"coarse right-hand side must have {mc * mc} nodal values")
+    fc = fc.reshape(mc, mc)                         # [j][i]
+    r = 1 << (level_fine - level_coarse)
+    mf = (1 << level_fine) + 1
+    x = np.arange(mf) / r
+    i0 = np.minimum(np.floor(x).astype(int), mc - 2) if mc > 1 else np.zeros(mf, dtype=int)
+    t = x - i0
+    rows = fc[i0] * (1 - t)[:, None] + fc[i0 + 1] * t[:, None]          # interpolate in j
+    return (rows[:, i0] * (1 - t)[None, :] + rows[:, i0 + 1] * t[None, :]).reshape(-1)
 
 
 def mean_over_cells(mesh, u, cells) -> float:

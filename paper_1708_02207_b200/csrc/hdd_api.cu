@@ -65,6 +65,7 @@ struct HddPlan {
 };
 
 static HddError g_create_err{};
+constexpr int kWideSketch = 72;   // compress_wide_kernel sketch columns (kLWW)
 static std::mutex g_mu;
 
 static int set_err(HddError* e, int code, const std::string& msg, int sample = -1, int64_t node = -1) {
@@ -162,6 +163,14 @@ static int setup_device(HddPlan* pl, int max_batch) {
     if ((rc = upload(pl, lg, &D.leaf_g))) return rc;
   }
   {
+    std::vector<int32_t> gp;
+    for (const Leaf& L : P.leaves) gp.insert(gp.end(), L.gpos.begin(), L.gpos.end());
+    if ((rc = upload(pl, gp, &D.leaf_gpos))) return rc;
+    D.gcall = nullptr;
+    D.f_stride = 0;
+    D.g_stride = 0;
+  }
+  {
     std::vector<int32_t> lc;
     for (const Leaf& L : P.leaves) {
       if (L.cmap.empty()) lc.insert(lc.end(), kLeafPerim, -1);
@@ -197,11 +206,14 @@ static int setup_device(HddPlan* pl, int max_batch) {
   pl->depth_rows.assign(P.upper_by_depth.size(), 0);
   pl->depth_nb.assign(P.upper_by_depth.size(), 32);
   const char* force_l = std::getenv("HDD_FORCE_TIER_L");   // test hook: every depth on the HBM panel
+  // panels above this many KB of shared memory run on the HBM-panel tier (tuning hook)
+  const int tier_l_kb = std::getenv("HDD_TIER_L_KB") ? std::atoi(std::getenv("HDD_TIER_L_KB")) : 220;
   for (size_t u = 0; u < P.upper.size(); ++u) {
     const UpperNode& U = P.upper[u];
     const int ngp32 = (U.ng + 31) / 32 * 32;
     const int ldp32 = panel_ld(U.k + ngp32 + U.nc);
-    if (merge_m2_smem_bytes(ngp32, ldp32, U.K, U.nc) > 220 * 1024 || (force_l && force_l[0] == '1')) pl->depth_tier[U.depth] = 1;
+    if (merge_m2_smem_bytes(ngp32, ldp32, U.K, U.nc) > size_t(tier_l_kb) * 1024 || (force_l && force_l[0] == '1'))
+      pl->depth_tier[U.depth] = 1;
   }
   for (size_t u = 0; u < P.upper.size(); ++u) {
     const UpperNode& U = P.upper[u];
@@ -338,6 +350,19 @@ static int setup_device(HddPlan* pl, int max_batch) {
       if (i + 1 < om.size()) om[i + 1] = rr * std::sin(2.0 * M_PI * u2);
     }
     if ((rc = upload(pl, om, &D.lr_omega))) return rc;
+    D.lr_pmax = 0;
+    for (int v : pl->lr_pmax) D.lr_pmax = std::max(D.lr_pmax, v);
+    D.lr_qmax = std::max(lr_qmax, 1);
+    if (P.lr_kmax > 24) {
+      std::vector<double> omw(size_t(D.lr_qmax) * kWideSketch);
+      for (size_t i = 0; i < omw.size(); i += 2) {
+        const double u1 = std::max(next(), 1e-300), u2 = next();
+        const double rr = std::sqrt(-2.0 * std::log(u1));
+        omw[i] = rr * std::cos(2.0 * M_PI * u2);
+        if (i + 1 < omw.size()) omw[i + 1] = rr * std::sin(2.0 * M_PI * u2);
+      }
+      if ((rc = upload(pl, omw, &D.lr_omega_w))) return rc;
+    }
   }
   {
     const DevUpper* du = nullptr;
@@ -420,11 +445,34 @@ static int setup_device(HddPlan* pl, int max_batch) {
     D.buf[b] = static_cast<double*>(p);
   }
   D.lr_scale = nullptr;
+  D.lr_wide_list = nullptr;
+  D.lr_wide_n = nullptr;
+  D.lr_wide_scr = nullptr;
+  D.lr_wide_cap = 0;
+  D.lr_wide_ctas = 0;
+  D.lr_force_wide = (std::getenv("HDD_LR_FORCE_WIDE") && std::getenv("HDD_LR_FORCE_WIDE")[0] == '1') ? 1 : 0;
   if (P.lr_eps > 0) {
     void* q = nullptr;
     CU(cudaMalloc(&q, sizeof(double) * size_t(std::max(lr_nodes_max, 1)) * bcap));
     pl->allocs.push_back(q);
     D.lr_scale = static_cast<double*>(q);
+    if (P.lr_kmax > 24) {
+      int nb_max = 1;
+      for (int v : pl->lr_nblk) nb_max = std::max(nb_max, v);
+      D.lr_wide_cap = int(std::min<int64_t>(int64_t(nb_max) * bcap, 1 << 26));
+      D.lr_wide_ctas = 2 * 148;
+      D.lr_wide_stride = (int64_t(std::max(D.lr_pmax, 1)) * kWideSketch + int64_t(kWideSketch) * D.lr_qmax + 1) & ~int64_t(1);
+      CU(cudaMalloc(&q, sizeof(int2) * size_t(D.lr_wide_cap)));
+      pl->allocs.push_back(q);
+      D.lr_wide_list = static_cast<int2*>(q);
+      CU(cudaMalloc(&q, 2 * sizeof(int)));    // [0] per-depth queue length, [1] running total
+      pl->allocs.push_back(q);
+      D.lr_wide_n = static_cast<int*>(q);
+      CU(cudaMemset(q, 0, 2 * sizeof(int)));
+      CU(cudaMalloc(&q, sizeof(double) * size_t(D.lr_wide_ctas) * D.lr_wide_stride));
+      pl->allocs.push_back(q);
+      D.lr_wide_scr = static_cast<double*>(q);
+    }
   }
   D.fac = D.ubuf = D.fbuf = nullptr;
   for (auto pr : {std::make_pair(&D.fac, P.fac_elems), std::make_pair(&D.ubuf, P.u_elems),
@@ -480,7 +528,7 @@ static int setup_device(HddPlan* pl, int max_batch) {
     for (size_t dep = 0; dep < P.upper_by_depth.size(); ++dep) {
       if (P.upper_by_depth[dep].empty()) continue;
       n += 1 + (D.mode == 1 && pl->td_count[dep] > 0 ? 1 : 0);
-      if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0) n += 2;
+      if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0) n += D.lr_wide_list ? 3 : 2;
     }
     pl->n_launches = n;
   }
@@ -551,11 +599,19 @@ int hdd_plan_destroy(HddPlan* pl) {
 // kernel); U non-NULL: the full-solution path (primal sweep + in-leaf solves).
 // sample0 = global index of the sub-batch's first row (failure records).
 static int run_sub_batch(HddPlan* pl, const double* Z, const double* Kin, int B, double* S, double* ll, double* U,
-                         cudaStream_t st, int64_t sample0, cudaEvent_t* ev = nullptr) {
+                         cudaStream_t st, int64_t sample0, cudaEvent_t* ev = nullptr, const HddRhs* rhs = nullptr) {
   Plan& P = pl->plan;
   DevPlan D = pl->dev;                 // by-value copy: per-sub-batch fields
   D.sample0 = sample0;
   if (Kin) D.kappa = const_cast<double*>(Kin);
+  if (rhs && rhs->f) {                 // per-call rows (base pointers of the call, offset here)
+    D.f = rhs->f + sample0 * rhs->f_stride;
+    D.f_stride = rhs->f_stride;
+  }
+  if (rhs && rhs->g) {
+    D.gcall = rhs->g + sample0 * rhs->g_stride;
+    D.g_stride = rhs->g_stride;
+  }
   const int64_t nn = int64_t(P.m) * P.m;
   int e = 0;
   auto mark = [&]() -> int {
@@ -579,9 +635,12 @@ static int run_sub_batch(HddPlan* pl, const double* Z, const double* Kin, int B,
     if (!ids.empty()) {
       CU(launch_merge(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->ws, pl->depth_ws[dep],
                       pl->depth_tier[dep], pl->depth_rows[dep], pl->depth_smem[dep], pl->depth_nb[dep], st, dep));
-      if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0)
+      if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0) {
+        if (D.lr_wide_list) CU(cudaMemsetAsync(D.lr_wide_n, 0, sizeof(int), st));
         CU(launch_compress(D, pl->d_upper + ids.front(), int(ids.size()), pl->lr_blk0[dep], pl->lr_nblk[dep], B,
                            pl->lr_pmax[dep], st));
+        if (D.lr_wide_list) CU(launch_compress_wide(D, pl->d_upper + ids.front(), pl->lr_blk0[dep], st));
+      }
     }
     if ((rc = mark())) return rc;
   }
@@ -643,14 +702,14 @@ static int check_call(HddPlan* pl, int64_t B, const void* in, bool want_separabl
 
 // Sub-batched launch of a whole batch on `st` (asynchronous).
 static int run_batch(HddPlan* pl, const double* Z, const double* Kin, int64_t B, double* S, double* ll, double* U,
-                     cudaStream_t st) {
+                     cudaStream_t st, const HddRhs* rhs = nullptr) {
   const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
   const int64_t nt = int64_t(2) * pl->plan.N * pl->plan.N, nn = int64_t(pl->plan.m) * pl->plan.m;
   for (int64_t done = 0; done < B;) {
     const int b = int(std::min<int64_t>(pl->bcap, B - done));
     const int rc = run_sub_batch(pl, Z ? Z + done * nz : nullptr, Kin ? Kin + done * nt : nullptr, b,
                                  S ? S + done * no : nullptr, ll ? ll + done : nullptr, U ? U + done * nn : nullptr, st,
-                                 done);
+                                 done, nullptr, rhs);
     if (rc != HDD_OK) return rc;
     done += b;
   }
@@ -756,7 +815,8 @@ int hdd_forward_batch_timed(HddPlan* pl, const double* Z, int64_t B, double* S, 
 // stream in) and the D2H copy of sub-batch i-1's results (copy stream out) overlap
 // the compute of sub-batch i on the plan's stream.  Returns when the results are in
 // host memory.  `in_w` doubles per input row (n_z for Z, 2N^2 for kappa fields).
-static int run_host(HddPlan* pl, const double* Xh, int in_w, bool is_kappa, int64_t B, double* Sh, double* llh) {
+static int run_host(HddPlan* pl, const double* Xh, int in_w, bool is_kappa, int64_t B, double* Sh, double* llh,
+                    const HddRhs* rhs = nullptr) {
   const int no = int(pl->plan.obs_kind.size());
   const int64_t nb = (B + pl->bcap - 1) / pl->bcap;
   if (B > pl->io_cap || (is_kappa && !pl->io_kappa) || (!is_kappa && pl->io_kappa)) {
@@ -793,7 +853,7 @@ static int run_host(HddPlan* pl, const double* Xh, int in_w, bool is_kappa, int6
     CU(cudaStreamWaitEvent(st, pl->pipe_ev[2 * i], 0));
     const double* x = pl->d_Z + r0 * in_w;
     rc = run_sub_batch(pl, is_kappa ? nullptr : x, is_kappa ? x : nullptr, b, Sh ? pl->d_S + r0 * no : nullptr,
-                       llh ? pl->d_ll + r0 : nullptr, nullptr, st, r0);
+                       llh ? pl->d_ll + r0 : nullptr, nullptr, st, r0, nullptr, rhs);
     if (rc != HDD_OK) return rc;
     CU(cudaEventRecord(pl->pipe_ev[2 * i + 1], st));
     if (i + 1 < nb && (rc = h2d(i + 1))) return rc;
@@ -887,6 +947,129 @@ int hdd_solve_batch_kappa_host(HddPlan* pl, const double* Kh, int64_t B, double*
   return solve_host(pl, Kh, true, B, Uh);
 }
 
+// ---- per-call right-hand sides (general Psi^f / Phi^f maps applied to new data) ----
+static int check_rhs(HddPlan* pl, const HddRhs* rhs, bool host) {
+  if (!rhs) return HDD_OK;
+  const int64_t nn = int64_t(pl->plan.m) * pl->plan.m, ng = int64_t(4) * pl->plan.N;
+  if (rhs->f && rhs->f_stride != 0 && (host ? rhs->f_stride != nn : rhs->f_stride < nn))
+    return set_err(&pl->err, HDD_ERR_USAGE, "f_stride must be 0 (one row) or the row length (n_nodes)");
+  if (rhs->g && rhs->g_stride != 0 && (host ? rhs->g_stride != ng : rhs->g_stride < ng))
+    return set_err(&pl->err, HDD_ERR_USAGE, "g_stride must be 0 (one row) or the row length (4N)");
+  return HDD_OK;
+}
+
+int hdd_forward_batch_ex(HddPlan* pl, const double* Z, const double* K, int64_t B, const HddRhs* rhs, double* S,
+                         double* ll, void* stream) {
+  if (!pl) return HDD_ERR_USAGE;
+  if ((Z != nullptr) == (K != nullptr) && B > 0) return set_err(&pl->err, HDD_ERR_USAGE, "pass exactly one of Z and K");
+  int rc = check_call(pl, B, Z ? Z : K, Z != nullptr);
+  if (rc != HDD_OK) return rc;
+  if ((rc = check_rhs(pl, rhs, false)) != HDD_OK) return rc;
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  if ((rc = take_error(pl)) != HDD_OK) return rc;
+  return run_batch(pl, Z, K, B, S, ll, nullptr, static_cast<cudaStream_t>(stream), rhs);
+}
+
+// device copies of a host HddRhs (rows of n_nodes / 4N doubles)
+struct DevRhs {
+  HddRhs r{};
+  double* f = nullptr;
+  double* g = nullptr;
+  ~DevRhs() {
+    if (f) cudaFree(f);
+    if (g) cudaFree(g);
+  }
+};
+static int upload_rhs(HddPlan* pl, const HddRhs* h, int64_t B, DevRhs& d) {
+  if (!h) return HDD_OK;
+  const int64_t nn = int64_t(pl->plan.m) * pl->plan.m, ng = int64_t(4) * pl->plan.N;
+  if (h->f) {
+    const size_t n = size_t(h->f_stride ? B : 1) * nn;
+    CU(cudaMalloc(&d.f, n * 8));
+    CU(cudaMemcpy(d.f, h->f, n * 8, cudaMemcpyHostToDevice));
+    d.r.f = d.f;
+    d.r.f_stride = h->f_stride;
+  }
+  if (h->g) {
+    const size_t n = size_t(h->g_stride ? B : 1) * ng;
+    CU(cudaMalloc(&d.g, n * 8));
+    CU(cudaMemcpy(d.g, h->g, n * 8, cudaMemcpyHostToDevice));
+    d.r.g = d.g;
+    d.r.g_stride = h->g_stride;
+  }
+  return HDD_OK;
+}
+
+int hdd_forward_batch_ex_host(HddPlan* pl, const double* Zh, const double* Kh, int64_t B, const HddRhs* rhs,
+                              double* Sh, double* llh) {
+  if (!pl) return HDD_ERR_USAGE;
+  if ((Zh != nullptr) == (Kh != nullptr) && B > 0) return set_err(&pl->err, HDD_ERR_USAGE, "pass exactly one of Z and K");
+  int rc = check_call(pl, B, Zh ? Zh : Kh, Zh != nullptr);
+  if (rc != HDD_OK) return rc;
+  if ((rc = check_rhs(pl, rhs, true)) != HDD_OK) return rc;
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  if ((rc = take_error(pl)) != HDD_OK) return rc;
+  DevRhs d;
+  if ((rc = upload_rhs(pl, rhs, B, d)) != HDD_OK) return rc;
+  const int in_w = Zh ? pl->plan.n_z : 2 * pl->plan.N * pl->plan.N;
+  return run_host(pl, Zh ? Zh : Kh, in_w, Kh != nullptr, B, Sh, llh, rhs ? &d.r : nullptr);
+}
+
+int hdd_solve_batch_ex(HddPlan* pl, const double* Z, const double* K, int64_t B, const HddRhs* rhs, double* U,
+                       void* stream) {
+  if (!pl) return HDD_ERR_USAGE;
+  if ((Z != nullptr) == (K != nullptr) && B > 0) return set_err(&pl->err, HDD_ERR_USAGE, "pass exactly one of Z and K");
+  int rc = check_call(pl, B, Z ? Z : K, Z != nullptr);
+  if (rc != HDD_OK) return rc;
+  if ((rc = check_rhs(pl, rhs, false)) != HDD_OK) return rc;
+  if ((pl->dev.mode != 1 || !pl->plan.full_solve) && pl->plan.leaf_depth > 0)
+    return set_err(&pl->err, HDD_ERR_USAGE,
+                   "the full-solution sweep requires a full-solution plan (mode = 1, full_solve = 1 keeps every factor)");
+  if (B > 0 && !U) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  if ((rc = take_error(pl)) != HDD_OK) return rc;
+  return run_batch(pl, Z, K, B, nullptr, nullptr, U, static_cast<cudaStream_t>(stream), rhs);
+}
+
+int hdd_solve_batch_ex_host(HddPlan* pl, const double* Zh, const double* Kh, int64_t B, const HddRhs* rhs,
+                            double* Uh) {
+  if (!pl) return HDD_ERR_USAGE;
+  if ((Zh != nullptr) == (Kh != nullptr) && B > 0) return set_err(&pl->err, HDD_ERR_USAGE, "pass exactly one of Z and K");
+  int rc = check_call(pl, B, Zh ? Zh : Kh, Zh != nullptr);
+  if (rc != HDD_OK) return rc;
+  if ((rc = check_rhs(pl, rhs, true)) != HDD_OK) return rc;
+  if (B > 0 && !Uh) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  DevRhs d;
+  if ((rc = upload_rhs(pl, rhs, B, d)) != HDD_OK) return rc;
+  const bool is_kappa = Kh != nullptr;
+  const int64_t in_w = is_kappa ? int64_t(2) * pl->plan.N * pl->plan.N : pl->plan.n_z;
+  const int64_t nn = int64_t(pl->plan.m) * pl->plan.m;
+  double* dX = nullptr;
+  double* dU = nullptr;
+  CU(cudaMalloc(&dX, size_t(B) * std::max<int64_t>(in_w, 1) * 8));
+  if (cudaMalloc(&dU, size_t(B) * nn * 8) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(dX);
+    return set_err(&pl->err, HDD_ERR_NOMEM, "device allocation of the solution buffer failed");
+  }
+  cudaStream_t st = pl->stream;
+  if (cudaMemcpyAsync(dX, is_kappa ? Kh : Zh, size_t(B) * in_w * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    rc = HDD_ERR_CUDA;
+  if (rc == HDD_OK)
+    rc = hdd_solve_batch_ex(pl, is_kappa ? nullptr : dX, is_kappa ? dX : nullptr, B, rhs ? &d.r : nullptr, dU, st);
+  if (rc == HDD_OK && cudaMemcpyAsync(Uh, dU, size_t(B) * nn * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    rc = HDD_ERR_CUDA;
+  if (rc == HDD_OK) rc = sync_and_check(pl, st);
+  cudaFree(dX);
+  cudaFree(dU);
+  return rc;
+}
+
 int hdd_posterior_weights(const double* ll, const double* lp, int64_t n, double* w, int64_t* idx, double* lse,
                           void* stream) {
   if (n <= 0 || !ll || !w || !idx || !lse) return HDD_ERR_USAGE;
@@ -912,6 +1095,18 @@ int hdd_kappa_batch(HddPlan* pl, const double* Z, int64_t B, double* kappa, void
   }
   if ((rc = enqueue_error_copy(pl, st)) != HDD_OK) return rc;
   return sync_and_check(pl, st);
+}
+
+int hdd_debug_lowrank_wide(HddPlan* pl, int64_t* total) {
+  if (!pl || !total || pl->device < 0) return HDD_ERR_USAGE;
+  *total = 0;
+  if (!pl->dev.lr_wide_n) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  int v[2] = {0, 0};
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(v, pl->dev.lr_wide_n, sizeof(v), cudaMemcpyDeviceToHost));
+  *total = v[1];
+  return HDD_OK;
 }
 
 int hdd_last_error(const HddPlan* pl, HddError* out) {

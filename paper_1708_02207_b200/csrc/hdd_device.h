@@ -95,6 +95,15 @@ struct DevPlan {
   const int32_t* lr_blk;   // [n][5]: node (depth-local), row offset, p, col offset, q
   const double* lr_omega;  // [q_max][32] fixed Gaussian test matrix
   double* lr_scale;        // [max nodes per depth][bcap]  ||Psi||_F^2
+  // wide sketch (k_max 25..64): blocks queued by compress_kernel, l = k_max + 8 <= 72
+  const double* lr_omega_w;   // [q_max][72]
+  int2* lr_wide_list;         // [lr_wide_cap] (depth-local block, sample); NULL when k_max <= 24
+  int* lr_wide_n;
+  int lr_wide_cap, lr_wide_ctas;
+  double* lr_wide_scr;        // [lr_wide_ctas][lr_wide_stride]  Y [p_max][72] | B [72][q_max]
+  int64_t lr_wide_stride;
+  int lr_pmax, lr_qmax;
+  int lr_force_wide;          // test hook (HDD_LR_FORCE_WIDE=1): every block through the wide sketch
   int64_t fac_elems, u_elems;
   int n_fslots;
   double* fac;             // [bcap][fac_elems]  W | L^T | v rows of every upper node
@@ -117,6 +126,14 @@ struct DevPlan {
   int tiny;
   const double* gfull;     // [m*m] Dirichlet value at every boundary node (interior 0), NULL = g = 0
   long long root_ref;      // reference id of the root (error records)
+  // per-call right-hand sides (hdd_forward_batch_ex): f rows with stride f_stride
+  // (0 = one row for the batch; f above then points at the call's data), Dirichlet
+  // rows gcall [.][4N] with stride g_stride, boundary position of every leaf
+  // perimeter node leaf_gpos [n_leaves][64] (-1 off the domain boundary)
+  int64_t f_stride;
+  const double* gcall;
+  int64_t g_stride;
+  const int32_t* leaf_gpos;
 };
 
 // launchers (hdd_kernels.cu); all return cudaError_t of the launch
@@ -128,6 +145,7 @@ size_t merge_m2_smem_bytes(int ngp, int ldp, int K, int nc);
 size_t merge_l_smem_bytes(int K, int nc);
 cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int blk0, int nblk, int B,
                             int pmax, cudaStream_t s);
+cudaError_t launch_compress_wide(const DevPlan& p, const DevUpper* nodes_dev, int blk0, cudaStream_t s);
 cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_ng, cudaStream_t s);
 cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cudaStream_t s);
 cudaError_t launch_posterior(const double* ll, const double* lp, int64_t n, double* w, int64_t* idx, double* lse,

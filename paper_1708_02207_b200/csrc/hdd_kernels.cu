@@ -40,6 +40,26 @@ __device__ __forceinline__ void record_error(const DevPlan& p, int code, int sam
   atomicMin(&p.err->key, dev_error_key(p.sample0 + sample, code, node));
 }
 
+// Right-hand side of sample s: per-call rows (f_stride, hdd_forward_batch_ex) or the
+// plan's fixed f; NULL = f = 1.
+__device__ __forceinline__ const double* sample_f(const DevPlan& p, int s) {
+  return p.f ? p.f + int64_t(s) * p.f_stride : nullptr;
+}
+// Dirichlet value of perimeter node t of leaf `leaf` for sample s: per-call data
+// (leaf_gpos: position in the boundary vector, -1 off the domain boundary) or the plan's.
+__device__ __forceinline__ double leaf_gval(const DevPlan& p, int leaf, int s, int t) {
+  if (p.gcall) {
+    const int pos = p.leaf_gpos[int64_t(leaf) * 64 + t];
+    return pos >= 0 ? p.gcall[int64_t(s) * p.g_stride + pos] : 0.0;
+  }
+  return p.leaf_g ? p.leaf_g[int64_t(leaf) * 64 + t] : 0.0;
+}
+// Value of a constant observation route (boundary point: g there).
+__device__ __forceinline__ double route_const(const DevPlan& p, int o, int s) {
+  const int pos = p.route_node[o];
+  return (p.gcall && pos >= 0) ? p.gcall[int64_t(s) * p.g_stride + pos] : p.route_val[o];
+}
+
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
@@ -144,15 +164,23 @@ __constant__ LeafTabDev c_ltab;
 
 // per-phase clock64 stamps of CTA (0,0) of the last leaf launch (profiling hook)
 __device__ long long g_leaf_clk[64];
+#ifndef HDD_PROFILE_TICKS
+#define LEAF_TICK(i) do { } while (0)
+#else
 #define LEAF_TICK(i) \
   do { if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) g_leaf_clk[i] = clock64(); } while (0)
+#endif
 int read_leaf_clocks(long long* out) {
   return cudaMemcpyFromSymbol(out, g_leaf_clk, sizeof(long long) * 64) == cudaSuccess ? 0 : -1;
 }
 // per-phase clock64 stamps of CTA (sample 0, node 0) of every merge launch, by depth
 __device__ long long g_merge_clk[32][8];
+#ifndef HDD_PROFILE_TICKS
+#define MERGE_TICK(i) do { (void)slot; } while (0)
+#else
 #define MERGE_TICK(i) \
   do { if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && slot >= 0 && slot < 32) g_merge_clk[slot][i] = clock64(); } while (0)
+#endif
 int read_merge_clocks(long long* out) {
   return cudaMemcpyFromSymbol(out, g_merge_clk, sizeof(long long) * 32 * 8) == cudaSuccess ? 0 : -1;
 }
@@ -815,22 +843,22 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
       for (int t = tid; t < ctri(k); t += NT) gdst[t] = out[t];
     // Dirichlet data g on the domain boundary (known perimeter values u_D = g_D):
     // load rows r_a -= Psi_aD g_D, functional columns sigma_c += R_c(D)^T g_D
-    const double* lg = (EXT && p.leaf_g) ? p.leaf_g + int64_t(leaf) * kLeafPerim : nullptr;
+    const bool hasg = EXT && (p.leaf_g || p.gcall);
     for (int t = tid; t < (k + 1) * NC; t += NT) {
       const int a = t / NC, c = t - (t / NC) * NC;
       const int col = cinfo[5 * NC + c];
       if (col < 0) continue;
       const int ct = ctype[c];
       double raw = out[ctri(k) + a * NC + c];
-      if (lg) {
+      if (hasg) {
         if (ct == 0 && a < k) {
           for (int d = 0; d < k; ++d) {
-            const double gd = lg[d];
+            const double gd = leaf_gval(p, leaf, s, d);
             if (gd != 0.0) raw -= out[a >= d ? tri(a) + d : tri(d) + a] * gd;
           }
         } else if (ct != 0 && a == k) {
           for (int d = 0; d < k; ++d) {
-            const double gd = lg[d];
+            const double gd = leaf_gval(p, leaf, s, d);
             if (gd != 0.0) raw += out[ctri(k) + d * NC + c] * gd;
           }
         }
@@ -883,11 +911,13 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
     }
     cp_async_commit();
     stage_panel_program<5, NC, NTH>(tab1);
-    if (p.f)
+    if (p.f) {
+      const double* fs = sample_f(p, s);
       for (int t = tid; t < 289; t += NT) {
         int y = t / 17, x = t - y * 17;
-        fl[t] = p.f[int64_t(L.j0 + y) * p.m + L.i0 + x];
+        fl[t] = fs[int64_t(L.j0 + y) * p.m + L.i0 + x];
       }
+    }
     if (tid < NC) {
       // local column tid of this pass -> leaf column lc (column 0 = the load, in every pass)
       const int lc = tid == 0 ? 0 : 1 + (NC - 1) * pass + (tid - 1);
@@ -1169,7 +1199,7 @@ cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_ou
   leaf2_kernel<NCV, 256, SUBV><<<grid, 256, smem, s>>>(p, ord, ls, B);
     // sub-leaf mean columns and Dirichlet data only exist in plans that need them
     // (separate instantiation: the likelihood configs never pay for them)
-    if (p.has_submean || p.leaf_g) {
+    if (p.has_submean || p.leaf_g || p.gcall) {
       if (ncl == 2) { HDD_LAUNCH_LEAF(2, true) }
       else if (ncl == 4) { HDD_LAUNCH_LEAF(4, true) }
       else { HDD_LAUNCH_LEAF(8, true) }
@@ -2328,7 +2358,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
   double* LiT = G + 32 * kLdd;            // [32][kLdd]
   double* Bc = LiT + 32 * kLdd;           // [32][65] chunk of B (or D)
   double* red = Bc + 32 * 65;             // [64]
-  __shared__ int s_bad, s_k, s_piv[32];
+  __shared__ int s_bad, s_k, s_conv, s_piv[32];
   __shared__ double s_an2, s_bn2;
   auto A = [&](int i, int j) { const int r = R[i], c = Cc[j]; return r >= c ? psi[tri(r) + c] : psi[tri(c) + r]; };
   // ---- pass 1: Y = A Omega (thread per row, all sketch columns), ||A||^2 ----
@@ -2386,6 +2416,14 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
   __syncthreads();
   const double an2 = s_an2;
   const double scale2 = p.lr_scale[int64_t(ln) * p.bcap + s];
+  if (p.lr_force_wide && p.lr_wide_list && !(an2 <= 1e-28 * scale2)) {   // test hook: every block to the wide sketch
+    if (tid == 0) {
+      const int slot = atomicAdd(p.lr_wide_n, 1);
+      if (slot < p.lr_wide_cap) p.lr_wide_list[slot] = make_int2(blockIdx.y, s);
+      atomicAdd(p.lr_wide_n + 1, 1);
+    }
+    return;
+  }
   if (an2 <= 1e-28 * scale2) {          // ||A|| <= 1e-14 ||Psi||: rank 0
     for (int t = tid; t < P_ * Q_; t += 256) {
       const int i = t / Q_, j = t - i * Q_;
@@ -2529,11 +2567,28 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
       ++kk;
       __syncwarp();
     }
-    if (lane == 0) { s_k = kk; s_bn2 = bn2; }
+    if (lane == 0) { s_k = kk; s_bn2 = bn2; s_conv = (resid + trace <= budget) ? 1 : 0; }
   }
   __syncthreads();
   const int kk = s_k;
-  if (kk > p.lr_kmax || int64_t(kk) * (P_ + Q_) >= int64_t(P_) * Q_) return;   // stays dense
+  // ranks this sketch decides: up to L - 8 (the requested k_max when k_max <= 24)
+  const int kcap = min(p.lr_kmax, L - 8);
+  const bool decided = s_conv && kk <= kcap;
+  if (!decided && p.lr_kmax > kcap && p.lr_wide_list) {
+    // k_max > 24 requested and the block needs a rank above the 32-column sketch:
+    // if a rank in (kcap, k_max] can still satisfy the storage rule, hand the block
+    // to the wide-sketch kernel (l = k_max + 8 columns, compress_wide_kernel)
+    const int64_t kstore = (int64_t(P_) * Q_ - 1) / (P_ + Q_);    // largest k with k (p + q) < p q
+    if (kstore > kcap) {
+      if (tid == 0) {
+        const int slot = atomicAdd(p.lr_wide_n, 1);
+        if (slot < p.lr_wide_cap) p.lr_wide_list[slot] = make_int2(blockIdx.y, s);
+        atomicAdd(p.lr_wide_n + 1, 1);         // running total (hdd_debug_lowrank_wide)
+      }
+      return;
+    }
+  }
+  if (!decided || int64_t(kk) * (P_ + Q_) >= int64_t(P_) * Q_) return;   // stays dense
   // ---- pass 3: A_k = Q (C D) with D = L_SS^-1 B_S, per 64-column chunk ----
   double* Ec = red + 64;                  // [32][65]
   for (int j0 = 0; j0 < Q_; j0 += 64) {
@@ -2596,6 +2651,202 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
   }
 }
 
+// Wide sketch (k_max in 25..64): the blocks the 32-column kernel could not decide
+// (queued in lr_wide_list), l = k_max + 8 <= 72 sketch columns, the same algorithm
+// (randomized range finder, shifted CholeskyQR2, B = Q^T A, pivoted Cholesky of
+// B B^T with the exact error, storage rule) with Y / B in a global scratch slab per
+// CTA.  Rare path (ranks above 24 at the requested eps): plain loops, fixed-order
+// reductions (bitwise reproducible).
+constexpr int kLWW = 72;
+__global__ void __launch_bounds__(256) compress_wide_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int blk0) {
+  extern __shared__ __align__(16) double smw[];
+  double* G = smw;                          // [kLWW][kLWW + 1] Gram / M
+  double* Cm = G + kLWW * (kLWW + 1);       // [kLWW][kLWW + 1] pivoted factor C
+  double* red = Cm + kLWW * (kLWW + 1);     // [256]
+  __shared__ int s_piv[kLWW], s_k, s_conv;
+  __shared__ double s_an2;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int L = min(p.lr_kmax + 8, kLWW);
+  double* Y = p.lr_wide_scr + int64_t(blockIdx.x) * p.lr_wide_stride;     // [P][kLWW]
+  double* Bm = Y + int64_t(p.lr_pmax) * kLWW;                               // [kLWW][qmax]
+  const int n_items = min(*p.lr_wide_n, p.lr_wide_cap);
+  for (int e = blockIdx.x; e < n_items; e += gridDim.x) {
+    const int2 it = p.lr_wide_list[e];
+    const int32_t* bd = p.lr_blk + 5 * (blk0 + it.x);
+    const int ln = bd[0], roff = bd[1], P_ = bd[2], coff = bd[3], Q_ = bd[4];
+    const int QM = p.lr_qmax;
+    const DevUpper& U = nodes[ln];
+    const int s = it.y;
+    double* psi = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
+    const int32_t* R = p.lr_rows + roff;
+    const int32_t* Cc = p.lr_cols + coff;
+    auto A = [&](int i, int j) { const int r = R[i], c = Cc[j]; return r >= c ? psi[tri(r) + c] : psi[tri(c) + r]; };
+    // 1. Y = A Omega, ||A||^2
+    double an = 0.0;
+    for (int idx = tid; idx < P_ * L; idx += 256) {
+      const int i = idx / L, t = idx - (idx / L) * L;
+      double acc = 0.0;
+      for (int j = 0; j < Q_; ++j) acc = fma(A(i, j), p.lr_omega_w[j * kLWW + t], acc);
+      Y[int64_t(i) * kLWW + t] = acc;
+    }
+    for (int idx = tid; idx < P_ * Q_; idx += 256) {
+      const double a = A(idx / Q_, idx - (idx / Q_) * Q_);
+      an = fma(a, a, an);
+    }
+    red[tid] = an;
+    __syncthreads();
+    if (tid == 0) {
+      double t2 = 0.0;
+      for (int w = 0; w < 256; ++w) t2 += red[w];
+      s_an2 = t2;
+    }
+    __syncthreads();
+    const double an2 = s_an2;
+    // 2. shifted CholeskyQR2: Q = Y L^-T with Y^T Y + shift = L L^T, twice
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int idx = tid; idx < L * L; idx += 256) {
+        const int a = idx / L, b = idx - (idx / L) * L;
+        double v = 0.0;
+        for (int i = 0; i < P_; ++i) v = fma(Y[int64_t(i) * kLWW + a], Y[int64_t(i) * kLWW + b], v);
+        G[a * (kLWW + 1) + b] = v;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double tr = 0.0;
+        for (int a = 0; a < L; ++a) tr += G[a * (kLWW + 1) + a];
+        const double shift = 1e-13 * tr + 1e-300;
+        for (int a = 0; a < L; ++a) G[a * (kLWW + 1) + a] += shift;
+      }
+      __syncthreads();
+      for (int j = 0; j < L; ++j) {             // right-looking Cholesky, lower triangle
+        const double d = sqrt(G[j * (kLWW + 1) + j]);
+        __syncthreads();
+        for (int i = j + 1 + tid; i < L; i += 256) G[i * (kLWW + 1) + j] /= d;
+        if (tid == 0) G[j * (kLWW + 1) + j] = d;
+        __syncthreads();
+        const int w = L - j - 1;
+        for (int t = tid; t < w * w; t += 256) {
+          const int i = j + 1 + t / w, c = j + 1 + t % w;
+          if (c <= i) G[i * (kLWW + 1) + c] = fma(-G[i * (kLWW + 1) + j], G[c * (kLWW + 1) + j], G[i * (kLWW + 1) + c]);
+        }
+        __syncthreads();
+      }
+      for (int i = tid; i < P_; i += 256) {     // row i: q L^T = y
+        double* y = Y + int64_t(i) * kLWW;
+        for (int c = 0; c < L; ++c) {
+          double v = y[c];
+          for (int t = 0; t < c; ++t) v = fma(-y[t], G[c * (kLWW + 1) + t], v);
+          y[c] = v / G[c * (kLWW + 1) + c];
+        }
+      }
+      __syncthreads();
+    }
+    // 3. B = Q^T A, M = B B^T
+    for (int idx = tid; idx < L * Q_; idx += 256) {
+      const int a = idx / Q_, j = idx - (idx / Q_) * Q_;
+      double v = 0.0;
+      for (int i = 0; i < P_; ++i) v = fma(Y[int64_t(i) * kLWW + a], A(i, j), v);
+      Bm[int64_t(a) * QM + j] = v;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < L * L; idx += 256) {
+      const int a = idx / L, b = idx - (idx / L) * L;
+      double v = 0.0;
+      for (int j = 0; j < Q_; ++j) v = fma(Bm[int64_t(a) * QM + j], Bm[int64_t(b) * QM + j], v);
+      G[a * (kLWW + 1) + b] = v;
+    }
+    __syncthreads();
+    // 4. pivoted Cholesky of M (warp 0, lane owns rows lane, lane + 32, lane + 64)
+    if (tid < 32) {
+      constexpr int RPL = (kLWW + 31) / 32;
+      double dg[RPL];
+      bool used[RPL];
+      double bn2 = 0.0;
+      for (int a = 0; a < L; ++a) bn2 += G[a * (kLWW + 1) + a];
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const int r = lane + 32 * u;
+        used[u] = r >= L;
+        dg[u] = r < L ? G[r * (kLWW + 1) + r] : -1.0;
+      }
+      const double budget = p.lr_eps * p.lr_eps * an2;
+      const double resid = fmax(an2 - bn2, 0.0);
+      double trace = bn2;
+      int kk = 0;
+      while (kk < L && !(resid + trace <= budget)) {
+        double best = -1.0;
+        int bi = 1 << 30;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u)
+          if (!used[u] && (dg[u] > best)) { best = dg[u]; bi = lane + 32 * u; }
+        for (int off = 16; off > 0; off >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (best <= 0.0) break;
+        const int piv = bi;
+        const double sq = sqrt(best);
+        double v[RPL];
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          const int r = lane + 32 * u;
+          v[u] = 0.0;
+          if (r < L && (!used[u] || r == piv)) {
+            double t = G[r * (kLWW + 1) + piv];
+            for (int q = 0; q < kk; ++q) t = fma(-Cm[r * (kLWW + 1) + q], Cm[piv * (kLWW + 1) + q], t);
+            v[u] = t / sq;
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          const int r = lane + 32 * u;
+          if (r < L) Cm[r * (kLWW + 1) + kk] = r == piv ? sq : (used[u] ? 0.0 : v[u]);
+          if (r == piv) used[u] = true;
+          if (!used[u]) dg[u] -= v[u] * v[u];
+        }
+        if (lane == 0) s_piv[kk] = piv;
+        double mine = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) mine += used[u] ? 0.0 : fmax(dg[u], 0.0);
+        for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
+        trace = mine;
+        ++kk;
+        __syncwarp();
+      }
+      if (lane == 0) { s_k = kk; s_conv = (resid + trace <= budget) ? 1 : 0; }
+    }
+    __syncthreads();
+    const int kk = s_k;
+    if (s_conv && kk <= p.lr_kmax && int64_t(kk) * (P_ + Q_) < int64_t(P_) * Q_) {
+      // 5. A_k = Q (C D), D = L_SS^-1 B_S; column j of E = C D replaces column j of B
+      for (int j = tid; j < Q_; j += 256) {
+        double d[kLWW];
+        for (int u = 0; u < kk; ++u) {
+          double v = Bm[int64_t(s_piv[u]) * QM + j];
+          for (int w = 0; w < u; ++w) v = fma(-Cm[s_piv[u] * (kLWW + 1) + w], d[w], v);
+          d[u] = v / Cm[s_piv[u] * (kLWW + 1) + u];
+        }
+        for (int a = 0; a < L; ++a) {
+          double v = 0.0;
+          for (int u = 0; u < kk; ++u) v = fma(Cm[a * (kLWW + 1) + u], d[u], v);
+          Bm[int64_t(a) * QM + j] = v;
+        }
+      }
+      __syncthreads();
+      for (int idx = tid; idx < P_ * Q_; idx += 256) {
+        const int i = idx / Q_, j = idx - (idx / Q_) * Q_;
+        double v = 0.0;
+        for (int a = 0; a < L; ++a) v = fma(Y[int64_t(i) * kLWW + a], Bm[int64_t(a) * QM + j], v);
+        const int r = R[i], c = Cc[j];
+        psi[r >= c ? tri(r) + c : tri(c) + r] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int blk0, int nblk, int B,
                             int pmax, cudaStream_t s) {
   psi_norm_kernel<<<dim3(B, n_nodes), 256, 0, s>>>(p, nodes_dev, n_nodes);
@@ -2619,6 +2870,14 @@ cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_n
   if (p.lr_l <= 16) return go(compress_kernel<16, 2>);
   if (p.lr_l <= 24) return go(compress_kernel<24, 2>);
   return go(compress_kernel<32, 2>);
+}
+
+cudaError_t launch_compress_wide(const DevPlan& p, const DevUpper* nodes_dev, int blk0, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (2 * size_t(kLWW) * (kLWW + 1) + 256);
+  cudaError_t e = cudaFuncSetAttribute(compress_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  compress_wide_kernel<<<p.lr_wide_ctas, 256, smem, s>>>(p, nodes_dev, blk0);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_kng,
@@ -2647,7 +2906,7 @@ __global__ void finalize_kernel(DevPlan p, int B, double* __restrict__ S, double
     if (kind == 0) {
       v = sig[p.route_col[o]];
     } else if (kind == 1) {
-      v = p.route_val[o];
+      v = route_const(p, o, s);
     } else if (kind == 2) {
       // leaf point: l^T u_B(leaf) + sigma, u_B from the father's u_K
       const int l = p.route_node[o];
@@ -2782,7 +3041,7 @@ __global__ void __launch_bounds__(32) leaf_solve_kernel(DevPlan p, double* __res
   for (int t = lane; t < kLeafPerim; t += 32) {
     const int c = L.parent >= 0 ? p.leaf_cmap[int64_t(leaf) * kLeafPerim + t] : -1;
     ub[t] = c >= 0 ? p.ubuf[int64_t(s) * p.u_elems + p.upper[L.parent].u_off + c]
-                   : (p.leaf_g ? p.leaf_g[int64_t(leaf) * kLeafPerim + t] : 0.0);   // u = g on the domain boundary
+                   : leaf_gval(p, leaf, s, t);    // u = g on the domain boundary
   }
   __syncwarp();
   auto k0 = [&](int cx, int cy) { return kap[cx * 32 + 2 * cy]; };
@@ -2803,7 +3062,7 @@ __global__ void __launch_bounds__(32) leaf_solve_kernel(DevPlan p, double* __res
     for (int i = 2; i < kBW - 1; ++i) col[i] = 0.0;
     col[kBW - 1] = y < kIn ? Nn : 0.0;
     // lumped load (psi_f = h^2/6 diag(2,1,1,2) per cell -> h^2 f at an interior node)
-    double r = h2 * (p.f ? p.f[int64_t(L.j0 + y) * m + L.i0 + x] : 1.0);
+    double r = h2 * (p.f ? sample_f(p, s)[int64_t(L.j0 + y) * m + L.i0 + x] : 1.0);
     if (x == 1) r -= Wc * ub[perim_index(0, y)];
     if (x == kIn) r -= E * ub[perim_index(kLeafCells, y)];
     if (y == 1) r -= Sc * ub[perim_index(x, 0)];
@@ -2920,7 +3179,16 @@ __global__ void __launch_bounds__(32) tiny_kernel(DevPlan p, int B, double* __re
   const int N = p.N, m = p.m, ni = N - 1, n = ni * ni;
   const double* kb = p.kappa + int64_t(s) * 2 * N * N;
   for (int t = lane; t < 2 * N * N; t += 32) kap[t] = kb[t];
-  for (int t = lane; t < m * m; t += 32) u[t] = p.gfull ? p.gfull[t] : 0.0;
+  for (int t = lane; t < m * m; t += 32) {
+    double gv = p.gfull ? p.gfull[t] : 0.0;
+    if (p.gcall) {                          // boundary position in increasing-id order
+      const int i = t % m, j = t / m;
+      const bool bnd = i == 0 || j == 0 || i == N || j == N;
+      const int pos = j == 0 ? i : (j == N ? m + 2 * (N - 1) + i : m + 2 * (j - 1) + (i == N ? 1 : 0));
+      gv = bnd ? p.gcall[int64_t(s) * p.g_stride + pos] : 0.0;
+    }
+    u[t] = gv;
+  }
   for (int t = lane; t < n * n; t += 32) A[t] = 0.0;
   __syncwarp();
   auto k0 = [&](int cx, int cy) { return kap[2 * (cx * N + cy)]; };
@@ -2937,7 +3205,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(DevPlan p, int B, double* __re
     A[j * n + j] = Dg;
     if (x < ni) A[(j + 1) * n + j] = E;
     if (y < ni) A[(j + ni) * n + j] = Nn;
-    double r = h2 * (p.f ? p.f[y * m + x] : 1.0);
+    double r = h2 * (p.f ? sample_f(p, s)[y * m + x] : 1.0);
     if (x == 1) r -= Wc * u[y * m];
     if (x == ni) r -= E * u[y * m + N];
     if (y == 1) r -= Sc * u[x];
@@ -2985,7 +3253,7 @@ __global__ void __launch_bounds__(32) tiny_kernel(DevPlan p, int B, double* __re
     const int kind = p.route_kind[o];
     double v;
     if (kind == 1) {
-      v = p.route_val[o];
+      v = route_const(p, o, s);
     } else if (kind == 4) {
       v = u[p.route_col[o]];
     } else {                                // kind 5: mean over the node's cells

@@ -236,7 +236,13 @@ std::string build_tiny_plan(const HddPlanDesc* d, Plan& P, int* code) {
     const int64_t id = P.obs_id[o];
     if (P.obs_kind[o] == HDD_OBS_POINT) {
       if (id < 0 || id >= m * m) { *code = HDD_ERR_USAGE; return "mesh node " + std::to_string(id) + " not found on any interface"; }
-      P.route[o] = is_boundary(id) ? ObsRoute{1, -1, P.gfull[size_t(id)]} : ObsRoute{4, int(id), 0.0};
+      if (is_boundary(id)) {
+        const int64_t i = id % m, j = id / m;
+        const int pos = int(j == 0 ? i : (j == N ? m + 2 * (N - 1) + i : m + 2 * (j - 1) + (i == N ? 1 : 0)));
+        P.route[o] = ObsRoute{1, -1, P.gfull[size_t(id)], pos};
+      } else {
+        P.route[o] = ObsRoute{4, int(id), 0.0};
+      }
     } else if (P.obs_kind[o] == HDD_OBS_MEAN) {
       Rect r;
       if (!rect_of_id(P.level, id, &r)) { *code = HDD_ERR_USAGE; return "no tree node with id " + std::to_string(id); }
@@ -353,12 +359,11 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
   };
   // position of a boundary node in increasing-id order: the bottom row (m), then two
   // per interior row (left, right), then the top row
-  auto g_of = [&](int64_t id) -> double {
-    if (!P.has_g) return 0.0;
+  auto bpos_of = [&](int64_t id) -> int {
     const int64_t i = id % m, j = id / m;
-    const int64_t pos = j == 0 ? i : (j == N ? m + 2 * (N - 1) + i : m + 2 * (j - 1) + (i == N ? 1 : 0));
-    return P.g[size_t(pos)];
+    return int(j == 0 ? i : (j == N ? m + 2 * (N - 1) + i : m + 2 * (j - 1) + (i == N ? 1 : 0)));
   };
+  auto g_of = [&](int64_t id) -> double { return P.has_g ? P.g[size_t(bpos_of(id))] : 0.0; };
   for (int t = 0; t < int(all.size()); ++t) {
     const Tmp& T = all[t];
     int64_t rid = postorder_id(P.level, T.path);
@@ -368,10 +373,14 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
       L.i0 = T.r.i0;
       L.j0 = T.r.j0;
       L.gperim.assign(kLeafPerim, 0.0);
-      if (P.has_g) {
+      L.gpos.assign(kLeafPerim, -1);
+      {
         const std::vector<int64_t> per = perimeter(T.r, m);
         for (int a = 0; a < kLeafPerim; ++a)
-          if (is_boundary(per[a])) L.gperim[a] = g_of(per[a]);
+          if (is_boundary(per[a])) {
+            L.gperim[a] = g_of(per[a]);
+            L.gpos[a] = bpos_of(per[a]);
+          }
       }
       continue;
     }
@@ -403,7 +412,7 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     int64_t id = P.obs_id[o];
     if (P.obs_kind[o] == HDD_OBS_POINT) {
       if (id < 0 || id >= m * m) { *code = HDD_ERR_USAGE; return "mesh node " + std::to_string(id) + " not found on any interface"; }
-      if (is_boundary(id)) { P.route[o] = ObsRoute{1, -1, g_of(id)}; continue; }  // u = g there
+      if (is_boundary(id)) { P.route[o] = ObsRoute{1, -1, g_of(id), bpos_of(id)}; continue; }  // u = g there
       int64_t pi = id % m, pj = id / m;
       int t = 0;
       while (true) {
@@ -604,7 +613,11 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
   P.lr_kmax = d->lr_kmax > 0 ? d->lr_kmax : 64;
   P.lr_nmin = d->lr_nmin > 0 ? d->lr_nmin : 32;
   if (P.lr_eps > 0) {
-    P.lr_kmax = std::min(P.lr_kmax, 24);   // device sketch width 32 = k_max + 8
+    // sketch width k_max + 8: 16 / 24 / 32 columns for k_max <= 24 (compress_kernel),
+    // 72 for 25..64 (compress_wide_kernel takes the blocks the narrow sketch cannot decide)
+    if (P.lr_kmax > 64)
+      return "low-rank rank cap k_max = " + std::to_string(P.lr_kmax) +
+             " exceeds the device limit of 64 (sketch width k_max + 8 <= 72)";
     for (UpperNode& U : P.upper) {
       if (U.k <= P.lr_nmin) continue;
       std::vector<double> x(U.k), y(U.k);

@@ -74,13 +74,14 @@ struct Leaf {
   std::vector<int32_t> fslot;   // [ncols] functional slot of a primal point column, -1
   std::vector<int32_t> ccode;   // [ncols] device column code: 0 load, 1 own mean, 2 point, submean_code
   std::vector<double> gperim;   // [64] Dirichlet value of each perimeter node on the domain boundary, else 0
+  std::vector<int32_t> gpos;    // [64] position in the boundary vector g (increasing ids), -1 inside
 };
 
 struct ObsRoute {
   int kind;      // 0 = root column, 1 = constant, 2 = leaf point (primal), 3 = interface point (primal)
   int col;       // root column / leaf column / interface position
   double value;
-  int node = -1; // leaf index (kind 2) or upper index (kind 3)
+  int node = -1; // leaf index (kind 2), upper index (kind 3), boundary position (kind 1 point)
   int slot = -1; // leaf functional slot (kind 2)
 };
 

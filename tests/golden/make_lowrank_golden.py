@@ -11,7 +11,8 @@ Psi^g, Psi^f, Phi^g, Phi^f with the exact-SVD truncation lowrank.py:52-77) for:
 * dense (compression=None),
 * ToleranceSpec(1e-6, 16, 32)  — the BASELINE C5 spec,
 * ToleranceSpec()              — the reference default (1e-6, 64, 32),
-* ToleranceSpec(1e-4, 16, 32) and ToleranceSpec(1e-8, 16, 32) — the error envelope.
+* ToleranceSpec(1e-4, 16, 32) and ToleranceSpec(1e-8, 16, 32) — the error envelope,
+* ToleranceSpec(1e-13, 24 | 64, 32) — ranks above 24 (the device's wide-sketch path).
 
 and records S and ll per (spec, row) in lowrank_L<level>.npz together with Z, y, sigma and
 the observations.  The device tests compare the device low-rank path against these.
@@ -40,6 +41,8 @@ SPECS = {
     "default": (1e-6, 64, 32),
     "e4": (1e-4, 16, 32),
     "e8": (1e-8, 16, 32),
+    "e13k24": (1e-13, 24, 32),   # eps near the 1e-14 floor: ranks above 24 appear
+    "e13k64": (1e-13, 64, 32),   # ... and the device wide (72-column) sketch is needed
 }
 N_ROWS = 3
 

@@ -25,7 +25,7 @@ from paper_1708_02207_b200 import configs
 
 pytestmark = pytest.mark.gpu
 LEVELS = [5, 6, 7, 8]
-SPECS = ["c5", "default", "e4", "e8"]
+SPECS = ["c5", "default", "e4", "e8", "e13k24", "e13k64"]
 
 
 @pytest.fixture(scope="module")
@@ -106,3 +106,47 @@ def test_compressed_path_is_bitwise_reproducible(cuda, golden):
     b = hb.forward_functionals_batch(pr, Z)
     assert np.array_equal(a, b)
     assert np.array_equal(a[0], a[2]) and np.array_equal(a[:2], a[3:])
+
+
+def test_rank_cap_above_24_uses_wide_sketch(cuda, golden):
+    """k_max = 64 at eps = 1e-13: blocks the 32-column sketch cannot decide go to the
+    72-column sketch; the result lies inside the reference's envelope."""
+    import ctypes as C
+    g = have(golden, 8)
+    p64 = problem(g, g["spec_e13k64"])
+    S64 = hb.forward_functionals_batch(p64, g["Z"])
+    n = C.c_int64()
+    p64.plan().check(p64.plan().lib.hdd_debug_lowrank_wide(p64.plan().handle, C.byref(n)))
+    assert n.value > 0
+    for b in range(S64.shape[0]):
+        e_ref = rel(g["S_e13k64"][b], g["S_dense"][b])
+        assert rel(S64[b], g["S_dense"][b]) <= 2 * e_ref + 1e-12
+
+
+@pytest.mark.parametrize("level", [6, 7])
+def test_wide_sketch_alone_matches_reference_envelope(cuda, golden, monkeypatch, level):
+    """Every admissible block through the 72-column kernel (HDD_LR_FORCE_WIDE test
+    hook) with the reference default ToleranceSpec() (eps 1e-6, k_max 64): inside the
+    reference's own compressed-vs-dense envelope, close to the 32-column path, and
+    bitwise reproducible."""
+    import ctypes as C
+    g = have(golden, level)
+    monkeypatch.setenv("HDD_LR_FORCE_WIDE", "1")
+    pw = problem(g, g["spec_default"])
+    S = hb.forward_functionals_batch(pw, g["Z"])
+    n = C.c_int64()
+    pw.plan().check(pw.plan().lib.hdd_debug_lowrank_wide(pw.plan().handle, C.byref(n)))
+    assert n.value > 0
+    assert np.array_equal(S, hb.forward_functionals_batch(pw, g["Z"]))
+    monkeypatch.delenv("HDD_LR_FORCE_WIDE")
+    Sn = hb.forward_functionals_batch(problem(g, g["spec_default"]), g["Z"])
+    for b in range(S.shape[0]):
+        e_ref = rel(g["S_default"][b], g["S_dense"][b])
+        assert rel(S[b], g["S_dense"][b]) <= 2 * e_ref + 1e-12
+        assert rel(S[b], Sn[b]) <= 2 * e_ref + 1e-12
+
+
+def test_rank_cap_above_device_limit_is_config_error(cuda, golden):
+    g = have(golden, 5)
+    with pytest.raises(hb.ConfigError, match="64"):
+        problem(g, (1e-6, 65, 32)).plan()
