@@ -1,6 +1,8 @@
 // C ABI of libhdd_b200.so (see include/hdd.h): plan lifetime, device memory,
 // sub-batch scheduling of the kernels, error mapping.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -62,7 +64,26 @@ struct HddPlan {
   // primal top-down: DevUpper copies of the visited nodes, grouped by depth
   DevUpper* d_td = nullptr;
   std::vector<int> td_first, td_count;
+  // tier-L Schur update (schur_l_kernel): one TMA tensor map per tier-L node, grouped
+  // by depth in launch order, and the largest tile count of the depth
+  std::vector<CUtensorMap> h_tmaps;     // host copies, passed as __grid_constant__ parameters
+  std::vector<int> tm_ntiles;           // tile count per map
+  std::vector<int> tm_first, tm_tiles;
+  bool schur_split = false;
 };
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
 
 static HddError g_create_err{};
 constexpr int kWideSketch = 72;   // compress_wide_kernel sketch columns (kLWW)
@@ -495,6 +516,50 @@ static int setup_device(HddPlan* pl, int max_batch) {
     pl->allocs.push_back(p);
     pl->ws = static_cast<double*>(p);
   }
+  // tier-L Schur update kernel: tensor maps over each tier-L node's panel slice
+  // [bcap][ngp][ldp] of the workspace
+  {
+    // opt-in (HDD_SCHUR_L_SPLIT=1): measured slower than the fused epilogue on C4
+    // depths 5..1 and C5 depths 7..3, 4 % faster only on C5 depth 2
+    const char* sv = std::getenv("HDD_SCHUR_L_SPLIT");
+    pl->schur_split = sv && sv[0] == '1';
+    pl->tm_first.assign(P.upper_by_depth.size(), -1);
+    pl->tm_tiles.assign(P.upper_by_depth.size(), 0);
+    std::vector<CUtensorMap> maps;
+    auto enc = tensor_map_encoder();
+    if (!enc) pl->schur_split = false;
+    for (size_t dep = 0; dep < P.upper_by_depth.size() && pl->schur_split; ++dep) {
+      if (!pl->depth_tier[dep]) continue;
+      const auto& ids = P.upper_by_depth[dep];
+      pl->tm_first[dep] = int(maps.size());
+      for (size_t li = 0; li < ids.size(); ++li) {
+        const DevUpper& d = pl->h_upper[ids[li]];
+        const int ngp = (d.ng + d.nb - 1) / d.nb * d.nb;
+        CUtensorMap m;
+        std::memset(&m, 0, sizeof(m));
+        void* base = pl->ws + int64_t(li) * pl->depth_ws[dep] * bcap;
+        const cuuint64_t dims[3] = {cuuint64_t(d.ldp), cuuint64_t(ngp), cuuint64_t(bcap)};
+        const cuuint64_t strides[2] = {cuuint64_t(d.ldp) * 8, cuuint64_t(pl->depth_ws[dep]) * 8};
+        const cuuint32_t box[3] = {8, cuuint32_t(schur_l_box_rows()), 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+          return set_err(&pl->err, HDD_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+        if (std::getenv("HDD_SCHUR_L_DEBUG"))
+          std::fprintf(stderr, "tmap dep %zu node %zu: base %p ldp %d ngp %d bcap %d stride2 %lld k %d nc %d tiles %d\n",
+                       dep, li, base, d.ldp, ngp, bcap, (long long)pl->depth_ws[dep], d.k, d.nc,
+                       schur_l_tiles(d.k, d.nc));
+        maps.push_back(m);
+        pl->tm_ntiles.push_back(schur_l_tiles(d.k, d.nc));
+        pl->tm_tiles[dep] = std::max(pl->tm_tiles[dep], schur_l_tiles(d.k, d.nc));
+      }
+    }
+    if (maps.empty()) pl->schur_split = false;
+    pl->h_tmaps = std::move(maps);
+    D.schur_split = pl->schur_split ? 1 : 0;
+  }
   {
     void* p = nullptr;
     CU(cudaMalloc(&p, size_t(2) * P.N * P.N * bcap * sizeof(double)));
@@ -528,6 +593,8 @@ static int setup_device(HddPlan* pl, int max_batch) {
     for (size_t dep = 0; dep < P.upper_by_depth.size(); ++dep) {
       if (P.upper_by_depth[dep].empty()) continue;
       n += 1 + (D.mode == 1 && pl->td_count[dep] > 0 ? 1 : 0);
+      if (pl->depth_tier[dep] && D.schur_split)
+        for (size_t li = 0; li < P.upper_by_depth[dep].size(); ++li) n += pl->tm_ntiles[pl->tm_first[dep] + li] > 0;
       if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0) n += D.lr_wide_list ? 3 : 2;
     }
     pl->n_launches = n;
@@ -635,6 +702,9 @@ static int run_sub_batch(HddPlan* pl, const double* Z, const double* Kin, int B,
     if (!ids.empty()) {
       CU(launch_merge(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->ws, pl->depth_ws[dep],
                       pl->depth_tier[dep], pl->depth_rows[dep], pl->depth_smem[dep], pl->depth_nb[dep], st, dep));
+      if (pl->depth_tier[dep] && D.schur_split && pl->tm_tiles[dep] > 0)   // the root (k = 0) has no update
+        CU(launch_schur_l(D, pl->d_upper + ids.front(), pl->h_tmaps.data() + pl->tm_first[dep],
+                          pl->tm_ntiles.data() + pl->tm_first[dep], int(ids.size()), B, st));
       if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0) {
         if (D.lr_wide_list) CU(cudaMemsetAsync(D.lr_wide_n, 0, sizeof(int), st));
         CU(launch_compress(D, pl->d_upper + ids.front(), int(ids.size()), pl->lr_blk0[dep], pl->lr_nblk[dep], B,

@@ -1,6 +1,7 @@
 // Device-side plan tables and kernel launchers (internal header).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace hdd {
@@ -104,6 +105,7 @@ struct DevPlan {
   int64_t lr_wide_stride;
   int lr_pmax, lr_qmax;
   int lr_force_wide;          // test hook (HDD_LR_FORCE_WIDE=1): every block through the wide sketch
+  int schur_split;            // tier L: Schur update in schur_l_kernel (TMA-fed GEMM), not in merge_l_kernel
   int64_t fac_elems, u_elems;
   int n_fslots;
   double* fac;             // [bcap][fac_elems]  W | L^T | v rows of every upper node
@@ -145,6 +147,10 @@ size_t merge_m2_smem_bytes(int ngp, int ldp, int K, int nc);
 size_t merge_l_smem_bytes(int K, int nc);
 cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int blk0, int nblk, int B,
                             int pmax, cudaStream_t s);
+cudaError_t launch_schur_l(const DevPlan& p, const DevUpper* nodes_dev, const CUtensorMap* tmaps, const int* tiles,
+                           int n_nodes, int B, cudaStream_t s);
+int schur_l_tiles(int k, int nc);
+int schur_l_box_rows();
 cudaError_t launch_compress_wide(const DevPlan& p, const DevUpper* nodes_dev, int blk0, cudaStream_t s);
 cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_ng, cudaStream_t s);
 cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cudaStream_t s);

@@ -24,6 +24,8 @@
 #include <algorithm>
 #include <cstdio>
 
+#include <cuda.h>
+
 #include "hdd.h"
 #include "hdd_device.h"
 #include "hdd_plan.h"
@@ -2176,9 +2178,175 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
     out[tk + k * nc + c] = v;
   }
   MERGE_TICK(4);
-  schur_epilogue_l(mc, P, ldp, k, ngp, Kp, nc, out, sm);
+  if (!p.schur_split) schur_epilogue_l(mc, P, ldp, k, ngp, Kp, nc, out, sm);   // else schur_l_kernel
   MERGE_TICK(5);
 }
+
+// ---------------------------------------------------------------------------
+// Tier-L Schur update as its own batched GEMM (after merge_l_kernel has left the
+// eliminated panel [W | L^T | V] in the HBM workspace):
+//   out(a, b) = A~(a, b) - sum_g W[g][a] W[g][b]      (lower Psi, packed)
+//   out(a, c) = R~(a, c) - sum_g W[g][a] V[g][c]      (R block)
+// One CTA per (128 x 64 output tile, sample, node); the tiles of one node-sample are
+// adjacent in the grid so their panel re-reads hit L2.  The panel rows stream through
+// a kSS-stage ring of TMA tensor tiles (cp.async.bulk.tensor, one tensor map per
+// node: [bcap][ngp][ldp] doubles, box 8 columns x kSR rows -> [col block][row][8]
+// in smem, so every DMMA fragment load is bank-conflict free), completing on
+// mbarriers; 8 warps as 4 x 2 of 32 x 32 DMMA tiles (16 m8n8k4 per k-step).  The
+// assembled A~ / R~ values are gathered from the sons after the K loop.
+// ---------------------------------------------------------------------------
+constexpr int kSA = 128, kSB = 64, kSR = 16, kSS = 4;
+constexpr int kSBX = kSB / 8 + 1;                        // B boxes: one extra for an odd R-block start
+constexpr int kStageD = (kSA + 8 * kSBX) * kSR;          // doubles per stage
+size_t schur_l_smem_bytes() { return sizeof(double) * size_t(kSS) * kStageD + 128; }
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+      ::"r"(smem_u32(dst)), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
+
+// tile t of a node with k boundary rows and nc columns -> (a0, b0, is_r); false past the end
+__device__ __forceinline__ bool schur_tile(int t, int k, int nc, int& a0, int& b0, bool& is_r) {
+  const int na = (k + kSA - 1) / kSA, nbk = (k + kSB - 1) / kSB;
+  for (int ia = 0; ia < na; ++ia) {
+    const int nb = min(nbk, (ia * kSA + kSA) / kSB);     // b tiles with b0 <= a0 + 127 (lower part)
+    if (t < nb) { a0 = ia * kSA; b0 = t * kSB; is_r = false; return true; }
+    t -= nb;
+  }
+  const int nr = (nc + kSB - 1) / kSB;
+  if (t < na * nr) { a0 = (t / nr) * kSA; b0 = (t % nr) * kSB; is_r = true; return true; }
+  return false;
+}
+
+__global__ void __launch_bounds__(256, 2) schur_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
+                                                       const __grid_constant__ CUtensorMap tmap, int node) {
+  extern __shared__ __align__(128) double sst_raw[];
+  // TMA tensor destinations must be 128-byte aligned
+  double* sst = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sst_raw) + 127) & ~uintptr_t(127));
+  __shared__ __align__(8) uint64_t s_full[kSS];
+  const int s = blockIdx.y;
+  const DevUpper& U = nodes[node];
+  const int k = U.k, nc = U.nc;
+  int a0, b0;
+  bool is_r;
+  if (!schur_tile(blockIdx.x, k, nc, a0, b0, is_r)) return;
+  const int ngp = upper_ngp(U), Kp = k + ngp;
+  const int nch = ngp / kSR;
+  // B operand columns start at bcol; TMA box starts must be 16-byte aligned, so the
+  // boxes start at the even column below it and the fragments skip boff columns
+  const int bcol = is_r ? Kp + b0 : b0;
+  const int bstart = bcol & ~1, boff = bcol - bstart;
+  const CUtensorMap* tm = &tmap;
+  const int ldp = U.ldp;
+  auto box_col = [&](int bx) { return bx < kSA / 8 ? a0 + 8 * bx : bstart + 8 * (bx - kSA / 8); };
+  int nbox = 0;
+  for (int bx = 0; bx < kSA / 8 + kSBX; ++bx) nbox += box_col(bx) < ldp;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < kSS; ++i) mbar_init(&s_full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int c) {
+    const int slot = c % kSS;
+    double* st = sst + slot * kStageD;
+    // boxes that start past the panel row (ldp) are not issued (a box entirely outside
+    // the tensor faults); their columns are never stored
+    mbar_arrive_expect_tx(&s_full[slot], uint32_t(nbox * kSR * 8 * 8));
+#pragma unroll 1
+    for (int bx = 0; bx < kSA / 8 + kSBX; ++bx) {
+      const int col = box_col(bx);
+      if (col < ldp) tma_load_3d(st + bx * kSR * 8, tm, col, c * kSR, s, &s_full[slot]);
+    }
+  };
+#ifndef HDD_SL_NOTMA
+  if (tid == 0)
+    for (int c = 0; c < kSS && c < nch; ++c) issue(c);
+#endif
+  const int gq = lane & 3, gr = lane >> 2;
+  const int wa = (warp >> 1) * 32, wb = (warp & 1) * 32;  // warp tile origin inside the CTA tile
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int c = 0; c < nch; ++c) {
+    const int slot = c % kSS;
+#ifndef HDD_SL_NOTMA
+    mbar_wait(&s_full[slot], uint32_t((c / kSS) & 1));
+#endif
+    const double* st = sst + slot * kStageD;
+    const double* As = st + (wa / 8) * kSR * 8;           // 4 A boxes of [kSR][8]
+    const double* Bs = st + (kSA / 8) * kSR * 8;          // B boxes
+#pragma unroll
+    for (int kk = 0; kk < kSR; kk += 4) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[i * kSR * 8 + (kk + gq) * 8 + gr];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int cb = wb + 8 * j + gr + boff;
+        bv[j] = Bs[(cb >> 3) * kSR * 8 + (kk + gq) * 8 + (cb & 7)];
+      }
+#ifndef HDD_SL_NOMMA
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], av[i], bv[j]);
+#else
+      acc[0][0][0] += av[0] * bv[0];
+#endif
+    }
+    __syncthreads();                                       // slot free for the next fill
+#ifndef HDD_SL_NOTMA
+    if (tid == 0 && c + kSS < nch) issue(c + kSS);
+#endif
+  }
+  // epilogue: gather A~ / R~ from the sons, subtract, store packed
+  const MergeCtx mc = merge_ctx(p, U, s);
+  double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
+  const int tk = tri(k);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int a = a0 + wa + 8 * i + gr;
+    if (a >= k) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int b = b0 + wb + 8 * j + 2 * gq + e;
+        if (!is_r) {
+          if (b <= a) out[tri(a) + b] = gather_A(mc, a, b) - acc[i][j][e];
+        } else if (b < nc) {
+          out[tk + a * nc + b] = gather_R(mc, a, b) - acc[i][j][e];
+        }
+      }
+  }
+}
+
+// one launch per node: the node's tensor map travels as a __grid_constant__ parameter
+cudaError_t launch_schur_l(const DevPlan& p, const DevUpper* nodes_dev, const CUtensorMap* tmaps, const int* tiles,
+                           int n_nodes, int B, cudaStream_t s) {
+  const size_t smem = schur_l_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(schur_l_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  for (int n = 0; n < n_nodes; ++n) {
+    if (tiles[n] == 0) continue;                          // k = 0 (root): nothing to update
+    schur_l_kernel<<<dim3(tiles[n], B, 1), 256, smem, s>>>(p, nodes_dev, tmaps[n], n);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+int schur_l_tiles(int k, int nc) {
+  const int na = (k + kSA - 1) / kSA, nbk = (k + kSB - 1) / kSB;
+  int t = 0;
+  for (int ia = 0; ia < na; ++ia) t += std::min(nbk, (ia * kSA + kSA) / kSB);
+  return t + na * ((nc + kSB - 1) / kSB);
+}
+int schur_l_box_rows() { return kSR; }
 
 cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
                          int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s, int slot) {

@@ -448,3 +448,22 @@ def test_solve_requires_primal_plan(torch_cuda):
         plan.check(plan.lib.hdd_solve_batch(plan.handle, C.c_void_p(Z.data_ptr()), 2, C.c_void_p(U.data_ptr()), None))
     # the Python route builds a primal plan for the sweep on its own
     assert np.isfinite(hb.solve_batch(prob, Z.cpu().numpy())).all()
+
+
+def test_tier_l_split_schur_kernel_matches(torch_cuda, golden, monkeypatch):
+    """The opt-in TMA-fed tier-L Schur-update kernel (HDD_SCHUR_L_SPLIT=1, schur_l_kernel)
+    gives the fused epilogue's numbers on C4 / C5 (every tier-L depth) and on C2 with
+    every depth forced onto tier L."""
+    g4, g5, g2 = golden("cfg_C4"), golden("cfg_C5"), golden("cfg_C2")
+    ref4 = hb.forward_functionals_batch(configs.make_problem("C4"), g4["Z"])
+    ref5 = hb.forward_functionals_batch(configs.make_problem("C5"), g5["Z"])
+    monkeypatch.setenv("HDD_SCHUR_L_SPLIT", "1")
+    s4 = hb.forward_functionals_batch(configs.make_problem("C4"), g4["Z"])
+    s5 = hb.forward_functionals_batch(configs.make_problem("C5"), g5["Z"])
+    assert rel(s4, ref4) <= 1e-13 and rel(s5, ref5) <= 1e-13
+    for b in range(s4.shape[0]):
+        assert rel(s4[b], g4["S"][b]) <= TOL
+    monkeypatch.setenv("HDD_FORCE_TIER_L", "1")
+    s2 = hb.forward_functionals_batch(configs.make_problem("C2"), g2["Z"])
+    for b in range(s2.shape[0]):
+        assert rel(s2[b], g2["S"][b]) <= TOL
