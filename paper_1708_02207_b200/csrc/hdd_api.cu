@@ -34,7 +34,8 @@ struct HddPlan {
   std::vector<int> depth_rows;         // max k + ngp over the depth's nodes
   std::vector<int> depth_nb;           // elimination block rows (8 or 32)
   std::vector<int> depth_kng;          // max k + 2 ng (top-down smem)
-  std::vector<int> lr_blk0, lr_nblk, lr_pmax;   // low-rank blocks per depth
+  std::vector<int> lr_blk0, lr_nblk, lr_pmax;   // low-rank blocks per depth (lr_pmax: large blocks)
+  std::vector<int> lr_nsmall, lr_pmax_s, lr_qmax_s;   // leading small blocks (one warp each)
   double* ws = nullptr;                // tier-L workspace
   size_t leaf_smem = 0;
   HddError err{};
@@ -314,6 +315,11 @@ static int setup_device(HddPlan* pl, int max_batch) {
   pl->lr_blk0.assign(P.upper_by_depth.size(), 0);
   pl->lr_nblk.assign(P.upper_by_depth.size(), 0);
   pl->lr_pmax.assign(P.upper_by_depth.size(), 0);
+  pl->lr_nsmall.assign(P.upper_by_depth.size(), 0);
+  pl->lr_pmax_s.assign(P.upper_by_depth.size(), 0);
+  pl->lr_qmax_s.assign(P.upper_by_depth.size(), 0);
+  // HDD_LR_NO_WARP=1: every block on the CTA kernel (A/B hook)
+  const bool no_warp = std::getenv("HDD_LR_NO_WARP") && std::getenv("HDD_LR_NO_WARP")[0] == '1';
   int lr_qmax = 0;
   int lr_nodes_max = 0;
   if (P.lr_eps > 0) {
@@ -322,19 +328,32 @@ static int setup_device(HddPlan* pl, int max_batch) {
       const auto& ids = P.upper_by_depth[dep];
       lr_nodes_max = std::max(lr_nodes_max, int(ids.size()));
       pl->lr_blk0[dep] = int(blk.size() / 5);
-      for (size_t li = 0; li < ids.size(); ++li) {
-        const UpperNode& U = P.upper[ids[li]];
-        for (size_t b = 0; b + 3 < U.lr_desc.size(); b += 4) {
-          blk.push_back(int32_t(li));
-          blk.push_back(int32_t(rows.size()));
-          blk.push_back(U.lr_desc[b + 1]);
-          blk.push_back(int32_t(cols.size()));
-          blk.push_back(U.lr_desc[b + 3]);
-          rows.insert(rows.end(), U.lr_rows.begin() + U.lr_desc[b], U.lr_rows.begin() + U.lr_desc[b] + U.lr_desc[b + 1]);
-          cols.insert(cols.end(), U.lr_cols.begin() + U.lr_desc[b + 2], U.lr_cols.begin() + U.lr_desc[b + 2] + U.lr_desc[b + 3]);
-          pl->lr_pmax[dep] = std::max(pl->lr_pmax[dep], int(U.lr_desc[b + 1]));
-          lr_qmax = std::max(lr_qmax, int(U.lr_desc[b + 3]));
+      // small blocks (p, q <= 64: one warp each, compress_warp_kernel) first, then the
+      // large ones (one CTA each, compress_kernel)
+      for (int pass_small = 1; pass_small >= 0; --pass_small) {
+        for (size_t li = 0; li < ids.size(); ++li) {
+          const UpperNode& U = P.upper[ids[li]];
+          for (size_t b = 0; b + 3 < U.lr_desc.size(); b += 4) {
+            const int pb = U.lr_desc[b + 1], qb = U.lr_desc[b + 3];
+            const bool small = pb <= 64 && qb <= 64 && !no_warp;
+            if (small != bool(pass_small)) continue;
+            blk.push_back(int32_t(li));
+            blk.push_back(int32_t(rows.size()));
+            blk.push_back(pb);
+            blk.push_back(int32_t(cols.size()));
+            blk.push_back(qb);
+            rows.insert(rows.end(), U.lr_rows.begin() + U.lr_desc[b], U.lr_rows.begin() + U.lr_desc[b] + pb);
+            cols.insert(cols.end(), U.lr_cols.begin() + U.lr_desc[b + 2], U.lr_cols.begin() + U.lr_desc[b + 2] + qb);
+            if (small) {
+              pl->lr_pmax_s[dep] = std::max(pl->lr_pmax_s[dep], pb);
+              pl->lr_qmax_s[dep] = std::max(pl->lr_qmax_s[dep], qb);
+            } else {
+              pl->lr_pmax[dep] = std::max(pl->lr_pmax[dep], pb);
+            }
+            lr_qmax = std::max(lr_qmax, qb);
+          }
         }
+        if (pass_small) pl->lr_nsmall[dep] = int(blk.size() / 5) - pl->lr_blk0[dep];
       }
       pl->lr_nblk[dep] = int(blk.size() / 5) - pl->lr_blk0[dep];
       if (std::getenv("HDD_LR_STATS")) {   // diagnostics: admissible blocks per depth
@@ -372,7 +391,8 @@ static int setup_device(HddPlan* pl, int max_batch) {
     }
     if ((rc = upload(pl, om, &D.lr_omega))) return rc;
     D.lr_pmax = 0;
-    for (int v : pl->lr_pmax) D.lr_pmax = std::max(D.lr_pmax, v);
+    for (size_t dep = 0; dep < pl->lr_pmax.size(); ++dep)    // wide scratch rows: any queued block
+      D.lr_pmax = std::max(D.lr_pmax, std::max(pl->lr_pmax[dep], pl->lr_pmax_s[dep]));
     D.lr_qmax = std::max(lr_qmax, 1);
     if (P.lr_kmax > 24) {
       std::vector<double> omw(size_t(D.lr_qmax) * kWideSketch);
@@ -595,7 +615,8 @@ static int setup_device(HddPlan* pl, int max_batch) {
       n += 1 + (D.mode == 1 && pl->td_count[dep] > 0 ? 1 : 0);
       if (pl->depth_tier[dep] && D.schur_split)
         for (size_t li = 0; li < P.upper_by_depth[dep].size(); ++li) n += pl->tm_ntiles[pl->tm_first[dep] + li] > 0;
-      if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0) n += D.lr_wide_list ? 3 : 2;
+      if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0)
+        n += 1 + (pl->lr_nblk[dep] > pl->lr_nsmall[dep]) + (pl->lr_nsmall[dep] > 0) + (D.lr_wide_list ? 1 : 0);
     }
     pl->n_launches = n;
   }
@@ -707,9 +728,13 @@ static int run_sub_batch(HddPlan* pl, const double* Z, const double* Kin, int B,
                           pl->tm_ntiles.data() + pl->tm_first[dep], int(ids.size()), B, st));
       if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0) {
         if (D.lr_wide_list) CU(cudaMemsetAsync(D.lr_wide_n, 0, sizeof(int), st));
-        CU(launch_compress(D, pl->d_upper + ids.front(), int(ids.size()), pl->lr_blk0[dep], pl->lr_nblk[dep], B,
-                           pl->lr_pmax[dep], st));
-        if (D.lr_wide_list) CU(launch_compress_wide(D, pl->d_upper + ids.front(), pl->lr_blk0[dep], st));
+        const int ns = pl->lr_nsmall[dep];
+        // psi norms, then the large blocks (CTA each), then the small ones (warp each)
+        CU(launch_compress(D, pl->d_upper + ids.front(), int(ids.size()), pl->lr_blk0[dep] + ns,
+                           pl->lr_nblk[dep] - ns, B, pl->lr_pmax[dep], st));
+        CU(launch_compress_warp(D, pl->d_upper + ids.front(), pl->lr_blk0[dep], ns, B, pl->lr_pmax_s[dep],
+                                pl->lr_qmax_s[dep], st));
+        if (D.lr_wide_list) CU(launch_compress_wide(D, pl->d_upper + ids.front(), st));
       }
     }
     if ((rc = mark())) return rc;

@@ -151,7 +151,9 @@ cudaError_t launch_schur_l(const DevPlan& p, const DevUpper* nodes_dev, const CU
                            int n_nodes, int B, cudaStream_t s);
 int schur_l_tiles(int k, int nc);
 int schur_l_box_rows();
-cudaError_t launch_compress_wide(const DevPlan& p, const DevUpper* nodes_dev, int blk0, cudaStream_t s);
+cudaError_t launch_compress_wide(const DevPlan& p, const DevUpper* nodes_dev, cudaStream_t s);
+cudaError_t launch_compress_warp(const DevPlan& p, const DevUpper* nodes_dev, int blk0, int nblk, int B, int pmax,
+                                 int qmax, cudaStream_t s);
 cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_ng, cudaStream_t s);
 cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cudaStream_t s);
 cudaError_t launch_posterior(const double* ll, const double* lp, int64_t n, double* w, int64_t* idx, double* lse,

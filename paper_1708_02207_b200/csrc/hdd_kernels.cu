@@ -2587,7 +2587,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
   if (p.lr_force_wide && p.lr_wide_list && !(an2 <= 1e-28 * scale2)) {   // test hook: every block to the wide sketch
     if (tid == 0) {
       const int slot = atomicAdd(p.lr_wide_n, 1);
-      if (slot < p.lr_wide_cap) p.lr_wide_list[slot] = make_int2(blockIdx.y, s);
+      if (slot < p.lr_wide_cap) p.lr_wide_list[slot] = make_int2(blk0 + blockIdx.y, s);
       atomicAdd(p.lr_wide_n + 1, 1);
     }
     return;
@@ -2750,7 +2750,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
     if (kstore > kcap) {
       if (tid == 0) {
         const int slot = atomicAdd(p.lr_wide_n, 1);
-        if (slot < p.lr_wide_cap) p.lr_wide_list[slot] = make_int2(blockIdx.y, s);
+        if (slot < p.lr_wide_cap) p.lr_wide_list[slot] = make_int2(blk0 + blockIdx.y, s);
         atomicAdd(p.lr_wide_n + 1, 1);         // running total (hdd_debug_lowrank_wide)
       }
       return;
@@ -2826,7 +2826,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
 // CTA.  Rare path (ranks above 24 at the requested eps): plain loops, fixed-order
 // reductions (bitwise reproducible).
 constexpr int kLWW = 72;
-__global__ void __launch_bounds__(256) compress_wide_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int blk0) {
+__global__ void __launch_bounds__(256) compress_wide_kernel(DevPlan p, const DevUpper* __restrict__ nodes) {
   extern __shared__ __align__(16) double smw[];
   double* G = smw;                          // [kLWW][kLWW + 1] Gram / M
   double* Cm = G + kLWW * (kLWW + 1);       // [kLWW][kLWW + 1] pivoted factor C
@@ -2840,7 +2840,7 @@ __global__ void __launch_bounds__(256) compress_wide_kernel(DevPlan p, const Dev
   const int n_items = min(*p.lr_wide_n, p.lr_wide_cap);
   for (int e = blockIdx.x; e < n_items; e += gridDim.x) {
     const int2 it = p.lr_wide_list[e];
-    const int32_t* bd = p.lr_blk + 5 * (blk0 + it.x);
+    const int32_t* bd = p.lr_blk + 5 * it.x;               // absolute block index
     const int ln = bd[0], roff = bd[1], P_ = bd[2], coff = bd[3], Q_ = bd[4];
     const int QM = p.lr_qmax;
     const DevUpper& U = nodes[ln];
@@ -3040,12 +3040,316 @@ cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_n
   return go(compress_kernel<32, 2>);
 }
 
-cudaError_t launch_compress_wide(const DevPlan& p, const DevUpper* nodes_dev, int blk0, cudaStream_t s) {
+cudaError_t launch_compress_wide(const DevPlan& p, const DevUpper* nodes_dev, cudaStream_t s) {
   const size_t smem = sizeof(double) * (2 * size_t(kLWW) * (kLWW + 1) + 256);
   cudaError_t e = cudaFuncSetAttribute(compress_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
-  compress_wide_kernel<<<p.lr_wide_ctas, 256, smem, s>>>(p, nodes_dev, blk0);
+  compress_wide_kernel<<<p.lr_wide_ctas, 256, smem, s>>>(p, nodes_dev);
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Small admissible blocks (p, q <= 64; 75 % of the C5 blocks, all of the deepest
+// levels): one WARP per (block, sample), eight per CTA, no block-wide barriers.  Same
+// algorithm and decisions as compress_kernel (randomized range finder with the
+// same Omega, shifted CholeskyQR2, B = Q^T A kept as H = A^T Q, pivoted Cholesky
+// of M = H^T H with the exact error, storage rule, wide-sketch handoff), with lanes
+// owning block rows (sketch, CholeskyQR) or block columns (H, re-densification) and
+// the L x L factorizations in registers (lane = row, shuffles).  Per warp smem:
+// Q [pmax][LW] | H [qmax][LW] | C [LW][LW + 1] | pivots.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int cw_stride(int pmax, int qmax, int lw) {
+  return ((pmax + qmax) * lw + lw * (lw + 1) + lw / 2 + 2 + 1) & ~1;
+}
+
+template <int LW>
+__global__ void __launch_bounds__(256) compress_warp_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int blk0,
+                                                            int nblk, int B, int pmax, int qmax) {
+  extern __shared__ __align__(16) double smc[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (item >= nblk * B) return;                            // warp-uniform
+  const int bl = item / B, s = item - (item / B) * B;     // samples fastest: a CTA shares the block's tables
+  const int32_t* bd = p.lr_blk + 5 * (blk0 + bl);
+  const int ln = bd[0], roff = bd[1], P_ = bd[2], coff = bd[3], Q_ = bd[4];
+  const DevUpper& U = nodes[ln];
+  double* psi = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
+  const int32_t* R = p.lr_rows + roff;
+  const int32_t* Cc = p.lr_cols + coff;
+  const int L = p.lr_l;
+  double* Yw = smc + int64_t(warp) * cw_stride(pmax, qmax, LW);   // [P][LW]  (Y, then Q)
+  double* Hw = Yw + pmax * LW;                                    // [Q][LW]  (H = A^T Q = B^T)
+  double* Cw = Hw + qmax * LW;                                    // [LW][LW + 1] (CholeskyQR L, then C)
+  int* pv = reinterpret_cast<int*>(Cw + LW * (LW + 1));           // [LW] pivots
+  auto A = [&](int i, int j) { const int r = R[i], c = Cc[j]; return r >= c ? psi[tri(r) + c] : psi[tri(c) + r]; };
+  auto wsum = [&](double v) {
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+  };
+  // ---- Y = A Omega (lane owns rows lane, lane + 32), ||A||^2 ----
+  double y0[LW], y1[LW];
+#pragma unroll
+  for (int t = 0; t < LW; ++t) y0[t] = y1[t] = 0.0;
+  double an = 0.0;
+  const bool v0 = lane < P_, v1 = lane + 32 < P_;
+  const int r0 = v0 ? R[lane] : 0, r1 = v1 ? R[lane + 32] : 0;
+  for (int j = 0; j < Q_; ++j) {
+    const int c = Cc[j];
+    const double a0 = v0 ? (r0 >= c ? psi[tri(r0) + c] : psi[tri(c) + r0]) : 0.0;
+    const double a1 = v1 ? (r1 >= c ? psi[tri(r1) + c] : psi[tri(c) + r1]) : 0.0;
+    an = fma(a0, a0, fma(a1, a1, an));
+    const double2* om = reinterpret_cast<const double2*>(p.lr_omega + j * 32);
+#pragma unroll
+    for (int t = 0; t < LW; t += 2) {
+      const double2 o = __ldg(om + t / 2);
+      y0[t] = fma(a0, o.x, y0[t]);
+      y0[t + 1] = fma(a0, o.y, y0[t + 1]);
+      y1[t] = fma(a1, o.x, y1[t]);
+      y1[t + 1] = fma(a1, o.y, y1[t + 1]);
+    }
+  }
+  const double an2 = wsum(an);
+  const double scale2 = p.lr_scale[int64_t(ln) * p.bcap + s];
+  if (p.lr_force_wide && p.lr_wide_list && !(an2 <= 1e-28 * scale2)) {
+    if (lane == 0) {
+      const int slot = atomicAdd(p.lr_wide_n, 1);
+      if (slot < p.lr_wide_cap) p.lr_wide_list[slot] = make_int2(blk0 + bl, s);
+      atomicAdd(p.lr_wide_n + 1, 1);
+    }
+    return;
+  }
+  if (an2 <= 1e-28 * scale2) {                            // ||A|| <= 1e-14 ||Psi||: rank 0
+    for (int t = lane; t < P_ * Q_; t += 32) {
+      const int i = t / Q_, j = t - (t / Q_) * Q_;
+      const int r = R[i], c = Cc[j];
+      psi[r >= c ? tri(r) + c : tri(c) + r] = 0.0;
+    }
+    return;
+  }
+#pragma unroll
+  for (int t = 0; t < LW; ++t) {                          // columns past L stay zero
+    if (t >= L) { y0[t] = 0.0; y1[t] = 0.0; }
+  }
+  // ---- shifted CholeskyQR2: Q = Y L^-T with Y^T Y + shift = L L^T (twice) ----
+  for (int pass = 0; pass < 2; ++pass) {
+    if (v0)
+#pragma unroll
+      for (int t = 0; t < LW; ++t) Yw[lane * LW + t] = y0[t];
+    if (v1)
+#pragma unroll
+      for (int t = 0; t < LW; ++t) Yw[(lane + 32) * LW + t] = y1[t];
+    __syncwarp();
+    double g[LW];                                           // lane a: row a of Y^T Y
+#pragma unroll
+    for (int b = 0; b < LW; ++b) g[b] = 0.0;
+    const int ar = lane < LW ? lane : 0;
+    for (int i = 0; i < P_; ++i) {
+      const double ya = Yw[i * LW + ar];
+#pragma unroll
+      for (int b = 0; b < LW; ++b) g[b] = fma(ya, Yw[i * LW + b], g[b]);
+    }
+    double gd = 0.0;
+#pragma unroll
+    for (int b = 0; b < LW; ++b) gd = (b == lane) ? g[b] : gd;
+    const double tr = wsum(lane < L ? gd : 0.0);
+    const double shift = 1e-13 * tr + 1e-300;
+#pragma unroll
+    for (int b = 0; b < LW; ++b) {
+      if (lane >= L || b >= L) g[b] = (b == lane) ? 1.0 : 0.0;   // identity past the sketch width
+      else if (b == lane) g[b] += shift;
+    }
+    // register Cholesky, lane = row (rows >= LW are idle copies of row LW - 1)
+    double ild = 1.0;
+#pragma unroll
+    for (int j = 0; j < LW; ++j) {
+      const double dj = __shfl_sync(0xffffffffu, g[j], j);
+      const double il = rsqrt_nr(dj);
+      const double lij = g[j] * il;
+#pragma unroll
+      for (int l = j + 1; l < LW; ++l) g[l] = fma(-lij, __shfl_sync(0xffffffffu, lij, l), g[l]);
+      if (lane == j) ild = il;
+      g[j] = lij;
+    }
+    __syncwarp();
+    if (lane < LW)                                          // L (lower, row-major) with 1/L_jj on the diagonal
+#pragma unroll
+      for (int l = 0; l < LW; ++l)
+        if (l <= lane) Cw[lane * (LW + 1) + l] = l == lane ? ild : g[l];
+    __syncwarp();
+    // rows: q L^T = y  ->  q_c = (y_c - sum_{t < c} q_t L_ct) / L_cc
+#pragma unroll
+    for (int c = 0; c < LW; ++c) {
+      double a = y0[c], b = y1[c];
+#pragma unroll
+      for (int t = 0; t < c; ++t) {
+        const double lct = Cw[c * (LW + 1) + t];
+        a = fma(-y0[t], lct, a);
+        b = fma(-y1[t], lct, b);
+      }
+      const double il = Cw[c * (LW + 1) + c];
+      y0[c] = a * il;
+      y1[c] = b * il;
+    }
+    __syncwarp();
+  }
+  if (v0)
+#pragma unroll
+    for (int t = 0; t < LW; ++t) Yw[lane * LW + t] = y0[t];
+  if (v1)
+#pragma unroll
+    for (int t = 0; t < LW; ++t) Yw[(lane + 32) * LW + t] = y1[t];
+  __syncwarp();
+  // ---- H = A^T Q (lane owns columns lane, lane + 32) ----
+  {
+    double h0[LW], h1[LW];
+#pragma unroll
+    for (int t = 0; t < LW; ++t) h0[t] = h1[t] = 0.0;
+    const bool w0 = lane < Q_, w1 = lane + 32 < Q_;
+    const int c0 = w0 ? Cc[lane] : 0, c1 = w1 ? Cc[lane + 32] : 0;
+    for (int i = 0; i < P_; ++i) {
+      const int r = R[i];
+      const double x0 = w0 ? (r >= c0 ? psi[tri(r) + c0] : psi[tri(c0) + r]) : 0.0;
+      const double x1 = w1 ? (r >= c1 ? psi[tri(r) + c1] : psi[tri(c1) + r]) : 0.0;
+#pragma unroll
+      for (int t = 0; t < LW; ++t) {
+        const double q = Yw[i * LW + t];
+        h0[t] = fma(q, x0, h0[t]);
+        h1[t] = fma(q, x1, h1[t]);
+      }
+    }
+    if (w0)
+#pragma unroll
+      for (int t = 0; t < LW; ++t) Hw[lane * LW + t] = h0[t];
+    if (w1)
+#pragma unroll
+      for (int t = 0; t < LW; ++t) Hw[(lane + 32) * LW + t] = h1[t];
+  }
+  __syncwarp();
+  // ---- M = H^T H (lane a: row a), pivoted Cholesky in registers ----
+  double m[LW];
+#pragma unroll
+  for (int c = 0; c < LW; ++c) m[c] = 0.0;
+  {
+    const int ar = lane < LW ? lane : 0;
+    for (int j = 0; j < Q_; ++j) {
+      const double ha = Hw[j * LW + ar];
+#pragma unroll
+      for (int c = 0; c < LW; ++c) m[c] = fma(ha, Hw[j * LW + c], m[c]);
+    }
+  }
+  double dg = -1.0;
+#pragma unroll
+  for (int c = 0; c < LW; ++c) dg = (c == lane) ? m[c] : dg;
+  bool used = lane >= L;
+  if (used) dg = -1.0;
+  const double bn2 = wsum(used ? 0.0 : dg);
+  const double budget = p.lr_eps * p.lr_eps * an2;
+  const double resid = fmax(an2 - bn2, 0.0);
+  double trace = bn2;
+  double crow[LW];                                         // row `lane` of C
+#pragma unroll
+  for (int u = 0; u < LW; ++u) crow[u] = 0.0;
+  int kk = 0;
+  while (kk < L && !(resid + trace <= budget)) {
+    double best = used ? -1.0 : dg;
+    int bi = lane;
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (best <= 0.0) break;
+    const int piv = bi;
+    const double sq = sqrt(best);
+    double mp = 0.0;                                       // M[lane][piv]
+#pragma unroll
+    for (int c = 0; c < LW; ++c) mp = (c == piv) ? m[c] : mp;
+    double v = mp;
+#pragma unroll
+    for (int u = 0; u < LW; ++u)
+      if (u < kk) v = fma(-crow[u], __shfl_sync(0xffffffffu, crow[u], piv), v);
+    v /= sq;
+    const double cval = lane == piv ? sq : (used ? 0.0 : v);
+#pragma unroll
+    for (int u = 0; u < LW; ++u)
+      if (u == kk) crow[u] = cval;
+    if (lane == piv) used = true;
+    if (!used) dg -= v * v;
+    if (lane == 0) pv[kk] = piv;
+    trace = wsum(used ? 0.0 : fmax(dg, 0.0));
+    ++kk;
+  }
+  const bool conv = resid + trace <= budget;
+  const int kcap = min(p.lr_kmax, L - 8);
+  const bool decided = conv && kk <= kcap;
+  if (!decided && p.lr_kmax > kcap && p.lr_wide_list) {
+    const int64_t kstore = (int64_t(P_) * Q_ - 1) / (P_ + Q_);
+    if (kstore > kcap) {
+      if (lane == 0) {
+        const int slot = atomicAdd(p.lr_wide_n, 1);
+        if (slot < p.lr_wide_cap) p.lr_wide_list[slot] = make_int2(blk0 + bl, s);
+        atomicAdd(p.lr_wide_n + 1, 1);
+      }
+      return;
+    }
+  }
+  if (!decided || int64_t(kk) * (P_ + Q_) >= int64_t(P_) * Q_) return;   // stays dense
+  // ---- A_k = Q (C D), D = L_SS^-1 B_S with B_S[u][j] = H[j][piv_u] ----
+  __syncwarp();
+  if (lane < LW)
+#pragma unroll
+    for (int u = 0; u < LW; ++u) Cw[lane * (LW + 1) + u] = crow[u];
+  __syncwarp();
+  for (int j = lane; j < Q_; j += 32) {
+    double d[LW], e[LW];
+#pragma unroll
+    for (int u = 0; u < LW; ++u) {
+      d[u] = 0.0;
+      if (u < kk) {
+        const int pu = pv[u];
+        double t = Hw[j * LW + pu];
+#pragma unroll
+        for (int w = 0; w < u; ++w) t = fma(-Cw[pu * (LW + 1) + w], d[w], t);
+        d[u] = t / Cw[pu * (LW + 1) + u];
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < LW; ++a) {
+      double t = 0.0;
+#pragma unroll
+      for (int u = 0; u < LW; ++u)
+        if (u < kk) t = fma(Cw[a * (LW + 1) + u], d[u], t);
+      e[a] = a < L ? t : 0.0;
+    }
+    const int c = Cc[j];
+    for (int i = 0; i < P_; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int a = 0; a < LW; ++a) t = fma(Yw[i * LW + a], e[a], t);
+      const int r = R[i];
+      psi[r >= c ? tri(r) + c : tri(c) + r] = t;
+    }
+  }
+}
+
+cudaError_t launch_compress_warp(const DevPlan& p, const DevUpper* nodes_dev, int blk0, int nblk, int B, int pmax,
+                                 int qmax, cudaStream_t s) {
+  if (nblk == 0) return cudaSuccess;
+  const int lw = p.lr_l <= 16 ? 16 : (p.lr_l <= 24 ? 24 : 32);
+  const size_t per_warp = sizeof(double) * size_t(cw_stride(pmax, qmax, lw));
+  const int nw = int(std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / per_warp)));   // warps per CTA
+  const size_t smem = per_warp * nw;
+  const int64_t items = int64_t(nblk) * B;
+  const dim3 grid(unsigned((items + nw - 1) / nw));
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 32 * nw, smem, s>>>(p, nodes_dev, blk0, nblk, B, pmax, qmax);
+    return cudaGetLastError();
+  };
+  if (lw == 16) return go(compress_warp_kernel<16>);
+  if (lw == 24) return go(compress_warp_kernel<24>);
+  return go(compress_warp_kernel<32>);
 }
 
 cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, int max_kng,
