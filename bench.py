@@ -304,9 +304,10 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------
-def traffic_from_capture(cfg_name, stage, launches_per_stage):
-    """DRAM bytes per launch of `stage` from a committed ncu --set full capture of the
-    same config (profiles/traffic.json), or None."""
+def traffic_from_capture(cfg_name, stage, samples_per_launch):
+    """DRAM bytes (read + write) per launch of `stage`: the per-sample figure of a
+    committed ncu --set full capture of the same config and kernel
+    (profiles/traffic.json) times the samples of one launch, or None."""
     try:
         with open(ROOT / "profiles" / "traffic.json") as f:
             rec = json.load(f).get(cfg_name, {}).get(stage)
@@ -314,8 +315,8 @@ def traffic_from_capture(cfg_name, stage, launches_per_stage):
         return None
     if not rec:
         return None
-    return {"bytes_per_launch": rec["dram_bytes_per_launch"], "launches_per_stage_per_step": launches_per_stage,
-            "source": rec["source"], "binding": rec.get("binding")}
+    return {"bytes_per_launch": rec["dram_bytes_per_sample"] * samples_per_launch,
+            "samples_per_launch": samples_per_launch, "source": rec["source"], "binding": rec.get("binding")}
 
 
 def per_config_measurements(dev):
@@ -424,16 +425,20 @@ def main_rank(args):
     ms_max = float(t.item())
     value = G / (ms_max * 1e-3)
 
-    # per-stage (kernel) times: one timed pass, same stream, CUDA events between launches
+    # per-stage (kernel) times: one timed pass over the first two sub-batches (per-sample
+    # stage cost does not depend on the batch once a sub-batch fills the GPU), same
+    # stream, CUDA events between launches; stage_ms is scaled to the whole step
     flush.zero_()
-    plan.check(plan.lib.hdd_forward_batch_timed(plan.handle, C.c_void_p(Zd.data_ptr()), B, None,
+    B_st = min(B, 2 * info.max_batch)
+    plan.check(plan.lib.hdd_forward_batch_timed(plan.handle, C.c_void_p(Zd.data_ptr()), B_st, None,
                                                 C.c_void_p(ll.data_ptr()), C.c_void_p(stream.cuda_stream),
                                                 stage.ctypes.data_as(_lib._f64p), n_stages))
+    stage *= B / B_st
 
     # ---- e2e through the public API: pinned host Z -> device -> ll -> host ----
     Zh = torch.from_numpy(Zl).pin_memory()
     Zh_np = Zh.numpy()
-    n_e2e = 3
+    n_e2e = 2
     e2e_ms = []
     if world > 1:
         dist.barrier()
@@ -470,7 +475,7 @@ def main_rank(args):
     total_fl = leaf_fl + sum(merge_fl.values())
     hbm_gbs, hbm_src = hbm_peak()
     kappa_bytes = (2 * (1 << cfg.level) ** 2 * 8 + cfg.n_z * 8) * B
-    tr = traffic_from_capture(args.config, top, n_sub)
+    tr = traffic_from_capture(args.config, top, B / n_sub)
     algo_per_launch = flops[top] * B / n_sub
 
     cpu = None
@@ -521,6 +526,7 @@ def main_rank(args):
                           "frac_fp64": total_fl * G / (ms_max * 1e-3) / 1e12 / FP64_PEAK_TFLOPS / world,
                           "flops_per_sample": total_fl},
         "stage_ms": shares,
+        "stage_ms_note": f"one CUDA-event-timed pass over the first {B_st} rows, scaled to the {B}-row step",
         "kappa_hbm": {"achieved_gbs": kappa_bytes / (shares["kappa"] * 1e-3) / 1e9, "peak": hbm_gbs,
                       "peak_source": hbm_src},
         "e2e": {"value": G / (e2e_max * 1e-3), "unit": "samples/s",
