@@ -467,3 +467,19 @@ def test_tier_l_split_schur_kernel_matches(torch_cuda, golden, monkeypatch):
     s2 = hb.forward_functionals_batch(configs.make_problem("C2"), g2["Z"])
     for b in range(s2.shape[0]):
         assert rel(s2[b], g2["S"][b]) <= TOL
+
+
+def test_posterior_weights_nan_and_checks(torch_cuda):
+    """numpy's argmax rule with NaN (the first NaN wins) and the argument checks of
+    posterior_weights_device: log_prior length, empty batch."""
+    import torch
+    from paper_1708_02207_b200 import parallel
+    ll = np.array([1.0, np.nan, 3.0, np.nan, 3.0])
+    w, i, lse = parallel.posterior_weights_device(torch.from_numpy(ll).cuda())
+    assert int(i) == int(np.argmax(ll)) == 1
+    ll2 = np.array([1.0, 5.0, -2.0, 5.0])
+    assert int(parallel.posterior_weights_device(torch.from_numpy(ll2).cuda())[1]) == 1
+    with pytest.raises(hb.UsageError):
+        parallel.posterior_weights_device(torch.from_numpy(ll2).cuda(), torch.zeros(3, dtype=torch.float64).cuda())
+    with pytest.raises(hb.UsageError):
+        parallel.posterior_weights_device(torch.zeros(0, dtype=torch.float64).cuda())
