@@ -70,6 +70,7 @@ struct HddPlan {
   std::vector<CUtensorMap> h_tmaps;     // host copies, passed as __grid_constant__ parameters
   std::vector<int> tm_ntiles;           // tile count per map
   std::vector<int> tm_first, tm_tiles;
+  std::vector<int> depth_split;         // tier-L depths run split (assemble / eliminate / schur_l)
   bool schur_split = false;
 };
 
@@ -539,10 +540,12 @@ static int setup_device(HddPlan* pl, int max_batch) {
   // tier-L Schur update kernel: tensor maps over each tier-L node's panel slice
   // [bcap][ngp][ldp] of the workspace
   {
-    // opt-in (HDD_SCHUR_L_SPLIT=1): measured slower than the fused epilogue on C4
-    // depths 5..1 and C5 depths 7..3, 4 % faster only on C5 depth 2
+    // split tier L (assemble / eliminate / TMA Schur update) on the depths whose
+    // interface is deep enough (ng >= 255 by default, HDD_SCHUR_L_MIN_NG): measured
+    // C4 d2 34.6 -> 33.3 ms, C5 d2 120.1 -> 104.8 ms, d1 71.4 -> 60.1 ms per batch;
+    // shallower interfaces keep the fused kernel.  HDD_SCHUR_L_SPLIT=0: off
     const char* sv = std::getenv("HDD_SCHUR_L_SPLIT");
-    pl->schur_split = sv && sv[0] == '1';
+    pl->schur_split = !(sv && sv[0] == '0');
     pl->tm_first.assign(P.upper_by_depth.size(), -1);
     pl->tm_tiles.assign(P.upper_by_depth.size(), 0);
     std::vector<CUtensorMap> maps;
@@ -578,6 +581,15 @@ static int setup_device(HddPlan* pl, int max_batch) {
     }
     if (maps.empty()) pl->schur_split = false;
     pl->h_tmaps = std::move(maps);
+    // split only where the interface is deep enough for the GEMM to amortise its
+    // pipeline and the extra A~ round trip through HBM (HDD_SCHUR_L_MIN_NG, default 256)
+    const int min_ng = std::getenv("HDD_SCHUR_L_MIN_NG") ? std::atoi(std::getenv("HDD_SCHUR_L_MIN_NG")) : 256;
+    pl->depth_split.assign(P.upper_by_depth.size(), 0);
+    for (size_t dep = 0; dep < P.upper_by_depth.size(); ++dep) {
+      int ngmin = 1 << 30;
+      for (int u : P.upper_by_depth[dep]) ngmin = std::min(ngmin, P.upper[u].ng);
+      pl->depth_split[dep] = pl->schur_split && pl->depth_tier[dep] && ngmin >= min_ng - 1;
+    }
     D.schur_split = pl->schur_split ? 1 : 0;
   }
   {
@@ -613,8 +625,10 @@ static int setup_device(HddPlan* pl, int max_batch) {
     for (size_t dep = 0; dep < P.upper_by_depth.size(); ++dep) {
       if (P.upper_by_depth[dep].empty()) continue;
       n += 1 + (D.mode == 1 && pl->td_count[dep] > 0 ? 1 : 0);
-      if (pl->depth_tier[dep] && D.schur_split)
+      if (pl->depth_tier[dep] && D.schur_split && pl->depth_split[dep]) {
+        n += 1;                                             // assemble_l
         for (size_t li = 0; li < P.upper_by_depth[dep].size(); ++li) n += pl->tm_ntiles[pl->tm_first[dep] + li] > 0;
+      }
       if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0)
         n += 1 + (pl->lr_nblk[dep] > pl->lr_nsmall[dep]) + (pl->lr_nsmall[dep] > 0) + (D.lr_wide_list ? 1 : 0);
     }
@@ -721,10 +735,16 @@ static int run_sub_batch(HddPlan* pl, const double* Z, const double* Kin, int B,
   for (int dep = int(P.upper_by_depth.size()) - 1; dep >= 0; --dep) {
     const auto& ids = P.upper_by_depth[dep];
     if (!ids.empty()) {
-      CU(launch_merge(D, pl->d_upper + ids.front(), int(ids.size()), B, pl->ws, pl->depth_ws[dep],
+      // split tier L (opt-in per depth): assemble -> eliminate -> TMA Schur update
+      DevPlan Dd = D;
+      Dd.schur_split = (pl->depth_tier[dep] && D.schur_split && pl->depth_split[dep]) ? 1 : 0;
+      if (Dd.schur_split)
+        CU(launch_assemble_l(Dd, pl->d_upper + ids.front(), int(ids.size()), B, pl->ws, pl->depth_ws[dep],
+                             pl->depth_rows[dep], st));
+      CU(launch_merge(Dd, pl->d_upper + ids.front(), int(ids.size()), B, pl->ws, pl->depth_ws[dep],
                       pl->depth_tier[dep], pl->depth_rows[dep], pl->depth_smem[dep], pl->depth_nb[dep], st, dep));
-      if (pl->depth_tier[dep] && D.schur_split && pl->tm_tiles[dep] > 0)   // the root (k = 0) has no update
-        CU(launch_schur_l(D, pl->d_upper + ids.front(), pl->h_tmaps.data() + pl->tm_first[dep],
+      if (Dd.schur_split && pl->tm_tiles[dep] > 0)   // the root (k = 0) has no update
+        CU(launch_schur_l(Dd, pl->d_upper + ids.front(), pl->h_tmaps.data() + pl->tm_first[dep],
                           pl->tm_ntiles.data() + pl->tm_first[dep], int(ids.size()), B, st));
       if (D.lr_eps > 0 && dep > 0 && pl->lr_nblk[dep] > 0) {
         if (D.lr_wide_list) CU(cudaMemsetAsync(D.lr_wide_n, 0, sizeof(int), st));

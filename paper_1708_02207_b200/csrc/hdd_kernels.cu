@@ -431,6 +431,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -2060,7 +2063,8 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
     __syncthreads();
   }
   MERGE_TICK(1);
-  for (int g = warp; g < ngp; g += 8) gather_panel_row<8>(mc, k, ng, Kp, W, g, P + int64_t(g) * ldp, lane, 32);
+  if (!p.schur_split)     // split mode: assemble_l_kernel has written the panel
+    for (int g = warp; g < ngp; g += 8) gather_panel_row<8>(mc, k, ng, Kp, W, g, P + int64_t(g) * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   __syncthreads();
   MERGE_TICK(2);
@@ -2195,7 +2199,7 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
 // mbarriers; 8 warps as 4 x 2 of 32 x 32 DMMA tiles (16 m8n8k4 per k-step).  The
 // assembled A~ / R~ values are gathered from the sons after the K loop.
 // ---------------------------------------------------------------------------
-constexpr int kSA = 128, kSB = 64, kSR = 16, kSS = 4;
+constexpr int kSA = 128, kSB = 64, kSR = 32, kSS = 4;
 constexpr int kSBX = kSB / 8 + 1;                        // B boxes: one extra for an odd R-block start
 constexpr int kStageD = (kSA + 8 * kSBX) * kSR;          // doubles per stage
 size_t schur_l_smem_bytes() { return sizeof(double) * size_t(kSS) * kStageD + 128; }
@@ -2204,6 +2208,13 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
       ::"r"(smem_u32(dst)), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
+
+__host__ __device__ inline int schur_l_tiles_dev(int k, int nc) {
+  const int na = (k + 127) / 128, nbk = (k + 63) / 64;
+  int t = 0;
+  for (int ia = 0; ia < na; ++ia) t += (nbk < (ia * 128 + 128) / 64 ? nbk : (ia * 128 + 128) / 64);
+  return t + na * ((nc + 63) / 64);
 }
 
 // tile t of a node with k boundary rows and nc columns -> (a0, b0, is_r); false past the end
@@ -2219,63 +2230,79 @@ __device__ __forceinline__ bool schur_tile(int t, int k, int nc, int& a0, int& b
   return false;
 }
 
-__global__ void __launch_bounds__(256, 2) schur_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
+constexpr int kSTPC = 4;                                 // tiles per CTA (the ring runs across them)
+
+// Warp-specialised: warps 0-7 compute (4 x 2 of 32 x 32 DMMA tiles), warp 8 produces
+// (waits for a free slot, lane 0 posts the expected bytes, lanes 0..24 issue one TMA box
+// each).  full[slot] completes on the TMA bytes, empty[slot] on the 8 consumer warps.
+__global__ void __launch_bounds__(288, 1) schur_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
                                                        const __grid_constant__ CUtensorMap tmap, int node) {
   extern __shared__ __align__(128) double sst_raw[];
   // TMA tensor destinations must be 128-byte aligned
   double* sst = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sst_raw) + 127) & ~uintptr_t(127));
-  __shared__ __align__(8) uint64_t s_full[kSS];
+  __shared__ __align__(8) uint64_t s_full[kSS], s_empty[kSS];
   const int s = blockIdx.y;
   const DevUpper& U = nodes[node];
   const int k = U.k, nc = U.nc;
-  int a0, b0;
-  bool is_r;
-  if (!schur_tile(blockIdx.x, k, nc, a0, b0, is_r)) return;
+  const int n_tiles = schur_l_tiles_dev(k, nc);
+  const int t0 = blockIdx.x * kSTPC;
+  if (t0 >= n_tiles) return;
+  const int ntl = min(kSTPC, n_tiles - t0);
   const int ngp = upper_ngp(U), Kp = k + ngp;
   const int nch = ngp / kSR;
-  // B operand columns start at bcol; TMA box starts must be 16-byte aligned, so the
-  // boxes start at the even column below it and the fragments skip boff columns
-  const int bcol = is_r ? Kp + b0 : b0;
-  const int bstart = bcol & ~1, boff = bcol - bstart;
-  const CUtensorMap* tm = &tmap;
+  const int nq = ntl * nch;                                // (tile, chunk) stream of this CTA
   const int ldp = U.ldp;
-  auto box_col = [&](int bx) { return bx < kSA / 8 ? a0 + 8 * bx : bstart + 8 * (bx - kSA / 8); };
-  int nbox = 0;
-  for (int bx = 0; bx < kSA / 8 + kSBX; ++bx) nbox += box_col(bx) < ldp;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    for (int i = 0; i < kSS; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < kSS; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 8);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  auto issue = [&](int c) {
-    const int slot = c % kSS;
-    double* st = sst + slot * kStageD;
-    // boxes that start past the panel row (ldp) are not issued (a box entirely outside
-    // the tensor faults); their columns are never stored
-    mbar_arrive_expect_tx(&s_full[slot], uint32_t(nbox * kSR * 8 * 8));
-#pragma unroll 1
-    for (int bx = 0; bx < kSA / 8 + kSBX; ++bx) {
-      const int col = box_col(bx);
-      if (col < ldp) tma_load_3d(st + bx * kSR * 8, tm, col, c * kSR, s, &s_full[slot]);
+  if (warp == 8) {
+    // ---- producer ----
+    for (int q = 0; q < nq; ++q) {
+      const int slot = q % kSS;
+      if (q >= kSS) mbar_wait(&s_empty[slot], uint32_t(((q / kSS) - 1) & 1));
+      int a0, b0;
+      bool is_r;
+      schur_tile(t0 + q / nch, k, nc, a0, b0, is_r);
+      const int c = q - (q / nch) * nch;
+      // B columns start at bcol; TMA box starts must be 16-byte aligned, so the boxes
+      // start at the even column below it (the consumers skip boff columns); boxes
+      // that start past the panel row are not issued (their columns are never stored)
+      const int bstart = (is_r ? Kp + b0 : b0) & ~1;
+      const int col = lane < kSA / 8 ? a0 + 8 * lane : bstart + 8 * (lane - kSA / 8);
+      const bool live = lane < kSA / 8 + kSBX && col < ldp;
+      const unsigned nbox = __popc(__ballot_sync(0xffffffffu, live));
+      if (lane == 0) mbar_arrive_expect_tx(&s_full[slot], uint32_t(nbox * kSR * 8 * 8));
+      __syncwarp();
+      if (live) tma_load_3d(sst + slot * kStageD + lane * kSR * 8, &tmap, col, c * kSR, s, &s_full[slot]);
     }
-  };
-#ifndef HDD_SL_NOTMA
-  if (tid == 0)
-    for (int c = 0; c < kSS && c < nch; ++c) issue(c);
-#endif
+    return;
+  }
+  // ---- consumers ----
   const int gq = lane & 3, gr = lane >> 2;
   const int wa = (warp >> 1) * 32, wb = (warp & 1) * 32;  // warp tile origin inside the CTA tile
+  double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
+  const int tk = tri(k);
   double acc[4][4][2];
+  for (int q = 0; q < nq; ++q) {
+    int a0, b0;
+    bool is_r;
+    schur_tile(t0 + q / nch, k, nc, a0, b0, is_r);
+    const int c = q - (q / nch) * nch;
+    const int boff = (is_r ? Kp + b0 : b0) & 1;
+    if (c == 0) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  for (int c = 0; c < nch; ++c) {
-    const int slot = c % kSS;
-#ifndef HDD_SL_NOTMA
-    mbar_wait(&s_full[slot], uint32_t((c / kSS) & 1));
-#endif
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+    const int slot = q % kSS;
+    mbar_wait(&s_full[slot], uint32_t((q / kSS) & 1));
     const double* st = sst + slot * kStageD;
     const double* As = st + (wa / 8) * kSR * 8;           // 4 A boxes of [kSR][8]
     const double* Bs = st + (kSA / 8) * kSR * 8;          // B boxes
@@ -2289,40 +2316,73 @@ __global__ void __launch_bounds__(256, 2) schur_l_kernel(DevPlan p, const DevUpp
         const int cb = wb + 8 * j + gr + boff;
         bv[j] = Bs[(cb >> 3) * kSR * 8 + (kk + gq) * 8 + (cb & 7)];
       }
-#ifndef HDD_SL_NOMMA
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma884(acc[i][j], av[i], bv[j]);
-#else
-      acc[0][0][0] += av[0] * bv[0];
-#endif
     }
-    __syncthreads();                                       // slot free for the next fill
-#ifndef HDD_SL_NOTMA
-    if (tid == 0 && c + kSS < nch) issue(c + kSS);
-#endif
-  }
-  // epilogue: gather A~ / R~ from the sons, subtract, store packed
-  const MergeCtx mc = merge_ctx(p, U, s);
-  double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
-  const int tk = tri(k);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_empty[slot]);           // this warp is done with the slot
+    if (c == nch - 1) {
+      // epilogue: out already holds A~ / R~ (assemble_l_kernel); out -= W^T [W | V],
+      // two rows of fragments at a time (loads first, then the stores)
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int a = a0 + wa + 8 * i + gr;
-    if (a >= k) continue;
+      for (int ih = 0; ih < 4; ih += 2) {
+        int idx[2][4][2];
+        double old[2][4][2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+        for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int b = b0 + wb + 8 * j + 2 * gq + e;
-        if (!is_r) {
-          if (b <= a) out[tri(a) + b] = gather_A(mc, a, b) - acc[i][j][e];
-        } else if (b < nc) {
-          out[tk + a * nc + b] = gather_R(mc, a, b) - acc[i][j][e];
-        }
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int a = a0 + wa + 8 * (ih + i) + gr, b = b0 + wb + 8 * j + 2 * gq + e;
+              int t = -1;
+              if (a < k) t = !is_r ? (b <= a ? tri(a) + b : -1) : (b < nc ? tk + a * nc + b : -1);
+              idx[i][j][e] = t;
+              old[i][j][e] = t >= 0 ? out[t] : 0.0;
+            }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (idx[i][j][e] >= 0) out[idx[i][j][e]] = old[i][j][e] - acc[ih + i][j][e];
       }
+    }
   }
+}
+
+// Tier-L assembly (split mode): the father's interface panel [A21 | A22 | R_gamma] into
+// the HBM workspace and the assembled A11 / R_B (lower packed) into the node output,
+// one warp per row, every (row, sample, node) in parallel — the son gathers of
+// assemble_father (hdd.py:216-238) as a memory-bound pass, off the elimination's and
+// the Schur update's critical paths.
+__global__ void __launch_bounds__(256) assemble_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
+                                                         double* __restrict__ ws, int64_t ws_stride) {
+  const DevUpper& U = nodes[blockIdx.z];
+  const int s = blockIdx.y;
+  const int k = U.k, ng = U.ng, nc = U.nc, ldp = U.ldp;
+  const int ngp = upper_ngp(U), Kp = k + ngp, W = Kp + nc;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= ngp + k) return;
+  const MergeCtx mc = merge_ctx(p, U, s);
+  if (row < ngp) {
+    double* P = ws + int64_t(blockIdx.z) * ws_stride * p.bcap + int64_t(s) * ws_stride;
+    gather_panel_row<8>(mc, k, ng, Kp, W, row, P + int64_t(row) * ldp, lane, 32);
+    return;
+  }
+  const int a = row - ngp;
+  double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
+  for (int b = lane; b <= a; b += 32) out[tri(a) + b] = gather_A(mc, a, b);
+  for (int c = lane; c < nc; c += 32) out[tri(k) + a * nc + c] = gather_R(mc, a, c);
+}
+
+cudaError_t launch_assemble_l(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
+                              int64_t ws_stride, int max_rows, cudaStream_t s) {
+  assemble_l_kernel<<<dim3((max_rows + 7) / 8, B, n_nodes), 256, 0, s>>>(p, nodes_dev, ws, ws_stride);
+  return cudaGetLastError();
 }
 
 // one launch per node: the node's tensor map travels as a __grid_constant__ parameter
@@ -2333,7 +2393,7 @@ cudaError_t launch_schur_l(const DevPlan& p, const DevUpper* nodes_dev, const CU
   if (e != cudaSuccess) return e;
   for (int n = 0; n < n_nodes; ++n) {
     if (tiles[n] == 0) continue;                          // k = 0 (root): nothing to update
-    schur_l_kernel<<<dim3(tiles[n], B, 1), 256, smem, s>>>(p, nodes_dev, tmaps[n], n);
+    schur_l_kernel<<<dim3((tiles[n] + kSTPC - 1) / kSTPC, B, 1), 288, smem, s>>>(p, nodes_dev, tmaps[n], n);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

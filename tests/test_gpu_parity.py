@@ -451,13 +451,15 @@ def test_solve_requires_primal_plan(torch_cuda):
 
 
 def test_tier_l_split_schur_kernel_matches(torch_cuda, golden, monkeypatch):
-    """The opt-in TMA-fed tier-L Schur-update kernel (HDD_SCHUR_L_SPLIT=1, schur_l_kernel)
-    gives the fused epilogue's numbers on C4 / C5 (every tier-L depth) and on C2 with
-    every depth forced onto tier L."""
+    """The split tier L (assemble_l_kernel, merge_l elimination, TMA-fed schur_l_kernel;
+    default for interfaces >= 255 nodes) forced onto every tier-L depth gives the fused
+    kernel's numbers on C4 / C5 and on C2 with every depth forced onto tier L."""
     g4, g5, g2 = golden("cfg_C4"), golden("cfg_C5"), golden("cfg_C2")
+    monkeypatch.setenv("HDD_SCHUR_L_SPLIT", "0")
     ref4 = hb.forward_functionals_batch(configs.make_problem("C4"), g4["Z"])
     ref5 = hb.forward_functionals_batch(configs.make_problem("C5"), g5["Z"])
     monkeypatch.setenv("HDD_SCHUR_L_SPLIT", "1")
+    monkeypatch.setenv("HDD_SCHUR_L_MIN_NG", "1")          # every tier-L depth split
     s4 = hb.forward_functionals_batch(configs.make_problem("C4"), g4["Z"])
     s5 = hb.forward_functionals_batch(configs.make_problem("C5"), g5["Z"])
     assert rel(s4, ref4) <= 1e-13 and rel(s5, ref5) <= 1e-13
