@@ -96,6 +96,11 @@ typedef struct {
    * hdd.py:120-138); 0 = likelihood plans keep them only on the
    * root-to-observation paths the top-down sweep visits.                      */
   int32_t full_solve;
+  /* >= 0: reference node id of a solve_subdomain target (hdd.py:435-490): the plan
+   * keeps factors only on the root-to-target path and the target's subtree (the
+   * reference's SolveMode.keep_path, hdd.py:186-203) for hdd_solve_subdomain_batch;
+   * -1 = none.                                                                 */
+  int64_t solve_target;
 } HddPlanDesc;
 
 typedef struct {
@@ -115,6 +120,8 @@ typedef struct {
   int32_t tiny;            /* 1: level <= 3, one warp per sample (no tree)    */
   int32_t separable;       /* 1: Z entry points (K1); 0: kappa entry points   */
   int32_t full_solve;      /* 1: factors of every node kept (hdd_solve_batch) */
+  int32_t n_omega;         /* solve_subdomain plans: |idx_omega| of the target */
+  int64_t factor_doubles;  /* primal factor storage per sample (doubles)      */
 } HddPlanInfo;
 
 typedef struct {
@@ -248,6 +255,17 @@ int hdd_solve_batch_ex(HddPlan* plan, const double* Z_dev, const double* K_dev, 
                        double* U_dev, void* stream);
 int hdd_solve_batch_ex_host(HddPlan* plan, const double* Z_host, const double* K_host, int64_t B,
                             const HddRhs* rhs_host, double* U_host);
+
+/* solve_subdomain (hdd.py:435-490) as a partial inverse: the solution on the plan's
+ * target node only, Usub [B][n_omega] aligned with the target's idx_omega (sorted
+ * global ids of the closed subdomain).  Only the root-to-target path and the target's
+ * subtree are factored, swept top-down and solved in-leaf.  Exactly one of Z / K;
+ * rhs optional (as in hdd_forward_batch_ex).  HDD_ERR_USAGE unless the plan was
+ * created with solve_target >= 0. */
+int hdd_solve_subdomain_batch(HddPlan* plan, const double* Z_dev, const double* K_dev, int64_t B,
+                              const HddRhs* rhs, double* Usub_dev, void* stream);
+int hdd_solve_subdomain_batch_host(HddPlan* plan, const double* Z_host, const double* K_host, int64_t B,
+                                   const HddRhs* rhs_host, double* Usub_host);
 
 int hdd_last_error(const HddPlan* plan, HddError* out);
 /* Error of the last failed hdd_plan_create (no plan exists then). */

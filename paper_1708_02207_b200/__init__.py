@@ -28,6 +28,7 @@ from .bayes import (  # noqa: F401
     prolong_rhs,
     solve_batch,
     solve_subdomain,
+    solve_subdomain_batch,
 )
 from .errors import ConfigError, GeometryError, NumericalError, UsageError  # noqa: F401
 from .geometry import (  # noqa: F401

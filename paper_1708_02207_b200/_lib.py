@@ -38,7 +38,7 @@ class HddPlanDesc(C.Structure):
         ("sigma", _f64p), ("y", _f64p),
         ("max_batch", C.c_int32), ("device", C.c_int32), ("keep_nodes", C.c_int32),
         ("mode", C.c_int32), ("lr_eps", C.c_double), ("lr_kmax", C.c_int32), ("lr_nmin", C.c_int32),
-        ("g", _f64p), ("full_solve", C.c_int32),
+        ("g", _f64p), ("full_solve", C.c_int32), ("solve_target", C.c_int64),
     ]
 
 
@@ -56,7 +56,8 @@ class HddPlanInfo(C.Structure):
                 ("leaf_depth", C.c_int32), ("n_upper", C.c_int32), ("n_leaves", C.c_int32),
                 ("n_obs", C.c_int32), ("leaf_cols", C.c_int32), ("max_batch", C.c_int32),
                 ("n_kernels_per_batch", C.c_int32), ("workspace_bytes", C.c_int64), ("mode", C.c_int32),
-                ("n_topdown", C.c_int32), ("tiny", C.c_int32), ("separable", C.c_int32), ("full_solve", C.c_int32)]
+                ("n_topdown", C.c_int32), ("tiny", C.c_int32), ("separable", C.c_int32), ("full_solve", C.c_int32),
+                ("n_omega", C.c_int32), ("factor_doubles", C.c_int64)]
 
 
 class HddNodeInfo(C.Structure):
@@ -114,6 +115,10 @@ EXPORTS = {
     "hdd_debug_leaf_clocks": (C.c_int, [C.POINTER(C.c_longlong)]),
     "hdd_debug_merge_clocks": (C.c_int, [C.POINTER(C.c_longlong)]),
     "hdd_debug_lowrank_wide": (C.c_int, [C.c_void_p, _i64p]),
+    "hdd_solve_subdomain_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(HddRhs),
+                                            C.c_void_p, C.c_void_p]),
+    "hdd_solve_subdomain_batch_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(HddRhs),
+                                                 C.c_void_p]),
     "hdd_version": (C.c_char_p, []),
 }
 

@@ -36,7 +36,7 @@ from .geometry import DDTree, Mesh, Rect, cell_centroid_tables
 __all__ = [
     "ParamField", "SineKLField", "Prior", "ToleranceSpec", "MeasurementModel", "BayesProblem", "mean_observations",
     "aligned_partition", "kl_pairs", "forward_functionals", "forward_functionals_batch", "log_likelihood",
-    "log_likelihood_batch", "gaussian_log_likelihood", "posterior_weights", "synchronize", "prolong_rhs",
+    "log_likelihood_batch", "gaussian_log_likelihood", "posterior_weights", "synchronize", "prolong_rhs", "solve_subdomain_batch",
 ]
 
 
@@ -236,7 +236,7 @@ class _Plan:
     """Owns one HddPlan* (device tables + workspace)."""
 
     def __init__(self, problem: "BayesProblem", device: int, max_batch: int, keep_nodes: bool = False,
-                 mode: int = -1, full_solve: bool = False):
+                 mode: int = -1, full_solve: bool = False, solve_target: int = -1):
         L = _lib.lib()
         mesh = problem.tree.mesh
         param = problem.param
@@ -271,7 +271,7 @@ class _Plan:
             lr_eps=float(getattr(problem.compression, "eps", 0.0) or 0.0) if problem.compression is not None else 0.0,
             lr_kmax=int(getattr(problem.compression, "k_max", 64)) if problem.compression is not None else 0,
             lr_nmin=int(getattr(problem.compression, "n_min", 32)) if problem.compression is not None else 0,
-            g=ptr(k["g"], _lib._f64p), full_solve=int(full_solve))
+            g=ptr(k["g"], _lib._f64p), full_solve=int(full_solve), solve_target=int(solve_target))
         h = C.c_void_p()
         rc = L.hdd_plan_create(C.byref(desc), C.byref(h))
         if rc != _lib.HDD_OK:
@@ -331,6 +331,7 @@ class BayesProblem:
     mode: int = -1          # -1 auto, 0 adjoint functionals, 1 primal top-down for points
     _plan: object = field(default=None, repr=False)
     _solve_plan: object = field(default=None, repr=False)
+    _sub_plans: dict = field(default_factory=dict, repr=False)
 
     def __post_init__(self):
         mesh = self.tree.mesh
@@ -631,17 +632,41 @@ def forward_full_solve(problem: BayesProblem, z) -> np.ndarray:
     return observe_solution(problem.tree, u, problem.model)
 
 
+def solve_subdomain_batch(problem: BayesProblem, Z, target_id: int, f=None, g=None) -> np.ndarray:
+    """Solution restricted to one tree node for every row of Z: [B, |idx_omega|], aligned
+    with the node's idx_omega (sorted global ids of the closed subdomain).  A partial
+    inverse like the reference's solve_subdomain with SolveMode.keep_path(target)
+    (hdd.py:435-490, :186-203): the device plan factors, sweeps top-down and solves
+    in-leaf only on the root-to-target path and the target's subtree
+    (hdd_solve_subdomain_batch).  `f` / `g` as in forward_functionals_batch."""
+    tid = int(target_id)
+    problem.tree.node(tid)                                   # UsageError for an unknown id
+    plan = problem._sub_plans.get(tid)
+    if plan is None:
+        plan = _Plan(problem, problem.device, problem.max_batch, mode=1, solve_target=tid)
+        problem._sub_plans[tid] = plan
+    n_z = plan.n_z if plan.separable else int(getattr(problem.param, "n_z", np.asarray(Z).shape[-1]))
+    Zb = _as_batch(Z, n_z)
+    if not isinstance(Zb, np.ndarray):
+        Zb = Zb.detach().cpu().numpy()
+    B = Zb.shape[0]
+    K = None if plan.separable else _kappa_rows(problem, Zb)
+    rows = _Rows(problem, B, f, g) if (f is not None or g is not None) else None
+    Us = np.empty((B, plan.info().n_omega))
+    plan.check(plan.lib.hdd_solve_subdomain_batch_host(
+        plan.handle, None if K is not None else Zb.ctypes.data, None if K is None else K.ctypes.data, B,
+        None if rows is None else C.byref(rows.rhs), Us.ctypes.data))
+    return Us
+
+
 def solve_subdomain(problem: BayesProblem, z, target_id: int) -> np.ndarray:
     """Solution restricted to one tree node, aligned with its idx_omega (sorted
-    global node ids of the closed subdomain) — solve_subdomain, hdd.py:435-490.
-    The device sweep computes every interface anyway; the restriction is a gather."""
-    from .geometry import omega_nodes
-    target = problem.tree.node(int(target_id))
+    global node ids of the closed subdomain) — solve_subdomain, hdd.py:435-490, as a
+    partial inverse (solve_subdomain_batch)."""
     z = np.asarray(z, dtype=float)
     if z.ndim != 1:
         raise ConfigError("parameter vector must be one-dimensional")
-    u = solve_batch(problem, z[None])[0]
-    return u[omega_nodes(problem.tree.mesh, target.cells)]
+    return solve_subdomain_batch(problem, z[None], target_id)[0]
 
 
 def gaussian_log_likelihood(y, s, sigma) -> float:

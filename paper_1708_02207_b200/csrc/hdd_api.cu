@@ -71,6 +71,9 @@ struct HddPlan {
   std::vector<int> tm_ntiles;           // tile count per map
   std::vector<int> tm_first, tm_tiles;
   std::vector<int> depth_split;         // tier-L depths run split (assemble / eliminate / schur_l)
+  // solve_subdomain plans: the target's kernel leaves and the idx_omega position map
+  const int32_t* d_solve_leaves = nullptr;
+  const int32_t* d_omega_pos = nullptr;
   bool schur_split = false;
 };
 
@@ -426,6 +429,10 @@ static int setup_device(HddPlan* pl, int max_batch) {
     if ((rc = upload(pl, td, &dt))) return rc;
     pl->d_td = const_cast<DevUpper*>(dt);
   }
+  if (P.solve_target >= 0) {
+    if ((rc = upload(pl, P.solve_leaves, &pl->d_solve_leaves))) return rc;
+    if ((rc = upload(pl, P.omega_pos, &pl->d_omega_pos))) return rc;
+  }
   D.tiny = P.tiny ? 1 : 0;
   D.root_ref = P.root_ref;
   D.gfull = nullptr;
@@ -701,7 +708,8 @@ int hdd_plan_destroy(HddPlan* pl) {
 // kernel); U non-NULL: the full-solution path (primal sweep + in-leaf solves).
 // sample0 = global index of the sub-batch's first row (failure records).
 static int run_sub_batch(HddPlan* pl, const double* Z, const double* Kin, int B, double* S, double* ll, double* U,
-                         cudaStream_t st, int64_t sample0, cudaEvent_t* ev = nullptr, const HddRhs* rhs = nullptr) {
+                         cudaStream_t st, int64_t sample0, cudaEvent_t* ev = nullptr, const HddRhs* rhs = nullptr,
+                         bool sub = false) {
   Plan& P = pl->plan;
   DevPlan D = pl->dev;                 // by-value copy: per-sub-batch fields
   D.sample0 = sample0;
@@ -765,8 +773,12 @@ static int run_sub_batch(HddPlan* pl, const double* Z, const double* Kin, int B,
       if (pl->td_count[dep] > 0)
         CU(launch_topdown(D, pl->d_td + pl->td_first[dep], pl->td_count[dep], B, pl->depth_kng[dep], st));
   }
-  if (U) CU(launch_leaf_solve(D, B, U, nn, st));
-  else CU(launch_finalize(D, B, S, ll, st));
+  if (U && sub)   // the target's leaves, written in idx_omega order
+    CU(launch_leaf_solve(D, B, U, P.n_omega, st, pl->d_solve_leaves, int(P.solve_leaves.size()), pl->d_omega_pos));
+  else if (U)
+    CU(launch_leaf_solve(D, B, U, nn, st));
+  else
+    CU(launch_finalize(D, B, S, ll, st));
   return mark();
 }
 
@@ -817,14 +829,15 @@ static int check_call(HddPlan* pl, int64_t B, const void* in, bool want_separabl
 
 // Sub-batched launch of a whole batch on `st` (asynchronous).
 static int run_batch(HddPlan* pl, const double* Z, const double* Kin, int64_t B, double* S, double* ll, double* U,
-                     cudaStream_t st, const HddRhs* rhs = nullptr) {
+                     cudaStream_t st, const HddRhs* rhs = nullptr, bool sub = false) {
   const int nz = pl->plan.n_z, no = int(pl->plan.obs_kind.size());
-  const int64_t nt = int64_t(2) * pl->plan.N * pl->plan.N, nn = int64_t(pl->plan.m) * pl->plan.m;
+  const int64_t nt = int64_t(2) * pl->plan.N * pl->plan.N;
+  const int64_t nn = sub ? int64_t(pl->plan.n_omega) : int64_t(pl->plan.m) * pl->plan.m;
   for (int64_t done = 0; done < B;) {
     const int b = int(std::min<int64_t>(pl->bcap, B - done));
     const int rc = run_sub_batch(pl, Z ? Z + done * nz : nullptr, Kin ? Kin + done * nt : nullptr, b,
                                  S ? S + done * no : nullptr, ll ? ll + done : nullptr, U ? U + done * nn : nullptr, st,
-                                 done, nullptr, rhs);
+                                 done, nullptr, rhs, sub);
     if (rc != HDD_OK) return rc;
     done += b;
   }
@@ -1185,6 +1198,81 @@ int hdd_solve_batch_ex_host(HddPlan* pl, const double* Zh, const double* Kh, int
   return rc;
 }
 
+// ---- solve_subdomain as a partial inverse ----
+__global__ void gather_omega_kernel(const double* __restrict__ U, int64_t nn, const int32_t* __restrict__ pos,
+                                    double* __restrict__ Us, int n_omega, int B) {
+  const int s = blockIdx.y;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < nn; t += int64_t(gridDim.x) * blockDim.x)
+    if (pos[t] >= 0) Us[int64_t(s) * n_omega + pos[t]] = U[int64_t(s) * nn + t];
+}
+
+int hdd_solve_subdomain_batch(HddPlan* pl, const double* Z, const double* K, int64_t B, const HddRhs* rhs,
+                              double* Us, void* stream) {
+  if (!pl) return HDD_ERR_USAGE;
+  if ((Z != nullptr) == (K != nullptr) && B > 0) return set_err(&pl->err, HDD_ERR_USAGE, "pass exactly one of Z and K");
+  int rc = check_call(pl, B, Z ? Z : K, Z != nullptr);
+  if (rc != HDD_OK) return rc;
+  if ((rc = check_rhs(pl, rhs, false)) != HDD_OK) return rc;
+  if (pl->plan.solve_target < 0)
+    return set_err(&pl->err, HDD_ERR_USAGE,
+                   "plan has no subdomain target: create it with solve_target (the SolveMode.keep_path analogue)");
+  if (B > 0 && !Us) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  if ((rc = take_error(pl)) != HDD_OK) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (pl->plan.leaf_depth > 0) return run_batch(pl, Z, K, B, nullptr, nullptr, Us, st, rhs, true);
+  // a single-leaf or sub-leaf mesh: the whole solution, then the target's nodes
+  const int64_t nn = int64_t(pl->plan.m) * pl->plan.m;
+  double* U = nullptr;
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&U), size_t(B) * nn * 8, st));
+  rc = run_batch(pl, Z, K, B, nullptr, nullptr, U, st, rhs);
+  if (rc == HDD_OK) {
+    gather_omega_kernel<<<dim3(unsigned((nn + 255) / 256), unsigned(B)), 256, 0, st>>>(U, nn, pl->d_omega_pos, Us,
+                                                                                       pl->plan.n_omega, int(B));
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = set_err(&pl->err, HDD_ERR_CUDA, cudaGetErrorString(e));
+  }
+  cudaFreeAsync(U, st);
+  return rc;
+}
+
+int hdd_solve_subdomain_batch_host(HddPlan* pl, const double* Zh, const double* Kh, int64_t B, const HddRhs* rhs,
+                                   double* Ush) {
+  if (!pl) return HDD_ERR_USAGE;
+  if ((Zh != nullptr) == (Kh != nullptr) && B > 0) return set_err(&pl->err, HDD_ERR_USAGE, "pass exactly one of Z and K");
+  int rc = check_call(pl, B, Zh ? Zh : Kh, Zh != nullptr);
+  if (rc != HDD_OK) return rc;
+  if ((rc = check_rhs(pl, rhs, true)) != HDD_OK) return rc;
+  if (B > 0 && !Ush) return set_err(&pl->err, HDD_ERR_USAGE, "invalid batch");
+  if (B == 0) return HDD_OK;
+  CU(cudaSetDevice(pl->device));
+  DevRhs d;
+  if ((rc = upload_rhs(pl, rhs, B, d)) != HDD_OK) return rc;
+  const bool is_kappa = Kh != nullptr;
+  const int64_t in_w = is_kappa ? int64_t(2) * pl->plan.N * pl->plan.N : pl->plan.n_z;
+  const int64_t no = pl->plan.n_omega;
+  double* dX = nullptr;
+  double* dU = nullptr;
+  CU(cudaMalloc(&dX, size_t(B) * std::max<int64_t>(in_w, 1) * 8));
+  if (cudaMalloc(&dU, size_t(B) * std::max<int64_t>(no, 1) * 8) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(dX);
+    return set_err(&pl->err, HDD_ERR_NOMEM, "device allocation of the subdomain buffer failed");
+  }
+  cudaStream_t st = pl->stream;
+  if (cudaMemcpyAsync(dX, is_kappa ? Kh : Zh, size_t(B) * in_w * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    rc = HDD_ERR_CUDA;
+  if (rc == HDD_OK)
+    rc = hdd_solve_subdomain_batch(pl, is_kappa ? nullptr : dX, is_kappa ? dX : nullptr, B, rhs ? &d.r : nullptr, dU, st);
+  if (rc == HDD_OK && cudaMemcpyAsync(Ush, dU, size_t(B) * no * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    rc = HDD_ERR_CUDA;
+  if (rc == HDD_OK) rc = sync_and_check(pl, st);
+  cudaFree(dX);
+  cudaFree(dU);
+  return rc;
+}
+
 int hdd_posterior_weights(const double* ll, const double* lp, int64_t n, double* w, int64_t* idx, double* lse,
                           void* stream) {
   if (n <= 0 || !ll || !w || !idx || !lse) return HDD_ERR_USAGE;
@@ -1253,6 +1341,8 @@ int hdd_plan_info(const HddPlan* pl, HddPlanInfo* out) {
   out->tiny = P.tiny ? 1 : 0;
   out->separable = P.separable ? 1 : 0;
   out->full_solve = P.full_solve ? 1 : 0;
+  out->n_omega = P.n_omega;
+  out->factor_doubles = P.fac_elems;
   return HDD_OK;
 }
 

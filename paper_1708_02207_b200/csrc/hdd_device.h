@@ -160,7 +160,8 @@ cudaError_t launch_topdown(const DevPlan& p, const DevUpper* nodes_dev, int n_no
 cudaError_t launch_finalize(const DevPlan& p, int B, double* S, double* ll, cudaStream_t s);
 cudaError_t launch_posterior(const double* ll, const double* lp, int64_t n, double* w, int64_t* idx, double* lse,
                              cudaStream_t s);
-cudaError_t launch_leaf_solve(const DevPlan& p, int B, double* U, int64_t n_nodes, cudaStream_t s);
+cudaError_t launch_leaf_solve(const DevPlan& p, int B, double* U, int64_t n_nodes, cudaStream_t s,
+                              const int32_t* leaf_list = nullptr, int n_list = 0, const int32_t* omega_pos = nullptr);
 cudaError_t launch_kappa_check(const DevPlan& p, const double* kappa, int B, cudaStream_t s);
 cudaError_t launch_tiny(const DevPlan& p, int B, double* S, double* ll, double* U, int64_t n_nodes, cudaStream_t s);
 size_t leaf_smem_bytes(int leaf_cols);

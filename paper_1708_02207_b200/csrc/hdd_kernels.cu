@@ -3560,12 +3560,17 @@ __device__ __forceinline__ int perim_index(int x, int y) {
   return y == 0 ? x : (y == kLeafCells ? 3 * kLeafCells - 1 + x : kLeafCells + 1 + 2 * (y - 1) + (x == kLeafCells));
 }
 
-__global__ void __launch_bounds__(32) leaf_solve_kernel(DevPlan p, double* __restrict__ U, int64_t n_nodes) {
+// leaf_list: the kernel leaves to solve (NULL = all); omega_pos: global node id -> output
+// column (solve_subdomain: the target's idx_omega order, -1 = not in the target), NULL =
+// full U rows of n_nodes
+__global__ void __launch_bounds__(32) leaf_solve_kernel(DevPlan p, double* __restrict__ U, int64_t n_nodes,
+                                                        const int32_t* __restrict__ leaf_list,
+                                                        const int32_t* __restrict__ omega_pos) {
   __shared__ double band[kNI * kBW];       // column j: rows j .. j+15 of L
   __shared__ double rhs[kNI], invd[kNI];
   __shared__ double kap[512];
   __shared__ double ub[kLeafPerim];
-  const int leaf = blockIdx.x, s = blockIdx.y, lane = threadIdx.x;
+  const int leaf = leaf_list ? leaf_list[blockIdx.x] : int(blockIdx.x), s = blockIdx.y, lane = threadIdx.x;
   const DevLeaf& L = p.leaves[leaf];
   const int N = p.N, m = p.m;
   const double* kb = p.kappa + int64_t(s) * 2 * N * N;
@@ -3650,20 +3655,25 @@ __global__ void __launch_bounds__(32) leaf_solve_kernel(DevPlan p, double* __res
   double* Us = U + int64_t(s) * n_nodes;
   for (int j = lane; j < kNI; j += 32) {
     const int x = j % kIn + 1, y = j / kIn + 1;
-    Us[int64_t(L.j0 + y) * m + L.i0 + x] = rhs[j];
+    const int64_t id = int64_t(L.j0 + y) * m + L.i0 + x;
+    if (!omega_pos) Us[id] = rhs[j];
+    else if (omega_pos[id] >= 0) Us[omega_pos[id]] = rhs[j];
   }
   for (int t = lane; t < kLeafPerim; t += 32) {
     int x, y;
     if (t <= kLeafCells) { x = t; y = 0; }
     else if (t >= 3 * kLeafCells - 1) { x = t - (3 * kLeafCells - 1); y = kLeafCells; }
     else { y = (t - kLeafCells - 1) / 2 + 1; x = ((t - kLeafCells - 1) & 1) ? kLeafCells : 0; }
-    Us[int64_t(L.j0 + y) * m + L.i0 + x] = ub[t];
+    const int64_t id = int64_t(L.j0 + y) * m + L.i0 + x;
+    if (!omega_pos) Us[id] = ub[t];
+    else if (omega_pos[id] >= 0) Us[omega_pos[id]] = ub[t];
   }
 }
 
-cudaError_t launch_leaf_solve(const DevPlan& p, int B, double* U, int64_t n_nodes, cudaStream_t s) {
-  dim3 grid(p.n_leaves, B);
-  leaf_solve_kernel<<<grid, 32, 0, s>>>(p, U, n_nodes);
+cudaError_t launch_leaf_solve(const DevPlan& p, int B, double* U, int64_t n_nodes, cudaStream_t s,
+                              const int32_t* leaf_list, int n_list, const int32_t* omega_pos) {
+  dim3 grid(leaf_list ? n_list : p.n_leaves, B);
+  leaf_solve_kernel<<<grid, 32, 0, s>>>(p, U, n_nodes, leaf_list, omega_pos);
   return cudaGetLastError();
 }
 

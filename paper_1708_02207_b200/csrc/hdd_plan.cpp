@@ -308,6 +308,18 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     for (double v : P.y) if (!std::isfinite(v)) return "data vector y is not finite";
   }
   P.root_ref = subtree_size(P.level, 0) - 1;
+  P.solve_target = d->solve_target;
+  if (d->solve_target >= 0) {
+    Rect r;
+    if (!rect_of_id(P.level, d->solve_target, &r)) {
+      *code = HDD_ERR_USAGE;
+      return "no tree node with id " + std::to_string(d->solve_target);
+    }
+    P.solve_rect = {r.i0, r.i1, r.j0, r.j1};
+    P.omega_pos.assign(size_t(m) * m, -1);
+    for (int j = r.j0; j <= r.j1; ++j)          // idx_omega: sorted global ids (ddtree.py:40-57)
+      for (int i = r.i0; i <= r.i1; ++i) P.omega_pos[size_t(j) * m + i] = P.n_omega++;
+  }
   if (P.level < 4) return build_tiny_plan(d, P, code);
   const int dl = 2 * (P.level - 4);   // depth of the 16x16-cell kernel leaves
   P.leaf_depth = dl;
@@ -484,6 +496,7 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     int n_points = 0;
     for (int o = 0; o < n_obs; ++o) n_points += births[o].where >= 0;
     P.mode = d->mode >= 0 ? d->mode : (n_points > 384 ? 1 : 0);   // measured crossover
+    if (d->solve_target >= 0) P.mode = 1;   // the subdomain sweep is a primal top-down
     if (dl == 0) P.mode = 0;     // the root is a kernel leaf: nothing to solve top-down
   }
   const bool primal = P.mode == 1;
@@ -678,6 +691,32 @@ std::string build_plan(const HddPlanDesc* d, Plan& P, int* code) {
     for (const ObsRoute& r : P.route) {
       if (r.kind == 2) mark_up(P.leaves[r.node].parent);
       else if (r.kind == 3) mark_up(r.node);
+    }
+    if (d->solve_target >= 0) {
+      // solve_subdomain (hdd.py:435-490, SolveMode.keep_path, hdd.py:186-203): the
+      // root-to-target path and the target's subtree only — the partial inverse
+      int t = 0;
+      const Rect tr{P.solve_rect.i0, P.solve_rect.i1, P.solve_rect.j0, P.solve_rect.j1};
+      while (all[t].depth < dl && !(all[t].r.i0 == tr.i0 && all[t].r.i1 == tr.i1 && all[t].r.j0 == tr.j0 &&
+                                    all[t].r.j1 == tr.j1)) {
+        const Rect& s0 = all[all[t].son[0]].r;
+        t = (tr.i0 >= s0.i0 && tr.i1 <= s0.i1 && tr.j0 >= s0.j0 && tr.j1 <= s0.j1) ? all[t].son[0] : all[t].son[1];
+      }
+      std::vector<int> st{t};
+      while (!st.empty()) {
+        const int q = st.back();
+        st.pop_back();
+        if (all[q].depth == dl) {
+          const int li = -1 - to_plan[q];
+          P.solve_leaves.push_back(li);
+          mark_up(P.leaves[li].parent);
+        } else {
+          mark_up(to_plan[q]);
+          st.push_back(all[q].son[0]);
+          st.push_back(all[q].son[1]);
+        }
+      }
+      std::sort(P.solve_leaves.begin(), P.solve_leaves.end());
     }
     int64_t fo = 0, uo = 0;
     P.td_by_depth.assign(P.upper_by_depth.size(), {});

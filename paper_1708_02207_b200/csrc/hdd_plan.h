@@ -119,6 +119,11 @@ struct Plan {
   int64_t fac_elems = 0, u_elems = 0;         // per-sample sizes of the primal buffers
   std::vector<int64_t> buf_elems_per_sample;  // per buffer
   bool full_solve = false;                    // primal factors kept for every node
+  int64_t solve_target = -1;                  // solve_subdomain plan: reference node id, -1 none
+  struct { int i0, i1, j0, j1; } solve_rect{0, 0, 0, 0};
+  std::vector<int32_t> solve_leaves;          // kernel leaves of the target's subtree (or its container)
+  std::vector<int32_t> omega_pos;             // [m*m] position in the target's idx_omega, -1 outside
+  int n_omega = 0;
   std::vector<std::vector<int>> td_by_depth;  // primal: upper nodes the top-down sweep visits
   bool separable = true;                      // sx/sy/coef given (else kappa per call)
   bool tiny = false;                          // level <= 3: tiny_kernel, no tree sweep

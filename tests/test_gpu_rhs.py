@@ -122,3 +122,34 @@ def test_bad_rows_are_usage_errors(cuda):
         hb.forward_functionals_batch(prob, np.zeros((3, 2)), f=np.ones(7))
     with pytest.raises(hb.UsageError):
         hb.forward_functionals_batch(prob, np.zeros((3, 2)), g=np.ones((2, 4 * mesh.n_cells)))
+
+
+@pytest.mark.parametrize("level, depth", [(2, 2), (4, 5), (6, 0), (6, 3), (7, 6), (7, 9), (7, 13)])
+def test_solve_subdomain_partial_inverse(cuda, level, depth):
+    """solve_subdomain as a partial inverse (hdd.py:435-490 with keep_path): only the
+    path and the target's subtree are factored and swept; the values equal the
+    full-solution sweep bitwise (same arithmetic on the visited nodes) and the direct
+    solve at 1e-10, also with per-call f and g."""
+    rng, mesh, prob, obs = setup(level, 3, 40 + level + depth)
+    tree = prob.tree
+    nodes = tree.nodes_at_depth(depth)
+    target = nodes[int(rng.integers(len(nodes)))]
+    Z = rng.standard_normal((3, 3))
+    Us = hb.solve_subdomain_batch(prob, Z, target.id)
+    U = hb.solve_batch(prob, Z)
+    idx = hb.omega_nodes(mesh, target.cells)
+    assert Us.shape == (3, idx.size)
+    assert np.array_equal(Us, U[:, idx])
+    F = rng.standard_normal((3, mesh.n_nodes))
+    G = rng.standard_normal((3, 4 * mesh.n_cells))
+    Us2 = hb.solve_subdomain_batch(prob, Z, target.id, f=F, g=G)
+    grid = geometry.Grid(level)
+    fo = fields.SineKLField(grid, 3)
+    for b in range(3):
+        u = direct.solve(grid, fo.kappa_values(Z[b]), f=F[b], g=G[b])
+        assert rel(Us2[b], u[idx]) <= TOL
+    assert np.array_equal(hb.solve_subdomain(prob, Z[1], target.id), Us[1])
+    sub = prob._sub_plans[target.id].info()
+    full = prob.solve_plan().info()
+    if full.leaf_depth > 0 and depth > 0:
+        assert sub.factor_doubles < full.factor_doubles and sub.n_topdown < full.n_topdown

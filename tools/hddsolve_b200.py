@@ -36,7 +36,7 @@ class _Desc(C.Structure):            # HddPlanDesc, include/hdd.h (field order m
                 ("sigma", _f64), ("y", _f64), ("max_batch", C.c_int32),
                 ("device", C.c_int32), ("keep_nodes", C.c_int32), ("mode", C.c_int32),
                 ("lr_eps", C.c_double), ("lr_kmax", C.c_int32), ("lr_nmin", C.c_int32),
-                ("g", _f64), ("full_solve", C.c_int32)]
+                ("g", _f64), ("full_solve", C.c_int32), ("solve_target", C.c_int64)]
 
 
 class _Err(C.Structure):             # HddError
@@ -86,7 +86,8 @@ class DeviceForward:
                   sigma=sig.ctypes.data_as(_f64), y=None if y is None else y.ctypes.data_as(_f64),
                   max_batch=0, device=device, keep_nodes=0, mode=-1,
                   lr_eps=float(tol.eps) if tol else 0.0, lr_kmax=int(tol.k_max) if tol else 0,
-                  lr_nmin=int(tol.n_min) if tol else 0, g=g.ctypes.data_as(_f64), full_solve=0)
+                  lr_nmin=int(tol.n_min) if tol else 0, g=g.ctypes.data_as(_f64), full_solve=0,
+                  solve_target=-1)
         h = C.c_void_p()
         rc = L.hdd_plan_create(C.byref(d), C.byref(h))
         if rc != 0:
