@@ -1700,102 +1700,150 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
 
 
 constexpr int kEC = 16;     // tier-L epilogue: interface rows per staged chunk
-// Tier-L Schur update: 64 x 64 output tiles, X chunks of kEC interface rows
-// double-buffered HBM -> smem with cp.async, 8 warps as 2 x 4 of 32 x 16 DMMA tiles.
-// E: [2][2][32][kLds] smem (A chunk, B chunk) x double buffer.
+// Tier-L Schur update on 64 x 64 output tiles: the lower Psi tiles (b0 <= a0, columns
+// < k) and, when nc > 8, 64-column R tiles.  With nc <= 8 (most depths: the load column
+// and a few functionals) the R block rides on the diagonal tiles: their two strictly
+// upper 32 x 16 warp tiles compute rows a0..a0+63 x the R columns instead (B chunk
+// columns 64..71), so no tile pass stages A for a mostly empty R tile and no DMMA runs
+// on padding columns.  X chunks of kEC interface rows are double-buffered HBM -> smem
+// with cp.async; 8 warps as 2 x 4 of 32 x 16 DMMA tiles.
+// E: [2][2][kEC][kLds] smem (A chunk, B chunk) x double buffer.
 __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const double* __restrict__ P, int ldp, int k,
                                                  int ngp, int Kp, int nc, double* __restrict__ out, double* E) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane & 3, gr = lane >> 2;
-  const int ow = k + nc;
   const int m0 = (warp >> 2) * 32, n0 = (warp & 3) * 16;
-  const int na = (k + 63) / 64, nbt = (ow + 63) / 64;
+  const int na = (k + 63) / 64;
+  const bool fold = nc <= 8;
+  const int nbr = fold ? 0 : (nc + 63) / 64;
   const int nch = ngp / kEC;
-  for (int t = 0; t < na * nbt; ++t) {
-    const int a0 = (t / nbt) * 64, b0 = (t % nbt) * 64;
-    if (b0 + 64 <= k && b0 >= a0 + 64) continue;   // strictly upper Psi tile
-    auto stage = [&](int c, int buf) {
-      double* Ea = E + buf * 2 * kEC * kLds;
-      double* Eb = Ea + kEC * kLds;
-      const int g0 = c * kEC;
-      // column pairs as 16-byte copies: the panel rows are 16-byte aligned (even ldp),
-      // A21 pairs start at even columns, and the R block's pairs at Kp + (even - k),
-      // Kp - k = ngp even; only the pair straddling k (odd k) goes element-wise
-      for (int tt = tid; tt < kEC * 32; tt += 256) {
-        const int g = tt >> 5, i = 2 * (tt & 31);
-        const double* src = P + int64_t(g0 + g) * ldp;
-        double* ea = Ea + g * kLds + i;
-        double* eb = Eb + g * kLds + i;
-        const int aa = a0 + i;
-        if (aa + 1 < k) cp_async16(ea, src + aa);
-        else {
-          if (aa < k) cp_async8(ea, src + aa);
-          else ea[0] = 0.0;
-          ea[1] = 0.0;
+  const int tk = tri(k);
+  for (int ia = 0; ia < na; ++ia) {
+    const int a0 = ia * 64;
+    for (int jb = 0; jb <= ia + nbr; ++jb) {
+      const bool is_r = jb > ia;
+      const int b0 = is_r ? (jb - ia - 1) * 64 : jb * 64;   // Psi column / R column origin
+      const bool rfold = fold && jb == ia;
+      // warp role: 0 idle, 1 its 32 x 16 part of the tile, 2 folded R rows (a0 + rm0 ..)
+      int role = 1, rm0 = 0;
+      if (is_r) {
+        if (b0 + n0 >= nc || a0 + m0 >= k) role = 0;
+      } else if (b0 + n0 > a0 + m0 + 31 || b0 + n0 >= k || a0 + m0 >= k) {
+        role = 0;
+        if (rfold && m0 == 0 && n0 >= 32) {
+          rm0 = n0 == 32 ? 0 : 32;
+          role = a0 + rm0 < k ? 2 : 0;
         }
-        const int bb = b0 + i;
-        if (bb + 1 < k) cp_async16(eb, src + bb);
-        else if (bb >= k && bb + 1 < ow) cp_async16(eb, src + Kp + (bb - k));
-        else {
+      }
+      const int lim = is_r ? nc : k;          // B columns: R columns or Psi columns
+      const int base = is_r ? Kp : 0;
+      auto stage = [&](int c, int buf) {
+        double* Ea = E + buf * 2 * kEC * kLds;
+        double* Eb = Ea + kEC * kLds;
+        const int g0 = c * kEC;
+        // column pairs as 16-byte copies (even ldp, even starts); odd starts element-wise
+        for (int tt = tid; tt < kEC * 32; tt += 256) {
+          const int g = tt >> 5, i = 2 * (tt & 31);
+          const double* src = P + int64_t(g0 + g) * ldp;
+          double* ea = Ea + g * kLds + i;
+          double* eb = Eb + g * kLds + i;
+          const int aa = a0 + i;
+          if (aa + 1 < k) cp_async16(ea, src + aa);
+          else {
+            if (aa < k) cp_async8(ea, src + aa);
+            else ea[0] = 0.0;
+            ea[1] = 0.0;
+          }
+          const int bb = b0 + i;
+          if (bb + 1 < lim && ((base + bb) & 1) == 0) cp_async16(eb, src + base + bb);
+          else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              if (bb + e < lim) cp_async8(eb + e, src + base + bb + e);
+              else eb[e] = 0.0;
+            }
+          }
+        }
+        if (rfold)
+          for (int tt = tid; tt < kEC * 8; tt += 256) {
+            const int g = tt >> 3, cc = tt & 7;
+            double* eb = Eb + g * kLds + 64 + cc;
+            if (cc < nc) cp_async8(eb, P + int64_t(g0 + g) * ldp + Kp + cc);
+            else *eb = 0.0;
+          }
+        cp_async_commit();
+      };
+      __syncthreads();
+      stage(0, 0);
+      // the assembled A~ / R~ values of this warp's outputs, loaded ahead of the DMMAs
+      double pre[4][2][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int aa = a0 + (role == 2 ? rm0 : m0) + 8 * i + gr;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int b = bb + e;
-            const int col = b < k ? b : (b < ow ? Kp + (b - k) : -1);
-            if (col >= 0) cp_async8(eb + e, src + col);
-            else eb[e] = 0.0;
+            double v = 0.0;
+            if (role == 1 && aa < k) {
+              const int bb = b0 + n0 + 8 * j + 2 * gq + e;
+              if (is_r) { if (bb < nc) v = gather_R(mc, aa, bb); }
+              else if (bb <= aa) v = gather_A(mc, aa, bb);
+            } else if (role == 2 && j == 0 && aa < k) {
+              const int rc = 2 * gq + e;
+              if (rc < nc) v = gather_R(mc, aa, rc);
+            }
+            pre[i][j][e] = v;
           }
-        }
       }
-      cp_async_commit();
-    };
-    __syncthreads();
-    stage(0, 0);
-    double pre[4][2][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int aa = a0 + m0 + 8 * i + gr;
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int bb = b0 + n0 + 8 * j + 2 * gq + e;
-          double v = 0.0;
-          if (aa < k && bb < ow) {
-            if (bb < k) { if (bb <= aa) v = gather_A(mc, aa, bb); }
-            else v = gather_R(mc, aa, bb - k);
-          }
-          pre[i][j][e] = v;
+      double acc[4][2][2] = {};
+      for (int c = 0; c < nch; ++c) {
+        if (c + 1 < nch) {
+          stage(c + 1, (c + 1) & 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
         }
-    }
-    double acc[4][2][2] = {};
-    for (int c = 0; c < nch; ++c) {
-      if (c + 1 < nch) {
-        stage(c + 1, (c + 1) & 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
+        __syncthreads();
+        const double* Ea = E + (c & 1) * 2 * kEC * kLds;
+        const double* Eb = Ea + kEC * kLds;
+        if (role == 1) {
+          warp_gemm_tn<4, 2>(acc, Ea, kLds, m0, Eb, kLds, n0, kEC);
+        } else if (role == 2) {
+#pragma unroll
+          for (int kk = 0; kk < kEC; kk += 4) {
+            double av[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = Ea[(kk + gq) * kLds + rm0 + 8 * i + gr];
+            const double bv = Eb[(kk + gq) * kLds + 64 + gr];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dmma884(acc[i][0], av[i], bv);
+          }
+        }
+        __syncthreads();
       }
-      __syncthreads();
-      const double* Ea = E + (c & 1) * 2 * kEC * kLds;
-      warp_gemm_tn<4, 2>(acc, Ea, kLds, m0, Ea + kEC * kLds, kLds, n0, kEC);
-      __syncthreads();
-    }
+      if (role == 0) continue;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int aa = a0 + m0 + 8 * i + gr;
-      if (aa >= k) continue;
+      for (int i = 0; i < 4; ++i) {
+        const int aa = a0 + (role == 2 ? rm0 : m0) + 8 * i + gr;
+        if (aa >= k) continue;
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int bb = b0 + n0 + 8 * j + 2 * gq + e;
-          if (bb >= ow) continue;
-          if (bb < k) {
-            if (bb <= aa) out[tri(aa) + bb] = pre[i][j][e] - acc[i][j][e];
-          } else {
-            out[tri(k) + aa * nc + (bb - k)] = pre[i][j][e] - acc[i][j][e];
+          for (int e = 0; e < 2; ++e) {
+            if (role == 2) {
+              const int rc = 2 * gq + e;
+              if (j == 0 && rc < nc) out[tk + aa * nc + rc] = pre[i][0][e] - acc[i][0][e];
+            } else {
+              const int bb = b0 + n0 + 8 * j + 2 * gq + e;
+              if (is_r) {
+                if (bb < nc) out[tk + aa * nc + bb] = pre[i][j][e] - acc[i][j][e];
+              } else if (bb <= aa) {
+                out[tri(aa) + bb] = pre[i][j][e] - acc[i][j][e];
+              }
+            }
           }
-        }
+      }
     }
   }
 }
