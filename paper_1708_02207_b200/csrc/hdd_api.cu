@@ -580,10 +580,10 @@ static int setup_device(HddPlan* pl, int max_batch) {
         if (std::getenv("HDD_SCHUR_L_DEBUG"))
           std::fprintf(stderr, "tmap dep %zu node %zu: base %p ldp %d ngp %d bcap %d stride2 %lld k %d nc %d tiles %d\n",
                        dep, li, base, d.ldp, ngp, bcap, (long long)pl->depth_ws[dep], d.k, d.nc,
-                       schur_l_tiles(d.k, d.nc));
+                       schur_l_tiles(d.k, d.nc, ngp));
         maps.push_back(m);
-        pl->tm_ntiles.push_back(schur_l_tiles(d.k, d.nc));
-        pl->tm_tiles[dep] = std::max(pl->tm_tiles[dep], schur_l_tiles(d.k, d.nc));
+        pl->tm_ntiles.push_back(schur_l_tiles(d.k, d.nc, ngp));
+        pl->tm_tiles[dep] = std::max(pl->tm_tiles[dep], schur_l_tiles(d.k, d.nc, ngp));
       }
     }
     if (maps.empty()) pl->schur_split = false;

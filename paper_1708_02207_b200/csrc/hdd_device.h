@@ -149,7 +149,7 @@ cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_n
                             int pmax, cudaStream_t s);
 cudaError_t launch_schur_l(const DevPlan& p, const DevUpper* nodes_dev, const CUtensorMap* tmaps, const int* tiles,
                            int n_nodes, int B, cudaStream_t s);
-int schur_l_tiles(int k, int nc);
+int schur_l_tiles(int k, int nc, int ngp);   // ngp: padded interface rows
 cudaError_t launch_assemble_l(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
                               int64_t ws_stride, int max_rows, cudaStream_t s);
 int schur_l_box_rows();

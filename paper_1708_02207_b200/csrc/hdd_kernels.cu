@@ -2249,7 +2249,8 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
 // ---------------------------------------------------------------------------
 constexpr int kSA = 128, kSB = 64, kSR = 32, kSS = 4;
 constexpr int kSBX = kSB / 8 + 1;                        // B boxes: one extra for an odd R-block start
-constexpr int kStageD = (kSA + 8 * kSBX) * kSR;          // doubles per stage
+constexpr int kSRB = kSA / 8 + kSBX;                     // box index of the folded R columns
+constexpr int kStageD = (kSA + 8 * kSBX + 8) * kSR;      // doubles per stage (A | B | R boxes)
 size_t schur_l_smem_bytes() { return sizeof(double) * size_t(kSS) * kStageD + 128; }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
@@ -2258,31 +2259,48 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
       ::"r"(smem_u32(dst)), "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
 }
 
-__host__ __device__ inline int schur_l_tiles_dev(int k, int nc) {
-  const int na = (k + 127) / 128, nbk = (k + 63) / 64;
+// The R block (nc columns at panel column Kp) rides on tile (a0, a0 + 64) of a 128-row
+// block when it fits one 8-column box (nc <= 8 - (Kp & 1)) and that tile exists: the
+// tile's strictly upper warp tiles compute rows a0..a0+127 x the R columns.  Other row
+// blocks get 64-column R tiles.
+__host__ __device__ inline bool schur_fold_row(int ia, int k, int nc, int kp_odd) {
+  return nc <= 8 - kp_odd && ia * kSA + kSB < k;
+}
+__host__ __device__ inline int schur_l_tiles_dev(int k, int nc, int kp_odd) {
+  const int na = (k + kSA - 1) / kSA, nbk = (k + kSB - 1) / kSB, nr = (nc + kSB - 1) / kSB;
   int t = 0;
-  for (int ia = 0; ia < na; ++ia) t += (nbk < (ia * 128 + 128) / 64 ? nbk : (ia * 128 + 128) / 64);
-  return t + na * ((nc + 63) / 64);
+  for (int ia = 0; ia < na; ++ia) {
+    t += (nbk < (ia * kSA + kSA) / kSB ? nbk : (ia * kSA + kSA) / kSB);
+    if (!schur_fold_row(ia, k, nc, kp_odd)) t += nr;
+  }
+  return t;
 }
 
-// tile t of a node with k boundary rows and nc columns -> (a0, b0, is_r); false past the end
-__device__ __forceinline__ bool schur_tile(int t, int k, int nc, int& a0, int& b0, bool& is_r) {
-  const int na = (k + kSA - 1) / kSA, nbk = (k + kSB - 1) / kSB;
+// tile t of a node -> (a0, b0, is_r, fold: carries the R columns); false past the end
+__device__ __forceinline__ bool schur_tile(int t, int k, int nc, int kp_odd, int& a0, int& b0, bool& is_r,
+                                           bool& fold) {
+  const int na = (k + kSA - 1) / kSA, nbk = (k + kSB - 1) / kSB, nr = (nc + kSB - 1) / kSB;
   for (int ia = 0; ia < na; ++ia) {
     const int nb = min(nbk, (ia * kSA + kSA) / kSB);     // b tiles with b0 <= a0 + 127 (lower part)
-    if (t < nb) { a0 = ia * kSA; b0 = t * kSB; is_r = false; return true; }
+    const bool fr = schur_fold_row(ia, k, nc, kp_odd);
+    a0 = ia * kSA;
+    if (t < nb) { b0 = t * kSB; is_r = false; fold = fr && b0 == a0 + kSB; return true; }
     t -= nb;
+    if (!fr) {
+      if (t < nr) { b0 = t * kSB; is_r = true; fold = false; return true; }
+      t -= nr;
+    }
   }
-  const int nr = (nc + kSB - 1) / kSB;
-  if (t < na * nr) { a0 = (t / nr) * kSA; b0 = (t % nr) * kSB; is_r = true; return true; }
   return false;
 }
 
 constexpr int kSTPC = 4;                                 // tiles per CTA (the ring runs across them)
 
 // Warp-specialised: warps 0-7 compute (4 x 2 of 32 x 32 DMMA tiles), warp 8 produces
-// (waits for a free slot, lane 0 posts the expected bytes, lanes 0..24 issue one TMA box
+// (waits for a free slot, lane 0 posts the expected bytes, lanes 0..25 issue one TMA box
 // each).  full[slot] completes on the TMA bytes, empty[slot] on the 8 consumer warps.
+// In a tile that carries the R columns, the warps whose 32 x 32 part is strictly upper
+// compute the R rows instead.
 __global__ void __launch_bounds__(288, 1) schur_l_kernel(DevPlan p, const DevUpper* __restrict__ nodes,
                                                        const __grid_constant__ CUtensorMap tmap, int node) {
   extern __shared__ __align__(128) double sst_raw[];
@@ -2292,11 +2310,12 @@ __global__ void __launch_bounds__(288, 1) schur_l_kernel(DevPlan p, const DevUpp
   const int s = blockIdx.y;
   const DevUpper& U = nodes[node];
   const int k = U.k, nc = U.nc;
-  const int n_tiles = schur_l_tiles_dev(k, nc);
+  const int ngp = upper_ngp(U), Kp = k + ngp;
+  const int kp_odd = Kp & 1;
+  const int n_tiles = schur_l_tiles_dev(k, nc, kp_odd);
   const int t0 = blockIdx.x * kSTPC;
   if (t0 >= n_tiles) return;
   const int ntl = min(kSTPC, n_tiles - t0);
-  const int ngp = upper_ngp(U), Kp = k + ngp;
   const int nch = ngp / kSR;
   const int nq = ntl * nch;                                // (tile, chunk) stream of this CTA
   const int ldp = U.ldp;
@@ -2315,15 +2334,16 @@ __global__ void __launch_bounds__(288, 1) schur_l_kernel(DevPlan p, const DevUpp
       const int slot = q % kSS;
       if (q >= kSS) mbar_wait(&s_empty[slot], uint32_t(((q / kSS) - 1) & 1));
       int a0, b0;
-      bool is_r;
-      schur_tile(t0 + q / nch, k, nc, a0, b0, is_r);
+      bool is_r, fold;
+      schur_tile(t0 + q / nch, k, nc, kp_odd, a0, b0, is_r, fold);
       const int c = q - (q / nch) * nch;
       // B columns start at bcol; TMA box starts must be 16-byte aligned, so the boxes
       // start at the even column below it (the consumers skip boff columns); boxes
       // that start past the panel row are not issued (their columns are never stored)
       const int bstart = (is_r ? Kp + b0 : b0) & ~1;
-      const int col = lane < kSA / 8 ? a0 + 8 * lane : bstart + 8 * (lane - kSA / 8);
-      const bool live = lane < kSA / 8 + kSBX && col < ldp;
+      const int col = lane < kSA / 8 ? a0 + 8 * lane
+                    : (lane < kSRB ? bstart + 8 * (lane - kSA / 8) : (Kp & ~1));
+      const bool live = (lane < kSRB || (lane == kSRB && fold)) && col < ldp;
       const unsigned nbox = __popc(__ballot_sync(0xffffffffu, live));
       if (lane == 0) mbar_arrive_expect_tx(&s_full[slot], uint32_t(nbox * kSR * 8 * 8));
       __syncwarp();
@@ -2337,10 +2357,11 @@ __global__ void __launch_bounds__(288, 1) schur_l_kernel(DevPlan p, const DevUpp
   double* out = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
   const int tk = tri(k);
   double acc[4][4][2];
+  int role = 1, ra = 0;
   for (int q = 0; q < nq; ++q) {
     int a0, b0;
-    bool is_r;
-    schur_tile(t0 + q / nch, k, nc, a0, b0, is_r);
+    bool is_r, fold;
+    schur_tile(t0 + q / nch, k, nc, kp_odd, a0, b0, is_r, fold);
     const int c = q - (q / nch) * nch;
     const int boff = (is_r ? Kp + b0 : b0) & 1;
     if (c == 0) {
@@ -2348,26 +2369,49 @@ __global__ void __launch_bounds__(288, 1) schur_l_kernel(DevPlan p, const DevUpp
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      // role: 1 its 32 x 32 part of the tile, 2 the folded R columns of rows a0 + ra ..
+      // + 31 (a strictly upper warp tile of an R-carrying tile)
+      role = 1;
+      ra = wa;
+      if (fold && wa < 64) {
+        ra = wa + (wb ? 64 : 0);
+        role = 2;
+      }
     }
     const int slot = q % kSS;
     mbar_wait(&s_full[slot], uint32_t((q / kSS) & 1));
     const double* st = sst + slot * kStageD;
-    const double* As = st + (wa / 8) * kSR * 8;           // 4 A boxes of [kSR][8]
-    const double* Bs = st + (kSA / 8) * kSR * 8;          // B boxes
+    if (role == 1) {
+      const double* As = st + (wa / 8) * kSR * 8;         // 4 A boxes of [kSR][8]
+      const double* Bs = st + (kSA / 8) * kSR * 8;        // B boxes
 #pragma unroll
-    for (int kk = 0; kk < kSR; kk += 4) {
-      double av[4], bv[4];
+      for (int kk = 0; kk < kSR; kk += 4) {
+        double av[4], bv[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = As[i * kSR * 8 + (kk + gq) * 8 + gr];
+        for (int i = 0; i < 4; ++i) av[i] = As[i * kSR * 8 + (kk + gq) * 8 + gr];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int cb = wb + 8 * j + gr + boff;
-        bv[j] = Bs[(cb >> 3) * kSR * 8 + (kk + gq) * 8 + (cb & 7)];
+        for (int j = 0; j < 4; ++j) {
+          const int cb = wb + 8 * j + gr + boff;
+          bv[j] = Bs[(cb >> 3) * kSR * 8 + (kk + gq) * 8 + (cb & 7)];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j], av[i], bv[j]);
       }
+    } else {
+      const double* As = st + (ra / 8) * kSR * 8;
+      const double* Rs = st + kSRB * kSR * 8;
+      const int cr = gr + kp_odd;                         // R column gr sits at box column gr + (Kp & 1)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int kk = 0; kk < kSR; kk += 4) {
+        double av[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], av[i], bv[j]);
+        for (int i = 0; i < 4; ++i) av[i] = As[i * kSR * 8 + (kk + gq) * 8 + gr];
+        const double bv = cr < 8 ? Rs[(kk + gq) * 8 + cr] : 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dmma884(acc[i][0], av[i], bv);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&s_empty[slot]);           // this warp is done with the slot
@@ -2384,9 +2428,17 @@ __global__ void __launch_bounds__(288, 1) schur_l_kernel(DevPlan p, const DevUpp
           for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int a = a0 + wa + 8 * (ih + i) + gr, b = b0 + wb + 8 * j + 2 * gq + e;
+              const int a = a0 + ra + 8 * (ih + i) + gr;
               int t = -1;
-              if (a < k) t = !is_r ? (b <= a ? tri(a) + b : -1) : (b < nc ? tk + a * nc + b : -1);
+              if (a < k) {
+                if (role == 2) {
+                  const int rc = 2 * gq + e;
+                  t = (j == 0 && rc < nc) ? tk + a * nc + rc : -1;
+                } else {
+                  const int b = b0 + wb + 8 * j + 2 * gq + e;
+                  t = !is_r ? (b <= a ? tri(a) + b : -1) : (b < nc ? tk + a * nc + b : -1);
+                }
+              }
               idx[i][j][e] = t;
               old[i][j][e] = t >= 0 ? out[t] : 0.0;
             }
@@ -2448,12 +2500,7 @@ cudaError_t launch_schur_l(const DevPlan& p, const DevUpper* nodes_dev, const CU
   return cudaSuccess;
 }
 
-int schur_l_tiles(int k, int nc) {
-  const int na = (k + kSA - 1) / kSA, nbk = (k + kSB - 1) / kSB;
-  int t = 0;
-  for (int ia = 0; ia < na; ++ia) t += std::min(nbk, (ia * kSA + kSA) / kSB);
-  return t + na * ((nc + kSB - 1) / kSB);
-}
+int schur_l_tiles(int k, int nc, int ngp) { return schur_l_tiles_dev(k, nc, (k + ngp) & 1); }
 int schur_l_box_rows() { return kSR; }
 
 cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
