@@ -2250,7 +2250,8 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
 constexpr int kSA = 128, kSB = 64, kSR = 32, kSS = 4;
 constexpr int kSBX = kSB / 8 + 1;                        // B boxes: one extra for an odd R-block start
 constexpr int kSRB = kSA / 8 + kSBX;                     // box index of the folded R columns
-constexpr int kStageD = (kSA + 8 * kSBX + 8) * kSR;      // doubles per stage (A | B | R boxes)
+constexpr int kSRN = 2;                                  // R boxes (up to 16 folded R columns)
+constexpr int kStageD = (kSA + 8 * kSBX + 8 * kSRN) * kSR;   // doubles per stage (A | B | R boxes)
 size_t schur_l_smem_bytes() { return sizeof(double) * size_t(kSS) * kStageD + 128; }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
@@ -2260,11 +2261,11 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 }
 
 // The R block (nc columns at panel column Kp) rides on tile (a0, a0 + 64) of a 128-row
-// block when it fits one 8-column box (nc <= 8 - (Kp & 1)) and that tile exists: the
+// block when it fits two 8-column boxes (nc <= 16 - (Kp & 1)) and that tile exists: the
 // tile's strictly upper warp tiles compute rows a0..a0+127 x the R columns.  Other row
 // blocks get 64-column R tiles.
 __host__ __device__ inline bool schur_fold_row(int ia, int k, int nc, int kp_odd) {
-  return nc <= 8 - kp_odd && ia * kSA + kSB < k;
+  return nc <= 8 * kSRN - kp_odd && ia * kSA + kSB < k;
 }
 __host__ __device__ inline int schur_l_tiles_dev(int k, int nc, int kp_odd) {
   const int na = (k + kSA - 1) / kSA, nbk = (k + kSB - 1) / kSB, nr = (nc + kSB - 1) / kSB;
@@ -2297,7 +2298,7 @@ __device__ __forceinline__ bool schur_tile(int t, int k, int nc, int kp_odd, int
 constexpr int kSTPC = 4;                                 // tiles per CTA (the ring runs across them)
 
 // Warp-specialised: warps 0-7 compute (4 x 2 of 32 x 32 DMMA tiles), warp 8 produces
-// (waits for a free slot, lane 0 posts the expected bytes, lanes 0..25 issue one TMA box
+// (waits for a free slot, lane 0 posts the expected bytes, lanes 0..26 issue one TMA box
 // each).  full[slot] completes on the TMA bytes, empty[slot] on the 8 consumer warps.
 // In a tile that carries the R columns, the warps whose 32 x 32 part is strictly upper
 // compute the R rows instead.
@@ -2342,8 +2343,9 @@ __global__ void __launch_bounds__(288, 1) schur_l_kernel(DevPlan p, const DevUpp
       // that start past the panel row are not issued (their columns are never stored)
       const int bstart = (is_r ? Kp + b0 : b0) & ~1;
       const int col = lane < kSA / 8 ? a0 + 8 * lane
-                    : (lane < kSRB ? bstart + 8 * (lane - kSA / 8) : (Kp & ~1));
-      const bool live = (lane < kSRB || (lane == kSRB && fold)) && col < ldp;
+                    : (lane < kSRB ? bstart + 8 * (lane - kSA / 8) : (Kp & ~1) + 8 * (lane - kSRB));
+      const bool live = (lane < kSRB || (lane < kSRB + kSRN && fold && 8 * (lane - kSRB) < nc + kp_odd)) &&
+                        col < ldp;
       const unsigned nbox = __popc(__ballot_sync(0xffffffffu, live));
       if (lane == 0) mbar_arrive_expect_tx(&s_full[slot], uint32_t(nbox * kSR * 8 * 8));
       __syncwarp();
@@ -2402,15 +2404,22 @@ __global__ void __launch_bounds__(288, 1) schur_l_kernel(DevPlan p, const DevUpp
     } else {
       const double* As = st + (ra / 8) * kSR * 8;
       const double* Rs = st + kSRB * kSR * 8;
-      const int cr = gr + kp_odd;                         // R column gr sits at box column gr + (Kp & 1)
+      // R column 8 j + gr sits at box column 8 j + gr + (Kp & 1)
+      const int cr0 = gr + kp_odd, cr1 = 8 + gr + kp_odd;
+      const bool two = nc + kp_odd > 8;
 #pragma unroll
       for (int kk = 0; kk < kSR; kk += 4) {
         double av[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) av[i] = As[i * kSR * 8 + (kk + gq) * 8 + gr];
-        const double bv = cr < 8 ? Rs[(kk + gq) * 8 + cr] : 0.0;
+        const double bv0 = Rs[(cr0 >> 3) * kSR * 8 + (kk + gq) * 8 + (cr0 & 7)];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) dmma884(acc[i][0], av[i], bv);
+        for (int i = 0; i < 4; ++i) dmma884(acc[i][0], av[i], bv0);
+        if (two) {
+          const double bv1 = cr1 < 16 ? Rs[kSR * 8 + (kk + gq) * 8 + (cr1 & 7)] : 0.0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dmma884(acc[i][1], av[i], bv1);
+        }
       }
     }
     __syncwarp();
@@ -2432,8 +2441,8 @@ __global__ void __launch_bounds__(288, 1) schur_l_kernel(DevPlan p, const DevUpp
               int t = -1;
               if (a < k) {
                 if (role == 2) {
-                  const int rc = 2 * gq + e;
-                  t = (j == 0 && rc < nc) ? tk + a * nc + rc : -1;
+                  const int rc = 8 * j + 2 * gq + e;
+                  t = (j < kSRN && rc < nc) ? tk + a * nc + rc : -1;
                 } else {
                   const int b = b0 + wb + 8 * j + 2 * gq + e;
                   t = !is_r ? (b <= a ? tri(a) + b : -1) : (b < nc ? tk + a * nc + b : -1);
