@@ -517,31 +517,37 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
   cp_async_wait<1>();   // this level's panel program (issued one level earlier) has landed
   __syncthreads();
   // ---- A: gather the interface panel (precomputed program) ----
+  // The program of a level is the same for its nf nodes: a thread decodes item t once
+  // and applies it to every node q (compile-time strides 2 Sin / ng W), UT items in
+  // flight when nf is small.
   {
     const LeafItemP* prog = kLeafStage ? reinterpret_cast<const LeafItemP*>(tabP) : c_ltab.P[CI] + c_ltab.poff[CI][R];
-    constexpr int UA = 4;
-    const int stride = gsz * 32;
-    for (int q = warp / gsz; q < nf; q += qstep) {
-      const double* s1 = in + (2 * q) * Sin;
-      const double* s2 = in + (2 * q + 1) * Sin;
-      double* P = Pp + q * ng * W;
-      for (int t0 = sub * 32 + lane; t0 < NPI; t0 += UA * stride) {
-        LeafItemP it[UA];
-        double v[UA];
+    constexpr int UT = nf >= 4 ? 1 : 4 / nf;
+    for (int t0 = tid; t0 < NPI; t0 += UT * NT) {
+      int o1[UT], o2[UT];
 #pragma unroll
-        for (int u = 0; u < UA; ++u) {
-          const int t = t0 + u * stride;
-          if constexpr (kLeafStage)
-            it[u] = t < NPI ? prog[t] : LeafItemP{int16_t(Sin - 2), int16_t(Sin - 2), -1, 0};
-          else
-            it[u] = t < NPI ? load_item(prog, t) : LeafItemP{int16_t(Sin - 2), int16_t(Sin - 2), -1, 0};
+      for (int u = 0; u < UT; ++u) {
+        const int t = t0 + u * NT;
+        LeafItemP it = LeafItemP{int16_t(Sin - 2), int16_t(Sin - 2), -1, 0};
+        if (t < NPI) {
+          if constexpr (kLeafStage) it = prog[t];
+          else it = load_item(prog, t);
         }
+        o1[u] = it.o1;
+        o2[u] = Sin + it.o2;
+      }
+      double v[UT][nf];
 #pragma unroll
-        for (int u = 0; u < UA; ++u) v[u] = s1[it[u].o1] + s2[it[u].o2];
+      for (int u = 0; u < UT; ++u)
 #pragma unroll
-        for (int u = 0; u < UA; ++u) {
-          const int t = t0 + u * stride;
-          if (t < NPI) P[(t / WL) * W + (t - (t / WL) * WL)] = v[u];
+        for (int q = 0; q < nf; ++q) v[u][q] = in[2 * q * Sin + o1[u]] + in[2 * q * Sin + o2[u]];
+#pragma unroll
+      for (int u = 0; u < UT; ++u) {
+        const int t = t0 + u * NT;
+        if (t < NPI) {
+          double* P = Pp + (t / WL) * W + (t - (t / WL) * WL);
+#pragma unroll
+          for (int q = 0; q < nf; ++q) P[q * ng * W] = v[u][q];
         }
       }
     }
@@ -592,29 +598,34 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
     if (R == 0) asm volatile("bar.sync 1, %0;" ::"n"(NT));
 #endif
     // ---- B': sons' contributions to the outputs, A~ = Psi_s1 + Psi_s2 | R_s1 + R_s2 ----
+    // (item t decoded once for the level's nf nodes, as in A)
     const LeafItemU* uprog = kLeafStage ? reinterpret_cast<const LeafItemU*>(tabU) : c_ltab.U[CI] + c_ltab.uoff[CI][R];
-    constexpr int UB = 4;
+    constexpr int UB = nf >= 4 ? 1 : 4 / nf;
     const int wt = (warp - NWB) * 32 + lane, nth = (NW - NWB) * 32;
-    for (int i0 = wt; i0 < nf * NUI; i0 += UB * nth) {
-      double v[UB];
+    for (int t0 = wt; t0 < NUI; t0 += UB * nth) {
+      int o1[UB], o2[UB];
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
-        const int idx = i0 + u * nth;
-        const int q = idx < nf * NUI ? idx / NUI : 0;
+        const int t = t0 + u * nth;
         LeafItemU it = LeafItemU{0, 0, int16_t(Sin - 2), int16_t(Sin - 2)};
-        if (idx < nf * NUI) {
-          if constexpr (kLeafStage) it = uprog[idx - q * NUI];
-          else it = load_item(uprog, idx - q * NUI);
+        if (t < NUI) {
+          if constexpr (kLeafStage) it = uprog[t];
+          else it = load_item(uprog, t);
         }
-        v[u] = in[(2 * q) * Sin + it.o1] + in[(2 * q + 1) * Sin + it.o2];
+        o1[u] = it.o1;
+        o2[u] = Sin + it.o2;
       }
+      double v[UB][nf];
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+#pragma unroll
+        for (int q = 0; q < nf; ++q) v[u][q] = in[2 * q * Sin + o1[u]] + in[2 * q * Sin + o2[u]];
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
-        const int idx = i0 + u * nth;
-        if (idx < nf * NUI) {
-          const int q = idx / NUI;
-          out[q * Sout + (idx - q * NUI)] = v[u];
-        }
+        const int t = t0 + u * nth;
+        if (t < NUI)
+#pragma unroll
+          for (int q = 0; q < nf; ++q) out[q * Sout + t] = v[u][q];
       }
     }
     // functional births at this level: +1 in the panel's R_gamma column
