@@ -441,6 +441,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// TMA bulk store shared -> global (bulk group; wait with bulk_wait_read0 before the smem
+// is reused or the CTA exits); generic-proxy smem writes need fence_proxy_async_smem first
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+               ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 // TMA bulk prefetch of a global range into L2 (no shared memory, no completion)
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
@@ -849,14 +858,17 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
       if (c < 2) o[Sout - 2 + c] = 0.0;    // zero slot
     }
   }
+  if constexpr (R == 0) fence_proxy_async_smem();   // the Psi block is read by the bulk copy below
   __syncthreads();
   if constexpr (R == 0) {
     // leaf output: Psi packed lower, R [64][leaf_cols] (mean columns rescaled by
     // 1/|leaf|, an exact power of two), sigma; primal-mode leaf functionals
     const double inv_area = 1.0 / (double(kLeafCells * kLeafCells) * p.h * p.h);
     double* gdst = p.buf[p.leaf_buf] + int64_t(leaf) * p.leaf_elems * p.bcap + int64_t(s) * p.leaf_elems;
-    if (blockIdx.z == 0)
-      for (int t = tid; t < ctri(k); t += NT) gdst[t] = out[t];
+    // Psi (tri(64) doubles, 16-byte aligned at both ends): one TMA bulk store, waited
+    // for (smem reads done) before the CTA exits
+    static_assert((ctri(k) * 8) % 16 == 0, "bulk copies move 16-byte multiples");
+    if (blockIdx.z == 0 && tid == 0) bulk_s2g(gdst, out, uint32_t(ctri(k) * 8));
     // Dirichlet data g on the domain boundary (known perimeter values u_D = g_D):
     // load rows r_a -= Psi_aD g_D, functional columns sigma_c += R_c(D)^T g_D
     const bool hasg = EXT && (p.leaf_g || p.gcall);
@@ -1195,6 +1207,7 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
   leaf_level<2, NC, NTH>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
   leaf_level<1, NC, NTH>(p, bufA, bufB, pan, cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
   leaf_level<0, NC, NTH, SUB>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
+  if (tid == 0) bulk_wait_read0();   // the Psi bulk store has read its shared memory
   LEAF_TICK(63);
 }
 
