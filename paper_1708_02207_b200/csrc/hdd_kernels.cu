@@ -504,6 +504,9 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
   constexpr int qstep = NW / gsz;
   constexpr int CI = NC == 2 ? 0 : (NC == 4 ? 1 : 2);
   constexpr int NPI = ng * WL, NUI = ctri(k) + k * NC;
+  // ng = 3 levels (4 and 3): the sons' contributions and the rank-3 Schur update run as
+  // one pass per output element (phase E) instead of B' plus DMMA blocks
+  constexpr bool kE = ng == 3;
   constexpr int LPN = ng <= 1 ? 1 : (ng <= 4 ? 4 : (ng <= 8 ? 8 : 16));   // Cholesky lanes per node
   constexpr int NPW = 32 / LPN;                                           // nodes per Cholesky warp
   constexpr int NWB = (nf + NPW - 1) / NPW;                               // Cholesky warps
@@ -611,7 +614,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
     const LeafItemU* uprog = kLeafStage ? reinterpret_cast<const LeafItemU*>(tabU) : c_ltab.U[CI] + c_ltab.uoff[CI][R];
     constexpr int UB = nf >= 4 ? 1 : 4 / nf;
     const int wt = (warp - NWB) * 32 + lane, nth = (NW - NWB) * 32;
-    for (int t0 = wt; t0 < NUI; t0 += UB * nth) {
+    for (int t0 = wt; !kE && t0 < NUI; t0 += UB * nth) {
       int o1[UB], o2[UB];
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
@@ -664,7 +667,26 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
   __syncthreads();
   LEAF_TICK(10 + 8 * (5 - R) + 2);
   // ---- D: out -= W^T [W | V]; sigma += V_0^T V ----
-  if constexpr (ng >= 3) {
+  if constexpr (kE) {
+    // ---- E: out = Psi_s1 + Psi_s2 - W^T [W | V] per output element (item t decoded once
+    // for the nf nodes; rank-3 update in DFMA) ----
+    const LeafItemU* uprog = kLeafStage ? reinterpret_cast<const LeafItemU*>(tabU) : c_ltab.U[CI] + c_ltab.uoff[CI][R];
+    for (int t = tid; t < NUI; t += NT) {
+      const LeafItemU it = kLeafStage ? uprog[t] : load_item(uprog, t);
+      const int a = it.a, bc = it.bx < k ? it.bx : K + (it.bx - k);
+      const int o1 = it.o1, o2 = Sin + it.o2;
+      double v[nf];
+#pragma unroll
+      for (int q = 0; q < nf; ++q) v[q] = in[2 * q * Sin + o1] + in[2 * q * Sin + o2];
+#pragma unroll
+      for (int q = 0; q < nf; ++q) {
+        const double* P = Pp + q * ng * W;
+#pragma unroll
+        for (int g = 0; g < ng; ++g) v[q] = fma(-P[g * W + a], P[g * W + bc], v[q]);
+        out[q * Sout + t] = v[q];
+      }
+    }
+  } else if constexpr (ng >= 3) {
     // 16x16 output blocks (2x2 DMMA m8n8k4 tiles; interface dimension padded to 4):
     // lower-triangle Psi blocks, then 16x8 blocks for the R columns
     constexpr int nB = (k + 15) / 16, TPN = ctri(nB) + nB, KS = (ng + 3) / 4;
