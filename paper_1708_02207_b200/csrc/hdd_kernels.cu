@@ -922,6 +922,139 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
   LEAF_TICK(10 + 8 * (5 - R) + 3);
 }
 
+// ---- levels 6 + 5 fused: per-node algebra (leaf2_kernel) ----
+// A level-5 node (2 x 4 cells, 3 x 5 nodes) has 12 boundary nodes and 3 interior ones
+// (the 2x2-block centres c1 = (1,1), c2 = (1,3) and the level-5 interface node
+// m = (1,2)); A_II is tridiagonal and every boundary node couples to at most one
+// interior node, so  Psi = A_BB - v_a M(g_a, g_b) v_b,  R = r_B - v_a (M r_I)(g_a),
+// sigma_c = r_0I^T M r_cI  with M = A_II^-1 in closed form: the block elimination of
+// the level-6 and level-5 steps (fem.py:126-145 cell patterns).
+// Boundary index <-> local node (sorted (y, x) like the leaf template); interior
+// neighbour 0 = c1, 1 = m, 2 = c2, -1 none.
+__host__ __device__ constexpr int l56_bx(int i) { return i < 3 ? i : (i < 9 ? (((i - 3) & 1) ? 2 : 0) : i - 9); }
+__host__ __device__ constexpr int l56_by(int i) { return i < 3 ? 0 : (i < 9 ? (i - 3) / 2 + 1 : 4); }
+__host__ __device__ constexpr int l56_bg(int i) {
+  return i == 1 || i == 3 || i == 4 ? 0 : (i == 5 || i == 6 ? 1 : (i == 7 || i == 8 || i == 10 ? 2 : -1));
+}
+// boundary neighbours of row a with a smaller index: left (x - 1) and down (y - 1), -1 none
+__host__ __device__ constexpr int l56_left(int a) {
+  return (l56_bx(a) >= 1 && (l56_by(a) == 0 || l56_by(a) == 4 || l56_bx(a) == 2))
+             ? (l56_bx(a) == 2 && l56_by(a) >= 1 && l56_by(a) <= 3 ? -1 : a - 1) : -1;
+}
+__host__ __device__ constexpr int l56_down(int a) {
+  return (l56_by(a) >= 1 && l56_bx(a) != 1)
+             ? (l56_by(a) == 1 ? (l56_bx(a) == 0 ? 0 : 2) : (l56_by(a) == 4 ? (l56_bx(a) == 0 ? 7 : 8) : a - 2)) : -1;
+}
+
+struct L56Node {
+  const double* kap;    // the leaf's kappa, [x][2 y + type]
+  const double* fl;     // nodal f of the leaf (17 x 17) or null
+  int ox, oy;
+  double h2_6, h2;
+  __device__ __forceinline__ double k0(int cx, int cy) const { return kap[(ox + cx) * 32 + 2 * (oy + cy)]; }
+  __device__ __forceinline__ double k1(int cx, int cy) const { return kap[(ox + cx) * 32 + 2 * (oy + cy) + 1]; }
+  static __device__ __forceinline__ bool in_(int cx, int cy) { return cx >= 0 && cx < 2 && cy >= 0 && cy < 4; }
+  __device__ __forceinline__ double Dl(int x, int y) const {
+    double d = 0.0;
+    if (in_(x, y)) d += 0.5 * (k0(x, y) + k1(x, y));
+    if (in_(x - 1, y)) d += k0(x - 1, y);
+    if (in_(x, y - 1)) d += k1(x, y - 1);
+    if (in_(x - 1, y - 1)) d += 0.5 * (k0(x - 1, y - 1) + k1(x - 1, y - 1));
+    return d;
+  }
+  __device__ __forceinline__ double El(int x, int y) const {   // (x,y)-(x+1,y)
+    double e = 0.0;
+    if (in_(x, y)) e -= 0.5 * k0(x, y);
+    if (in_(x, y - 1)) e -= 0.5 * k1(x, y - 1);
+    return e;
+  }
+  __device__ __forceinline__ double Nl(int x, int y) const {   // (x,y)-(x,y+1)
+    double e = 0.0;
+    if (in_(x, y)) e -= 0.5 * k1(x, y);
+    if (in_(x - 1, y)) e -= 0.5 * k0(x - 1, y);
+    return e;
+  }
+  __device__ __forceinline__ double wl(int x, int y) const {   // lumped load weight
+    double w = 0.0;
+    if (in_(x, y)) w += 2.0;
+    if (in_(x - 1, y)) w += 1.0;
+    if (in_(x, y - 1)) w += 1.0;
+    if (in_(x - 1, y - 1)) w += 2.0;
+    return w * h2_6;
+  }
+  __device__ __forceinline__ double fv(int x, int y) const { return fl ? fl[(oy + y) * 17 + ox + x] : 1.0; }
+  // boundary-interior coupling of boundary node b (compile-time b)
+  __device__ __forceinline__ double vb(int b) const {
+    return b == 1 ? Nl(1, 0) : b == 3 ? El(0, 1) : b == 4 ? El(1, 1) : b == 5 ? El(0, 2) : b == 6 ? El(1, 2)
+         : b == 7 ? El(0, 3) : b == 8 ? El(1, 3) : b == 10 ? Nl(1, 3) : 0.0;
+  }
+};
+
+// Row A of one node's outputs (Psi row, R row; sigma and the zero slot with row 0): the
+// lane owns the node, the warp owns the row, so every index below is a compile-time
+// constant and only the kappa-dependent values are computed.
+template <int A, int NC, bool SUB>
+__device__ __forceinline__ void l56_row(const L56Node& n, const double (&M)[6], double* __restrict__ out,
+                                        const int* ctype, const int* br, const int* bq, int q) {
+  constexpr int k5 = 12;
+  constexpr int S5 = ctri(k5) + k5 * NC + NC + 2;
+  constexpr int xa = l56_bx(A), ya = l56_by(A), ga = l56_bg(A);
+  constexpr int il = l56_left(A), idn = l56_down(A);
+  // M = [[M0 M1 M2] [M1 M3 M4] [M2 M4 M5]]
+  auto Mg = [&](int g, int h) -> double {
+    const int lo = g < h ? g : h, hi = g < h ? h : g;
+    return lo == 0 ? M[hi] : (lo == 1 ? M[2 + hi] : M[5]);
+  };
+  double ma0 = 0.0, ma1 = 0.0, ma2 = 0.0;      // row g_a of M, times v_a
+  if constexpr (ga >= 0) {
+    const double va = n.vb(A);
+    ma0 = Mg(ga, 0) * va;
+    ma1 = Mg(ga, 1) * va;
+    ma2 = Mg(ga, 2) * va;
+  }
+#pragma unroll
+  for (int b = 0; b <= A; ++b) {
+    double val = b == A ? n.Dl(xa, ya) : (b == il ? n.El(xa - 1, ya) : (b == idn ? n.Nl(xa, ya - 1) : 0.0));
+    const int gb = l56_bg(b);
+    if (ga >= 0 && gb >= 0) val -= (gb == 0 ? ma0 : (gb == 1 ? ma1 : ma2)) * n.vb(b);
+    out[ctri(A) + b] = val;
+  }
+  const double wa = n.wl(xa, ya), fa = n.fv(xa, ya);
+  const double fI0 = n.fv(1, 1), fI1 = n.fv(1, 2), fI2 = n.fv(1, 3);
+  double r00 = 0.0, r01 = 0.0, r02 = 0.0;        // load column interior rhs
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int ct = ctype[c];
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+    if (ct == 0) { r0 = n.h2 * fI0; r1 = n.h2 * fI1; r2 = n.h2 * fI2; }
+    else if (ct == 1) { r0 = n.h2; r1 = n.h2; r2 = n.h2; }
+    else if (SUB && ct >= kSubMeanCode) {
+      r0 = n.h2_6 * submean_weight(ct, n.ox + 1, n.oy + 1, n.ox, n.ox + 2, n.oy, n.oy + 4);
+      r1 = n.h2_6 * submean_weight(ct, n.ox + 1, n.oy + 2, n.ox, n.ox + 2, n.oy, n.oy + 4);
+      r2 = n.h2_6 * submean_weight(ct, n.ox + 1, n.oy + 3, n.ox, n.ox + 2, n.oy, n.oy + 4);
+    }
+    if (br[c] == 6 && bq[c] == 2 * q) r0 += 1.0;
+    if (br[c] == 6 && bq[c] == 2 * q + 1) r2 += 1.0;
+    if (br[c] == 5 && bq[c] == q) r1 += 1.0;
+    if (c == 0) { r00 = r0; r01 = r1; r02 = r2; }
+    double val = ct == 0 ? wa * fa : (ct == 1 ? wa : 0.0);
+    if (SUB && ct >= kSubMeanCode) val = n.h2_6 * submean_weight(ct, n.ox + xa, n.oy + ya, n.ox, n.ox + 2, n.oy, n.oy + 4);
+    if constexpr (ga >= 0) val -= ma0 * r0 + ma1 * r1 + ma2 * r2;
+    out[ctri(k5) + A * NC + c] = val;
+    if constexpr (A == 0) {
+      double sg = 0.0;
+      if (c >= 1) {
+        const double t0 = M[0] * r0 + M[1] * r1 + M[2] * r2;
+        const double t1 = M[1] * r0 + M[3] * r1 + M[4] * r2;
+        const double t2 = M[2] * r0 + M[4] * r1 + M[5] * r2;
+        sg = r00 * t0 + r01 * t1 + r02 * t2;
+      }
+      out[ctri(k5) + k5 * NC + c] = sg;
+    }
+  }
+  if constexpr (A == 0) { out[S5 - 2] = 0.0; out[S5 - 1] = 0.0; }   // zero slot
+}
+
 // One CTA per (16x16-cell leaf, sample).  Level 6 (2x2-cell blocks) is built per
 // thread in registers straight from the cells' kappa; levels 5..0 run
 // level-synchronously in shared memory with lower-packed Schur complements:
@@ -1073,147 +1206,39 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
 
 #else
   // ---------------- levels 6 + 5 fused: 2x4-cell nodes condensed directly ----------------
-  // A level-5 node (2 x 4 cells, 3 x 5 nodes) has 12 boundary nodes and 3 interior ones
-  // (the 2x2-block centres c1 = (1,1), c2 = (1,3) and the level-5 interface node
-  // m = (1,2)); A_II is tridiagonal and every boundary node couples to at most one
-  // interior node, so  Psi = A_BB - v_a M(g_a, g_b) v_b,  R = r_B - v_a (M r_I)(g_a),
-  // sigma_c = r_0I^T M r_cI  with M = A_II^-1 in closed form: the block elimination of
-  // the level-6 and level-5 steps (fem.py:126-145 cell patterns), one warp per two nodes
-  // at a time, lane = boundary row (16 lanes per node).
+  // (l56_row): lane = node (32 nodes), warp w = boundary rows w and w + 8
   {
     constexpr int k5 = 12;
     constexpr int S5 = ctri(k5) + k5 * NC + NC + 2;
-    const int lane = tid & 31, wid = tid >> 5;
-    const int half = lane >> 4, a = lane & 15;
-    const double h2 = p.h * p.h;
-    // boundary index <-> local node (sorted (y, x) like the leaf template); interior
-    // neighbour 0 = c1, 1 = m, 2 = c2, -1 none
-    auto bx_f = [](int i) { return i < 3 ? i : (i < 9 ? (((i - 3) & 1) ? 2 : 0) : i - 9); };
-    auto by_f = [](int i) { return i < 3 ? 0 : (i < 9 ? (i - 3) / 2 + 1 : 4); };
-    auto bg_f = [](int i) { return i == 1 || i == 3 || i == 4 ? 0 : (i == 5 || i == 6 ? 1 : (i == 7 || i == 8 || i == 10 ? 2 : -1)); };
-    for (int pass = 0; pass < 2; ++pass) {
-      const int q = wid * 4 + pass * 2 + half;
-      const int o = c_orig[31 + q];
-      const int ox = o & 255, oy = o >> 8;
-      auto k0 = [&](int cx, int cy) -> double { return kap[(ox + cx) * 32 + 2 * (oy + cy)]; };
-      auto k1 = [&](int cx, int cy) -> double { return kap[(ox + cx) * 32 + 2 * (oy + cy) + 1]; };
-      auto in_ = [](int cx, int cy) { return cx >= 0 && cx < 2 && cy >= 0 && cy < 4; };
-      auto Dl = [&](int x, int y) -> double {
-        double d = 0.0;
-        if (in_(x, y)) d += 0.5 * (k0(x, y) + k1(x, y));
-        if (in_(x - 1, y)) d += k0(x - 1, y);
-        if (in_(x, y - 1)) d += k1(x, y - 1);
-        if (in_(x - 1, y - 1)) d += 0.5 * (k0(x - 1, y - 1) + k1(x - 1, y - 1));
-        return d;
-      };
-      auto El = [&](int x, int y) -> double {      // (x,y)-(x+1,y)
-        double e = 0.0;
-        if (in_(x, y)) e -= 0.5 * k0(x, y);
-        if (in_(x, y - 1)) e -= 0.5 * k1(x, y - 1);
-        return e;
-      };
-      auto Nl = [&](int x, int y) -> double {      // (x,y)-(x,y+1)
-        double e = 0.0;
-        if (in_(x, y)) e -= 0.5 * k1(x, y);
-        if (in_(x - 1, y)) e -= 0.5 * k0(x - 1, y);
-        return e;
-      };
-      auto wl = [&](int x, int y) -> double {      // lumped load weight
-        double w = 0.0;
-        if (in_(x, y)) w += 2.0;
-        if (in_(x - 1, y)) w += 1.0;
-        if (in_(x, y - 1)) w += 1.0;
-        if (in_(x - 1, y - 1)) w += 2.0;
-        return w * h2_6;
-      };
-      auto fv = [&](int x, int y) -> double { return p.f ? fl[(oy + y) * 17 + ox + x] : 1.0; };
-      // interior block and its inverse (every lane of the node, broadcast loads)
-      const double ia = Dl(1, 1), ib = Nl(1, 1), ic = Dl(1, 2), idd = Nl(1, 2), ie = Dl(1, 3);
-      const double p1 = ia * ic - ib * ib;
-      const double det = p1 * ie - ia * idd * idd;
-      if (a == 0 && (!(ia > 0.0) || !(p1 > 0.0) || !(det > 0.0)))
-        record_error(p, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, 5, q));
-      const double rdet = 1.0 / det;
-      const double M00 = (ic * ie - idd * idd) * rdet, M01 = -ib * ie * rdet, M02 = ib * idd * rdet;
-      const double M11 = ia * ie * rdet, M12 = -ia * idd * rdet, M22 = p1 * rdet;
-      auto Mrow = [&](int g, double& x0, double& x1, double& x2) {
-        x0 = g == 0 ? M00 : (g == 1 ? M01 : M02);
-        x1 = g == 0 ? M01 : (g == 1 ? M11 : M12);
-        x2 = g == 0 ? M02 : (g == 1 ? M12 : M22);
-      };
-      // boundary-interior couplings of every boundary node
-      double vb[12];
-      vb[0] = 0.0; vb[2] = 0.0; vb[9] = 0.0; vb[11] = 0.0;
-      vb[1] = Nl(1, 0);
-      vb[3] = El(0, 1);
-      vb[4] = El(1, 1);
-      vb[5] = El(0, 2);
-      vb[6] = El(1, 2);
-      vb[7] = El(0, 3);
-      vb[8] = El(1, 3);
-      vb[10] = Nl(1, 3);
-      if (a < k5) {
-        double* out = bufB + q * S5;
-        const int xa = bx_f(a), ya = by_f(a), ga = bg_f(a);
-        double va = 0.0;
-#pragma unroll
-        for (int b = 0; b < 12; ++b)
-          if (b == a) va = vb[b];
-        double ma0 = 0.0, ma1 = 0.0, ma2 = 0.0;      // row g_a of M, times v_a
-        if (ga >= 0) {
-          Mrow(ga, ma0, ma1, ma2);
-          ma0 *= va; ma1 *= va; ma2 *= va;
-        }
-        // Psi row a (packed lower): own diagonal and the couplings to the left / lower
-        // boundary neighbours computed once per lane, then a uniform loop over b
-        const double dself = Dl(xa, ya);
-        const int il = (xa >= 1 && (ya == 0 || ya == 4 || xa == 2)) ? (xa == 2 && ya >= 1 && ya <= 3 ? -1 : a - 1) : -1;
-        const int idn = (ya >= 1 && xa != 1) ? (ya == 1 ? (xa == 0 ? 0 : 2) : (ya == 4 ? (xa == 0 ? 7 : 8) : a - 2)) : -1;
-        const double eleft = il >= 0 ? El(xa - 1, ya) : 0.0;
-        const double ndown = idn >= 0 ? Nl(xa, ya - 1) : 0.0;
-#pragma unroll
-        for (int b = 0; b < 12; ++b) {
-          const int gb = bg_f(b);
-          double val = b == a ? dself : (b == il ? eleft : (b == idn ? ndown : 0.0));
-          if (gb >= 0) val -= (gb == 0 ? ma0 : (gb == 1 ? ma1 : ma2)) * vb[b];
-          if (b <= a) out[ctri(a) + b] = val;
-        }
-        // R row a and (lane 0) sigma: interior right-hand sides per column
-        const double wa = wl(xa, ya), fa = fv(xa, ya);
-        const double fI0 = fv(1, 1), fI1 = fv(1, 2), fI2 = fv(1, 3);
-        double r00 = 0.0, r01 = 0.0, r02 = 0.0;        // load column interior rhs
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const int ct = ctype[c];
-          double r0 = 0.0, r1 = 0.0, r2 = 0.0;
-          if (ct == 0) { r0 = h2 * fI0; r1 = h2 * fI1; r2 = h2 * fI2; }
-          else if (ct == 1) { r0 = h2; r1 = h2; r2 = h2; }
-          else if (SUB && ct >= kSubMeanCode) {
-            r0 = h2_6 * submean_weight(ct, ox + 1, oy + 1, ox, ox + 2, oy, oy + 4);
-            r1 = h2_6 * submean_weight(ct, ox + 1, oy + 2, ox, ox + 2, oy, oy + 4);
-            r2 = h2_6 * submean_weight(ct, ox + 1, oy + 3, ox, ox + 2, oy, oy + 4);
-          }
-          if (br[c] == 6 && bq[c] == 2 * q) r0 += 1.0;
-          if (br[c] == 6 && bq[c] == 2 * q + 1) r2 += 1.0;
-          if (br[c] == 5 && bq[c] == q) r1 += 1.0;
-          if (c == 0) { r00 = r0; r01 = r1; r02 = r2; }
-          double val = ct == 0 ? wa * fa : (ct == 1 ? wa : 0.0);
-          if (SUB && ct >= kSubMeanCode) val = h2_6 * submean_weight(ct, ox + xa, oy + ya, ox, ox + 2, oy, oy + 4);
-          if (ga >= 0) val -= ma0 * r0 + ma1 * r1 + ma2 * r2;
-          out[ctri(k5) + a * NC + c] = val;
-          if (a == 0) {
-            double sg = 0.0;
-            if (c >= 1) {
-              const double t0 = M00 * r0 + M01 * r1 + M02 * r2;
-              const double t1 = M01 * r0 + M11 * r1 + M12 * r2;
-              const double t2 = M02 * r0 + M12 * r1 + M22 * r2;
-              sg = r00 * t0 + r01 * t1 + r02 * t2;
-            }
-            out[ctri(k5) + k5 * NC + c] = sg;
-          }
-        }
-        if (a == 0) { out[S5 - 2] = 0.0; out[S5 - 1] = 0.0; }   // zero slot
-      }
+    static_assert(NTH == 256, "8 warps x 32 nodes");
+    const int q = tid & 31, wid = tid >> 5;
+    const int o = c_orig[31 + q];
+    L56Node n;
+    n.kap = kap;
+    n.fl = p.f ? fl : nullptr;
+    n.ox = o & 255;
+    n.oy = o >> 8;
+    n.h2_6 = h2_6;
+    n.h2 = p.h * p.h;
+    // interior block (tridiagonal) and its inverse M
+    const double ia = n.Dl(1, 1), ib = n.Nl(1, 1), ic = n.Dl(1, 2), idd = n.Nl(1, 2), ie = n.Dl(1, 3);
+    const double p1 = ia * ic - ib * ib;
+    const double det = p1 * ie - ia * idd * idd;
+    if (wid == 0 && (!(ia > 0.0) || !(p1 > 0.0) || !(det > 0.0)))
+      record_error(p, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, 5, q));
+    const double rdet = 1.0 / det;
+    const double M[6] = {(ic * ie - idd * idd) * rdet, -ib * ie * rdet, ib * idd * rdet,
+                         ia * ie * rdet, -ia * idd * rdet, p1 * rdet};
+    double* out = bufB + q * S5;
+    switch (wid) {   // warp-uniform
+      case 0: l56_row<0, NC, SUB>(n, M, out, ctype, br, bq, q); l56_row<8, NC, SUB>(n, M, out, ctype, br, bq, q); break;
+      case 1: l56_row<1, NC, SUB>(n, M, out, ctype, br, bq, q); l56_row<9, NC, SUB>(n, M, out, ctype, br, bq, q); break;
+      case 2: l56_row<2, NC, SUB>(n, M, out, ctype, br, bq, q); l56_row<10, NC, SUB>(n, M, out, ctype, br, bq, q); break;
+      case 3: l56_row<3, NC, SUB>(n, M, out, ctype, br, bq, q); l56_row<11, NC, SUB>(n, M, out, ctype, br, bq, q); break;
+      case 4: l56_row<4, NC, SUB>(n, M, out, ctype, br, bq, q); break;
+      case 5: l56_row<5, NC, SUB>(n, M, out, ctype, br, bq, q); break;
+      case 6: l56_row<6, NC, SUB>(n, M, out, ctype, br, bq, q); break;
+      default: l56_row<7, NC, SUB>(n, M, out, ctype, br, bq, q); break;
     }
   }
   __syncthreads();
