@@ -2127,7 +2127,7 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
     out[tk + k * nc + c] = v;
   }
   MERGE_TICK(4);
-  schur_epilogue<true, MINB <= 2, MINB <= 2>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
+  schur_epilogue<true, MINB <= 3, MINB <= 2>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
   MERGE_TICK(5);
 }
 
@@ -2592,7 +2592,8 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
   if (tier == 0) {
     // occupancy by panel size: 1 x 512 threads for big panels; 4 x 256 threads (64
     // registers) when 4 panels fit an SM, else 3 x 256 (80 registers; measured)
-    if (smem > 100 * 1024 && smem <= 113 * 1024) {
+    static const int force_minb = std::getenv("HDD_M2_MINB") ? std::atoi(std::getenv("HDD_M2_MINB")) : 0;   // A/B hook
+    if ((smem > 100 * 1024 && smem <= 113 * 1024) || (force_minb == 2 && smem <= 113 * 1024)) {
       e = cudaFuncSetAttribute(merge_m2_kernel<8, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
       merge_m2_kernel<8, 256, 2><<<grid, 256, smem, s>>>(p, nodes_dev, slot);
@@ -2600,7 +2601,7 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
       e = cudaFuncSetAttribute(merge_m2_kernel<8, 512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
       merge_m2_kernel<8, 512, 1><<<grid, 512, smem, s>>>(p, nodes_dev, slot);
-    } else if (smem <= 55 * 1024) {
+    } else if (smem <= 55 * 1024 && force_minb != 3) {
       e = cudaFuncSetAttribute(merge_m2_kernel<8, 256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
       merge_m2_kernel<8, 256, 4><<<grid, 256, smem, s>>>(p, nodes_dev, slot);
