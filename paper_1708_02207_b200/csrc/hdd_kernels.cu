@@ -2615,7 +2615,10 @@ cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_node
     // fill them and the panel region fits three per SM (measured: C4 depths 3-5 -12 %)
     // (the 2-CTA/SM variant has the smem for 128-column elimination chunks: twice the
     // DMMA work per staged A operand, measured -18 % on the C5 root)
-    if (int64_t(n_nodes) * B >= 148 * 3 * 2 && smem <= 74 * 1024) {
+    // (split depths below the root run only the elimination here: the 128-column chunks of
+    // the 2-CTA/SM variant win there, measured C5 d2 104.8 -> 99.1 ms, d1 60.3 -> 54.0 ms
+    // per 512; the root (slot = depth 0) keeps 3 CTAs/SM: C3 3.15 vs 3.53 ms)
+    if ((!p.schur_split || slot == 0) && int64_t(n_nodes) * B >= 148 * 3 * 2 && smem <= 74 * 1024) {
       e = cudaFuncSetAttribute(merge_l_kernel<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
       merge_l_kernel<3, 64><<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride, slot);
