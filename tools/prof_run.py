@@ -1,5 +1,6 @@
 """Minimal driver for ncu captures: one warm forward + one profiled forward.
 usage: python tools/prof_run.py CONFIG BATCH [lr]   (lr: the config's low-rank ToleranceSpec)"""
+import os
 import sys
 from pathlib import Path
 
@@ -24,8 +25,10 @@ ll = torch.empty(B, dtype=torch.float64, device="cuda")
 ns = info.leaf_depth + 3
 for it in range(2):
     st = np.zeros(ns)
-    plan.check(plan.lib.hdd_forward_batch_timed(plan.handle, C.c_void_p(Z.data_ptr()), B, None,
-                                                C.c_void_p(ll.data_ptr()), None, st.ctypes.data_as(_lib._f64p), ns))
+    rc = plan.lib.hdd_forward_batch_timed(plan.handle, C.c_void_p(Z.data_ptr()), B, None,
+                                          C.c_void_p(ll.data_ptr()), None, st.ctypes.data_as(_lib._f64p), ns)
+    if not os.environ.get("HDD_PROF_IGNORE_ERR"):      # A/B builds with deliberately wrong numerics
+        plan.check(rc)
 torch.cuda.synchronize()
 names = ["kappa", "leaf"] + [f"merge_d{d}" for d in range(info.leaf_depth - 1, -1, -1)] + ["finalize"]
 print(name, B, {n: round(float(v), 3) for n, v in zip(names, st)}, "total", round(float(st.sum()), 3))
