@@ -238,7 +238,7 @@ int upload_leaf_template() {
           const int W = K + NC;
           auto tri_h = [](int a) { return a * (a + 1) / 2; };
           auto symoff = [&](int i, int j) { return i >= j ? tri_h(i) + j : tri_h(j) + i; };
-          const int zs = tri_h(ks) + ks * NC + NC;   // son zero slot
+          const int zs = tri_h(ks) + ks * NC;        // son zero slot: sigma_0 (always 0, see leaf_level)
           tab.poff[ci][r] = int(vp.size());
           for (int g = 0; g < ng; ++g)
             for (int j = 0; j < W; ++j) {
@@ -335,14 +335,6 @@ __device__ __forceinline__ double submean_inv_area(int code, double h) {
   return 1.0 / (double((((code >> 5) & 31) - (code & 31)) * (((code >> 15) & 31) - ((code >> 10) & 31))) * h * h);
 }
 
-// Levels 6 and 5 of the leaf condensed directly per 2x4-cell node (HDD_LEAF_UNFUSED
-// restores the register 2x2 base + shared-memory level 5).
-#ifdef HDD_LEAF_UNFUSED
-constexpr bool kLeafFused56 = false;
-#else
-constexpr bool kLeafFused56 = true;
-#endif
-
 // Gather programs: read through L1 (__ldg; the tables of a class are shared by every
 // CTA) — no staging buffers, so the 2-column class fits 3 CTAs per SM and the
 // 8-column class 2 (measured: C2 leaf 7.01 -> 6.11 ms, C4 26.8 -> 22.8 ms against
@@ -353,41 +345,49 @@ constexpr bool kLeafStage = true;
 constexpr bool kLeafStage = false;
 #endif
 
-// Leaf smem layout (doubles): col info [32] | bufA[bufa] (even-level outputs) |
-// bufB[bufb] (odd-level outputs; kappa[512] and f[289] alias its head until level 5
-// writes it) | panel[pand] | gather programs: panel program of even levels [tp0] | of
-// odd levels [tp1] | update program [tu].  The panel program of level r-1 is
-// prefetched (cp.async) while level r eliminates; the update program of level r
-// streams in behind level r's gather and factorization.
+// Leaf smem layout (doubles): col info [hdr] | arena [T] | gather programs (only with
+// HDD_LEAF_STAGE_ITEMS: panel program of even levels [tp0] | of odd levels [tp1] | update
+// program [tu]).  In the arena the level outputs ping-pong between its two ends: even
+// levels write at the bottom, odd levels (and the fused 6+5 output) at the top, and a
+// level's interface panel sits right above the bottom region.  kappa[512] and f[289]
+// occupy the bottom until level 4 writes it.  T is the largest (input + output + panel)
+// of any level, so the 2-column class fits four CTAs per SM.
+// A node block is [Psi packed tri(k) | R k x NC | sigma NC]; sigma_0 (the load column)
+// is 0 at every in-leaf level and doubles as the gather programs' zero slot.
+__host__ __device__ constexpr int leaf_node_elems(int k, int nc) { return ctri(k) + k * nc + nc; }
+// node blocks of a level sit at an odd stride (doubles): lane-per-node accesses (the fused
+// 6+5 build) hit 16 distinct 8-byte banks
+__host__ __device__ constexpr int leaf_node_stride(int k, int nc) { return leaf_node_elems(k, nc) | 1; }
+__host__ __device__ constexpr int leaf_out_elems(int r, int nc) { return (1 << r) * leaf_node_stride(leaf_shape(r).k, nc); }
+// panel row stride: DMMA-conflict-free padding where phase D runs on DMMA (ng > 3)
+__host__ __device__ constexpr int leaf_panel_w(int r, int nc) {
+  return leaf_shape(r).ng == 3 ? leaf_shape(r).K + nc : leaf_wpad(leaf_shape(r).K + nc);
+}
+__host__ __device__ constexpr int leaf_panel_elems(int r, int nc) { return (1 << r) * leaf_shape(r).ng * leaf_panel_w(r, nc); }
+__host__ __device__ constexpr int leaf_hdr(int nc) { return (3 * nc + 1) & ~1; }   // 6 NC ints
 struct LeafSmem {
-  int bufa, bufb, pand, tp0, tp1, tu;
+  int T, hdr, tp0, tp1, tu;
 };
 static LeafSmem leaf_sizes(int ncl) {
-  const auto& T = leaf_template();
-  LeafSmem s{kLeafFused56 ? 808 : 0, kLeafFused56 ? 0 : 808, 0, 0, 0, 0};   // kappa + f alias
-  for (int r = 0; r < kLeafLevels; ++r) {
-    const int nf = 1 << r, k = T[r].k, K = T[r].K, ng = T[r].ng;
-    if (r >= 1 && r <= (kLeafFused56 ? 5 : 6)) {
-      int& b = (r & 1) ? s.bufb : s.bufa;
-      b = std::max(b, nf * (k * (k + 1) / 2 + k * ncl + ncl + 2));
-    }
-    if (r <= 5) {
-      s.pand = std::max(s.pand, nf * ng * leaf_wpad(K + ncl));
-      int& tp = (r & 1) ? s.tp1 : s.tp0;
-      if (kLeafStage) {
-        tp = std::max(tp, ng * (K + ncl));
-        s.tu = std::max(s.tu, k * (k + 1) / 2 + k * ncl);
-      }
+  const auto& Tm = leaf_template();
+  LeafSmem s{808 + leaf_out_elems(5, ncl), leaf_hdr(ncl), 0, 0, 0};   // kappa + f below the fused 6+5 output
+  for (int r = 0; r <= 4; ++r)
+    s.T = std::max(s.T, leaf_out_elems(r, ncl) + leaf_out_elems(r + 1, ncl) + leaf_panel_elems(r, ncl));
+  for (int r = 0; r < kLeafLevels && r <= 5; ++r) {
+    const int k = Tm[r].k, K = Tm[r].K, ng = Tm[r].ng;
+    int& tp = (r & 1) ? s.tp1 : s.tp0;
+    if (kLeafStage) {
+      tp = std::max(tp, ng * (K + ncl));
+      s.tu = std::max(s.tu, k * (k + 1) / 2 + k * ncl);
     }
   }
-  for (int* v : {&s.bufa, &s.bufb, &s.pand, &s.tp0, &s.tp1, &s.tu}) *v = (*v + 1) & ~1;
+  for (int* v : {&s.T, &s.tp0, &s.tp1, &s.tu}) *v = (*v + 1) & ~1;
   return s;
 }
-constexpr int kLeafHdr = 32;
 
 size_t leaf_smem_bytes(int ncl) {
   const LeafSmem s = leaf_sizes(ncl);
-  return sizeof(double) * (size_t(kLeafHdr) + s.bufa + s.bufb + s.pand + s.tp0 + s.tp1 + s.tu);
+  return sizeof(double) * (size_t(s.hdr) + s.T + s.tp0 + s.tp1 + s.tu);
 }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -494,10 +494,11 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
   constexpr LeafLevelShape S = leaf_shape(R);
   constexpr int K = S.K, k = S.k, ng = S.ng, ks = S.ks;
   constexpr int nf = 1 << R;
-  constexpr int Sin = ctri(ks) + ks * NC + NC + 2;    // +2: zero slot at [Sin - 2] (even stride)
-  constexpr int Sout = ctri(k) + k * NC + NC + 2;
+  constexpr int Sin = leaf_node_stride(ks, NC);
+  constexpr int Sout = leaf_node_stride(k, NC);
+  constexpr int Zin = ctri(ks) + ks * NC;              // zero slot: the sons' sigma_0
   constexpr int WL = K + NC;                // logical panel row (program layout)
-  constexpr int W = leaf_wpad(WL);          // padded panel row stride
+  constexpr int W = leaf_panel_w(R, NC);    // panel row stride
   constexpr int WX = k + NC;
   constexpr int NT = NTH, NW = NTH / 32;
   constexpr int gsz = nf >= NW ? 1 : NW / nf;
@@ -540,7 +541,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 #pragma unroll
       for (int u = 0; u < UT; ++u) {
         const int t = t0 + u * NT;
-        LeafItemP it = LeafItemP{int16_t(Sin - 2), int16_t(Sin - 2), -1, 0};
+        LeafItemP it = LeafItemP{int16_t(Zin), int16_t(Zin), -1, 0};
         if (t < NPI) {
           if constexpr (kLeafStage) it = prog[t];
           else it = load_item(prog, t);
@@ -619,7 +620,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
         const int t = t0 + u * nth;
-        LeafItemU it = LeafItemU{0, 0, int16_t(Sin - 2), int16_t(Sin - 2)};
+        LeafItemU it = LeafItemU{0, 0, int16_t(Zin), int16_t(Zin)};
         if (t < NUI) {
           if constexpr (kLeafStage) it = uprog[t];
           else it = load_item(uprog, t);
@@ -876,8 +877,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 #pragma unroll
         for (int g = 0; g < ng; ++g) sg = fma(P[g * W + K], P[g * W + K + c], sg);
       double* o = out + q * Sout;
-      o[ctri(k) + k * NC + c] = sg;
-      if (c < 2) o[Sout - 2 + c] = 0.0;    // zero slot
+      o[ctri(k) + k * NC + c] = sg;        // sigma_0 = 0 + 0: the next level's zero slot
     }
   }
   if constexpr (R == 0) fence_proxy_async_smem();   // the Psi block is read by the bulk copy below
@@ -997,7 +997,6 @@ template <int A, int NC, bool SUB>
 __device__ __forceinline__ void l56_row(const L56Node& n, const double (&M)[6], double* __restrict__ out,
                                         const int* ctype, const int* br, const int* bq, int q) {
   constexpr int k5 = 12;
-  constexpr int S5 = ctri(k5) + k5 * NC + NC + 2;
   constexpr int xa = l56_bx(A), ya = l56_by(A), ga = l56_bg(A);
   constexpr int il = l56_left(A), idn = l56_down(A);
   // M = [[M0 M1 M2] [M1 M3 M4] [M2 M4 M5]]
@@ -1052,7 +1051,6 @@ __device__ __forceinline__ void l56_row(const L56Node& n, const double (&M)[6], 
       out[ctri(k5) + k5 * NC + c] = sg;
     }
   }
-  if constexpr (A == 0) { out[S5 - 2] = 0.0; out[S5 - 1] = 0.0; }   // zero slot
 }
 
 // One CTA per (16x16-cell leaf, sample).  Level 6 (2x2-cell blocks) is built per
@@ -1061,7 +1059,7 @@ __device__ __forceinline__ void l56_row(const L56Node& n, const double (&M)[6], 
 // gather the interface panel, Gauss-Jordan interface inverse (warp per node),
 // Y = A22^-1 [A21 | R], then the Schur update A11 - A21^T Y on DMMA tiles.
 template <int NC, int NTH, bool SUB>   // SUB: sub-leaf mean columns or Dirichlet data present
-__global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && kLeafFused56))) ? 3 : 2) leaf2_kernel(DevPlan p, const int* __restrict__ order, LeafSmem ls,
+__global__ void __launch_bounds__(NTH, kLeafStage ? 2 : (NC == 2 ? 4 : (NC == 4 ? 3 : 2))) leaf2_kernel(DevPlan p, const int* __restrict__ order, LeafSmem ls,
                                                        int B) {
   extern __shared__ __align__(16) double sm[];
   const int leaf = order[blockIdx.x];
@@ -1073,17 +1071,16 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
   const DevLeaf& L = p.leaves[leaf];
   if (pass > 0 && 1 + (NC - 1) * pass >= L.ncols) return;   // no columns left for this pass
   int* cinfo = reinterpret_cast<int*>(sm);                       // ctype, br, bq, bg, fslot
-  double* bufA = sm + kLeafHdr;
-  double* bufB = bufA + ls.bufa;
-  double* pan = bufB + ls.bufb;
-  uint64_t* tab0 = reinterpret_cast<uint64_t*>(pan + ls.pand);   // panel programs, even levels
+  double* arena = sm + leaf_hdr(NC);
+  const int T = ls.T;
+  // level r output: even r at the bottom of the arena, odd r at the top; level r's panel
+  // right above the bottom region (its output for even r, its input for odd r)
+  auto lout = [&](int r) -> double* { return (r & 1) ? arena + T - leaf_out_elems(r, NC) : arena; };
+  auto lpan = [&](int r) -> double* { return arena + leaf_out_elems((r & 1) ? r + 1 : r, NC); };
+  uint64_t* tab0 = reinterpret_cast<uint64_t*>(arena + T);      // panel programs, even levels
   uint64_t* tab1 = tab0 + ls.tp0;                                // odd levels
   uint64_t* tabU = tab1 + ls.tp1;
-#ifdef HDD_LEAF_UNFUSED
-  double* kap = bufB;                                             // [512], aliases bufB until level 5
-#else
-  double* kap = bufA;                                             // [512], aliases bufA until level 4
-#endif
+  double* kap = arena;                                            // [512], the bottom until level 4
   double* fl = kap + 512;                                         // [289]
   const int N = p.N;
   {
@@ -1120,96 +1117,11 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
   const int* bq = cinfo + 2 * NC;
   const double h2_6 = p.h * p.h / 6.0;
 
-#ifdef HDD_LEAF_UNFUSED
-  // ---------------- level 6: 2x2-cell blocks in registers ----------------
-  {
-    constexpr int k6 = 8;
-    const int S6 = tri(k6) + k6 * NC + NC + 2;
-    for (int q = tid; q < 64; q += NT) {
-      const int o = c_orig[63 + q];
-      const int x0 = o & 255, y0 = o >> 8;
-      double A[45];
-      double rl[9], rm[9];
-#pragma unroll
-      for (int i = 0; i < 45; ++i) A[i] = 0.0;
-#pragma unroll
-      for (int i = 0; i < 9; ++i) { rl[i] = 0.0; rm[i] = 0.0; }
-#pragma unroll
-      for (int cy = 0; cy < 2; ++cy)
-#pragma unroll
-        for (int cx = 0; cx < 2; ++cx) {
-          const double k0 = kap[(x0 + cx) * 32 + 2 * (y0 + cy)];
-          const double k1 = kap[(x0 + cx) * 32 + 2 * (y0 + cy) + 1];
-          const int a = cy * 3 + cx, b = a + 1, c = a + 3, d = a + 4;
-          // P1 (a,b,d) and P2 (a,d,c) of fem.py:126-145
-          A[tri(a) + a] += fma(k0, 0.5, k1 * 0.5);
-          A[tri(b) + b] += k0;
-          A[tri(c) + c] += k1;
-          A[tri(d) + d] += fma(k0, 0.5, k1 * 0.5);
-          A[tri(b) + a] += -0.5 * k0;
-          A[tri(d) + b] += -0.5 * k0;
-          A[tri(c) + a] += -0.5 * k1;
-          A[tri(d) + c] += -0.5 * k1;
-          const int nx = x0 + cx, ny = y0 + cy;
-          const double w2 = h2_6 + h2_6;
-          if (p.f) {
-            rl[a] += w2 * fl[ny * 17 + nx];
-            rl[b] += h2_6 * fl[ny * 17 + nx + 1];
-            rl[c] += h2_6 * fl[(ny + 1) * 17 + nx];
-            rl[d] += w2 * fl[(ny + 1) * 17 + nx + 1];
-          } else {
-            rl[a] += w2; rl[b] += h2_6; rl[c] += h2_6; rl[d] += w2;
-          }
-          // mean column carried as the area integral (coefficient 1 at every
-          // in-leaf merge); rescaled by 1/|leaf| at the leaf output
-          rm[a] += w2; rm[b] += h2_6; rm[c] += h2_6; rm[d] += w2;
-        }
-      // eliminate the centre node 4
-      const double dpiv = A[tri(4) + 4];
-      if (!(dpiv > 0.0)) record_error(p, HDD_ERR_NUMERICAL, s, inleaf_ref_id(L.ref_id, 6, q));
-      const double inv = 1.0 / sqrt(dpiv);
-      double xv[9];
-#pragma unroll
-      for (int n = 0; n < 9; ++n) xv[n] = (n == 4) ? 0.0 : (n < 4 ? A[tri(4) + n] : A[tri(n) + 4]) * inv;
-      double* out = bufA + q * S6;
-      constexpr int P8[8] = {0, 1, 2, 3, 5, 6, 7, 8};
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int jj = 0; jj <= i; ++jj) out[tri(i) + jj] = fma(-xv[P8[i]], xv[P8[jj]], A[tri(P8[i]) + P8[jj]]);
-      double v[NC];
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const int ct = ctype[c];
-        double rc4 = ct == 0 ? rl[4] : (ct == 1 ? rm[4] : 0.0);
-        if (SUB && ct >= kSubMeanCode) rc4 = h2_6 * submean_weight(ct, x0 + 1, y0 + 1, x0, x0 + 2, y0, y0 + 2);
-        if (br[c] == 6 && bq[c] == q) rc4 += 1.0;
-        v[c] = rc4 * inv;
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const int ct = ctype[c];
-          double rb = ct == 0 ? rl[P8[i]] : (ct == 1 ? rm[P8[i]] : 0.0);
-          if (SUB && ct >= kSubMeanCode)
-            rb = h2_6 * submean_weight(ct, x0 + P8[i] % 3, y0 + P8[i] / 3, x0, x0 + 2, y0, y0 + 2);
-          out[tri(k6) + i * NC + c] = fma(-xv[P8[i]], v[c], rb);
-        }
-#pragma unroll
-      for (int c = 0; c < NC; ++c) out[tri(k6) + k6 * NC + c] = c == 0 ? 0.0 : v[0] * v[c];
-      out[S6 - 2] = 0.0;
-      out[S6 - 1] = 0.0;
-    }
-  }
-  __syncthreads();
-
-#else
   // ---------------- levels 6 + 5 fused: 2x4-cell nodes condensed directly ----------------
   // (l56_row): lane = node (32 nodes), warp w = boundary rows w and w + 8
   {
     constexpr int k5 = 12;
-    constexpr int S5 = ctri(k5) + k5 * NC + NC + 2;
+    constexpr int S5 = leaf_node_stride(k5, NC);
     static_assert(NTH == 256, "8 warps x 32 nodes");
     const int q = tid & 31, wid = tid >> 5;
     const int o = c_orig[31 + q];
@@ -1229,7 +1141,7 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
     const double rdet = 1.0 / det;
     const double M[6] = {(ic * ie - idd * idd) * rdet, -ib * ie * rdet, ib * idd * rdet,
                          ia * ie * rdet, -ia * idd * rdet, p1 * rdet};
-    double* out = bufB + q * S5;
+    double* out = lout(5) + q * S5;
     switch (wid) {   // warp-uniform
       case 0: l56_row<0, NC, SUB>(n, M, out, ctype, br, bq, q); l56_row<8, NC, SUB>(n, M, out, ctype, br, bq, q); break;
       case 1: l56_row<1, NC, SUB>(n, M, out, ctype, br, bq, q); l56_row<9, NC, SUB>(n, M, out, ctype, br, bq, q); break;
@@ -1242,18 +1154,14 @@ __global__ void __launch_bounds__(NTH, (!kLeafStage && (NC == 2 || (NC == 4 && k
     }
   }
   __syncthreads();
-#endif
 
   LEAF_TICK(1);
   // ---------------- levels 5..0 in shared memory ----------------
-#ifdef HDD_LEAF_UNFUSED
-  leaf_level<5, NC, NTH>(p, bufA, bufB, pan, cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
-#endif
-  leaf_level<4, NC, NTH>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
-  leaf_level<3, NC, NTH>(p, bufA, bufB, pan, cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
-  leaf_level<2, NC, NTH>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
-  leaf_level<1, NC, NTH>(p, bufA, bufB, pan, cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
-  leaf_level<0, NC, NTH, SUB>(p, bufB, bufA, pan, cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
+  leaf_level<4, NC, NTH>(p, lout(5), lout(4), lpan(4), cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
+  leaf_level<3, NC, NTH>(p, lout(4), lout(3), lpan(3), cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
+  leaf_level<2, NC, NTH>(p, lout(3), lout(2), lpan(2), cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
+  leaf_level<1, NC, NTH>(p, lout(2), lout(1), lpan(1), cinfo, leaf, s, L.ref_id, tab1, tab0, tabU);
+  leaf_level<0, NC, NTH, SUB>(p, lout(1), lout(0), lpan(0), cinfo, leaf, s, L.ref_id, tab0, tab1, tabU);
   if (tid == 0) bulk_wait_read0();   // the Psi bulk store has read its shared memory
   LEAF_TICK(63);
 }

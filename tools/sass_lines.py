@@ -26,11 +26,20 @@ rows = list(csv.reader(gzip.open(cap, "rt")))
 hdr = rows[1]
 data = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
 assert len(data) == len(inst), (len(data), len(inst))
-ex, st = collections.Counter(), collections.Counter()
+ex, st, wf, wi = collections.Counter(), collections.Counter(), collections.Counter(), collections.Counter()
 for d, (ln, _) in zip(data, inst):
     ex[ln] += int(d["Instructions Executed"] or 0)
     st[ln] += int(d["Warp Stall Sampling (All Samples)"] or 0)
+    wf[ln] += int(d.get("L1 Wavefronts Shared") or 0)
+    wi[ln] += int(d.get("L1 Wavefronts Shared Ideal") or 0)
 te, ts = sum(ex.values()), sum(st.values())
+tw = max(1, sum(wf.values()))
+if len(sys.argv) > 5 and sys.argv[5] == "smem":   # rank by shared-memory wavefronts
+    src = (Path(__file__).resolve().parents[1] / "paper_1708_02207_b200" / "csrc" / "hdd_kernels.cu").read_text().splitlines()
+    print(f"{tw} shared wavefronts ({sum(wi.values())} ideal)")
+    for ln, c in sorted(wf.items(), key=lambda kv: -kv[1])[:top]:
+        print(f"{100 * c / tw:5.1f} wf  ideal {100 * wi[ln] / tw:5.1f}  L{ln}: {src[ln - 1].strip()[:95] if ln else '?'}")
+    sys.exit(0)
 src = (Path(__file__).resolve().parents[1] / "paper_1708_02207_b200" / "csrc" / "hdd_kernels.cu").read_text().splitlines()
 print(f"{te} warp instructions, {ts} stall samples")
 for ln, c in sorted(ex.items(), key=lambda kv: -(kv[1] / te + st[kv[0]] / ts))[:top]:
