@@ -951,8 +951,14 @@ struct L56Node {
   const double* fl;     // nodal f of the leaf (17 x 17) or null
   int ox, oy;
   double h2_6, h2;
-  __device__ __forceinline__ double k0(int cx, int cy) const { return kap[(ox + cx) * 32 + 2 * (oy + cy)]; }
-  __device__ __forceinline__ double k1(int cx, int cy) const { return kap[(ox + cx) * 32 + 2 * (oy + cy) + 1]; }
+  // kappa rows are rotated by (x >> 1) & 7 doubles (leaf2_kernel's load): the 32 nodes'
+  // lane-parallel reads spread over the banks
+  __device__ __forceinline__ double k0(int cx, int cy) const {
+    return kap[(ox + cx) * 32 + ((2 * (oy + cy) + (ox >> 1)) & 31)];
+  }
+  __device__ __forceinline__ double k1(int cx, int cy) const {
+    return kap[(ox + cx) * 32 + ((2 * (oy + cy) + 1 + (ox >> 1)) & 31)];
+  }
   static __device__ __forceinline__ bool in_(int cx, int cy) { return cx >= 0 && cx < 2 && cy >= 0 && cy < 4; }
   __device__ __forceinline__ double Dl(int x, int y) const {
     double d = 0.0;
@@ -1087,7 +1093,7 @@ __global__ void __launch_bounds__(NTH, kLeafStage ? 2 : (NC == 2 ? 4 : (NC == 4 
     const double* kb = p.kappa + int64_t(s) * 2 * N * N;
     for (int t = tid; t < 512; t += NT) {
       const int x = t >> 5, r = t & 31;
-      cp_async8(kap + t, kb + 2 * (int64_t(L.i0 + x) * N + L.j0) + r);
+      cp_async8(kap + x * 32 + ((r + ((x >> 1) & 7)) & 31), kb + 2 * (int64_t(L.i0 + x) * N + L.j0) + r);
     }
     cp_async_commit();
     stage_panel_program<5, NC, NTH>(tab1);
