@@ -122,7 +122,13 @@ static int upload(HddPlan* pl, const std::vector<T>& v, const T** out) {
 
 // panel row stride: the smallest ld >= w with ld = 8 (mod 16) doubles (conflict-free
 // DMMA fragments of 4 rows x 8 columns)
-static int panel_ld(int w) { return w + ((24 - (w & 15)) & 15); }
+// panel row stride: = 4 (mod 8) doubles, so the DMMA operand fragments (4 rows x 8
+// consecutive doubles, one 16-lane half-warp = 4 rows x 4 columns) hit 16 distinct 8-byte
+// banks; HDD_PANEL_LD8=1 restores the earlier = 8 (mod 16) stride (A/B hook)
+static int panel_ld(int w) {
+  static const bool ld8 = std::getenv("HDD_PANEL_LD8") && std::getenv("HDD_PANEL_LD8")[0] == '1';
+  return ld8 ? w + ((24 - (w & 15)) & 15) : w + ((12 - (w & 7)) & 7);
+}
 
 static int setup_device(HddPlan* pl, int max_batch) {
   Plan& P = pl->plan;

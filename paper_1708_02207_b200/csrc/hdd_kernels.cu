@@ -1236,8 +1236,20 @@ __device__ __forceinline__ void warp_gemm_tn(double (&acc)[FM][FN][2], const dou
 }
 
 constexpr int kLB = 32;     // elimination block (rows)
+#ifdef HDD_LDS8
 constexpr int kLds = 72;    // smem leading dim for 64-wide tiles (= 8 mod 16)
 constexpr int kLdd = 40;    // smem leading dim for 32-wide tiles (= 8 mod 16)
+#else
+// = 4 or 12 (mod 16): a half-warp's DMMA fragment (4 rows x 4 columns) hits 16 distinct
+// 8-byte banks (= 8 (mod 16) put rows 0 and 2 on the same banks)
+constexpr int kLds = 76;    // smem leading dim for 64-wide tiles (+ 8 folded R columns)
+constexpr int kLdd = 36;    // smem leading dim for 32-wide tiles
+#endif
+#ifdef HDD_LDS8
+constexpr int kLwPad = 8;
+#else
+constexpr int kLwPad = 12;  // elimination chunk rows: LW + 12 = 12 (mod 16)
+#endif
 
 __device__ __forceinline__ int upper_ngp(const DevUpper& U) { return (U.ng + U.nb - 1) / U.nb * U.nb; }
 
@@ -2052,7 +2064,7 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
 // staged rows per step kLH
 constexpr int kLH = 16;
 __host__ __device__ constexpr size_t l_region(int lw) {
-  const size_t lws = size_t(lw) + 8;
+  const size_t lws = size_t(lw) + kLwPad;
   const size_t stream = 2 * size_t(kLH) * (kLdd + lws);                 // 2 x (A chunk | B chunk)
   const size_t ll = 2 * 32 * kLdd + (stream > 32 * lws ? stream : 32 * lws);
   const size_t epi = 4 * kEC * kLds;                                     // Schur epilogue chunks
@@ -2114,7 +2126,7 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
     double* LsB = sm;                        // [32][kLdd] factor scratch
     double* LiB = sm + 32 * kLdd;            // [32][kLdd] L_bb^-1 (transposed)
     double* St = sm + 2 * 32 * kLdd;         // stream buffers / T tile [32][kLWs]
-    constexpr int kLW = LW, kLWs = LW + 8;
+    constexpr int kLW = LW, kLWs = LW + kLwPad;
     constexpr int SB = kLH * (kLdd + kLWs);
     constexpr int FN = kLW / 32;
     const int gq = lane & 3, gr = lane >> 2;
