@@ -2712,6 +2712,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
       if (live) {
         const int r = R[i];
         const int tr = tri(r);
+        #pragma unroll 4   // the block reads of 4 iterations in flight before their FMAs
         for (int j = jg; j < Q_; j += JG) {
           const int c = Cc[j];
           const double a = r >= c ? psi[tr + c] : psi[tri(c) + r];
@@ -2826,6 +2827,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
       if (j < Q_) {
         const int c = Cc[j];
         const int tc = tri(c);
+        #pragma unroll 4   // the block reads of 4 iterations in flight before their FMAs
         for (int i = ig; i < P_; i += 4) {
           const int r = R[i];
           const double x = r >= c ? psi[tri(r) + c] : psi[tc + r];
@@ -2938,6 +2940,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
         int pvt[LW];
 #pragma unroll
         for (int u = 0; u < LW; ++u) pvt[u] = u < kk ? s_piv[u] : 0;
+        #pragma unroll 4   // the block reads of 4 iterations in flight before their FMAs
         for (int i = ig; i < P_; i += 4) {
           const int r = R[i];
           const double x = r >= c ? psi[tri(r) + c] : psi[tc + r];
