@@ -295,6 +295,14 @@ int hdd_debug_merge_clocks(long long* out);
  * 72-column wide sketch since the plan was created (0 otherwise). */
 int hdd_debug_lowrank_wide(HddPlan* plan, int64_t* total);
 
+/* Which kernel(s) the merge of tree depth `depth` launches for a sub-batch of B
+ * samples, as the ncu launch list names them (e.g. "merge_l_kernel<3,64>", or
+ * "assemble_l_kernel+merge_l_kernel<2,128>+schur_l_kernel" on the split tier-L
+ * depths); depth = -1: the kernel-leaf launch.  Used by bench.py to group the
+ * CUDA-event stage times by kernel (reference: one `schur_eliminate` call per
+ * node, hdd.py:241-277).  Returns HDD_ERR_USAGE for a depth without nodes. */
+int hdd_plan_stage_kernel(const HddPlan* plan, int32_t depth, int32_t B, char* buf, int32_t cap);
+
 const char* hdd_version(void);
 
 #ifdef __cplusplus

@@ -119,6 +119,7 @@ EXPORTS = {
                                             C.c_void_p, C.c_void_p]),
     "hdd_solve_subdomain_batch_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(HddRhs),
                                                  C.c_void_p]),
+    "hdd_plan_stage_kernel": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.c_int32]),
     "hdd_version": (C.c_char_p, []),
 }
 

@@ -657,6 +657,35 @@ int hdd_debug_merge_clocks(long long* out) { return read_merge_clocks(out); }
 
 const char* hdd_version(void) { return "hdd_b200 0.1 (sm_100a)"; }
 
+int hdd_plan_stage_kernel(const HddPlan* pl, int32_t depth, int32_t B, char* buf, int32_t cap) {
+  if (!pl || !buf || cap <= 0 || pl->device < 0) return HDD_ERR_USAGE;
+  const Plan& P = pl->plan;
+  std::string name;
+  if (depth < 0) {
+    if (P.tiny) name = "tiny_kernel";
+    else {
+      const bool sub = pl->dev.has_submean || pl->dev.leaf_g;
+      for (int c = 0; c < 3; ++c)
+        if (pl->dev.leaf_class_count[c] > 0)
+          name += std::string(name.empty() ? "" : "+") + "leaf2_kernel<" + (c == 0 ? "2" : (c == 1 ? "4" : "8")) +
+                  ",256," + (sub ? "true" : "false") + ">";
+    }
+  } else {
+    if (depth >= int(P.upper_by_depth.size()) || P.upper_by_depth[depth].empty()) return HDD_ERR_USAGE;
+    DevPlan Dd = pl->dev;
+    Dd.schur_split = (pl->depth_tier[depth] && pl->dev.schur_split && pl->depth_split[depth]) ? 1 : 0;
+    const int v = merge_variant(Dd, int(P.upper_by_depth[depth].size()), B, pl->depth_tier[depth],
+                                pl->depth_smem[depth], depth);
+    name = merge_variant_name(v);
+    if (Dd.schur_split) {
+      name = "assemble_l_kernel+" + name;
+      if (pl->tm_tiles[depth] > 0) name += "+schur_l_kernel";
+    }
+  }
+  std::snprintf(buf, size_t(cap), "%s", name.c_str());
+  return HDD_OK;
+}
+
 int hdd_create_error(HddError* out) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (out) *out = g_create_err;

@@ -141,6 +141,8 @@ struct DevPlan {
 // launchers (hdd_kernels.cu); all return cudaError_t of the launch
 cudaError_t launch_kappa(const DevPlan& p, const double* Z, int B, double* kappa, cudaStream_t s);
 cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_out);
+int merge_variant(const DevPlan& p, int n_nodes, int B, int tier, size_t smem, int slot);
+const char* merge_variant_name(int v);
 cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
                          int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s, int slot = -1);
 size_t merge_m2_smem_bytes(int ngp, int ldp, int K, int nc);

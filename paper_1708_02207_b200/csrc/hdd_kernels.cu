@@ -2509,46 +2509,69 @@ cudaError_t launch_schur_l(const DevPlan& p, const DevUpper* nodes_dev, const CU
 int schur_l_tiles(int k, int nc, int ngp) { return schur_l_tiles_dev(k, nc, (k + ngp) & 1); }
 int schur_l_box_rows() { return kSR; }
 
+// Which merge kernel instantiation a depth launches (shared by launch_merge and the
+// bench's per-kernel grouping, hdd_plan_stage_kernel): 0..3 merge_m2_kernel<8,256,2> /
+// <8,512,1> / <8,256,4> / <8,256,3>, 4 merge_l_kernel<3,64>, 5 merge_l_kernel<2,128>.
+int merge_variant(const DevPlan& p, int n_nodes, int B, int tier, size_t smem, int slot) {
+  if (tier == 0) {
+    // occupancy by panel size: 1 x 512 threads for big panels; 4 x 256 threads (64
+    // registers) when 4 panels fit an SM, else 3 x 256 (80 registers; measured)
+    static const int force_minb = std::getenv("HDD_M2_MINB") ? std::atoi(std::getenv("HDD_M2_MINB")) : 0;   // A/B hook
+    if ((smem > 100 * 1024 && smem <= 113 * 1024) || (force_minb == 2 && smem <= 113 * 1024)) return 0;
+    if (smem > 100 * 1024) return 1;
+    if (smem <= 55 * 1024 && force_minb != 3) return 2;
+    return 3;
+  }
+  // 3 CTAs/SM (80 registers, some spills) pays when the launch has enough CTAs to
+  // fill them and the panel region fits three per SM (measured: C4 depths 3-5 -12 %)
+  // (the 2-CTA/SM variant has the smem for 128-column elimination chunks: twice the
+  // DMMA work per staged A operand, measured -18 % on the C5 root)
+  // (split depths below the root run only the elimination here: the 128-column chunks of
+  // the 2-CTA/SM variant win there, measured C5 d2 104.8 -> 99.1 ms, d1 60.3 -> 54.0 ms
+  // per 512; the root (slot = depth 0) keeps 3 CTAs/SM: C3 3.15 vs 3.53 ms)
+  if ((!p.schur_split || slot == 0) && int64_t(n_nodes) * B >= 148 * 3 * 2 && smem <= 74 * 1024) return 4;
+  return 5;
+}
+
+const char* merge_variant_name(int v) {
+  static const char* names[] = {"merge_m2_kernel<8,256,2>", "merge_m2_kernel<8,512,1>", "merge_m2_kernel<8,256,4>",
+                                "merge_m2_kernel<8,256,3>", "merge_l_kernel<3,64>",     "merge_l_kernel<2,128>"};
+  return names[v];
+}
+
 cudaError_t launch_merge(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int B, double* ws,
                          int64_t ws_stride, int tier, int max_rows, size_t smem, int nb, cudaStream_t s, int slot) {
   (void)max_rows;
   (void)nb;
   cudaError_t e;
   dim3 grid(B, n_nodes);
-  if (tier == 0) {
-    // occupancy by panel size: 1 x 512 threads for big panels; 4 x 256 threads (64
-    // registers) when 4 panels fit an SM, else 3 x 256 (80 registers; measured)
-    static const int force_minb = std::getenv("HDD_M2_MINB") ? std::atoi(std::getenv("HDD_M2_MINB")) : 0;   // A/B hook
-    if ((smem > 100 * 1024 && smem <= 113 * 1024) || (force_minb == 2 && smem <= 113 * 1024)) {
+  switch (merge_variant(p, n_nodes, B, tier, smem, slot)) {
+    case 0:
       e = cudaFuncSetAttribute(merge_m2_kernel<8, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
       merge_m2_kernel<8, 256, 2><<<grid, 256, smem, s>>>(p, nodes_dev, slot);
-    } else if (smem > 100 * 1024) {
+      break;
+    case 1:
       e = cudaFuncSetAttribute(merge_m2_kernel<8, 512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
       merge_m2_kernel<8, 512, 1><<<grid, 512, smem, s>>>(p, nodes_dev, slot);
-    } else if (smem <= 55 * 1024 && force_minb != 3) {
+      break;
+    case 2:
       e = cudaFuncSetAttribute(merge_m2_kernel<8, 256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
       merge_m2_kernel<8, 256, 4><<<grid, 256, smem, s>>>(p, nodes_dev, slot);
-    } else {
+      break;
+    case 3:
       e = cudaFuncSetAttribute(merge_m2_kernel<8, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
       merge_m2_kernel<8, 256, 3><<<grid, 256, smem, s>>>(p, nodes_dev, slot);
-    }
-  } else {
-    // 3 CTAs/SM (80 registers, some spills) pays when the launch has enough CTAs to
-    // fill them and the panel region fits three per SM (measured: C4 depths 3-5 -12 %)
-    // (the 2-CTA/SM variant has the smem for 128-column elimination chunks: twice the
-    // DMMA work per staged A operand, measured -18 % on the C5 root)
-    // (split depths below the root run only the elimination here: the 128-column chunks of
-    // the 2-CTA/SM variant win there, measured C5 d2 104.8 -> 99.1 ms, d1 60.3 -> 54.0 ms
-    // per 512; the root (slot = depth 0) keeps 3 CTAs/SM: C3 3.15 vs 3.53 ms)
-    if ((!p.schur_split || slot == 0) && int64_t(n_nodes) * B >= 148 * 3 * 2 && smem <= 74 * 1024) {
+      break;
+    case 4:
       e = cudaFuncSetAttribute(merge_l_kernel<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e != cudaSuccess) return e;
       merge_l_kernel<3, 64><<<grid, 256, smem, s>>>(p, nodes_dev, ws, ws_stride, slot);
-    } else {
+      break;
+    default: {
       const size_t sm2 = smem + sizeof(double) * (l_region(128) - kLRegion);
       e = cudaFuncSetAttribute(merge_l_kernel<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2));
       if (e != cudaSuccess) return e;
