@@ -169,8 +169,12 @@ __device__ long long g_leaf_clk[64];
 #ifndef HDD_PROFILE_TICKS
 #define LEAF_TICK(i) do { } while (0)
 #else
+#ifndef HDD_TICK_X          // which CTA stamps (default the first; a mid-launch CTA shows the steady state)
+#define HDD_TICK_X 0
+#define HDD_TICK_Y 0
+#endif
 #define LEAF_TICK(i) \
-  do { if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) g_leaf_clk[i] = clock64(); } while (0)
+  do { if (blockIdx.x == HDD_TICK_X && blockIdx.y == HDD_TICK_Y && threadIdx.x == 0) g_leaf_clk[i] = clock64(); } while (0)
 #endif
 int read_leaf_clocks(long long* out) {
   return cudaMemcpyFromSymbol(out, g_leaf_clk, sizeof(long long) * 64) == cudaSuccess ? 0 : -1;
@@ -181,7 +185,7 @@ __device__ long long g_merge_clk[32][8];
 #define MERGE_TICK(i) do { (void)slot; } while (0)
 #else
 #define MERGE_TICK(i) \
-  do { if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && slot >= 0 && slot < 32) g_merge_clk[slot][i] = clock64(); } while (0)
+  do { if (blockIdx.x == HDD_TICK_X && blockIdx.y == HDD_TICK_Y && threadIdx.x == 0 && slot >= 0 && slot < 32) g_merge_clk[slot][i] = clock64(); } while (0)
 #endif
 int read_merge_clocks(long long* out) {
   return cudaMemcpyFromSymbol(out, g_merge_clk, sizeof(long long) * 32 * 8) == cudaSuccess ? 0 : -1;
@@ -1470,6 +1474,23 @@ __device__ __forceinline__ double gather_A(const MergeCtx& c, int a, int j) {
   if (pa1 >= 0 && pb1 >= 0) v += son_psi(c.sv[1], pa1, pb1);
   return v;
 }
+// gather_A where at most ONE son holds the pair (a, j): every pair except those of two
+// nodes shared by both sons (the ends of the interface).  One load and no add, so the
+// value is first used after the caller's DMMA loop (gather_shared tells the caller
+// whether its rows and columns can hold such a pair).
+__device__ __forceinline__ double gather_A1(const MergeCtx& c, int a, int j) {
+  const int pa0 = c.gm[a], pa1 = c.gm[c.K + a];
+  const int pb0 = c.gm[j], pb1 = c.gm[c.K + j];
+  const bool h0 = (pa0 | pb0) >= 0, h1 = (pa1 | pb1) >= 0;
+  const double* b = h0 ? c.sv[0].b : c.sv[1].b;
+  const int pi = h0 ? pa0 : pa1, pj = h0 ? pb0 : pb1;
+  const int hi = max(pi, pj), lo = min(pi, pj);
+  return (h0 || h1) ? b[tri(hi) + lo] : 0.0;
+}
+// father index a (< k) on the boundary of BOTH sons
+__device__ __forceinline__ bool gather_shared(const MergeCtx& c, int a, int k) {
+  return a < k && (c.gm[a] | c.gm[c.K + a]) >= 0;
+}
 // assembled R~(a, col)
 __device__ __forceinline__ double gather_R(const MergeCtx& c, int a, int col) {
   double v = 0.0;
@@ -1697,6 +1718,9 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
 
 
 constexpr int kEC = 16;     // tier-L epilogue: interface rows per staged chunk
+#ifndef HDD_EPI_STAGES
+#define HDD_EPI_STAGES 2    // smem buffers of the tier-L epilogue's X chunks
+#endif
 // Tier-L Schur update on 64 x 64 output tiles: the lower Psi tiles (b0 <= a0, columns
 // < k) and, when nc > 8, 64-column R tiles.  With nc <= 8 (most depths: the load column
 // and a few functionals) the R block rides on the diagonal tiles: their two strictly
@@ -1772,8 +1796,30 @@ __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const doubl
       };
       __syncthreads();
       stage(0, 0);
+#if HDD_EPI_STAGES == 3
+      if (nch > 1) stage(1, 1);
+#endif
       // the assembled A~ / R~ values of this warp's outputs, loaded ahead of the DMMAs
       double pre[4][2][2];
+      // warp-uniform: can this warp's 32 rows x 16 columns hold a pair of two nodes shared
+      // by both sons?  (two such nodes per merge: almost every warp tile takes the
+      // single-load gather)
+      const bool both = role == 1 && !is_r &&
+                        __any_sync(0xffffffffu, gather_shared(mc, a0 + m0 + lane, k)) &&
+                        __any_sync(0xffffffffu, gather_shared(mc, b0 + n0 + (lane & 15), k));
+      if (role == 1 && !is_r && !both) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int aa = a0 + m0 + 8 * i + gr;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int bb = b0 + n0 + 8 * j + 2 * gq + e;
+              pre[i][j][e] = (aa < k && bb <= aa) ? gather_A1(mc, aa, bb) : 0.0;
+            }
+        }
+      } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int aa = a0 + (role == 2 ? rm0 : m0) + 8 * i + gr;
@@ -1793,8 +1839,18 @@ __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const doubl
             pre[i][j][e] = v;
           }
       }
+      }
       double acc[4][2][2] = {};
       for (int c = 0; c < nch; ++c) {
+#if HDD_EPI_STAGES == 3
+        // three buffers, one barrier per chunk: it publishes chunk c and frees the
+        // buffer of chunk c - 1 for chunk c + 2
+        if (c + 1 < nch) cp_async_wait<1>();
+        else cp_async_wait<0>();
+        __syncthreads();
+        if (c + 2 < nch) stage(c + 2, (c + 2) % 3);
+        const double* Ea = E + (c % 3) * 2 * kEC * kLds;
+#else
         if (c + 1 < nch) {
           stage(c + 1, (c + 1) & 1);
           cp_async_wait<1>();
@@ -1803,6 +1859,7 @@ __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const doubl
         }
         __syncthreads();
         const double* Ea = E + (c & 1) * 2 * kEC * kLds;
+#endif
         const double* Eb = Ea + kEC * kLds;
         if (role == 1) {
           warp_gemm_tn<4, 2>(acc, Ea, kLds, m0, Eb, kLds, n0, kEC);
@@ -1817,7 +1874,9 @@ __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const doubl
             for (int i = 0; i < 4; ++i) dmma884(acc[i][0], av[i], bv);
           }
         }
+#if HDD_EPI_STAGES != 3
         __syncthreads();
+#endif
       }
       if (role == 0) continue;
 #pragma unroll
@@ -2067,7 +2126,7 @@ __host__ __device__ constexpr size_t l_region(int lw) {
   const size_t lws = size_t(lw) + kLwPad;
   const size_t stream = 2 * size_t(kLH) * (kLdd + lws);                 // 2 x (A chunk | B chunk)
   const size_t ll = 2 * 32 * kLdd + (stream > 32 * lws ? stream : 32 * lws);
-  const size_t epi = 4 * kEC * kLds;                                     // Schur epilogue chunks
+  const size_t epi = 2 * HDD_EPI_STAGES * kEC * kLds;                    // Schur epilogue chunks
   return epi > ll ? epi : ll;
 }
 constexpr size_t kLRegion = l_region(64);
