@@ -288,6 +288,16 @@ static int setup_device(HddPlan* pl, int max_batch) {
         d.son_off[sn] = int64_t(l) * P.leaf_elems;
       }
     }
+    {   // boundary nodes held by both sons: the two ends of the interface (fewer when an
+        // end lies on the domain boundary); their pairs get both sons' Psi entries
+      d.sh[0] = d.sh[1] = -1;
+      int nsh = 0;
+      for (int a = 0; a < U.k; ++a)
+        if (U.gmap[a] >= 0 && U.gmap[U.K + a] >= 0) {
+          if (nsh >= 2) return set_err(&pl->err, HDD_ERR_CONFIG, "more than two boundary nodes shared by both sons");
+          d.sh[nsh++] = a;
+        }
+    }
     d.gmap_off = int(gmap.size());
     gmap.insert(gmap.end(), U.gmap.begin(), U.gmap.end());
     d.parent = U.parent;

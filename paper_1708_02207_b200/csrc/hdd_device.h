@@ -26,6 +26,7 @@ struct DevUpper {
   int cmap_off;            // offset into the cmap pool: [k] father K-index of each boundary node
   int64_t fac_off, u_off;  // per-sample offsets in the factor / interface-solution buffers
   int col_off;             // offset into column pools: csrc/ccoef [nc][2], cbirth [nc]
+  int sh[2];               // father indices (< k) of the boundary nodes on BOTH sons (interface ends), -1
   int64_t ref_id;
 };
 

@@ -1447,6 +1447,7 @@ struct MergeCtx {
   const double* ccoef;   // [nc][2]
   const int32_t* cbirth; // [nc]
   int K;
+  int sh[2];             // son-shared boundary nodes (DevUpper::sh)
 };
 
 __device__ __forceinline__ MergeCtx merge_ctx(const DevPlan& p, const DevUpper& U, int s) {
@@ -1462,6 +1463,8 @@ __device__ __forceinline__ MergeCtx merge_ctx(const DevPlan& p, const DevUpper& 
   c.ccoef = p.ccoef + 2 * U.col_off;
   c.cbirth = p.cbirth + U.col_off;
   c.K = U.K;
+  c.sh[0] = U.sh[0];
+  c.sh[1] = U.sh[1];
   return c;
 }
 
@@ -1474,10 +1477,11 @@ __device__ __forceinline__ double gather_A(const MergeCtx& c, int a, int j) {
   if (pa1 >= 0 && pb1 >= 0) v += son_psi(c.sv[1], pa1, pb1);
   return v;
 }
-// gather_A where at most ONE son holds the pair (a, j): every pair except those of two
-// nodes shared by both sons (the ends of the interface).  One load and no add, so the
-// value is first used after the caller's DMMA loop (gather_shared tells the caller
-// whether its rows and columns can hold such a pair).
+// gather_A with ONE load and no add: the entry of the first son that holds the pair
+// (a, j).  Only the pairs of two nodes shared by both sons (the ends of the interface,
+// MergeCtx::sh: at most three lower pairs per node) have a second term; the Schur
+// epilogues add it afterwards (shared_pair_fixup), so the gathered value is first used
+// after the DMMA loop.
 __device__ __forceinline__ double gather_A1(const MergeCtx& c, int a, int j) {
   const int pa0 = c.gm[a], pa1 = c.gm[c.K + a];
   const int pb0 = c.gm[j], pb1 = c.gm[c.K + j];
@@ -1486,6 +1490,18 @@ __device__ __forceinline__ double gather_A1(const MergeCtx& c, int a, int j) {
   const int pi = h0 ? pa0 : pa1, pj = h0 ? pb0 : pb1;
   const int hi = max(pi, pj), lo = min(pi, pj);
   return (h0 || h1) ? b[tri(hi) + lo] : 0.0;
+}
+// second son's term of the son-shared pairs, added to the written output (call after
+// a CTA barrier that follows the epilogue's stores)
+__device__ __forceinline__ void shared_pair_fixup(const MergeCtx& c, double* __restrict__ out) {
+  const int t = threadIdx.x;
+  if (t < 3) {
+    int a = c.sh[t == 0 ? 0 : 1], b = c.sh[t == 2 ? 1 : 0];
+    if (a >= 0 && b >= 0) {
+      if (a < b) { const int u = a; a = b; b = u; }
+      out[tri(a) + b] += son_psi(c.sv[1], c.gm[c.K + a], c.gm[c.K + b]);
+    }
+  }
 }
 // father index a (< k) on the boundary of BOTH sons
 __device__ __forceinline__ bool gather_shared(const MergeCtx& c, int a, int k) {
@@ -1563,7 +1579,7 @@ __device__ __forceinline__ void gather_panel_row(const MergeCtx& c, int k, int n
 // Schur-update epilogue on 32 x 64 output tiles (lower-triangle Psi tiles and
 // the R columns), the assembled A~ values gathered from the sons and issued
 // before the DMMA loop; output packed-lower.
-template <bool SMEM, bool FAST = false, bool SPLIT = false>
+template <bool SMEM, bool FAST = false, bool SPLIT = false, bool G1 = false>
 __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double* __restrict__ P, int ldp, int k,
                                                int ngp, int Kp, int nc, double* __restrict__ out, double* Ea,
                                                double* Eb) {
@@ -1610,7 +1626,8 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
           for (int j = 0; j < 2; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              if constexpr (SPLIT) gather_A2(mc, aa, bc0 + 8 * j + 2 * gq + e, pre[i][j][e], pre1[i][j][e]);
+              if constexpr (G1) { pre[i][j][e] = gather_A1(mc, aa, bc0 + 8 * j + 2 * gq + e); pre1[i][j][e] = 0.0; }
+              else if constexpr (SPLIT) gather_A2(mc, aa, bc0 + 8 * j + 2 * gq + e, pre[i][j][e], pre1[i][j][e]);
               else { pre[i][j][e] = gather_A(mc, aa, bc0 + 8 * j + 2 * gq + e); pre1[i][j][e] = 0.0; }
             }
         }
@@ -1655,11 +1672,19 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
           double v = 0.0, v1 = 0.0;
           if (aa < k && bb < ow) {
             if constexpr (SPLIT) {
-              if (bb < k) { if (bb <= aa) gather_A2(mc, aa, bb, v, v1); }
-              else gather_R2(mc, aa, bb - k, v, v1);
+              if (bb < k) {
+                if (bb <= aa) {
+                  if constexpr (G1) v = gather_A1(mc, aa, bb);
+                  else gather_A2(mc, aa, bb, v, v1);
+                }
+              } else gather_R2(mc, aa, bb - k, v, v1);
             } else {
-              if (bb < k) { if (bb <= aa) v = gather_A(mc, aa, bb); }
-              else v = gather_R(mc, aa, bb - k);
+              if (bb < k) {
+                if (bb <= aa) {
+                  if constexpr (G1) v = gather_A1(mc, aa, bb);
+                  else v = gather_A(mc, aa, bb);
+                }
+              } else v = gather_R(mc, aa, bb - k);
             }
           }
           pre[i][j][e] = v;
@@ -1713,6 +1738,10 @@ __device__ __forceinline__ void schur_epilogue(const MergeCtx& mc, const double*
           }
         }
     }
+  }
+  if constexpr (G1) {          // single-load gathers: the son-shared pairs' second term
+    __syncthreads();
+    shared_pair_fixup(mc, out);
   }
 }
 
@@ -2112,7 +2141,10 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
     out[tk + k * nc + c] = v;
   }
   MERGE_TICK(4);
-  schur_epilogue<true, MINB <= 3, MINB <= 2>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
+#ifndef HDD_G1_MINB_LO
+#define HDD_G1_MINB_LO 3   // tier-M instantiations (by CTAs/SM) whose epilogue uses the single-load gather
+#endif
+  schur_epilogue<true, MINB <= 3, MINB <= 2, (MINB <= 3 && MINB >= HDD_G1_MINB_LO)>(mc, P, ldp, k, ngp, Kp, nc, out, nullptr, nullptr);
   MERGE_TICK(5);
 }
 
