@@ -371,6 +371,7 @@ __host__ __device__ constexpr int leaf_panel_elems(int r, int nc) { return (1 <<
 __host__ __device__ constexpr int leaf_hdr(int nc) { return (3 * nc + 1) & ~1; }   // 6 NC ints
 struct LeafSmem {
   int T, hdr, tp0, tp1, tu;
+  int group_doubles;       // smem doubles per (leaf, sample) group of a CTA (HDD_LEAF_G)
 };
 static LeafSmem leaf_sizes(int ncl) {
   const auto& Tm = leaf_template();
@@ -424,7 +425,7 @@ __device__ __forceinline__ void stage_panel_program(uint64_t* dst) {
   constexpr int NPI = S.ng * (S.K + NC);
   const LeafItemP* g = c_ltab.P[CI] + c_ltab.poff[CI][R];
   if constexpr (kLeafStage)
-    for (int t = threadIdx.x; t < NPI; t += NTH) cp_async8(dst + t, g + t);
+    for (int t = threadIdx.x % NTH; t < NPI; t += NTH) cp_async8(dst + t, g + t);
   cp_async_commit();
 }
 
@@ -490,6 +491,16 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
 //      sons' contributions A~ = Psi_s1 + Psi_s2 (and R_B) into `out`
 //   C  [W | V] = L^-1 [A21 | R_gamma] in place (thread per column)
 //   D  out -= W^T [W | V] on 8x8 DMMA tiles; sigma += V_0^T V
+#ifndef HDD_LEAF_G
+#define HDD_LEAF_G 1     // (leaf, sample) groups per leaf CTA, see leaf2_kernel
+#endif
+// barrier of one (leaf, sample) group: the CTA barrier, or with HDD_LEAF_G > 1 and
+// HDD_LEAF_NAMED a named barrier per group (groups start together and may drift)
+#if defined(HDD_LEAF_NAMED) && HDD_LEAF_G > 1
+#define LEAF_SYNC() asm volatile("bar.sync %0, %1;" ::"r"(int(threadIdx.x / NTH) + 1), "n"(NTH) : "memory")
+#else
+#define LEAF_SYNC() __syncthreads()
+#endif
 template <int R, int NC, int NTH, bool EXT = false>
 __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __restrict__ in, double* __restrict__ out,
                                            double* __restrict__ pan, const int* __restrict__ cinfo, int leaf,
@@ -516,7 +527,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
   constexpr int NPW = 32 / LPN;                                           // nodes per Cholesky warp
   constexpr int NWB = (nf + NPW - 1) / NPW;                               // Cholesky warps
   static_assert(NWB < NW, "the sons' gather needs free warps");
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x % NTH, lane = tid & 31;   // NTH threads per (leaf, sample) group
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // provably warp-uniform
   const int sub = warp % gsz;
   const int* ctype = cinfo;
@@ -532,7 +543,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
     cp_async_commit();
   }
   cp_async_wait<1>();   // this level's panel program (issued one level earlier) has landed
-  __syncthreads();
+  LEAF_SYNC();
   // ---- A: gather the interface panel (precomputed program) ----
   // The program of a level is the same for its nf nodes: a thread decodes item t once
   // and applies it to every node q (compile-time strides 2 Sin / ng W), UT items in
@@ -570,7 +581,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
     }
   }
   cp_async_wait<0>();   // update program landed
-  __syncthreads();
+  LEAF_SYNC();
   if constexpr (R > 0) stage_panel_program<R - 1, NC, NTH>(tabPnext);
   LEAF_TICK(10 + 8 * (5 - R) + 0);
   if (warp < NWB) {
@@ -649,7 +660,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
     if (warp == NW - 1 && lane < NC && br[lane] == R)
       Pp[bq[lane] * ng * W + bg[lane] * W + K + lane] += 1.0;
   }
-  __syncthreads();
+  LEAF_SYNC();
   LEAF_TICK(10 + 8 * (5 - R) + 1);
   // ---- C: [W | V] = L^-1 [A21 | R_gamma] in place, a thread per column ----
   for (int t = tid; t < nf * WX; t += NT) {
@@ -669,7 +680,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
 #pragma unroll
     for (int g = 0; g < ng; ++g) P[g * W + col] = w[g];
   }
-  __syncthreads();
+  LEAF_SYNC();
   LEAF_TICK(10 + 8 * (5 - R) + 2);
   // ---- D: out -= W^T [W | V]; sigma += V_0^T V ----
   if constexpr (kE) {
@@ -885,7 +896,7 @@ __device__ __forceinline__ void leaf_level(const DevPlan& p, const double* __res
     }
   }
   if constexpr (R == 0) fence_proxy_async_smem();   // the Psi block is read by the bulk copy below
-  __syncthreads();
+  LEAF_SYNC();
   if constexpr (R == 0) {
     // leaf output: Psi packed lower, R [64][leaf_cols] (mean columns rescaled by
     // 1/|leaf|, an exact power of two), sigma; primal-mode leaf functionals
@@ -1068,15 +1079,25 @@ __device__ __forceinline__ void l56_row(const L56Node& n, const double (&M)[6], 
 // level-synchronously in shared memory with lower-packed Schur complements:
 // gather the interface panel, Gauss-Jordan interface inverse (warp per node),
 // Y = A22^-1 [A21 | R], then the Schur update A11 - A21^T Y on DMMA tiles.
+// HDD_LEAF_G > 1: G (leaf, sample) groups of NTH threads per CTA, the same leaf for G
+// consecutive samples.  The groups run in lockstep (every barrier is CTA-wide), so they
+// fetch each instruction line together: the kernel is ~120 KB of straight-line code run
+// once per item, far beyond the 32 KB L1.5 instruction cache (ncu: icc hit rate 75 %).
+__host__ __device__ constexpr int leaf_minb(int nc) { return kLeafStage ? 2 : (nc == 2 ? 4 : (nc == 4 ? 3 : 2)); }
+__host__ __device__ constexpr int leaf_groups(int nc) { return leaf_minb(nc) % HDD_LEAF_G == 0 ? HDD_LEAF_G : 1; }
 template <int NC, int NTH, bool SUB>   // SUB: sub-leaf mean columns or Dirichlet data present
-__global__ void __launch_bounds__(NTH, kLeafStage ? 2 : (NC == 2 ? 4 : (NC == 4 ? 3 : 2))) leaf2_kernel(DevPlan p, const int* __restrict__ order, LeafSmem ls,
+__global__ void __launch_bounds__(NTH * leaf_groups(NC), leaf_minb(NC) / leaf_groups(NC)) leaf2_kernel(DevPlan p, const int* __restrict__ order, LeafSmem ls,
                                                        int B) {
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(16) double sm_all[];
+  constexpr int G = leaf_groups(NC);
+  const int grp = G > 1 ? threadIdx.x / NTH : 0;
+  double* sm = sm_all + size_t(grp) * ls.group_doubles;
   const int leaf = order[blockIdx.x];
-  const int s = blockIdx.y;
+  // a ragged last CTA recomputes the last sample in its spare groups (identical stores)
+  const int s = G > 1 ? min(int(blockIdx.y) * G + grp, B - 1) : int(blockIdx.y);
   const int pass = blockIdx.z;
   LEAF_TICK(0);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x % NTH;
   constexpr int NT = NTH;
   const DevLeaf& L = p.leaves[leaf];
   if (pass > 0 && 1 + (NC - 1) * pass >= L.ncols) return;   // no columns left for this pass
@@ -1121,7 +1142,7 @@ __global__ void __launch_bounds__(NTH, kLeafStage ? 2 : (NC == 2 ? 4 : (NC == 4 
     }
     cp_async_wait<1>();
   }
-  __syncthreads();
+  LEAF_SYNC();
   const int* ctype = cinfo;
   const int* br = cinfo + NC;
   const int* bq = cinfo + 2 * NC;
@@ -1163,7 +1184,7 @@ __global__ void __launch_bounds__(NTH, kLeafStage ? 2 : (NC == 2 ? 4 : (NC == 4 
       default: l56_row<7, NC, SUB>(n, M, out, ctype, br, bq, q); break;
     }
   }
-  __syncthreads();
+  LEAF_SYNC();
 
   LEAF_TICK(1);
   // ---------------- levels 5..0 in shared memory ----------------
@@ -1181,16 +1202,18 @@ cudaError_t launch_leaf(const DevPlan& p, int B, cudaStream_t s, size_t* smem_ou
     const int cnt = p.leaf_class_count[cls];
     if (cnt == 0) continue;
     const int ncl = cls == 0 ? 2 : (cls == 1 ? 4 : 8);
-    const LeafSmem ls = leaf_sizes(ncl);
-    const size_t smem = leaf_smem_bytes(ncl);
+    LeafSmem ls = leaf_sizes(ncl);
+    const int G = leaf_groups(ncl);
+    ls.group_doubles = int((leaf_smem_bytes(ncl) / sizeof(double) + 1) & ~size_t(1));   // 16-byte aligned groups
+    const size_t smem = G > 1 ? size_t(G) * ls.group_doubles * sizeof(double) : leaf_smem_bytes(ncl);
     if (smem_out) *smem_out = smem;
-    dim3 grid(cnt, B, p.leaf_class_passes[cls]);
+    dim3 grid(cnt, (B + G - 1) / G, p.leaf_class_passes[cls]);
     const int* ord = p.leaf_order + p.leaf_class_start[cls];
     cudaError_t e;
 #define HDD_LAUNCH_LEAF(NCV, SUBV)                                                                             \
   e = cudaFuncSetAttribute(leaf2_kernel<NCV, 256, SUBV>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
   if (e != cudaSuccess) return e;                                                                              \
-  leaf2_kernel<NCV, 256, SUBV><<<grid, 256, smem, s>>>(p, ord, ls, B);
+  leaf2_kernel<NCV, 256, SUBV><<<grid, 256 * G, smem, s>>>(p, ord, ls, B);
     // sub-leaf mean columns and Dirichlet data only exist in plans that need them
     // (separate instantiation: the likelihood configs never pay for them)
     if (p.has_submean || p.leaf_g || p.gcall) {
@@ -1955,8 +1978,13 @@ __device__ __forceinline__ void store_factors(const DevPlan& p, const DevUpper& 
 // registers, column broadcasts by shuffles; L -> Ls (lower, zero upper), 1/L_ii ->
 // Ld, then L^-1 -> Li column by column (lane = column).  *bad = 1 on a
 // non-positive pivot.
+#ifdef HDD_FACTOR8_NOINLINE     // A/B: one copy of the ~500-instruction factor (instruction-cache footprint)
+__device__ __noinline__ void factor_block8(const double* D, int ld, double* Ls, double* Li, double* Ld,
+                                           int* bad) {
+#else
 __device__ __forceinline__ void factor_block8(const double* D, int ld, double* Ls, double* Li, double* Ld,
                                               int* bad) {
+#endif
   const int lane = threadIdx.x & 31, i = lane & 7;
   double a[8];
 #pragma unroll
@@ -2072,7 +2100,11 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
   __syncthreads();                         // panel gathered
   MERGE_TICK(2);
   if (warp == 0) factor_block8(P + k, ldp, Ls, Li, piv, &s_bad);
+#ifdef HDD_PROFILE_TICKS
+  if (blockIdx.x == HDD_TICK_X && blockIdx.y == HDD_TICK_Y && threadIdx.x == 0 && slot >= 0 && slot < 16) g_merge_clk[slot + 16][0] = clock64();
+#endif
   __syncthreads();
+  MERGE_TICK(6);                           // first diagonal block factored
   for (int r0 = 0; r0 < ngp; r0 += NB) {
     // block rows X = L^-1 P[r0:r0+8, :] in place, 8-column DMMA tiles across warps
     for (int t = warp; t < (W + 7) / 8; t += NWp) {
@@ -2091,6 +2123,7 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
       }
     }
     __syncthreads();
+    if (r0 == 0) MERGE_TICK(7);            // first block row applied
     const int rn = r0 + NB;                // next block
     if (rn >= ngp) break;
     if (warp == 0) {

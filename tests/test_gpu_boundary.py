@@ -235,3 +235,34 @@ def test_device_mismatch_is_usage_error(cuda):
         with pytest.raises(hb.UsageError):
             hb.log_likelihood_batch(prob, torch.zeros((2, 2), dtype=torch.float64, device="cuda:0"))
         prob._plan.device = 0
+
+
+def test_stage_kernel_names_follow_the_launch_rules(cuda):
+    """hdd_plan_stage_kernel names the kernel each tree depth launches (bench.py groups
+    its CUDA-event stage times by it): the kernel leaves, then tier-M merges for C2; a
+    forced HBM-panel tier switches every depth to merge_l_kernel."""
+    import ctypes as C
+    import os
+
+    from paper_1708_02207_b200 import configs
+
+    def names(prob, B):
+        plan = prob.plan()
+        info = plan.info()
+        out = []
+        buf = C.create_string_buffer(160)
+        for dep in [-1] + list(range(info.leaf_depth - 1, -1, -1)):
+            plan.check(plan.lib.hdd_plan_stage_kernel(plan.handle, dep, B, buf, 160))
+            out.append(buf.value.decode())
+        assert plan.lib.hdd_plan_stage_kernel(plan.handle, info.leaf_depth + 3, B, buf, 160) != 0
+        return out
+
+    got = names(configs.make_problem("C2", device=0), 1024)
+    assert got[0].startswith("leaf2_kernel<") and len(got) == 1 + 6
+    assert all(n.startswith("merge_m2_kernel<8,") for n in got[1:])
+    os.environ["HDD_FORCE_TIER_L"] = "1"
+    try:
+        got_l = names(configs.make_problem("C2", device=0), 1024)
+    finally:
+        del os.environ["HDD_FORCE_TIER_L"]
+    assert all("merge_l_kernel<" in n for n in got_l[1:])

@@ -50,4 +50,8 @@ for d in range(info.leaf_depth - 1, -1, -1):
     c = [int(mc[d * 8 + i]) for i in range(6)]
     if c[0] == 0:
         continue
-    print(f"  d{d}: " + "  ".join(str(c[i + 1] - c[i]) for i in range(5)) + f"   total {c[5] - c[0]}")
+    c67 = [int(mc[d * 8 + 6]), int(mc[d * 8 + 7])]
+    fend = int(mc[(d + 16) * 8]) if d < 16 else 0
+    extra = (f"   [tier M: first factor {c67[0] - c[2]} (warp 0 alone {fend - c[2]}), first row apply {c67[1] - c67[0]}]"
+             if c67[0] > c[2] else "")
+    print(f"  d{d}: " + "  ".join(str(c[i + 1] - c[i]) for i in range(5)) + f"   total {c[5] - c[0]}" + extra)
