@@ -2032,6 +2032,9 @@ size_t merge_m2_smem_bytes(int ngp, int ldp, int K, int nc) {
   return sizeof(double) * (size_t(ngp) * ldp + 8 + 128 + ints / 2 + 2 * size_t(nc) + 2) + 64;   // +2: 16-byte alignment of the staged sons
 }
 
+#ifndef HDD_M2_GATHER8_MINB
+#define HDD_M2_GATHER8_MINB 2   // tier-M instantiations (by CTAs/SM) whose panel gather keeps 8 loads per thread in flight
+#endif
 template <int NB, int NTH, int MINB>
 __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int slot) {
   extern __shared__ __align__(16) double sm[];
@@ -2088,7 +2091,7 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
   __syncthreads();                         // maps staged; the mbarrier is initialised
   if (U.stage) mbar_wait(&s_bar, 0);
   MERGE_TICK(1);
-  for (int g = warp; g < ngp; g += NWp) gather_panel_row<MINB <= 2 ? 8 : 4>(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32);
+  for (int g = warp; g < ngp; g += NWp) gather_panel_row<(MINB <= HDD_M2_GATHER8_MINB) ? 8 : 4>(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   const int gq = lane & 3, gr = lane >> 2;
   double* Ls = piv + 8;                    // [8][8] diagonal-block factor L (piv: 1/L_ii)
