@@ -2267,6 +2267,7 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
         auto stage = [&](int h0, int buf) {
           double* Sa = St + buf * SB;
           double* Sb = Sa + kLH * kLdd;
+#ifdef HDD_ELIM_CP8
           for (int t = tid; t < kLH * 32; t += 256) {
             const int g = t >> 5, i = t & 31;
             cp_async8(Sa + g * kLdd + i, Arow + int64_t(h0 + g) * ldp + i);
@@ -2277,6 +2278,30 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
             if (v < nv) cp_async8(Sb + g * kLWs + j, P + int64_t(h0 + g) * ldp + phys(v));
             else Sb[g * kLWs + j] = 0.0;
           }
+#else
+          // column pairs as 16-byte copies where the panel columns are even-aligned and
+          // contiguous (even ldp; a pair never straddles the segment wrap), else per element
+          const bool a16 = ((k + r0) & 1) == 0;
+          for (int t = tid; t < kLH * 16; t += 256) {
+            const int g = t >> 4, i = 2 * (t & 15);
+            const double* src = Arow + int64_t(h0 + g) * ldp + i;
+            double* dst = Sa + g * kLdd + i;
+            if (a16) cp_async16(dst, src);
+            else { cp_async8(dst, src); cp_async8(dst + 1, src + 1); }
+          }
+          for (int t = tid; t < kLH * (kLW / 2); t += 256) {
+            const int g = t / (kLW / 2), j = 2 * (t - (t / (kLW / 2)) * (kLW / 2));
+            const int v = v0 + j;
+            double* dst = Sb + g * kLWs + j;
+            const double* row = P + int64_t(h0 + g) * ldp;
+            const int pc = phys(v);
+            if (v + 1 < nv && (pc & 1) == 0 && (v + 1 < nseg || v >= nseg)) cp_async16(dst, row + pc);
+            else {
+              if (v < nv) cp_async8(dst, row + pc); else dst[0] = 0.0;
+              if (v + 1 < nv) cp_async8(dst + 1, row + phys(v + 1)); else dst[1] = 0.0;
+            }
+          }
+#endif
           cp_async_commit();
         };
         // the block's own panel values, loaded ahead of the depth-r0 GEMM
