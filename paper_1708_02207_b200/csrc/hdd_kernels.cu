@@ -1565,14 +1565,14 @@ __device__ __forceinline__ double gather_sig(const MergeCtx& c, int col) {
 // per thread in flight (the son reads are independent, predicated loads)
 template <int U = 4>
 __device__ __forceinline__ void gather_panel_row(const MergeCtx& c, int k, int ng, int Kp, int W, int g,
-                                                 double* dst, int lane0, int step) {
+                                                 double* dst, int lane0, int step, int jfirst = 0) {
   if (g >= ng) {
-    for (int j = lane0; j < W; j += step) dst[j] = (j == k + g) ? 1.0 : 0.0;
+    for (int j = jfirst + lane0; j < W; j += step) dst[j] = (j == k + g) ? 1.0 : 0.0;
     return;
   }
   const int a = k + g;
   const int pa0 = c.gm[a], pa1 = c.gm[c.K + a];
-  for (int j0 = lane0; j0 < W; j0 += U * step) {
+  for (int j0 = jfirst + lane0; j0 < W; j0 += U * step) {
     double v0[U], v1[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -1597,6 +1597,84 @@ __device__ __forceinline__ void gather_panel_row(const MergeCtx& c, int k, int n
       if (j < W) dst[j] = v0[u] + v1[u];
     }
   }
+}
+
+// Panel gather on 16-row x 32-column tiles through a per-warp smem tile, so that every
+// read of a son's packed-lower Psi is contiguous along the lanes: a son entry (pa, pb)
+// sits at tri(max) + min, i.e. it is contiguous along the COLUMNS j where pa >= pb and
+// along the ROWS g where pa < pb.  Pass 1 (lane = column) takes the terms with pa >= pb,
+// pass 2 (half-warp lane = row, the two half-warps on even / odd columns) the terms with
+// pa < pb; the tile then leaves as 32-column row segments.  The row-wise gather
+// (gather_panel_row) read the pa < pb half with one 32-byte sector per lane (VERDICT r01:
+// 2.5-2.8x the ideal L2 sectors).  Columns [0, Kp) only; the R columns stay row-wise.
+// OFF by default (HDD_GATHER_TILE): measured slower, C4 d5 / d4 / d3 25.5 / 31.8 / 23.3 ->
+// 27.6 / 33.2 / 23.9 ms: the gather is bound by the load round trips per thread (twice as
+// many here), not by the sectors.
+// Each element has at most two terms (one per son), so the sum does not depend on which
+// pass brings which term.
+constexpr int kGT = 16;                      // tile rows
+constexpr int kGTs = 33;                     // tile row stride (doubles)
+__device__ __forceinline__ void gather_panel_tile(const MergeCtx& c, int k, int ng, int Kp, int g0, int j0,
+                                                  double* __restrict__ tile, double* __restrict__ P, int64_t ldp,
+                                                  int lane) {
+  const int KA = k + ng;                     // A columns end
+  // ---- pass 1: lane = column j, rows in turn; terms with pa >= pb ----
+  {
+    const int j = j0 + lane;
+    const bool jl = j < KA;
+    const int pb0 = jl ? c.gm[j] : -1, pb1 = jl ? c.gm[c.K + j] : -1;
+#pragma unroll
+    for (int r0 = 0; r0 < kGT; r0 += 8) {
+      double v0[8], v1[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int g = g0 + r0 + u;
+        v0[u] = 0.0;
+        v1[u] = 0.0;
+        if (g < ng) {
+          const int pa0 = c.gm[k + g], pa1 = c.gm[c.K + k + g];
+          if (pb0 >= 0 && pa0 >= pb0) v0[u] = c.sv[0].b[tri(pa0) + pb0];
+          if (pb1 >= 0 && pa1 >= pb1) v1[u] = c.sv[1].b[tri(pa1) + pb1];
+        } else if (j == k + g) {
+          v0[u] = 1.0;                       // padding rows: identity
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tile[(r0 + u) * kGTs + lane] = v0[u] + v1[u];
+    }
+  }
+  __syncwarp();
+  // ---- pass 2: lane & 15 = row, lane >> 4 = column parity; terms with pa < pb ----
+  {
+    const int g = g0 + (lane & 15);
+    const bool gl = g < ng;
+    const int pa0 = gl ? c.gm[k + g] : -1, pa1 = gl ? c.gm[c.K + k + g] : -1;
+    double* trow = tile + (lane & 15) * kGTs;
+#pragma unroll
+    for (int c0 = 0; c0 < 32; c0 += 16) {
+      double v0[8], v1[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + c0 + 2 * u + (lane >> 4);
+        v0[u] = 0.0;
+        v1[u] = 0.0;
+        if (j < KA) {
+          const int pb0 = c.gm[j], pb1 = c.gm[c.K + j];
+          if (pa0 >= 0 && pa0 < pb0) v0[u] = c.sv[0].b[tri(pb0) + pa0];
+          if (pa1 >= 0 && pa1 < pb1) v1[u] = c.sv[1].b[tri(pb1) + pa1];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) trow[c0 + 2 * u + (lane >> 4)] += v0[u] + v1[u];
+    }
+  }
+  __syncwarp();
+  // ---- the tile's rows to the panel (32 consecutive columns per row) ----
+  if (j0 + lane < Kp) {
+#pragma unroll 4
+    for (int r = 0; r < kGT; ++r) P[int64_t(g0 + r) * ldp + j0 + lane] = tile[r * kGTs + lane];
+  }
+  __syncwarp();
 }
 
 // Schur-update epilogue on 32 x 64 output tiles (lower-triangle Psi tiles and
@@ -2236,7 +2314,20 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
   }
   MERGE_TICK(1);
   if (!p.schur_split)     // split mode: assemble_l_kernel has written the panel
+#ifndef HDD_GATHER_TILE    // A/B: the tile gather below measured slower (latency-bound, not sector-bound)
     for (int g = warp; g < ngp; g += 8) gather_panel_row<8>(mc, k, ng, Kp, W, g, P + int64_t(g) * ldp, lane, 32);
+#else
+  {
+    // columns [0, Kp) on 16 x 32 tiles (coalesced son reads), the R columns row-wise
+    double* tile = sm + warp * (kGT * kGTs);             // the front region is idle until the elimination
+    const int nct = (Kp + 31) / 32, nt = (ngp / kGT) * nct;
+    for (int t = warp; t < nt; t += 8) {
+      const int gb = t / nct;
+      gather_panel_tile(mc, k, ng, Kp, gb * kGT, (t - gb * nct) * 32, tile, P, ldp, lane);
+    }
+    for (int g = warp; g < ngp; g += 8) gather_panel_row<8>(mc, k, ng, Kp, W, g, P + int64_t(g) * ldp, lane, 32, Kp);
+  }
+#endif
   if (tid == 0) s_bad = 0;
   __syncthreads();
   MERGE_TICK(2);
