@@ -1599,6 +1599,34 @@ __device__ __forceinline__ void gather_panel_row(const MergeCtx& c, int k, int n
   }
 }
 
+// Tier M (panel in shared memory, sons in global memory): the A21 columns j < k of panel
+// row g have ONE term except at the (at most two) son-shared columns, so they go straight
+// from the son's packed Psi into the panel with cp.async: no registers, every element of
+// the row in flight at once (the register gather keeps U elements per thread in flight and
+// pays one L2 round trip per U x 32 columns).  The A22 / R columns and the shared columns
+// keep the register path (two terms, coefficients).  The caller commits and waits.
+__device__ __forceinline__ void gather_panel_row_async(const MergeCtx& c, int k, int ng, int g, double* dst,
+                                                       int lane) {
+  if (g >= ng) {
+    for (int j = lane; j < k; j += 32) dst[j] = 0.0;
+    return;
+  }
+  const int pa0 = c.gm[k + g], pa1 = c.gm[c.K + k + g];
+  const int ta0 = tri(pa0), ta1 = tri(pa1);
+  for (int j = lane; j < k; j += 32) {
+    const int pb0 = c.gm[j], pb1 = c.gm[c.K + j];
+    if (pb0 >= 0 && pb1 >= 0) {              // son-shared column: both terms
+      dst[j] = son_psi(c.sv[0], pa0, pb0) + son_psi(c.sv[1], pa1, pb1);
+    } else if (pb0 >= 0) {
+      cp_async8(dst + j, c.sv[0].b + (pa0 >= pb0 ? ta0 + pb0 : tri(pb0) + pa0));
+    } else if (pb1 >= 0) {
+      cp_async8(dst + j, c.sv[1].b + (pa1 >= pb1 ? ta1 + pb1 : tri(pb1) + pa1));
+    } else {
+      dst[j] = 0.0;
+    }
+  }
+}
+
 // Panel gather on 16-row x 32-column tiles through a per-warp smem tile, so that every
 // read of a son's packed-lower Psi is contiguous along the lanes: a son entry (pa, pb)
 // sits at tri(max) + min, i.e. it is contiguous along the COLUMNS j where pa >= pb and
@@ -2169,6 +2197,15 @@ __global__ void __launch_bounds__(NTH, MINB) merge_m2_kernel(DevPlan p, const De
   __syncthreads();                         // maps staged; the mbarrier is initialised
   if (U.stage) mbar_wait(&s_bar, 0);
   MERGE_TICK(1);
+#ifdef HDD_M2_GATHER_ASYNC
+  if (!U.stage) {
+    for (int g = warp; g < ngp; g += NWp) gather_panel_row_async(mc, k, ng, g, P + g * ldp, lane);
+    cp_async_commit();
+    for (int g = warp; g < ngp; g += NWp)
+      gather_panel_row<(MINB <= HDD_M2_GATHER8_MINB) ? 8 : 4>(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32, k);
+    cp_async_wait<0>();
+  } else
+#endif
   for (int g = warp; g < ngp; g += NWp) gather_panel_row<(MINB <= HDD_M2_GATHER8_MINB) ? 8 : 4>(mc, k, ng, Kp, W, g, P + g * ldp, lane, 32);
   if (tid == 0) s_bad = 0;
   const int gq = lane & 3, gr = lane >> 2;
