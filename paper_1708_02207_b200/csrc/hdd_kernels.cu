@@ -2989,11 +2989,12 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
   double* psi = p.buf[U.buf] + U.out_off * p.bcap + int64_t(s) * U.out_elems;
   const int32_t* R = p.lr_rows + roff;
   const int32_t* Cc = p.lr_cols + coff;
-  double* Y = sm;                         // [P_][33]
-  double* G = Y + size_t(P_) * 33;        // [32][kLdd] gram / pivoted factor C
+  constexpr int YS = LW + 1;              // sketch row stride (odd: conflict-free column reads)
+  double* Y = sm;                         // [P_][YS]
+  double* G = Y + size_t(P_) * YS;        // [32][kLdd] gram / pivoted factor C
   double* LiT = G + 32 * kLdd;            // [32][kLdd]
-  double* Bc = LiT + 32 * kLdd;           // [32][65] chunk of B (or D)
-  double* red = Bc + 32 * 65;             // [64]
+  double* Bc = LiT + 32 * kLdd;           // [LW][65] chunk of B (or D)
+  double* red = Bc + LW * 65;             // [64]
   __shared__ int s_bad, s_k, s_conv, s_piv[32];
   __shared__ double s_an2, s_bn2;
   auto A = [&](int i, int j) { const int r = R[i], c = Cc[j]; return r >= c ? psi[tri(r) + c] : psi[tri(c) + r]; };
@@ -3029,12 +3030,12 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
           }
         }
       }
-      double* yr = Y + i * 33;
+      double* yr = Y + i * YS;
       for (int g = 0; g < JG; ++g) {
         if (live && jg == g) {
 #pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            const double v = (t < LW && t < L) ? acc[t < LW ? t : 0] : 0.0;
+          for (int t = 0; t < LW; ++t) {
+            const double v = t < L ? acc[t] : 0.0;
             yr[t] = g == 0 ? v : yr[t] + v;
           }
         }
@@ -3075,7 +3076,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
       const int a = t >> 5, b = t & 31;
       double v = 0.0;
       if (a < L && b < L)
-        for (int i = 0; i < P_; ++i) v = fma(Y[i * 33 + a], Y[i * 33 + b], v);
+        for (int i = 0; i < P_; ++i) v = fma(Y[i * YS + a], Y[i * YS + b], v);
       G[a * kLdd + b] = v;
     }
     __syncthreads();
@@ -3097,8 +3098,8 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
     for (int i0 = 0; i0 < P_; i0 += 32) {
       const int i = i0 + (tid >> 3), c0 = (tid & 7) * 4;
       double v[4] = {0.0, 0.0, 0.0, 0.0};
-      if (i < P_) {
-        const double* yr = Y + i * 33;
+      if (i < P_ && c0 < LW) {
+        const double* yr = Y + i * YS;
         for (int t = 0; t < c0 + 4; ++t) {
           const double yt = yr[t];
 #pragma unroll
@@ -3107,9 +3108,9 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
         }
       }
       __syncthreads();
-      if (i < P_)
+      if (i < P_ && c0 < LW)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) Y[i * 33 + c0 + u] = c0 + u < L ? v[u] : 0.0;
+        for (int u = 0; u < 4; ++u) Y[i * YS + c0 + u] = c0 + u < L ? v[u] : 0.0;
     }
     __syncthreads();
   }
@@ -3121,7 +3122,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
     {   // B chunk: thread per (column, quarter of the rows), all LW rows of B in
         // registers; each A entry read once, the quarters summed in smem in a fixed
         // order (quarter 0 stores, 1..3 add in turn: bitwise reproducible)
-      for (int t = tid; t < 32 * 65; t += 256) Bc[t] = 0.0;
+      for (int t = tid; t < LW * 65; t += 256) Bc[t] = 0.0;
       __syncthreads();
       const int jj = tid & 63, ig = tid >> 6, j = j0 + jj;
       double v[LW];
@@ -3134,7 +3135,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
         for (int i = ig; i < P_; i += 4) {
           const int r = R[i];
           const double x = r >= c ? psi[tri(r) + c] : psi[tc + r];
-          const double* yr = Y + i * 33;
+          const double* yr = Y + i * YS;
 #pragma unroll
           for (int u = 0; u < LW; ++u) v[u] = fma(yr[u], x, v[u]);
         }
@@ -3228,9 +3229,9 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
   }
   if (!decided || int64_t(kk) * (P_ + Q_) >= int64_t(P_) * Q_) return;   // stays dense
   // ---- pass 3: A_k = Q (C D) with D = L_SS^-1 B_S, per 64-column chunk ----
-  double* Ec = red + 64;                  // [32][65]
+  double* Ec = red + 64;                  // [LW][65]
   for (int j0 = 0; j0 < Q_; j0 += 64) {
-    for (int t = tid; t < 32 * 65; t += 256) Bc[t] = 0.0;     // B_S rows (pivot order)
+    for (int t = tid; t < LW * 65; t += 256) Bc[t] = 0.0;     // B_S rows (pivot order)
     __syncthreads();
     {
       const int jj = tid & 63, ig = tid >> 6, j = j0 + jj;
@@ -3247,7 +3248,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
         for (int i = ig; i < P_; i += 4) {
           const int r = R[i];
           const double x = r >= c ? psi[tri(r) + c] : psi[tc + r];
-          const double* yr = Y + i * 33;
+          const double* yr = Y + i * YS;
 #pragma unroll
           for (int u = 0; u < LW; ++u)
             if (u < kk) v[u] = fma(yr[pvt[u]], x, v[u]);
@@ -3270,7 +3271,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
       }
     }
     __syncthreads();
-    for (int t = tid; t < 32 * 64; t += 256) {    // E = C D  (L x 64)
+    for (int t = tid; t < LW * 64; t += 256) {    // E = C D  (L x 64)
       const int a = t >> 6, jj = t & 63;
       double v = 0.0;
       if (a < L)
@@ -3282,7 +3283,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
       const int i = t >> 6, jj = t & 63, j = j0 + jj;
       if (j >= Q_) continue;
       double v = 0.0;
-      for (int a = 0; a < L; ++a) v = fma(Y[i * 33 + a], Ec[a * 65 + jj], v);
+      for (int a = 0; a < L; ++a) v = fma(Y[i * YS + a], Ec[a * 65 + jj], v);
       const int r = R[i], c = Cc[j];
       psi[r >= c ? tri(r) + c : tri(c) + r] = v;
     }
@@ -3486,13 +3487,19 @@ __global__ void __launch_bounds__(256) compress_wide_kernel(DevPlan p, const Dev
   }
 }
 
+#ifdef HDD_LR_MINB3_BY_SMEM   // A/B: the 80-register 3-CTA/SM instantiation wherever three sketches fit an SM
+#define HDD_LR_MINB3(pmax, smem) ((smem) <= 74 * 1024)
+#else
+#define HDD_LR_MINB3(pmax, smem) ((pmax) <= 64)
+#endif
 cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_nodes, int blk0, int nblk, int B,
                             int pmax, cudaStream_t s) {
   psi_norm_kernel<<<dim3(B, n_nodes), 256, 0, s>>>(p, nodes_dev, n_nodes);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (nblk == 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * (size_t(pmax) * 33 + 2 * 32 * kLdd + 2 * 32 * 65 + 64) + 64;
+  const int lw = p.lr_l <= 16 ? 16 : (p.lr_l <= 24 ? 24 : 32);
+  const size_t smem = sizeof(double) * (size_t(pmax) * (lw + 1) + 2 * 32 * kLdd + 2 * size_t(lw) * 65 + 64) + 64;
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e2 != cudaSuccess) return e2;
@@ -3501,7 +3508,7 @@ cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_n
   };
   // levels of small blocks (<= 64 rows) are latency-bound: three CTAs per SM (80
   // registers) beat the spill-free two (measured on C5 depths 10-11)
-  if (pmax <= 64) {
+  if (HDD_LR_MINB3(pmax, smem)) {
     if (p.lr_l <= 16) return go(compress_kernel<16, 3>);
     if (p.lr_l <= 24) return go(compress_kernel<24, 3>);
     return go(compress_kernel<32, 3>);
