@@ -2008,6 +2008,14 @@ __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const doubl
         __syncthreads();
         if (c + 2 < nch) stage(c + 2, (c + 2) % 3);
         const double* Ea = E + (c % 3) * 2 * kEC * kLds;
+#elif defined(HDD_ONE_BARRIER)
+        // two buffers, one barrier per chunk: the barrier publishes chunk c and tells that
+        // every warp has left chunk c - 1, whose buffer then takes chunk c + 1 (same
+        // prefetch distance as staging before the wait: one chunk of DMMAs)
+        cp_async_wait<0>();
+        __syncthreads();
+        if (c + 1 < nch) stage(c + 1, (c + 1) & 1);
+        const double* Ea = E + (c & 1) * 2 * kEC * kLds;
 #else
         if (c + 1 < nch) {
           stage(c + 1, (c + 1) & 1);
@@ -2032,7 +2040,7 @@ __device__ __forceinline__ void schur_epilogue_l(const MergeCtx& mc, const doubl
             for (int i = 0; i < 4; ++i) dmma884(acc[i][0], av[i], bv);
           }
         }
-#if HDD_EPI_STAGES != 3
+#if HDD_EPI_STAGES != 3 && !defined(HDD_ONE_BARRIER)
         __syncthreads();
 #endif
       }
@@ -2448,6 +2456,16 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
         if (nch > 0) {
           __syncthreads();                   // previous users of the stream buffers are done
           stage(0, 0);
+#ifdef HDD_ONE_BARRIER
+          for (int c = 0; c < nch; ++c) {     // one barrier per chunk, see schur_epilogue_l
+            cp_async_wait<0>();
+            __syncthreads();
+            if (c + 1 < nch) stage((c + 1) * kLH, (c + 1) & 1);
+            const double* Sa = St + (c & 1) * SB;
+            warp_gemm_tn<2, FN>(acc, Sa, kLdd, m0, Sa + kLH * kLdd, kLWs, n0, kLH);
+          }
+          __syncthreads();                    // the T tile below overwrites the stream buffers
+#else
           for (int c = 0; c < nch; ++c) {
             if (c + 1 < nch) {
               stage((c + 1) * kLH, (c + 1) & 1);
@@ -2460,6 +2478,7 @@ __global__ void __launch_bounds__(256, MINB) merge_l_kernel(DevPlan p, const Dev
             warp_gemm_tn<2, FN>(acc, Sa, kLdd, m0, Sa + kLH * kLdd, kLWs, n0, kLH);
             __syncthreads();
           }
+#endif
         } else {
           __syncthreads();
         }
