@@ -3834,7 +3834,8 @@ cudaError_t launch_compress_warp(const DevPlan& p, const DevUpper* nodes_dev, in
   if (nblk == 0) return cudaSuccess;
   const int lw = p.lr_l <= 16 ? 16 : (p.lr_l <= 24 ? 24 : 32);
   const size_t per_warp = sizeof(double) * size_t(cw_stride(pmax, qmax, lw));
-  const int nw = int(std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / per_warp)));   // warps per CTA
+  static const int max_nw = std::getenv("HDD_LR_WARPS") ? std::atoi(std::getenv("HDD_LR_WARPS")) : 8;   // A/B hook
+  const int nw = int(std::max<size_t>(1, std::min<size_t>(size_t(max_nw), (220 * 1024) / per_warp)));   // warps per CTA
   const size_t smem = per_warp * nw;
   const int64_t items = int64_t(nblk) * B;
   const dim3 grid(unsigned((items + nw - 1) / nw));
