@@ -2996,8 +2996,8 @@ __global__ void __launch_bounds__(256) psi_norm_kernel(DevPlan p, const DevUpper
 // block once: a thread owns a row (pass 1) or a column (passes 2, 3) and keeps the LW
 // sketch / projection values of it in registers; partial sums over row or column
 // groups meet in shared memory.
-template <int LW, int MINB>
-__global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int blk0) {
+template <int LW, int MINB, int NT = 256>   // NT = 512: one CTA per SM (sketches above 113 KB), twice the warps
+__global__ void __launch_bounds__(NT, MINB) compress_kernel(DevPlan p, const DevUpper* __restrict__ nodes, int blk0) {
   extern __shared__ __align__(16) double sm[];
   const int32_t* bd = p.lr_blk + 5 * (blk0 + blockIdx.y);
   const int ln = bd[0], roff = bd[1], P_ = bd[2], coff = bd[3], Q_ = bd[4];
@@ -3019,8 +3019,8 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
   auto A = [&](int i, int j) { const int r = R[i], c = Cc[j]; return r >= c ? psi[tri(r) + c] : psi[tri(c) + r]; };
   // ---- pass 1: Y = A Omega (thread per row, all sketch columns), ||A||^2 ----
   // JG thread groups split the columns when the block has few rows
-  const int JG = P_ >= 256 ? 1 : (P_ >= 128 ? 2 : (P_ >= 64 ? 4 : 8));
-  const int RS = 256 / JG;
+  const int JG = P_ >= NT ? 1 : (P_ >= NT / 2 ? 2 : (P_ >= NT / 4 ? 4 : 8));
+  const int RS = NT / JG;
   double an = 0.0;
   {
     // the JG column groups of a row meet in smem in a fixed order (group 0 stores,
@@ -3067,7 +3067,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
   __syncthreads();
   if (tid == 0) {
     double t2 = 0.0;
-    for (int w = 0; w < 8; ++w) t2 += red[w];
+    for (int w = 0; w < NT / 32; ++w) t2 += red[w];
     s_an2 = t2;
   }
   __syncthreads();
@@ -3082,7 +3082,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
     return;
   }
   if (an2 <= 1e-28 * scale2) {          // ||A|| <= 1e-14 ||Psi||: rank 0
-    for (int t = tid; t < P_ * Q_; t += 256) {
+    for (int t = tid; t < P_ * Q_; t += NT) {
       const int i = t / Q_, j = t - i * Q_;
       const int r = R[i], c = Cc[j];
       psi[r >= c ? tri(r) + c : tri(c) + r] = 0.0;
@@ -3091,7 +3091,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
   }
   // ---- shifted CholeskyQR2: Q = Y R^-1 (in place) ----
   for (int pass = 0; pass < 2; ++pass) {
-    for (int t = tid; t < 32 * 32; t += 256) {
+    for (int t = tid; t < 32 * 32; t += NT) {
       const int a = t >> 5, b = t & 31;
       double v = 0.0;
       if (a < L && b < L)
@@ -3114,7 +3114,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
     }
     __syncthreads();
     // Y <- Y R^-1 in place, 32 rows x 8 column groups of 4 per chunk (compute, barrier, write)
-    for (int i0 = 0; i0 < P_; i0 += 32) {
+    for (int i0 = 0; i0 < P_; i0 += NT / 8) {
       const int i = i0 + (tid >> 3), c0 = (tid & 7) * 4;
       double v[4] = {0.0, 0.0, 0.0, 0.0};
       if (i < P_ && c0 < LW) {
@@ -3134,14 +3134,15 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
     __syncthreads();
   }
   // ---- pass 2: M = B B^T with B = Q^T A, in 64-column chunks ----
-  for (int t = tid; t < 32 * 32; t += 256) G[(t >> 5) * kLdd + (t & 31)] = 0.0;
-  double macc[4] = {0.0, 0.0, 0.0, 0.0};     // thread owns M entries tid + 256 u
+  for (int t = tid; t < 32 * 32; t += NT) G[(t >> 5) * kLdd + (t & 31)] = 0.0;
+  constexpr int MU = 1024 / NT;
+  double macc[MU] = {};                      // thread owns M entries tid + NT u
   for (int j0 = 0; j0 < Q_; j0 += 64) {
     __syncthreads();
     {   // B chunk: thread per (column, quarter of the rows), all LW rows of B in
         // registers; each A entry read once, the quarters summed in smem in a fixed
         // order (quarter 0 stores, 1..3 add in turn: bitwise reproducible)
-      for (int t = tid; t < LW * 65; t += 256) Bc[t] = 0.0;
+      for (int t = tid; t < LW * 65; t += NT) Bc[t] = 0.0;
       __syncthreads();
       const int jj = tid & 63, ig = tid >> 6, j = j0 + jj;
       double v[LW];
@@ -3151,7 +3152,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
         const int c = Cc[j];
         const int tc = tri(c);
         #pragma unroll 4   // the block reads of 4 iterations in flight before their FMAs
-        for (int i = ig; i < P_; i += 4) {
+        for (int i = ig; i < P_; i += NT / 64) {
           const int r = R[i];
           const double x = r >= c ? psi[tri(r) + c] : psi[tc + r];
           const double* yr = Y + i * YS;
@@ -3159,7 +3160,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
           for (int u = 0; u < LW; ++u) v[u] = fma(yr[u], x, v[u]);
         }
       }
-      for (int g = 0; g < 4; ++g) {
+      for (int g = 0; g < NT / 64; ++g) {
         if (ig == g && j < Q_)
 #pragma unroll
           for (int u = 0; u < LW; ++u)
@@ -3169,16 +3170,16 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
     }
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = tid + 256 * u, a = e >> 5, b = e & 31;
+    for (int u = 0; u < MU; ++u) {
+      const int e = tid + NT * u, a = e >> 5, b = e & 31;
       if (a < L && b < L)
         for (int jj = 0; jj < 64; ++jj) macc[u] = fma(Bc[a * 65 + jj], Bc[b * 65 + jj], macc[u]);
     }
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int e = tid + 256 * u;
+  for (int u = 0; u < MU; ++u) {
+    const int e = tid + NT * u;
     G[(e >> 5) * kLdd + (e & 31)] = macc[u];
   }
   __syncthreads();
@@ -3250,7 +3251,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
   // ---- pass 3: A_k = Q (C D) with D = L_SS^-1 B_S, per 64-column chunk ----
   double* Ec = red + 64;                  // [LW][65]
   for (int j0 = 0; j0 < Q_; j0 += 64) {
-    for (int t = tid; t < LW * 65; t += 256) Bc[t] = 0.0;     // B_S rows (pivot order)
+    for (int t = tid; t < LW * 65; t += NT) Bc[t] = 0.0;     // B_S rows (pivot order)
     __syncthreads();
     {
       const int jj = tid & 63, ig = tid >> 6, j = j0 + jj;
@@ -3264,7 +3265,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
 #pragma unroll
         for (int u = 0; u < LW; ++u) pvt[u] = u < kk ? s_piv[u] : 0;
         #pragma unroll 4   // the block reads of 4 iterations in flight before their FMAs
-        for (int i = ig; i < P_; i += 4) {
+        for (int i = ig; i < P_; i += NT / 64) {
           const int r = R[i];
           const double x = r >= c ? psi[tri(r) + c] : psi[tc + r];
           const double* yr = Y + i * YS;
@@ -3273,7 +3274,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
             if (u < kk) v[u] = fma(yr[pvt[u]], x, v[u]);
         }
       }
-      for (int g = 0; g < 4; ++g) {     // fixed-order sum of the row quarters
+      for (int g = 0; g < NT / 64; ++g) {     // fixed-order sum of the row groups
         if (ig == g && j < Q_)
 #pragma unroll
           for (int u = 0; u < LW; ++u)
@@ -3282,7 +3283,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
       }
     }
     __syncthreads();
-    for (int jj = tid; jj < 64; jj += 256) {      // forward substitution with L_SS
+    for (int jj = tid; jj < 64; jj += NT) {      // forward substitution with L_SS
       for (int u = 0; u < kk; ++u) {
         double v = Bc[u * 65 + jj];
         for (int w = 0; w < u; ++w) v = fma(-LiT[s_piv[u] * kLdd + w], Bc[w * 65 + jj], v);
@@ -3290,7 +3291,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
       }
     }
     __syncthreads();
-    for (int t = tid; t < LW * 64; t += 256) {    // E = C D  (L x 64)
+    for (int t = tid; t < LW * 64; t += NT) {    // E = C D  (L x 64)
       const int a = t >> 6, jj = t & 63;
       double v = 0.0;
       if (a < L)
@@ -3298,7 +3299,7 @@ __global__ void __launch_bounds__(256, MINB) compress_kernel(DevPlan p, const De
       Ec[a * 65 + jj] = v;
     }
     __syncthreads();
-    for (int t = tid; t < P_ * 64; t += 256) {
+    for (int t = tid; t < P_ * 64; t += NT) {
       const int i = t >> 6, jj = t & 63, j = j0 + jj;
       if (j >= Q_) continue;
       double v = 0.0;
@@ -3519,12 +3520,21 @@ cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_n
   if (nblk == 0) return cudaSuccess;
   const int lw = p.lr_l <= 16 ? 16 : (p.lr_l <= 24 ? 24 : 32);
   const size_t smem = sizeof(double) * (size_t(pmax) * (lw + 1) + 2 * 32 * kLdd + 2 * size_t(lw) * 65 + 64) + 64;
-  auto go = [&](auto kern) -> cudaError_t {
+  auto go = [&](auto kern, int nt = 256) -> cudaError_t {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e2 != cudaSuccess) return e2;
-    kern<<<dim3(B, nblk), 256, smem, s>>>(p, nodes_dev, blk0);
+    kern<<<dim3(B, nblk), nt, smem, s>>>(p, nodes_dev, blk0);
     return cudaGetLastError();
   };
+#ifndef HDD_LR_NO_512
+  // sketches too large for two CTAs per SM (blocks above 362 rows at the 24-column
+  // sketch): one 512-thread CTA per SM instead of one 256-thread CTA (16 warps, not 8)
+  if (smem > 113 * 1024) {
+    if (p.lr_l <= 16) return go(compress_kernel<16, 1, 512>, 512);
+    if (p.lr_l <= 24) return go(compress_kernel<24, 1, 512>, 512);
+    return go(compress_kernel<32, 1, 512>, 512);
+  }
+#endif
   // levels of small blocks (<= 64 rows) are latency-bound: three CTAs per SM (80
   // registers) beat the spill-free two (measured on C5 depths 10-11)
   if (HDD_LR_MINB3(pmax, smem)) {
