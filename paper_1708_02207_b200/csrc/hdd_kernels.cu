@@ -3529,7 +3529,8 @@ cudaError_t launch_compress(const DevPlan& p, const DevUpper* nodes_dev, int n_n
 #ifndef HDD_LR_NO_512
   // sketches too large for two CTAs per SM (blocks above 362 rows at the 24-column
   // sketch): one 512-thread CTA per SM instead of one 256-thread CTA (16 warps, not 8)
-  if (smem > 113 * 1024) {
+  static const bool force512 = std::getenv("HDD_LR_FORCE_512") && std::getenv("HDD_LR_FORCE_512")[0] == '1';   // test hook
+  if (smem > 113 * 1024 || force512) {
     if (p.lr_l <= 16) return go(compress_kernel<16, 1, 512>, 512);
     if (p.lr_l <= 24) return go(compress_kernel<24, 1, 512>, 512);
     return go(compress_kernel<32, 1, 512>, 512);

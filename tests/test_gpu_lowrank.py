@@ -150,3 +150,40 @@ def test_rank_cap_above_device_limit_is_config_error(cuda, golden):
     g = have(golden, 5)
     with pytest.raises(hb.ConfigError, match="64"):
         problem(g, (1e-6, 65, 32)).plan()
+
+
+def test_512_thread_compress_instantiation_within_envelope():
+    """Blocks above 362 rows (C5 depths 5, 4, 3, 1) run `compress_kernel<LW,1,512>`;
+    HDD_LR_FORCE_512 sends every large block of a level-8 problem through it, and the
+    result has to stay inside the same reference envelope.  The hook is read once per
+    process, hence a fresh interpreter."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = Path(__file__).resolve().parents[1]
+    if not (root / "tests" / "golden" / "lowrank_L8.npz").exists():
+        pytest.skip("lowrank_L8.npz not generated")
+    code = r"""
+import sys
+import numpy as np
+sys.path.insert(0, %r)
+sys.path.insert(0, %r)
+import test_gpu_lowrank as t
+g = dict(np.load(%r, allow_pickle=False))
+for spec in ("c5", "e8"):
+    pr = t.problem(g, g["spec_" + spec])
+    S = t.hb.forward_functionals_batch(pr, g["Z"])
+    for b in range(S.shape[0]):
+        e_ref = t.rel(g["S_" + spec][b], g["S_dense"][b])
+        assert t.rel(S[b], g["S_" + spec][b]) <= 2 * e_ref + 1e-12, (spec, b)
+        assert t.rel(S[b], g["S_dense"][b]) <= 2 * e_ref + 1e-12, (spec, b)
+print("ok")
+""" % (str(root), str(root / "tests"), str(root / "tests" / "golden" / "lowrank_L8.npz"))
+    env = dict(os.environ, HDD_LR_FORCE_512="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
